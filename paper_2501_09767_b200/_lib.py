@@ -1,0 +1,103 @@
+"""ctypes binding of liblemo.so (the C ABI in include/lemo.h).
+
+The library is built in-tree (``paper_2501_09767_b200/liblemo.so``).  There is
+no fallback: if the library is missing or a call fails, an exception is
+raised.  Argument types are derived from the declarations in
+``include/lemo.h`` itself, so the binding cannot drift from the header.
+Pointers are passed as integers (``tensor.data_ptr()``), streams as the raw
+``cudaStream_t`` of torch's current stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+import torch
+
+_PKG = Path(__file__).resolve().parent
+_LIB_PATH = _PKG / "liblemo.so"
+HEADER = _PKG.parent / "include" / "lemo.h"
+
+_CT = {"p": ctypes.c_void_p, "i": ctypes.c_int, "f": ctypes.c_float, "d": ctypes.c_double,
+       "l": ctypes.c_longlong}
+_RET = {"int": ctypes.c_int, "void": None, "const char*": ctypes.c_char_p, "double": ctypes.c_double}
+
+
+class LemoError(RuntimeError):
+    pass
+
+
+def _param_code(decl: str) -> str:
+    decl = decl.strip()
+    if "*" in decl:
+        return "p"
+    base = decl.rsplit(None, 1)[0] if " " in decl else decl
+    base = base.replace("const", "").strip()
+    if base in ("int", "int32_t"):
+        return "i"
+    if base == "float":
+        return "f"
+    if base == "double":
+        return "d"
+    if base in ("long long", "int64_t"):
+        return "l"
+    raise ValueError(f"unsupported parameter type in lemo.h: {decl!r}")
+
+
+def parse_header(path: Path = HEADER) -> dict[str, tuple[str, str]]:
+    """name -> (return type, parameter codes) for every lemo_* declaration."""
+    text = re.sub(r"/\*.*?\*/", "", path.read_text(), flags=re.S)
+    text = re.sub(r"//[^\n]*", "", text)
+    out: dict[str, tuple[str, str]] = {}
+    for m in re.finditer(r"(int|void|const char\*|double)\s+(lemo_\w+)\s*\(([^)]*)\)\s*;", text):
+        ret, name, params = m.group(1), m.group(2), m.group(3).strip()
+        if params in ("", "void"):
+            codes = ""
+        else:
+            codes = "".join(_param_code(p) for p in params.split(","))
+        out[name] = (ret, codes)
+    return out
+
+
+SIGNATURES = parse_header()
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise LemoError(
+                f"{_LIB_PATH} is missing: build it with `python -m paper_2501_09767_b200.build` "
+                "(there is no CPU fallback)")
+        handle = ctypes.CDLL(str(_LIB_PATH))
+        for name, (ret, codes) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.argtypes = [_CT[c] for c in codes]
+            fn.restype = _RET[ret]
+        _lib = handle
+    return _lib
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t) -> int | None:
+    """Device address of a tensor (None for None)."""
+    if t is None:
+        return None
+    return int(t.data_ptr())
+
+
+def call(name: str, *args):
+    """Invoke a status-returning entry point; raise LemoError on failure."""
+    fn = getattr(lib(), name)
+    rc = fn(*args)
+    if rc != 0:
+        msg = lib().lemo_last_error().decode(errors="replace")
+        raise LemoError(f"{name} failed ({rc}): {msg}")
+    return rc

@@ -1,0 +1,224 @@
+// Persistent warp-specialised tcgen05 GEMM for sm_100a:  C = A · Bᵀ
+//
+//   A : [M, K] bf16 row-major (K contiguous)      -> TMA box 128 x 64, SW128
+//   B : [N, K] bf16 row-major (K contiguous)      -> TMA box BN  x 64, SW128
+//   accumulator: fp32 in TMEM, two BN-column stages (MMA of tile i+1
+//   overlaps the epilogue of tile i).
+//
+// Warp roles (256 threads):  w0 TMA producer · w1 MMA issuer · w2 TMEM
+// allocator · w3 idle · w4..w7 epilogue (warp w%4 owns TMEM lanes 32·(w%4)…).
+// Every epilogue thread owns one output row of the 128-row tile and pulls
+// its accumulator row out of TMEM in 32-column chunks; the epilogue functor
+// decides what to do with it (plain store, scatter-add into the residual
+// stream at idx[row], RoPE + LoRA, SwiGLU scoring, …).  This is how the
+// "index-remapped epilogue" of the permutation-free path is realised: the
+// GEMM runs on the compact retained rows and the epilogue writes each row
+// straight back to its original position.
+#pragma once
+
+#include "common.cuh"
+
+namespace lemo {
+
+constexpr int kBlockM = 128;
+constexpr int kBlockK = 64;  // one 128-byte swizzle atom of bf16
+constexpr int kUmmaK = 16;
+constexpr int kGemmThreads = 256;
+constexpr int kGroupM = 16;  // rasterisation group (L2 reuse of B tiles)
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kStages = BN >= 256 ? 4 : 6;
+  static constexpr int kABytes = kBlockM * kBlockK * 2;
+  static constexpr int kBBytes = BN * kBlockK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;  // two accumulator stages
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct TileCoord {
+  int m, n;
+};
+
+__device__ __forceinline__ TileCoord tile_coord(int t, int num_m, int num_n) {
+  // grouped rasterisation: kGroupM m-tiles sweep all n before moving on
+  const int per_group = kGroupM * num_n;
+  const int g = t / per_group;
+  const int first_m = g * kGroupM;
+  const int gm = min(num_m - first_m, kGroupM);
+  const int r = t - g * per_group;
+  TileCoord c;
+  c.m = first_m + (r % gm);
+  c.n = r / gm;
+  return c;
+}
+
+// Epilogue contract:
+//   __device__ void operator()(int row, bool valid, int col0, uint32_t taddr) const
+// called by each epilogue thread for its row of the tile; `taddr` is the TMEM
+// address of (this warp's lane base, first accumulator column of the tile).
+// The functor must issue the same sequence of tcgen05.ld for every lane of
+// the warp (they are warp-collective) and only store when `valid`.
+template <int BN, class Epi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   int M, int N, int K, Epi epi) {
+  using Cfg = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + Cfg::kStages * Cfg::kABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + Cfg::kStages;
+  uint64_t* tfull_bar = bars + 2 * Cfg::kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_m = (M + kBlockM - 1) / kBlockM;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (K + kBlockK - 1) / kBlockK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);  // one elected lane per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const TileCoord tc = tile_coord(t, num_m, num_n);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
+          tma_load_2d(&tmA, &full_bar[stage], smem_a + stage * Cfg::kABytes, kb * kBlockK,
+                      tc.m * kBlockM);
+          tma_load_2d(&tmB, &full_bar[stage], smem_b + stage * Cfg::kBBytes, kb * kBlockK,
+                      tc.n * BN);
+          if (++stage == Cfg::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread) ----------------
+    constexpr uint32_t idesc = umma_idesc_bf16(kBlockM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(smem_a + stage * Cfg::kABytes);
+          const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBlockK / kUmmaK; ++k) {
+            // advancing K inside the 128-B swizzle atom = +32 B on the start address
+            const uint64_t da = umma_desc_k_sw128(a_addr + k * kUmmaK * 2);
+            const uint64_t db = umma_desc_k_sw128(b_addr + k * kUmmaK * 2);
+            umma_bf16_ss(d_tmem, da, db, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (kb == num_kb - 1) umma_commit(&tfull_bar[acc]);
+        }
+        __syncwarp();
+        if (++stage == Cfg::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const int wq = warp & 3;
+    int local = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      const TileCoord tc = tile_coord(t, num_m, num_n);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = tc.m * kBlockM + wq * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
+      epi(row, row < M, tc.n * BN, taddr);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+// --------------------------------------------------------------------------
+// host side
+
+struct GemmShape {
+  int M, N, K;
+};
+
+// Builds (or fetches from the per-process cache) a 2-D bf16 TMA descriptor
+// over a row-major [rows, cols] matrix with a (box_rows x 64) SW128 box.
+int make_tma_bf16_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols,
+                     uint64_t ld_elems, uint32_t box_rows);
+
+int gemm_num_sms();
+
+template <int BN, class Epi>
+int launch_gemm_tn(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
+                   const Epi& epi, cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return 0;
+  using Cfg = GemmCfg<BN>;
+  CUtensorMap ta, tb;
+  int rc = make_tma_bf16_2d(&ta, A, (uint64_t)M, (uint64_t)K, (uint64_t)lda, kBlockM);
+  if (rc) return rc;
+  rc = make_tma_bf16_2d(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, BN);
+  if (rc) return rc;
+  static bool attr_set = false;  // one per template instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN, Epi>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::kSmemBytes);
+    if (e != cudaSuccess) return (int)e;
+    attr_set = true;
+  }
+  const int tiles = ((M + kBlockM - 1) / kBlockM) * ((N + BN - 1) / BN);
+  const int grid = tiles < gemm_num_sms() ? tiles : gemm_num_sms();
+  gemm_tn_kernel<BN, Epi><<<grid, kGemmThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, epi);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace lemo

@@ -1,0 +1,406 @@
+// tcgen05 GEMM instantiations with the LeMo epilogues, exported through the
+// C ABI declared in include/lemo.h.
+//
+// Reference semantics each epilogue reproduces:
+//   EpiQKV        kernels.py:95-116 (_project + rope_rotate at positions idx)
+//   EpiScatterAdd tensor.py:536-550 (scatter_add_rows, in place, no atomics:
+//                 retained rows are disjoint)
+//   EpiGateUp     model.py:371-396 + sparsity.py:284-290 (SwiGLU inner and
+//                 mean |inner| token informativeness, fused in the epilogue)
+//   EpiDGateUp    tensor.py:283-292,377-384 (mul / silu backward)
+//   EpiStoreF32   matmul forward/backward (tensor.py:316-327) plus an optional
+//                 rank-R side term (the LoRA path of _project, kernels.py:95-100)
+#include "gemm.cuh"
+#include "lemo_internal.h"
+
+namespace lemo {
+
+constexpr int kMaxSideRank = 32;
+
+__device__ __forceinline__ void load_chunk(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  __syncwarp();  // tcgen05.ld is warp-collective: reconverge after masked stores
+  tmem_ld_32x32b_x32(taddr, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    d[q] = make_uint4(pack_bf16x2(v[8 * q + 0], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                      pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+  }
+}
+
+__device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float (&v)[32]) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u = s[q];
+    v[8 * q + 0] = bf16_lo(u.x);
+    v[8 * q + 1] = bf16_hi(u.x);
+    v[8 * q + 2] = bf16_lo(u.y);
+    v[8 * q + 3] = bf16_hi(u.y);
+    v[8 * q + 4] = bf16_lo(u.z);
+    v[8 * q + 5] = bf16_hi(u.z);
+    v[8 * q + 6] = bf16_lo(u.w);
+    v[8 * q + 7] = bf16_hi(u.w);
+  }
+}
+
+// v[i] += scale * sum_j U[j] * S[j*s_rs + (col0+i)*s_cs]  (rank-R side product)
+__device__ __forceinline__ void add_side(float (&v)[32], const float (&u)[kMaxSideRank], int R,
+                                         const float* __restrict__ S, int s_rs, int s_cs,
+                                         int col0, float scale) {
+  if (R == 0) return;
+#pragma unroll 4
+  for (int i = 0; i < 32; ++i) {
+    const float* sp = S + (size_t)(col0 + i) * s_cs;
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxSideRank; ++j) {
+      if (j < R) acc = fmaf(u[j], __ldg(sp + (size_t)j * s_rs), acc);
+    }
+    v[i] = fmaf(scale, acc, v[i]);
+  }
+}
+
+__device__ __forceinline__ void load_side_u(float (&u)[kMaxSideRank], const float* U, int ldu,
+                                            int R, int row, bool valid) {
+#pragma unroll
+  for (int j = 0; j < kMaxSideRank; ++j) u[j] = (valid && j < R) ? U[(size_t)row * ldu + j] : 0.f;
+}
+
+// ---------------------------------------------------------------------------
+
+struct EpiStoreBF16 {
+  __nv_bfloat16* C;
+  int ldc, N;
+  template <int BN>
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      load_chunk(taddr + c, v);
+      if (valid && col0 + c < N) store_bf16x32(C + (size_t)row * ldc + col0 + c, v);
+    }
+  }
+};
+
+struct EpiStoreF32 {
+  float* C;
+  int ldc, N;
+  const float* U;  // [M, ldu] side factors (rank R) or null
+  int ldu, R;
+  const float* S;  // side matrix, element (j, col) at S[j*s_rs + col*s_cs]
+  int s_rs, s_cs;
+  float scale;
+  int accumulate;
+  template <int BN>
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
+    float u[kMaxSideRank];
+    load_side_u(u, U, ldu, R, row, valid);
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      load_chunk(taddr + c, v);
+      if (valid && col0 + c < N) {
+        add_side(v, u, R, S, s_rs, s_cs, col0 + c, scale);
+        float4* d = reinterpret_cast<float4*>(C + (size_t)row * ldc + col0 + c);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          if (accumulate) {
+            float4 p = d[q];
+            o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+          }
+          d[q] = o;
+        }
+      }
+    }
+  }
+};
+
+// residual[idx[row]] += acc   (idx == nullptr: identity)
+struct EpiScatterAdd {
+  float* R;
+  int ldr, N;
+  const int* idx;
+  template <int BN>
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
+    const int dst_row = valid ? (idx ? __ldg(idx + row) : row) : 0;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      load_chunk(taddr + c, v);
+      if (valid && col0 + c < N) {
+        float4* d = reinterpret_cast<float4*>(R + (size_t)dst_row * ldr + col0 + c);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 p = d[q];
+          p.x += v[4 * q]; p.y += v[4 * q + 1]; p.z += v[4 * q + 2]; p.w += v[4 * q + 3];
+          d[q] = p;
+        }
+      }
+    }
+  }
+};
+
+// Fused q/k/v projection epilogue: + LoRA side term (q, v) then rotary
+// rotation at the retained tokens' ORIGINAL positions pos[row]
+// (kernels.py:109-114, tensor.py:604-634).  Tile never straddles q/k/v.
+struct EpiQKV {
+  __nv_bfloat16 *q, *k, *v;
+  int h, head_dim, rope;
+  const float2* rope_tab;  // [max_pos, head_dim/2] (cos, sin), f64-derived
+  const int* pos;
+  const float *tq, *tv;  // [M, ldt] LoRA x·A factors
+  int ldt, r;
+  const float *Bq, *Bv;  // [r, h]
+  float scale;
+  template <int BN>
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
+    const int which = col0 / h;
+    const int cbase = col0 - which * h;
+    __nv_bfloat16* out = which == 0 ? q : (which == 1 ? k : v);
+    const float* U = which == 0 ? tq : (which == 2 ? tv : nullptr);
+    const float* S = which == 0 ? Bq : Bv;
+    const int R = U ? r : 0;
+    float u[kMaxSideRank];
+    load_side_u(u, U, ldt, R, row, valid);
+    const int p = valid && rope ? __ldg(pos + row) : 0;
+    const int half = head_dim >> 1;
+#pragma unroll 1
+    for (int hd = 0; hd < BN; hd += head_dim) {
+#pragma unroll 1
+      for (int cp = 0; cp < half; cp += 32) {
+        float a[32], b[32];
+        load_chunk(taddr + hd + cp, a);
+        load_chunk(taddr + hd + half + cp, b);
+        if (!valid) continue;
+        const int ca = cbase + hd + cp, cb = ca + half;
+        add_side(a, u, R, S, h, 1, ca, scale);
+        add_side(b, u, R, S, h, 1, cb, scale);
+        if (rope) {
+          const float2* tab = rope_tab + (size_t)p * half + cp;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float2 cs = __ldg(tab + i);
+            const float xa = a[i], xb = b[i];
+            a[i] = xa * cs.x - xb * cs.y;
+            b[i] = xa * cs.y + xb * cs.x;
+          }
+        }
+        store_bf16x32(out + (size_t)row * h + ca, a);
+        store_bf16x32(out + (size_t)row * h + cb, b);
+      }
+    }
+  }
+};
+
+// SwiGLU / ReLU front half of the MLP with the token-informativeness
+// reduction in the epilogue.  Weight columns are interleaved in 128-column
+// chunks (gate chunk i at [256i, 256i+128), up chunk i at [256i+128, 256i+256)),
+// so one BN=256 tile holds matching gate/up columns.
+//   gu      : [M, N] bf16, same interleaved column order (saved for backward)
+//   inner   : [M, N/2] bf16 (silu) or [M, N] (relu), optional
+//   partial : [num_n_tiles, M] fp32 row sums of |inner| per tile, optional
+struct EpiGateUp {
+  __nv_bfloat16* gu;
+  int ldgu;
+  __nv_bfloat16* inner;
+  int ldi;
+  float* partial;
+  int M, relu;
+  template <int BN>
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
+    static_assert(BN == 256, "gate/up interleave assumes 256-column tiles");
+    float score = 0.f;
+    if (!relu) {
+#pragma unroll 1
+      for (int c = 0; c < 128; c += 32) {
+        float g[32], u[32];
+        load_chunk(taddr + c, g);
+        load_chunk(taddr + 128 + c, u);
+        if (!valid) continue;
+        // inner from the bf16-rounded gate/up that are saved for backward, so the
+        // dense path and the compaction path (mlp_compact) produce identical rows
+        float in[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          g[i] = round_bf16(g[i]);
+          u[i] = round_bf16(u[i]);
+          in[i] = g[i] * sigmoid_stable(g[i]) * u[i];
+          score += fabsf(in[i]);
+        }
+        if (gu) {
+          store_bf16x32(gu + (size_t)row * ldgu + col0 + c, g);
+          store_bf16x32(gu + (size_t)row * ldgu + col0 + 128 + c, u);
+        }
+        if (inner) store_bf16x32(inner + (size_t)row * ldi + (col0 >> 1) + c, in);
+      }
+    } else {
+#pragma unroll 1
+      for (int c = 0; c < 256; c += 32) {
+        float u[32];
+        load_chunk(taddr + c, u);
+        if (!valid) continue;
+        float in[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          u[i] = round_bf16(u[i]);
+          in[i] = fmaxf(u[i], 0.f);
+          score += in[i];
+        }
+        if (gu) store_bf16x32(gu + (size_t)row * ldgu + col0 + c, u);
+        if (inner) store_bf16x32(inner + (size_t)row * ldi + col0 + c, in);
+      }
+    }
+    if (valid && partial) partial[(size_t)(col0 / 256) * M + row] = score;
+  }
+};
+
+// dinner = dy · W_downᵀ ; epilogue turns it into d(gate), d(up) using the
+// saved gate/up (silu:  dg = dinner·u·σ(g)(1+g(1-σ(g))),  du = dinner·g·σ(g);
+// relu: du = dinner·[u>0]).  Output in the same interleaved layout as gu.
+struct EpiDGateUp {
+  const __nv_bfloat16* gu;
+  int ldgu;
+  __nv_bfloat16* dgu;
+  int relu;
+  template <int BN>
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float d[32];
+      load_chunk(taddr + c, d);
+      if (!valid) continue;
+      const int mc = col0 + c;
+      if (!relu) {
+        const int gcol = (mc >> 7) * 256 + (mc & 127);
+        float g[32], u[32];
+        load_bf16x32(gu + (size_t)row * ldgu + gcol, g);
+        load_bf16x32(gu + (size_t)row * ldgu + gcol + 128, u);
+        float dg[32], du[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float s = sigmoid_stable(g[i]);
+          du[i] = d[i] * (g[i] * s);
+          dg[i] = d[i] * u[i] * (s * (1.f + g[i] * (1.f - s)));
+        }
+        store_bf16x32(dgu + (size_t)row * ldgu + gcol, dg);
+        store_bf16x32(dgu + (size_t)row * ldgu + gcol + 128, du);
+      } else {
+        float u[32];
+        load_bf16x32(gu + (size_t)row * ldgu + mc, u);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) u[i] = u[i] > 0.f ? d[i] : 0.f;
+        store_bf16x32(dgu + (size_t)row * ldgu + mc, u);
+      }
+    }
+  }
+};
+
+}  // namespace lemo
+
+// The kernel template calls epi(row, valid, col0, taddr); wrap run<BN>.
+namespace lemo {
+template <int BN, class Epi>
+struct Bound {
+  Epi e;
+  __device__ void operator()(int row, bool valid, int col0, uint32_t taddr) const {
+    e.template run<BN>(row, valid, col0, taddr);
+  }
+};
+
+template <int BN, class Epi>
+static int gemm(const void* A, int lda, const void* B, int ldb, int M, int N, int K, const Epi& e,
+                cudaStream_t st) {
+  Bound<BN, Epi> b{e};
+  return launch_gemm_tn<BN>(A, lda, B, ldb, M, N, K, b, st);
+}
+
+template <class Epi>
+static int gemm_auto(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
+                     const Epi& e, cudaStream_t st) {
+  if (N % 256 == 0 || N > 256) return gemm<256>(A, lda, B, ldb, M, N, K, e, st);
+  return gemm<128>(A, lda, B, ldb, M, N, K, e, st);
+}
+}  // namespace lemo
+
+using namespace lemo;
+
+extern "C" {
+
+int lemo_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N,
+                   int K, void* stream) {
+  LEMO_ARG_CHECK(N % 32 == 0 && ldc % 8 == 0, "lemo_gemm_bf16: N and ldc must be multiples of 32/8");
+  EpiStoreBF16 e{reinterpret_cast<__nv_bfloat16*>(C), ldc, N};
+  LEMO_RETURN_RC("lemo_gemm_bf16", gemm_auto(A, lda, B, ldb, M, N, K, e, (cudaStream_t)stream));
+}
+
+int lemo_gemm_f32(const void* A, int lda, const void* B, int ldb, float* C, int ldc, int M, int N,
+                  int K, const float* U, int ldu, int R, const float* S, int s_rs, int s_cs,
+                  float scale, int accumulate, void* stream) {
+  LEMO_ARG_CHECK(N % 32 == 0 && ldc % 4 == 0, "lemo_gemm_f32: N and ldc must be multiples of 32/4");
+  LEMO_ARG_CHECK(R >= 0 && R <= kMaxSideRank, "lemo_gemm_f32: side rank out of range");
+  EpiStoreF32 e{C, ldc, N, U, ldu, R, S, s_rs, s_cs, scale, accumulate};
+  LEMO_RETURN_RC("lemo_gemm_f32", gemm_auto(A, lda, B, ldb, M, N, K, e, (cudaStream_t)stream));
+}
+
+int lemo_gemm_scatter_add(const void* A, int lda, const void* B, int ldb, float* R, int ldr,
+                          const int* idx, int M, int N, int K, void* stream) {
+  LEMO_ARG_CHECK(N % 32 == 0 && ldr % 4 == 0, "lemo_gemm_scatter_add: N%32, ldr%4");
+  EpiScatterAdd e{R, ldr, N, idx};
+  LEMO_RETURN_RC("lemo_gemm_scatter_add",
+                 gemm_auto(A, lda, B, ldb, M, N, K, e, (cudaStream_t)stream));
+}
+
+int lemo_gemm_qkv(const void* xn, const void* w_qkv_t, int M, int h, void* q, void* k, void* v,
+                  int head_dim, int rope, const void* rope_tab, const int* pos, const float* tq,
+                  const float* tv, int ldt, int r, const float* Bq, const float* Bv, float scale,
+                  void* stream) {
+  LEMO_ARG_CHECK(head_dim % 64 == 0, "lemo_gemm_qkv: head_dim must be a multiple of 64");
+  LEMO_ARG_CHECK(r >= 0 && r <= kMaxSideRank, "lemo_gemm_qkv: LoRA rank too large");
+  EpiQKV e{reinterpret_cast<__nv_bfloat16*>(q), reinterpret_cast<__nv_bfloat16*>(k),
+           reinterpret_cast<__nv_bfloat16*>(v), h, head_dim, rope,
+           reinterpret_cast<const float2*>(rope_tab), pos, tq, tv, ldt, r, Bq, Bv, scale};
+  int rc;
+  if (h % 256 == 0 && 256 % head_dim == 0)
+    rc = gemm<256>(xn, h, w_qkv_t, h, M, 3 * h, h, e, (cudaStream_t)stream);
+  else if (h % 128 == 0 && 128 % head_dim == 0)
+    rc = gemm<128>(xn, h, w_qkv_t, h, M, 3 * h, h, e, (cudaStream_t)stream);
+  else {
+    set_error_msg("lemo_gemm_qkv: hidden dim must be a multiple of 128 and of head_dim");
+    return LEMO_ERR_REPORTED;
+  }
+  LEMO_RETURN_RC("lemo_gemm_qkv", rc);
+}
+
+int lemo_gemm_gateup(const void* xn, int ldx, const void* w_gu_t, int M, int N, int K, void* gu,
+                     void* inner, float* partial, int relu, void* stream) {
+  LEMO_ARG_CHECK(N % 256 == 0, "lemo_gemm_gateup: N must be a multiple of 256 (padded mlp dim)");
+  EpiGateUp e{reinterpret_cast<__nv_bfloat16*>(gu), N, reinterpret_cast<__nv_bfloat16*>(inner),
+              relu ? N : N / 2, partial, M, relu};
+  LEMO_RETURN_RC("lemo_gemm_gateup",
+                 gemm<256>(xn, ldx, w_gu_t, K, M, N, K, e, (cudaStream_t)stream));
+}
+
+int lemo_gemm_dgateup(const void* dy, const void* w_down, int M, int m_pad, int h, const void* gu,
+                      void* dgu, int relu, void* stream) {
+  LEMO_ARG_CHECK(m_pad % 128 == 0, "lemo_gemm_dgateup: padded mlp dim must be a multiple of 128");
+  const int ldgu = relu ? m_pad : 2 * m_pad;
+  EpiDGateUp e{reinterpret_cast<const __nv_bfloat16*>(gu), ldgu,
+               reinterpret_cast<__nv_bfloat16*>(dgu), relu};
+  int rc;
+  if (m_pad % 256 == 0)
+    rc = gemm<256>(dy, h, w_down, h, M, m_pad, h, e, (cudaStream_t)stream);
+  else
+    rc = gemm<128>(dy, h, w_down, h, M, m_pad, h, e, (cudaStream_t)stream);
+  LEMO_RETURN_RC("lemo_gemm_dgateup", rc);
+}
+
+}  // extern "C"

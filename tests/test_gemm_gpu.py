@@ -1,0 +1,59 @@
+"""tcgen05 GEMM + epilogues vs a plain PyTorch fp32 reference."""
+
+import pytest
+import torch
+
+from paper_2501_09767_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(a, b):
+    return a.float() @ b.float().T
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 128), (300, 256, 4096),
+                                   (1000, 768, 320), (16, 128, 64), (4096, 4096, 4096),
+                                   (2048, 32000, 4096), (77, 96, 200)])
+def test_gemm_bf16(cuda, M, N, K):
+    g = torch.Generator(device=cuda).manual_seed(M * 7 + N)
+    a = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    b = torch.randn(N, K, device=cuda, generator=g).bfloat16()
+    c = ops.gemm_bf16(a, b)
+    torch.cuda.synchronize()
+    ref = _ref(a, b)
+    err = (c.float() - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    assert err <= 1e-2 * scale + 1e-3, (err, scale)
+
+
+@pytest.mark.parametrize("M,N,K,R", [(256, 512, 256, 0), (333, 256, 512, 16), (128, 4096, 4096, 8)])
+def test_gemm_f32_side(cuda, M, N, K, R):
+    g = torch.Generator(device=cuda).manual_seed(3)
+    a = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    b = torch.randn(N, K, device=cuda, generator=g).bfloat16()
+    out = torch.randn(M, N, device=cuda, generator=g)
+    base = out.clone()
+    u = torch.randn(M, max(R, 1), device=cuda, generator=g)[:, :R].contiguous() if R else None
+    s = torch.randn(N, max(R, 1), device=cuda, generator=g).contiguous() if R else None  # S(j,col)=s[col*R+j]
+    ops.gemm_f32(a, b, out, side_u=u, side_s=s, side_strides=(1, R), scale=0.5, accumulate=True)
+    torch.cuda.synchronize()
+    ref = base + _ref(a, b)
+    if R:
+        ref = ref + 0.5 * u @ s.T
+    err = (out - ref).abs().max().item()
+    assert err <= 1e-3 * ref.abs().max().item() + 1e-3
+
+
+def test_gemm_scatter_add(cuda):
+    g = torch.Generator(device=cuda).manual_seed(5)
+    s, h, K = 1024, 512, 256
+    idx = torch.randperm(s, device=cuda, generator=g)[:400].sort().values.int()
+    a = torch.randn(400, K, device=cuda, generator=g).bfloat16()
+    b = torch.randn(h, K, device=cuda, generator=g).bfloat16()
+    resid = torch.randn(s, h, device=cuda, generator=g)
+    ref = resid.clone()
+    ref[idx.long()] += _ref(a, b)
+    ops.gemm_scatter_add(a, b, resid, idx)
+    torch.cuda.synchronize()
+    assert torch.allclose(resid, ref, atol=1e-3, rtol=1e-3)
