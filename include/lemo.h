@@ -55,9 +55,11 @@ int lemo_gemm_scatter_add(const void* A, int lda, const void* B, int ldb, float*
 /* Fused q/k/v projection of attention_core (kernels.py:103-114):
  *   [q|k|v] = xn · W_qkv  (+ scale·(xn·A_q)·B_q on q, + scale·(xn·A_v)·B_v on v)
  *   then rope_rotate (tensor.py:610-634) at pos[i] (original token positions).
- * w_qkv_t: [3h, h] bf16 (rows = output features); tq/tv: [M, ldt] fp32 = xn·A;
+ * w_qkv_t: [3h, h] bf16 (rows = output features; nmat = 2 computes q, k only,
+ * as layer_qk does, model.py:356-368); tq/tv: [M, ldt] fp32 = xn·A;
  * Bq/Bv: [r, h] fp32; rope_tab: [max_pos, head_dim/2] float2 (cos, sin). */
-int lemo_gemm_qkv(const void* xn, const void* w_qkv_t, int M, int h, void* q, void* k, void* v,
+int lemo_gemm_qkv(const void* xn, const void* w_qkv_t, int M, int h, int nmat, void* q, void* k,
+                  void* v,
                   int head_dim, int rope, const void* rope_tab, const int* pos, const float* tq,
                   const float* tv, int ldt, int r, const float* Bq, const float* Bv, float scale,
                   void* stream);
@@ -76,6 +78,120 @@ int lemo_gemm_gateup(const void* xn, int ldx, const void* w_gu_t, int M, int N, 
  * 381-382) using the saved gu; dgu has gu's layout. */
 int lemo_gemm_dgateup(const void* dy, const void* w_down, int M, int m_pad, int h, const void* gu,
                       void* dgu, int relu, void* stream);
+
+/* ---- row kernels (HBM-bound) --------------------------------------------- */
+
+/* Fused gather + RMSNorm (tensor.py:578-597; idx NULL = all rows): xn (bf16),
+ * optional saved raw rows xg (bf16) and inv (fp32), and optional LoRA factors
+ * t[i, 0:r] = xn_i·A0, t[i, r:2r] = xn_i·A1 (kernels.py:97-98; A: [h, r] fp32
+ * with row stride lda). */
+int lemo_rmsnorm_gather(const float* x, int ldx, const int* idx, int M, int h, const float* w,
+                        void* xn, void* xg, float* inv, const float* A0, const float* A1, int lda,
+                        int r, float* t, int ldt, void* stream);
+
+/* dst[i] = bf16(src[idx[i]]) — gradient rows for the output-projection
+ * backward (the g[idx] of scatter_add_rows backward, tensor.py:547-548). */
+int lemo_gather_rows_bf16(const float* src, int ld, const int* idx, int M, int h, void* dst,
+                          void* stream);
+
+/* RMSNorm backward (tensor.py:396-400) of rows x (bf16 if x_bf16, else fp32),
+ * result written (accumulate=0) or added (1) into dx at row idx[i]
+ * (gather_rmsnorm backward, tensor.py:589-595). g is scaled by gscale. */
+int lemo_rmsnorm_bwd(const float* g, int ldg, const void* x, int x_bf16, int ldx,
+                     const float* inv, const float* w, const int* idx, int M, int h, float gscale,
+                     float* dx, int lddx, int accumulate, void* stream);
+
+/* x[i] = table[ids[i]] (+ pos_table[i])  (tensor.py:405-420, model.py:240-244). */
+int lemo_embed(const int* ids, int n, const float* table, int h, const float* pos_table, float* x,
+               void* stream);
+
+/* Retained-row compaction after MLP scoring: gu_out[i] = gu_all[idx[i]],
+ * inner_out[i] = silu(g)·u (or relu(u)), xg_out[i] = bf16(x[idx[i]]),
+ * inv_out[i] = inv_all[idx[i]]. */
+int lemo_mlp_compact(const void* gu_all, const float* x, int ldx, const float* inv_all,
+                     const int* idx, int M, int h, int m_pad, int relu, void* gu_out,
+                     void* inner_out, void* xg_out, float* inv_out, void* stream);
+
+/* After attention backward: RoPE backward of dq/dk (tensor.py:627-632; dq is
+ * rewritten in place pre-rotation), packed bf16 [dq|dk|dv] rows for the dX
+ * GEMM, and u = [dq·Bqᵀ | dv·Bvᵀ] (LoRA backward factors). */
+int lemo_qkv_grad_prep(float* dq, const float* dk, const float* dv, int M, int h, int head_dim,
+                       int rope, const void* rope_tab, const int* pos, const float* Bq,
+                       const float* Bv, int r, void* dqkv, float* u, int ldu, void* stream);
+
+/* LoRA weight gradients accumulated (+=) into dA0/dB0/dA1/dB1:
+ * dA[c,j] = s·Σ xn[i,c]u[i,j], dB[j,c] = s·Σ t[i,j]g[i,c] (tensor.py:324-325). */
+int lemo_lora_grads(const void* xg, const float* inv, const float* w, const float* t,
+                    const float* u, int ld, const float* g0, const float* g1, int M, int h, int r,
+                    float scale, int lda, float* dA0, float* dB0, float* dA1, float* dB1,
+                    void* stream);
+
+/* Cross-entropy rows of segmented_loss_and_grad (kernels.py:256-273): per-row
+ * loss terms and dlogits = (softmax - onehot)·inv_count (bf16); ignore rows
+ * get zeros; out-of-range targets set *bad. */
+int lemo_ce_rows(const float* logits, int ldl, const int* targets, int n, int V, int ignore,
+                 float inv_count, void* dlogits, int ldd, float* row_loss, int* bad,
+                 void* stream);
+
+/* *out (+)= Σ x[i] in float64 (deterministic single-CTA reduction). */
+int lemo_sum_f64(const float* x, int n, double* out, int accumulate, void* stream);
+
+/* Adam step over a flat fp32 parameter buffer (optim.py:37-53). */
+int lemo_adam(float* p, const float* g, float* m, float* v, long long n, float lr, float b1,
+              float b2, float eps, float wd, float bc1, float bc2, void* stream);
+
+/* ---- pattern scoring and selection ----------------------------------------- */
+
+/* Block means xb[n] = mean(x[n*b:(n+1)*b]) (predictor.py:117-123). */
+int lemo_block_embed(const float* x, int ldx, int s, int h, int b, float* xb, void* stream);
+
+/* fp32 GEMM C = act(A·op(B))·col_mask; op(B) = B [K,N] (b_trans=0) or Bᵀ
+ * with B [N,K] (b_trans=1); act = relu if relu.  Predictor.predict
+ * (predictor.py:83-89) and Eq. 3 eq·ekᵀ (predictor.py:186). */
+int lemo_sgemm(const float* A, int lda, const float* B, int ldb, int b_trans, float* C, int ldc,
+               int M, int N, int K, int relu, const unsigned char* col_mask, void* stream);
+
+/* vec[n] = Σ_{m>=n} max(S[m,n], 0) in float64, ascending m
+ * (model.py:575-578 + sparsity.py:253-260). */
+int lemo_colsum_clamped(const float* S, int lds, int nb, double* vec, void* stream);
+
+/* MLP block scores from per-tile row partials of lemo_gemm_gateup:
+ * token score = Σ partial / m_real, block = max over rows < n_valid
+ * (sparsity.py:284-305, model.py:383-395). */
+int lemo_mlp_block_scores(const float* partial, int n_tiles, int s, int n_valid, int b, int m_real,
+                          double* vec, void* stream);
+
+/* eliminate (sparsity.py:263-281) + token_indices (sparsity.py:95-104):
+ * keep block n iff vec[n] >= T (T = *thr_dev if thr_dev else thr), or
+ * force[n] != 0 (force_blocks, e.g. the sink block; force may be NULL).  Writes mask[nb], ascending blocks[], tokens[] (int32) and
+ * counts = {n_tokens_kept, n_blocks_kept, any_nonfinite}; thr_out = T. */
+int lemo_select(const double* vec, int nb, double thr, const double* thr_dev,
+                const unsigned char* force, int b, int n_tokens, unsigned char* mask, int* blocks, int* tokens, int* counts,
+                double* thr_out, void* stream);
+
+/* *out = sorted(data)[rank] (+1 if plus_one): np.quantile(..., method="lower")
+ * with rank = floor((n-1)q) (model.py:562, predictor.py:276). */
+int lemo_quantile_lower(const double* data, int n, long long rank, int plus_one, double* out,
+                        void* stream);
+
+/* Exact block informativeness (sparsity.py:173-219): out[m*ldo + n] (n <= m)
+ * = max over the 16x16 tile of Σ_h max(q·k, 0)/H with the causal / n_valid
+ * mask; q, k: [s, h] bf16 post-rotation (layer_qk, model.py:356-368). */
+int lemo_exact_block_scores(const void* q, const void* k, int s, int h, int head_dim, int block,
+                            int n_valid, float* out, int ldo, void* stream);
+
+/* ---- attention over the compact retained sequence --------------------------- */
+
+/* Causal softmax attention (tensor.py:646-691) on q/k/v [n, h] bf16 (heads
+ * side by side); o [n, h] bf16, lse [h/head_dim, n] fp32 (natural log). */
+int lemo_flash_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int n, int h,
+                   int head_dim, float scale, void* stream);
+
+/* Attention backward (tensor.py:693-722): dq/dk/dv fp32 [n, h]; delta is a
+ * caller workspace [h/head_dim, n] fp32. */
+int lemo_flash_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                   const float* lse, float* delta, float* dq, float* dk, float* dv, int n, int h,
+                   int head_dim, float scale, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,516 @@
+// Causal attention over the COMPACT retained sequence (kernels.py:103-116,
+// tensor.py:646-724).  Because GatherPlan indices are strictly increasing
+// (kernels.py:38-39), compact order == original order and a standard causal
+// mask on compact indices is exact; RoPE at original positions was already
+// applied by the q/k/v projection epilogue.
+//
+// Round-1 implementation: FlashAttention-2 style tiles on the warp-level
+// bf16 tensor-core path (mma.sync m16n8k16, ldmatrix, cp.async double
+// buffering), fp32 online softmax, saved per-row log-sum-exp.  Backward is
+// split into an atomic-free dK/dV kernel (one CTA per key block, transposed
+// formulation so Pᵀ/dSᵀ stay in registers) and a dQ kernel (one CTA per query
+// block), both recomputing P from the saved lse as the reference does.
+#include "lemo_internal.h"
+#include "mma_sync.cuh"
+
+namespace lemo {
+namespace fa {
+
+constexpr int kBr = 64;  // query rows per tile
+constexpr int kBc = 64;  // key rows per tile
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+// ---------------------------------------------------------------------------
+// forward
+
+template <int D>
+__global__ void __launch_bounds__(128) flash_fwd_kernel(const __nv_bfloat16* __restrict__ q,
+                                                        const __nv_bfloat16* __restrict__ k,
+                                                        const __nv_bfloat16* __restrict__ v,
+                                                        __nv_bfloat16* __restrict__ o,
+                                                        float* __restrict__ lse, int n, int h,
+                                                        float scale) {
+  using T = Tile<D>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sQ = smem_u32(smem);
+  const uint32_t sK[2] = {sQ + T::kBytes, sQ + 2 * T::kBytes};
+  const uint32_t sV[2] = {sQ + 3 * T::kBytes, sQ + 4 * T::kBytes};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int qb = (int)(gridDim.x - 1 - blockIdx.x);  // heavy (late) blocks first
+  const int hd = blockIdx.y;
+  const int q0 = qb * kBr, c0 = hd * D;
+  const float sl2 = scale * kLog2e;
+
+  T::load(sQ, q, h, q0, c0, n, tid, 128);
+  T::load(sK[0], k, h, 0, c0, n, tid, 128);
+  T::load(sV[0], v, h, 0, c0, n, tid, 128);
+  cp_async_commit();
+
+  uint32_t qf[D / 16][4];
+  float oacc[D / 8][4];
+#pragma unroll
+  for (int i = 0; i < D / 8; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nkv = qb + 1;
+
+  for (int j = 0; j < nkv; ++j) {
+    if (j + 1 < nkv) {
+      T::load(sK[(j + 1) & 1], k, h, (j + 1) * kBc, c0, n, tid, 128);
+      T::load(sV[(j + 1) & 1], v, h, (j + 1) * kBc, c0, n, tid, 128);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (j == 0) {
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const int r = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        ldsm_x4(sQ + T::off(r, kk * 16 + (lane >> 4) * 8), qf[kk]);
+      }
+    }
+    const uint32_t bk = sK[j & 1], bv = sV[j & 1];
+    float s[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+      for (int nt2 = 0; nt2 < 4; ++nt2) {
+        uint32_t b[4];
+        const int key = nt2 * 16 + (lane & 7) + (lane >> 4) * 8;
+        ldsm_x4(bk + T::off(key, kk * 16 + ((lane >> 3) & 1) * 8), b);
+        mma16816(s[2 * nt2], qf[kk], b[0], b[1]);
+        mma16816(s[2 * nt2 + 1], qf[kk], b[2], b[3]);
+      }
+    }
+    // scale (log2 domain) + causal / length mask
+    const bool diag = (j == qb);
+    const int kv0 = j * kBc;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int row = q0 + warp * 16 + g + (e >= 2 ? 8 : 0);
+        const int key = kv0 + nt * 8 + 2 * t4 + (e & 1);
+        float val = s[nt][e] * sl2;
+        if ((diag && key > row) || key >= n) val = -INFINITY;
+        s[nt][e] = val;
+      }
+    }
+    float corr[2];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      float mx = mrow[rr];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) mx = fmaxf(mx, fmaxf(s[nt][2 * rr], s[nt][2 * rr + 1]));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      corr[rr] = (mrow[rr] == -INFINITY) ? 0.f : exp2f(mrow[rr] - mx);
+      mrow[rr] = mx;
+      float sum = 0.f;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const float p0 = (s[nt][2 * rr] == -INFINITY) ? 0.f : exp2f(s[nt][2 * rr] - mx);
+        const float p1 = (s[nt][2 * rr + 1] == -INFINITY) ? 0.f : exp2f(s[nt][2 * rr + 1] - mx);
+        s[nt][2 * rr] = p0;
+        s[nt][2 * rr + 1] = p1;
+        sum += p0 + p1;
+      }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      lrow[rr] = lrow[rr] * corr[rr] + sum;
+    }
+#pragma unroll
+    for (int dt = 0; dt < D / 8; ++dt) {
+      oacc[dt][0] *= corr[0];
+      oacc[dt][1] *= corr[0];
+      oacc[dt][2] *= corr[1];
+      oacc[dt][3] *= corr[1];
+    }
+    // O += P·V
+#pragma unroll
+    for (int kk2 = 0; kk2 < 4; ++kk2) {
+      uint32_t a[4];
+      a[0] = pack_bf16x2(s[2 * kk2][0], s[2 * kk2][1]);
+      a[1] = pack_bf16x2(s[2 * kk2][2], s[2 * kk2][3]);
+      a[2] = pack_bf16x2(s[2 * kk2 + 1][0], s[2 * kk2 + 1][1]);
+      a[3] = pack_bf16x2(s[2 * kk2 + 1][2], s[2 * kk2 + 1][3]);
+#pragma unroll
+      for (int dt2 = 0; dt2 < D / 16; ++dt2) {
+        uint32_t b[4];
+        const int key = kk2 * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        ldsm_x4_t(bv + T::off(key, dt2 * 16 + (lane >> 4) * 8), b);
+        mma16816(oacc[2 * dt2], a, b[0], b[1]);
+        mma16816(oacc[2 * dt2 + 1], a, b[2], b[3]);
+      }
+    }
+    __syncthreads();
+  }
+  // finalize
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int row = q0 + warp * 16 + g + rr * 8;
+    if (row >= n) continue;
+    const float inv_l = 1.f / lrow[rr];
+    __nv_bfloat16* orow = o + (size_t)row * h + c0;
+#pragma unroll
+    for (int dt = 0; dt < D / 8; ++dt) {
+      const uint32_t pk = pack_bf16x2(oacc[dt][2 * rr] * inv_l, oacc[dt][2 * rr + 1] * inv_l);
+      *reinterpret_cast<uint32_t*>(orow + dt * 8 + 2 * t4) = pk;
+    }
+    if (t4 == 0) lse[(size_t)hd * n + row] = (mrow[rr] + log2f(lrow[rr])) * kLn2;
+  }
+}
+
+// delta[hd, i] = Σ_d dO[i, hd*D+d] · O[i, hd*D+d]   (tensor.py:696)
+__global__ void flash_bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
+                                       const __nv_bfloat16* __restrict__ dout,
+                                       float* __restrict__ delta, int n, int h, int D) {
+  const int row = blockIdx.x;
+  const int H = h / D;
+  for (int hd = threadIdx.x >> 5; hd < H; hd += blockDim.x >> 5) {
+    float acc = 0.f;
+    for (int d = (threadIdx.x & 31) * 2; d < D; d += 64) {
+      const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(o + (size_t)row * h + hd * D + d);
+      const __nv_bfloat162 b =
+          *reinterpret_cast<const __nv_bfloat162*>(dout + (size_t)row * h + hd * D + d);
+      acc += __bfloat162float(a.x) * __bfloat162float(b.x) + __bfloat162float(a.y) * __bfloat162float(b.y);
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) delta[(size_t)hd * n + row] = acc;
+  }
+}
+
+// dK, dV for one key block (64 keys), transposed formulation: each warp owns
+// 16 keys; Sᵀ = K·Qᵀ, Pᵀ = exp(Sᵀ - lse), dPᵀ = V·dOᵀ, dSᵀ = Pᵀ(dPᵀ - Δ);
+// dV += Pᵀ·dO, dK += dSᵀ·Q (scaled).  Query blocks processed in 32-row halves.
+template <int D>
+__global__ void __launch_bounds__(128) flash_bwd_dkdv_kernel(
+    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
+    const __nv_bfloat16* __restrict__ v, const __nv_bfloat16* __restrict__ dout,
+    const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dk,
+    float* __restrict__ dv, int n, int h, float scale) {
+  using T = Tile<D>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sK = smem_u32(smem), sV = sK + T::kBytes;
+  const uint32_t sQ[2] = {sK + 2 * T::kBytes, sK + 3 * T::kBytes};
+  const uint32_t sO[2] = {sK + 4 * T::kBytes, sK + 5 * T::kBytes};
+  float* sL = reinterpret_cast<float*>(smem + 6 * T::kBytes);  // [2][64] lse*log2e
+  float* sD = sL + 128;                                        // [2][64] delta
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int kb = blockIdx.x, hd = blockIdx.y;
+  const int k0 = kb * kBc, c0 = hd * D;
+  const int nqb = (n + kBr - 1) / kBr;
+  const int g = lane >> 2, t4 = lane & 3;
+  const float sl2 = scale * kLog2e;
+
+  T::load(sK, k, h, k0, c0, n, tid, 128);
+  T::load(sV, v, h, k0, c0, n, tid, 128);
+  auto load_q = [&](int i, int buf) {
+    T::load(sQ[buf], q, h, i * kBr, c0, n, tid, 128);
+    T::load(sO[buf], dout, h, i * kBr, c0, n, tid, 128);
+    for (int r = tid; r < kBr; r += 128) {
+      const int row = i * kBr + r;
+      sL[buf * 64 + r] = row < n ? lse[(size_t)hd * n + row] * kLog2e : 0.f;
+      sD[buf * 64 + r] = row < n ? delta[(size_t)hd * n + row] : 0.f;
+    }
+  };
+  load_q(kb, 0);
+  cp_async_commit();
+
+  float dka[D / 8][4], dva[D / 8][4];
+#pragma unroll
+  for (int i = 0; i < D / 8; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dka[i][e] = dva[i][e] = 0.f;
+
+  for (int i = kb; i < nqb; ++i) {
+    const int buf = (i - kb) & 1;
+    if (i + 1 < nqb) {
+      __syncthreads();  // previous iteration finished reading buf^1
+      load_q(i + 1, buf ^ 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int qrow0 = i * kBr;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      float st[4][4], dpt[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) st[a][e] = dpt[a][e] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        uint32_t ak[4], av[4];
+        const int r = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int cc = kk * 16 + (lane >> 4) * 8;
+        ldsm_x4(sK + T::off(r, cc), ak);
+        ldsm_x4(sV + T::off(r, cc), av);
+#pragma unroll
+        for (int nt2 = 0; nt2 < 2; ++nt2) {
+          uint32_t bq[4], bo[4];
+          const int qr = half * 32 + nt2 * 16 + (lane & 7) + (lane >> 4) * 8;
+          const int dc = kk * 16 + ((lane >> 3) & 1) * 8;
+          ldsm_x4(sQ[buf] + T::off(qr, dc), bq);
+          ldsm_x4(sO[buf] + T::off(qr, dc), bo);
+          mma16816(st[2 * nt2], ak, bq[0], bq[1]);
+          mma16816(st[2 * nt2 + 1], ak, bq[2], bq[3]);
+          mma16816(dpt[2 * nt2], av, bo[0], bo[1]);
+          mma16816(dpt[2 * nt2 + 1], av, bo[2], bo[3]);
+        }
+      }
+      // Pᵀ and dSᵀ (rows = keys, cols = queries)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int key = k0 + warp * 16 + g + (e >= 2 ? 8 : 0);
+          const int qc = half * 32 + nt * 8 + 2 * t4 + (e & 1);
+          const int qrow = qrow0 + qc;
+          float p = exp2f(st[nt][e] * sl2 - sL[buf * 64 + qc]);
+          if (key > qrow || qrow >= n || key >= n) p = 0.f;
+          st[nt][e] = p;
+          dpt[nt][e] = p * (dpt[nt][e] - sD[buf * 64 + qc]);
+        }
+      }
+      // dV += Pᵀ·dO ; dK += dSᵀ·Q   (k-dim = the 32 queries of this half)
+#pragma unroll
+      for (int kq = 0; kq < 2; ++kq) {
+        uint32_t ap[4], ad[4];
+        ap[0] = pack_bf16x2(st[2 * kq][0], st[2 * kq][1]);
+        ap[1] = pack_bf16x2(st[2 * kq][2], st[2 * kq][3]);
+        ap[2] = pack_bf16x2(st[2 * kq + 1][0], st[2 * kq + 1][1]);
+        ap[3] = pack_bf16x2(st[2 * kq + 1][2], st[2 * kq + 1][3]);
+        ad[0] = pack_bf16x2(dpt[2 * kq][0], dpt[2 * kq][1]);
+        ad[1] = pack_bf16x2(dpt[2 * kq][2], dpt[2 * kq][3]);
+        ad[2] = pack_bf16x2(dpt[2 * kq + 1][0], dpt[2 * kq + 1][1]);
+        ad[3] = pack_bf16x2(dpt[2 * kq + 1][2], dpt[2 * kq + 1][3]);
+#pragma unroll
+        for (int dt2 = 0; dt2 < D / 16; ++dt2) {
+          uint32_t bo[4], bq[4];
+          const int qr = half * 32 + kq * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+          const int dc = dt2 * 16 + (lane >> 4) * 8;
+          ldsm_x4_t(sO[buf] + T::off(qr, dc), bo);
+          ldsm_x4_t(sQ[buf] + T::off(qr, dc), bq);
+          mma16816(dva[2 * dt2], ap, bo[0], bo[1]);
+          mma16816(dva[2 * dt2 + 1], ap, bo[2], bo[3]);
+          mma16816(dka[2 * dt2], ad, bq[0], bq[1]);
+          mma16816(dka[2 * dt2 + 1], ad, bq[2], bq[3]);
+        }
+      }
+    }
+  }
+  // write dK (scaled), dV — fp32
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int key = k0 + warp * 16 + g + rr * 8;
+    if (key >= n) continue;
+    float* dkr = dk + (size_t)key * h + c0;
+    float* dvr = dv + (size_t)key * h + c0;
+#pragma unroll
+    for (int dt = 0; dt < D / 8; ++dt) {
+      *reinterpret_cast<float2*>(dkr + dt * 8 + 2 * t4) =
+          make_float2(dka[dt][2 * rr] * scale, dka[dt][2 * rr + 1] * scale);
+      *reinterpret_cast<float2*>(dvr + dt * 8 + 2 * t4) =
+          make_float2(dva[dt][2 * rr], dva[dt][2 * rr + 1]);
+    }
+  }
+}
+
+// dQ for one query block: loop over key blocks <= diagonal.
+template <int D>
+__global__ void __launch_bounds__(128) flash_bwd_dq_kernel(
+    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
+    const __nv_bfloat16* __restrict__ v, const __nv_bfloat16* __restrict__ dout,
+    const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq, int n,
+    int h, float scale) {
+  using T = Tile<D>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sQ = smem_u32(smem), sO = sQ + T::kBytes;
+  const uint32_t sK[2] = {sQ + 2 * T::kBytes, sQ + 3 * T::kBytes};
+  const uint32_t sV[2] = {sQ + 4 * T::kBytes, sQ + 5 * T::kBytes};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int qb = (int)(gridDim.x - 1 - blockIdx.x), hd = blockIdx.y;
+  const int q0 = qb * kBr, c0 = hd * D;
+  const int g = lane >> 2, t4 = lane & 3;
+  const float sl2 = scale * kLog2e;
+
+  T::load(sQ, q, h, q0, c0, n, tid, 128);
+  T::load(sO, dout, h, q0, c0, n, tid, 128);
+  T::load(sK[0], k, h, 0, c0, n, tid, 128);
+  T::load(sV[0], v, h, 0, c0, n, tid, 128);
+  cp_async_commit();
+  float lrow[2], drow[2];
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int row = q0 + warp * 16 + g + rr * 8;
+    lrow[rr] = row < n ? lse[(size_t)hd * n + row] * kLog2e : 0.f;
+    drow[rr] = row < n ? delta[(size_t)hd * n + row] : 0.f;
+  }
+  uint32_t qf[D / 16][4], of[D / 16][4];
+  float dqa[D / 8][4];
+#pragma unroll
+  for (int i = 0; i < D / 8; ++i) dqa[i][0] = dqa[i][1] = dqa[i][2] = dqa[i][3] = 0.f;
+
+  const int nkv = qb + 1;
+  for (int j = 0; j < nkv; ++j) {
+    if (j + 1 < nkv) {
+      T::load(sK[(j + 1) & 1], k, h, (j + 1) * kBc, c0, n, tid, 128);
+      T::load(sV[(j + 1) & 1], v, h, (j + 1) * kBc, c0, n, tid, 128);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (j == 0) {
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const int r = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        ldsm_x4(sQ + T::off(r, kk * 16 + (lane >> 4) * 8), qf[kk]);
+        ldsm_x4(sO + T::off(r, kk * 16 + (lane >> 4) * 8), of[kk]);
+      }
+    }
+    const uint32_t bk = sK[j & 1], bv = sV[j & 1];
+    float s[8][4], dp[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s[i][e] = dp[i][e] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+      for (int nt2 = 0; nt2 < 4; ++nt2) {
+        uint32_t b[4], c[4];
+        const int key = nt2 * 16 + (lane & 7) + (lane >> 4) * 8;
+        const int dc = kk * 16 + ((lane >> 3) & 1) * 8;
+        ldsm_x4(bk + T::off(key, dc), b);
+        ldsm_x4(bv + T::off(key, dc), c);
+        mma16816(s[2 * nt2], qf[kk], b[0], b[1]);
+        mma16816(s[2 * nt2 + 1], qf[kk], b[2], b[3]);
+        mma16816(dp[2 * nt2], of[kk], c[0], c[1]);
+        mma16816(dp[2 * nt2 + 1], of[kk], c[2], c[3]);
+      }
+    }
+    const int kv0 = j * kBc;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int rr = e >> 1;
+        const int row = q0 + warp * 16 + g + rr * 8;
+        const int key = kv0 + nt * 8 + 2 * t4 + (e & 1);
+        float p = exp2f(s[nt][e] * sl2 - lrow[rr]);
+        if (key > row || key >= n || row >= n) p = 0.f;
+        s[nt][e] = p * (dp[nt][e] - drow[rr]);  // dS
+      }
+    }
+    // dQ += dS · K
+#pragma unroll
+    for (int kk2 = 0; kk2 < 4; ++kk2) {
+      uint32_t a[4];
+      a[0] = pack_bf16x2(s[2 * kk2][0], s[2 * kk2][1]);
+      a[1] = pack_bf16x2(s[2 * kk2][2], s[2 * kk2][3]);
+      a[2] = pack_bf16x2(s[2 * kk2 + 1][0], s[2 * kk2 + 1][1]);
+      a[3] = pack_bf16x2(s[2 * kk2 + 1][2], s[2 * kk2 + 1][3]);
+#pragma unroll
+      for (int dt2 = 0; dt2 < D / 16; ++dt2) {
+        uint32_t b[4];
+        const int key = kk2 * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        ldsm_x4_t(bk + T::off(key, dt2 * 16 + (lane >> 4) * 8), b);
+        mma16816(dqa[2 * dt2], a, b[0], b[1]);
+        mma16816(dqa[2 * dt2 + 1], a, b[2], b[3]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int row = q0 + warp * 16 + g + rr * 8;
+    if (row >= n) continue;
+    float* dqr = dq + (size_t)row * h + c0;
+#pragma unroll
+    for (int dt = 0; dt < D / 8; ++dt)
+      *reinterpret_cast<float2*>(dqr + dt * 8 + 2 * t4) =
+          make_float2(dqa[dt][2 * rr] * scale, dqa[dt][2 * rr + 1] * scale);
+  }
+}
+
+template <class K>
+static int set_smem(K kernel, int bytes) {
+  return (int)cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+}  // namespace fa
+}  // namespace lemo
+
+using namespace lemo;
+using namespace lemo::fa;
+
+extern "C" {
+
+int lemo_flash_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int n, int h,
+                   int head_dim, float scale, void* stream) {
+  if (n <= 0) return 0;
+  LEMO_ARG_CHECK(head_dim == 64 || head_dim == 128, "lemo_flash_fwd: head_dim must be 64 or 128");
+  LEMO_ARG_CHECK(h % head_dim == 0, "lemo_flash_fwd: h % head_dim");
+  dim3 grid((n + kBr - 1) / kBr, h / head_dim);
+  cudaStream_t st = (cudaStream_t)stream;
+  auto* qp = reinterpret_cast<const __nv_bfloat16*>(q);
+  auto* kp = reinterpret_cast<const __nv_bfloat16*>(k);
+  auto* vp = reinterpret_cast<const __nv_bfloat16*>(v);
+  auto* op = reinterpret_cast<__nv_bfloat16*>(o);
+  if (head_dim == 128) {
+    const int smem = 5 * Tile<128>::kBytes;
+    static int once = set_smem(flash_fwd_kernel<128>, smem);
+    (void)once;
+    flash_fwd_kernel<128><<<grid, 128, smem, st>>>(qp, kp, vp, op, lse, n, h, scale);
+  } else {
+    const int smem = 5 * Tile<64>::kBytes;
+    static int once = set_smem(flash_fwd_kernel<64>, smem);
+    (void)once;
+    flash_fwd_kernel<64><<<grid, 128, smem, st>>>(qp, kp, vp, op, lse, n, h, scale);
+  }
+  LEMO_CHECK_LAUNCH("lemo_flash_fwd");
+  return 0;
+}
+
+int lemo_flash_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                   const float* lse, float* delta, float* dq, float* dk, float* dv, int n, int h,
+                   int head_dim, float scale, void* stream) {
+  if (n <= 0) return 0;
+  LEMO_ARG_CHECK(head_dim == 64 || head_dim == 128, "lemo_flash_bwd: head_dim must be 64 or 128");
+  cudaStream_t st = (cudaStream_t)stream;
+  auto* qp = reinterpret_cast<const __nv_bfloat16*>(q);
+  auto* kp = reinterpret_cast<const __nv_bfloat16*>(k);
+  auto* vp = reinterpret_cast<const __nv_bfloat16*>(v);
+  auto* op = reinterpret_cast<const __nv_bfloat16*>(o);
+  auto* dop = reinterpret_cast<const __nv_bfloat16*>(dout);
+  flash_bwd_delta_kernel<<<n, 256, 0, st>>>(op, dop, delta, n, h, head_dim);
+  dim3 grid((n + kBr - 1) / kBr, h / head_dim);
+  if (head_dim == 128) {
+    const int smem = 6 * Tile<128>::kBytes + 256 * 4;
+    static int once = set_smem(flash_bwd_dkdv_kernel<128>, smem) | set_smem(flash_bwd_dq_kernel<128>, smem);
+    (void)once;
+    flash_bwd_dkdv_kernel<128><<<grid, 128, smem, st>>>(qp, kp, vp, dop, lse, delta, dk, dv, n, h, scale);
+    flash_bwd_dq_kernel<128><<<grid, 128, smem, st>>>(qp, kp, vp, dop, lse, delta, dq, n, h, scale);
+  } else {
+    const int smem = 6 * Tile<64>::kBytes + 256 * 4;
+    static int once = set_smem(flash_bwd_dkdv_kernel<64>, smem) | set_smem(flash_bwd_dq_kernel<64>, smem);
+    (void)once;
+    flash_bwd_dkdv_kernel<64><<<grid, 128, smem, st>>>(qp, kp, vp, dop, lse, delta, dk, dv, n, h, scale);
+    flash_bwd_dq_kernel<64><<<grid, 128, smem, st>>>(qp, kp, vp, dop, lse, delta, dq, n, h, scale);
+  }
+  LEMO_CHECK_LAUNCH("lemo_flash_bwd");
+  return 0;
+}
+
+}  // extern "C"

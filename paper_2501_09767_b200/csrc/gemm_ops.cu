@@ -184,7 +184,7 @@ struct EpiQKV {
         const int ca = cbase + hd + cp, cb = ca + half;
         add_side(a, u, R, S, h, 1, ca, scale);
         add_side(b, u, R, S, h, 1, cb, scale);
-        if (rope) {
+        if (rope && which < 2) {  // only q and k are rotated (kernels.py:112-114)
           const float2* tab = rope_tab + (size_t)p * half + cp;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
@@ -359,20 +359,22 @@ int lemo_gemm_scatter_add(const void* A, int lda, const void* B, int ldb, float*
                  gemm_auto(A, lda, B, ldb, M, N, K, e, (cudaStream_t)stream));
 }
 
-int lemo_gemm_qkv(const void* xn, const void* w_qkv_t, int M, int h, void* q, void* k, void* v,
+int lemo_gemm_qkv(const void* xn, const void* w_qkv_t, int M, int h, int nmat, void* q, void* k,
+                  void* v,
                   int head_dim, int rope, const void* rope_tab, const int* pos, const float* tq,
                   const float* tv, int ldt, int r, const float* Bq, const float* Bv, float scale,
                   void* stream) {
   LEMO_ARG_CHECK(head_dim % 64 == 0, "lemo_gemm_qkv: head_dim must be a multiple of 64");
+  LEMO_ARG_CHECK(nmat == 2 || nmat == 3, "lemo_gemm_qkv: nmat must be 2 (q,k) or 3 (q,k,v)");
   LEMO_ARG_CHECK(r >= 0 && r <= kMaxSideRank, "lemo_gemm_qkv: LoRA rank too large");
   EpiQKV e{reinterpret_cast<__nv_bfloat16*>(q), reinterpret_cast<__nv_bfloat16*>(k),
            reinterpret_cast<__nv_bfloat16*>(v), h, head_dim, rope,
            reinterpret_cast<const float2*>(rope_tab), pos, tq, tv, ldt, r, Bq, Bv, scale};
   int rc;
   if (h % 256 == 0 && 256 % head_dim == 0)
-    rc = gemm<256>(xn, h, w_qkv_t, h, M, 3 * h, h, e, (cudaStream_t)stream);
+    rc = gemm<256>(xn, h, w_qkv_t, h, M, nmat * h, h, e, (cudaStream_t)stream);
   else if (h % 128 == 0 && 128 % head_dim == 0)
-    rc = gemm<128>(xn, h, w_qkv_t, h, M, 3 * h, h, e, (cudaStream_t)stream);
+    rc = gemm<128>(xn, h, w_qkv_t, h, M, nmat * h, h, e, (cudaStream_t)stream);
   else {
     set_error_msg("lemo_gemm_qkv: hidden dim must be a multiple of 128 and of head_dim");
     return LEMO_ERR_REPORTED;

@@ -1,0 +1,550 @@
+// Row-wise HBM-bound kernels of the LeMo step: fused gather+RMSNorm (+LoRA
+// x·A factors), residual gathers, RMSNorm backward with index-remapped
+// scatter-add, MLP retained-row compaction, q/k/v gradient preparation (RoPE
+// backward + LoRA factors), LoRA weight gradients, embedding, segmented
+// cross-entropy rows, Adam.  One CTA (or warp) per row, float4/16-B vector
+// accesses, no atomics on the residual stream (retained rows are disjoint).
+#include "common.cuh"
+#include "lemo_internal.h"
+
+namespace lemo {
+
+constexpr float kEps = 1e-6f;  // tensor.py:387
+
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < NT / 32; ++i) t += red[i];
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// gather_rmsnorm (tensor.py:578-597) fused with the LoRA down-projection
+// t = xn · [A0 | A1] (kernels.py:97-98).  idx == null: every row.
+
+template <int VPT>
+__global__ void __launch_bounds__(128) gather_rmsnorm_kernel(
+    const float* __restrict__ x, int ldx, const int* __restrict__ idx, int h,
+    const float* __restrict__ w, __nv_bfloat16* __restrict__ xn, __nv_bfloat16* __restrict__ xg,
+    float* __restrict__ inv_out, const float* __restrict__ A0, const float* __restrict__ A1, int lda,
+    int r, float* __restrict__ t, int ldt) {
+  __shared__ float red[4];
+  __shared__ float tred[4][32];
+  const int row = blockIdx.x;
+  const int src = idx ? __ldg(idx + row) : row;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)src * ldx);
+  const int nv = h >> 2;
+  float4 v[VPT];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    v[i] = c < nv ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+  }
+  ss = block_sum<128>(ss, red);
+  const float inv = 1.f / sqrtf(ss / (float)h + kEps);
+  if (threadIdx.x == 0 && inv_out) inv_out[row] = inv;
+  const float4* w4 = reinterpret_cast<const float4*>(w);
+  float tacc[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) tacc[j] = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    if (c >= nv) continue;
+    const float4 ww = __ldg(w4 + c);
+    float4 o;
+    o.x = v[i].x * inv * ww.x;
+    o.y = v[i].y * inv * ww.y;
+    o.z = v[i].z * inv * ww.z;
+    o.w = v[i].w * inv * ww.w;
+    uint2 ob = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
+    reinterpret_cast<uint2*>(xn + (size_t)row * h)[c] = ob;
+    if (xg) {
+      reinterpret_cast<uint2*>(xg + (size_t)row * h)[c] =
+          make_uint2(pack_bf16x2(v[i].x, v[i].y), pack_bf16x2(v[i].z, v[i].w));
+    }
+    if (A0) {
+      const float oc[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float* a0 = A0 + (size_t)(4 * c + e) * lda;
+        const float* a1 = A1 + (size_t)(4 * c + e) * lda;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (j < r) {
+            tacc[j] = fmaf(oc[e], __ldg(a0 + j), tacc[j]);
+            tacc[16 + j] = fmaf(oc[e], __ldg(a1 + j), tacc[16 + j]);
+          }
+        }
+      }
+    }
+  }
+  if (A0) {
+    const int wid = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      float s = warp_sum(tacc[j]);
+      if (l == 0) tred[wid][j] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int j = threadIdx.x;
+      const float s = tred[0][j] + tred[1][j] + tred[2][j] + tred[3][j];
+      if ((j & 15) < r) t[(size_t)row * ldt + (j >> 4) * r + (j & 15)] = s;
+    }
+  }
+}
+
+// dst[i] = bf16(src[idx[i]])
+__global__ void gather_rows_bf16_kernel(const float* __restrict__ src, int ld,
+                                        const int* __restrict__ idx, int h,
+                                        __nv_bfloat16* __restrict__ dst) {
+  const int row = blockIdx.x;
+  const int s = idx ? __ldg(idx + row) : row;
+  const float4* a = reinterpret_cast<const float4*>(src + (size_t)s * ld);
+  uint2* d = reinterpret_cast<uint2*>(dst + (size_t)row * h);
+  for (int c = threadIdx.x; c < (h >> 2); c += blockDim.x) {
+    const float4 v = a[c];
+    d[c] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+  }
+}
+
+// RMSNorm backward (tensor.py:396-400, 589-595) with the result scattered
+// (added) into dx at idx[row]: the gather_rmsnorm backward writes only
+// retained rows, so eliminated rows keep exactly the residual gradient.
+template <bool kXBf16>
+__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(
+    const float* __restrict__ g, int ldg, const void* __restrict__ xv, int ldx,
+    const float* __restrict__ inv_in, const float* __restrict__ w, const int* __restrict__ idx,
+    int h, float gscale, float* __restrict__ dx, int lddx, int accumulate) {
+  __shared__ float red[8];
+  const int row = blockIdx.x;
+  const float inv = inv_in[row];
+  const float* gr = g + (size_t)row * ldg;
+  float dot = 0.f;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) {
+    float xv_;
+    if (kXBf16)
+      xv_ = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(xv)[(size_t)row * ldx + c]);
+    else
+      xv_ = reinterpret_cast<const float*>(xv)[(size_t)row * ldx + c];
+    dot += gscale * gr[c] * w[c] * xv_;
+  }
+  dot = block_sum<256>(dot, red);
+  const float coef = inv * inv * inv * dot / (float)h;
+  const int dst = idx ? __ldg(idx + row) : row;
+  float* d = dx + (size_t)dst * lddx;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) {
+    float xv_;
+    if (kXBf16)
+      xv_ = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(xv)[(size_t)row * ldx + c]);
+    else
+      xv_ = reinterpret_cast<const float*>(xv)[(size_t)row * ldx + c];
+    const float val = gscale * gr[c] * w[c] * inv - xv_ * coef;
+    d[c] = accumulate ? d[c] + val : val;
+  }
+}
+
+__global__ void embed_kernel(const int* __restrict__ ids, const float* __restrict__ table, int h,
+                             const float* __restrict__ pos_table, float* __restrict__ x) {
+  const int row = blockIdx.x;
+  const float4* t = reinterpret_cast<const float4*>(table + (size_t)__ldg(ids + row) * h);
+  const float4* p = pos_table ? reinterpret_cast<const float4*>(pos_table + (size_t)row * h) : nullptr;
+  float4* o = reinterpret_cast<float4*>(x + (size_t)row * h);
+  for (int c = threadIdx.x; c < (h >> 2); c += blockDim.x) {
+    float4 v = t[c];
+    if (p) {
+      const float4 q = p[c];
+      v.x += q.x; v.y += q.y; v.z += q.z; v.w += q.w;
+    }
+    o[c] = v;
+  }
+}
+
+// Retained-row compaction after MLP scoring: copy gate/up rows (saved for
+// backward), form the inner activation for the down projection, and save
+// the raw gathered residual row + its inverse RMS.
+__global__ void mlp_compact_kernel(const __nv_bfloat16* __restrict__ gu_all, int ldgu,
+                                   const float* __restrict__ x, int ldx,
+                                   const float* __restrict__ inv_all, const int* __restrict__ idx,
+                                   int h, int m_pad, int relu, __nv_bfloat16* __restrict__ gu_out,
+                                   __nv_bfloat16* __restrict__ inner_out,
+                                   __nv_bfloat16* __restrict__ xg_out, float* __restrict__ inv_out) {
+  const int row = blockIdx.x;
+  const int s = __ldg(idx + row);
+  const uint4* src = reinterpret_cast<const uint4*>(gu_all + (size_t)s * ldgu);
+  uint4* dst = reinterpret_cast<uint4*>(gu_out + (size_t)row * ldgu);
+  for (int c = threadIdx.x; c < (ldgu >> 3); c += blockDim.x) dst[c] = src[c];
+  // inner: silu -> 8 columns at a time from one 8-col group of gate and up
+  for (int c8 = threadIdx.x; c8 < (m_pad >> 3); c8 += blockDim.x) {
+    const int mc = c8 * 8;
+    float in[8];
+    if (!relu) {
+      const int gcol = (mc >> 7) * 256 + (mc & 127);
+      const uint4 g = src[gcol >> 3];
+      const uint4 u = src[(gcol + 128) >> 3];
+      const uint32_t gv[4] = {g.x, g.y, g.z, g.w}, uv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float g0 = bf16_lo(gv[e]), g1 = bf16_hi(gv[e]);
+        in[2 * e] = g0 * sigmoid_stable(g0) * bf16_lo(uv[e]);
+        in[2 * e + 1] = g1 * sigmoid_stable(g1) * bf16_hi(uv[e]);
+      }
+    } else {
+      const uint4 u = src[mc >> 3];
+      const uint32_t uv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        in[2 * e] = fmaxf(bf16_lo(uv[e]), 0.f);
+        in[2 * e + 1] = fmaxf(bf16_hi(uv[e]), 0.f);
+      }
+    }
+    reinterpret_cast<uint4*>(inner_out + (size_t)row * m_pad)[c8] =
+        make_uint4(pack_bf16x2(in[0], in[1]), pack_bf16x2(in[2], in[3]),
+                   pack_bf16x2(in[4], in[5]), pack_bf16x2(in[6], in[7]));
+  }
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)s * ldx);
+  uint2* xo = reinterpret_cast<uint2*>(xg_out + (size_t)row * h);
+  for (int c = threadIdx.x; c < (h >> 2); c += blockDim.x) {
+    const float4 v = xr[c];
+    xo[c] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+  }
+  if (threadIdx.x == 0) inv_out[row] = inv_all[s];
+}
+
+// After FlashAttention backward: rotate dq/dk back (tensor.py:627-632), pack
+// [dq|dk|dv] as bf16 for the dX GEMM, keep fp32 pre-rotation dq (in place)
+// for the LoRA grads, and form u = [dq·Bqᵀ | dv·Bvᵀ] (kernels.py:97-99 bwd).
+__global__ void __launch_bounds__(256) qkv_grad_prep_kernel(
+    float* __restrict__ dq, const float* __restrict__ dk, const float* __restrict__ dv, int h,
+    int head_dim, int rope, const float2* __restrict__ rope_tab, const int* __restrict__ pos,
+    const float* __restrict__ Bq, const float* __restrict__ Bv, int r,
+    __nv_bfloat16* __restrict__ dqkv, float* __restrict__ u, int ldu) {
+  __shared__ float red[8][32];
+  const int row = blockIdx.x;
+  const int half = head_dim >> 1;
+  const int p = rope ? __ldg(pos + row) : 0;
+  float* dqr = dq + (size_t)row * h;
+  const float* dkr = dk + (size_t)row * h;
+  const float* dvr = dv + (size_t)row * h;
+  __nv_bfloat16* o = dqkv + (size_t)row * 3 * h;
+  float acc[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+  // each thread handles pairs (c, c+half) inside a head
+  for (int e = threadIdx.x; e < (h >> 1); e += blockDim.x) {
+    const int hd = e / half, j = e - hd * half;
+    const int ca = hd * head_dim + j, cb = ca + half;
+    float qa = dqr[ca], qb = dqr[cb], ka = dkr[ca], kb = dkr[cb];
+    if (rope) {
+      const float2 cs = rope_tab[(size_t)p * half + j];
+      const float nqa = qa * cs.x + qb * cs.y, nqb = -qa * cs.y + qb * cs.x;
+      const float nka = ka * cs.x + kb * cs.y, nkb = -ka * cs.y + kb * cs.x;
+      qa = nqa; qb = nqb; ka = nka; kb = nkb;
+    }
+    dqr[ca] = qa;
+    dqr[cb] = qb;
+    const float va = dvr[ca], vb = dvr[cb];
+    o[ca] = __float2bfloat16_rn(qa);
+    o[cb] = __float2bfloat16_rn(qb);
+    o[h + ca] = __float2bfloat16_rn(ka);
+    o[h + cb] = __float2bfloat16_rn(kb);
+    o[2 * h + ca] = __float2bfloat16_rn(va);
+    o[2 * h + cb] = __float2bfloat16_rn(vb);
+    if (Bq) {
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        if (jj < r) {
+          acc[jj] += qa * __ldg(Bq + (size_t)jj * h + ca) + qb * __ldg(Bq + (size_t)jj * h + cb);
+          acc[16 + jj] += va * __ldg(Bv + (size_t)jj * h + ca) + vb * __ldg(Bv + (size_t)jj * h + cb);
+        }
+      }
+    }
+  }
+  if (Bq) {
+    const int wid = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float s = warp_sum(acc[j]);
+      if (l == 0) red[wid][j] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int j = threadIdx.x;
+      float s = 0.f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][j];
+      if ((j & 15) < r) u[(size_t)row * ldu + (j >> 4) * r + (j & 15)] = s;
+    }
+  }
+}
+
+// LoRA weight gradients (kernels.py:95-100 through tensor.py:324-325):
+//   dA0[c,j] += s Σ_i xn[i,c] u0[i,j]     dB0[j,c] += s Σ_i t0[i,j] g0[i,c]
+// (same for adapter 1), xn recomputed from the saved bf16 rows, inv, w.
+constexpr int kLoraRows = 64;
+__global__ void __launch_bounds__(128) lora_grads_kernel(
+    const __nv_bfloat16* __restrict__ xg, const float* __restrict__ inv, const float* __restrict__ w,
+    const float* __restrict__ t, const float* __restrict__ u, int ld, const float* __restrict__ g0,
+    const float* __restrict__ g1, int M, int h, int r, float scale, int lda, float* __restrict__ dA0,
+    float* __restrict__ dB0, float* __restrict__ dA1, float* __restrict__ dB1) {
+  __shared__ float st[kLoraRows][32];
+  __shared__ float su[kLoraRows][32];
+  __shared__ float sinv[kLoraRows];
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r0 = blockIdx.y * kLoraRows;
+  const int nrow = min(kLoraRows, M - r0);
+  for (int e = threadIdx.x; e < nrow * 2 * r; e += blockDim.x) {
+    const int i = e / (2 * r), j = e - i * 2 * r;
+    st[i][j] = t[(size_t)(r0 + i) * ld + j];
+    su[i][j] = u[(size_t)(r0 + i) * ld + j];
+  }
+  for (int i = threadIdx.x; i < nrow; i += blockDim.x) sinv[i] = inv[r0 + i];
+  __syncthreads();
+  if (c >= h) return;
+  float a0[16], b0[16], a1[16], b1[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) a0[j] = b0[j] = a1[j] = b1[j] = 0.f;
+  const float wc = w[c];
+  for (int i = 0; i < nrow; ++i) {
+    const size_t off = (size_t)(r0 + i) * h + c;
+    const float xn = __bfloat162float(xg[off]) * sinv[i] * wc;
+    const float q = g0[off], v = g1[off];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j < r) {
+        a0[j] = fmaf(xn, su[i][j], a0[j]);
+        a1[j] = fmaf(xn, su[i][r + j], a1[j]);
+        b0[j] = fmaf(st[i][j], q, b0[j]);
+        b1[j] = fmaf(st[i][r + j], v, b1[j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (j < r) {
+      atomicAdd(dA0 + (size_t)c * lda + j, scale * a0[j]);
+      atomicAdd(dA1 + (size_t)c * lda + j, scale * a1[j]);
+      atomicAdd(dB0 + (size_t)j * h + c, scale * b0[j]);
+      atomicAdd(dB1 + (size_t)j * h + c, scale * b1[j]);
+    }
+  }
+}
+
+// Cross-entropy rows of segmented_loss_and_grad (kernels.py:256-273,
+// tensor.py:446-468): per row lse, loss term, and dlogits = (p - onehot)/count.
+__global__ void __launch_bounds__(256) ce_rows_kernel(const float* __restrict__ logits, int ldl,
+                                                      const int* __restrict__ targets, int V,
+                                                      int ignore, float inv_count,
+                                                      __nv_bfloat16* __restrict__ dlogits, int ldd,
+                                                      float* __restrict__ row_loss,
+                                                      int* __restrict__ bad) {
+  __shared__ float red[8];
+  const int row = blockIdx.x;
+  const float* l = logits + (size_t)row * ldl;
+  __nv_bfloat16* d = dlogits + (size_t)row * ldd;
+  const int t = targets[row];
+  if (t == ignore) {
+    for (int c = threadIdx.x; c < V; c += blockDim.x) d[c] = __float2bfloat16_rn(0.f);
+    if (threadIdx.x == 0) row_loss[row] = 0.f;
+    return;
+  }
+  if (t < 0 || t >= V) {
+    if (threadIdx.x == 0) atomicOr(bad, 1);
+    return;
+  }
+  float mx = -INFINITY;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) mx = fmaxf(mx, l[c]);
+  mx = warp_max(mx);
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  if (ln == 0) red[w] = mx;
+  __syncthreads();
+  mx = red[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) mx = fmaxf(mx, red[i]);
+  float se = 0.f;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) se += expf(l[c] - mx);
+  se = block_sum<256>(se, red);
+  const float inv_se = 1.f / se;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    float p = expf(l[c] - mx) * inv_se;
+    if (c == t) p -= 1.f;
+    d[c] = __float2bfloat16_rn(p * inv_count);
+  }
+  if (threadIdx.x == 0) row_loss[row] = logf(se) + mx - l[t];
+}
+
+__global__ void sum_f64_kernel(const float* __restrict__ x, int n, double* __restrict__ out,
+                               int accumulate) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += (double)x[i];
+  s = warp_sum_d(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    *out = accumulate ? *out + t : t;
+  }
+}
+
+// Adam (optim.py:37-53) over one flat buffer of all adapter parameters.
+__global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
+                            float* __restrict__ m, float* __restrict__ v, long long n, float lr,
+                            float b1, float b2, float eps, float wd, float bc1, float bc2) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float pi = p[i];
+    const float gi = g[i];
+    if (wd != 0.f) pi *= 1.f - lr * wd;
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * (gi * gi);
+    m[i] = mi;
+    v[i] = vi;
+    pi -= lr * ((mi / bc1) / (sqrtf(vi / bc2) + eps));
+    p[i] = pi;
+  }
+}
+
+}  // namespace lemo
+
+using namespace lemo;
+
+extern "C" {
+
+int lemo_rmsnorm_gather(const float* x, int ldx, const int* idx, int M, int h, const float* w,
+                        void* xn, void* xg, float* inv, const float* A0, const float* A1, int lda,
+                        int r, float* t, int ldt, void* stream) {
+  if (M <= 0) return 0;
+  LEMO_ARG_CHECK(h % 4 == 0 && ldx % 4 == 0, "lemo_rmsnorm_gather: h, ldx must be multiples of 4");
+  LEMO_ARG_CHECK(h <= 4 * 128 * 16, "lemo_rmsnorm_gather: h too large");
+  LEMO_ARG_CHECK(!A0 || (r > 0 && r <= 16 && A1 && t), "lemo_rmsnorm_gather: LoRA rank <= 16");
+  const int nv = h / 4;
+  const int vpt = (nv + 127) / 128;
+  cudaStream_t st = (cudaStream_t)stream;
+  auto* xnp = reinterpret_cast<__nv_bfloat16*>(xn);
+  auto* xgp = reinterpret_cast<__nv_bfloat16*>(xg);
+#define LAUNCH(V)                                                                              \
+  gather_rmsnorm_kernel<V><<<M, 128, 0, st>>>(x, ldx, idx, h, w, xnp, xgp, inv, A0, A1, lda, r, \
+                                              t, ldt)
+  if (vpt <= 1) LAUNCH(1);
+  else if (vpt <= 2) LAUNCH(2);
+  else if (vpt <= 4) LAUNCH(4);
+  else if (vpt <= 8) LAUNCH(8);
+  else LAUNCH(16);
+#undef LAUNCH
+  LEMO_CHECK_LAUNCH("lemo_rmsnorm_gather");
+  return 0;
+}
+
+int lemo_gather_rows_bf16(const float* src, int ld, const int* idx, int M, int h, void* dst,
+                          void* stream) {
+  if (M <= 0) return 0;
+  LEMO_ARG_CHECK(h % 4 == 0 && ld % 4 == 0, "lemo_gather_rows_bf16: h%4");
+  gather_rows_bf16_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(
+      src, ld, idx, h, reinterpret_cast<__nv_bfloat16*>(dst));
+  LEMO_CHECK_LAUNCH("lemo_gather_rows_bf16");
+  return 0;
+}
+
+int lemo_rmsnorm_bwd(const float* g, int ldg, const void* x, int x_bf16, int ldx,
+                     const float* inv, const float* w, const int* idx, int M, int h, float gscale,
+                     float* dx, int lddx, int accumulate, void* stream) {
+  if (M <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (x_bf16)
+    rmsnorm_bwd_kernel<true><<<M, 256, 0, st>>>(g, ldg, x, ldx, inv, w, idx, h, gscale, dx, lddx,
+                                                accumulate);
+  else
+    rmsnorm_bwd_kernel<false><<<M, 256, 0, st>>>(g, ldg, x, ldx, inv, w, idx, h, gscale, dx, lddx,
+                                                 accumulate);
+  LEMO_CHECK_LAUNCH("lemo_rmsnorm_bwd");
+  return 0;
+}
+
+int lemo_embed(const int* ids, int n, const float* table, int h, const float* pos_table, float* x,
+               void* stream) {
+  if (n <= 0) return 0;
+  LEMO_ARG_CHECK(h % 4 == 0, "lemo_embed: h%4");
+  embed_kernel<<<n, 256, 0, (cudaStream_t)stream>>>(ids, table, h, pos_table, x);
+  LEMO_CHECK_LAUNCH("lemo_embed");
+  return 0;
+}
+
+int lemo_mlp_compact(const void* gu_all, const float* x, int ldx, const float* inv_all,
+                     const int* idx, int M, int h, int m_pad, int relu, void* gu_out,
+                     void* inner_out, void* xg_out, float* inv_out, void* stream) {
+  if (M <= 0) return 0;
+  LEMO_ARG_CHECK(m_pad % 128 == 0 && h % 4 == 0, "lemo_mlp_compact: m_pad%128, h%4");
+  const int ldgu = relu ? m_pad : 2 * m_pad;
+  mlp_compact_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(gu_all), ldgu, x, ldx, inv_all, idx, h, m_pad, relu,
+      reinterpret_cast<__nv_bfloat16*>(gu_out), reinterpret_cast<__nv_bfloat16*>(inner_out),
+      reinterpret_cast<__nv_bfloat16*>(xg_out), inv_out);
+  LEMO_CHECK_LAUNCH("lemo_mlp_compact");
+  return 0;
+}
+
+int lemo_qkv_grad_prep(float* dq, const float* dk, const float* dv, int M, int h, int head_dim,
+                       int rope, const void* rope_tab, const int* pos, const float* Bq,
+                       const float* Bv, int r, void* dqkv, float* u, int ldu, void* stream) {
+  if (M <= 0) return 0;
+  LEMO_ARG_CHECK(r <= 16, "lemo_qkv_grad_prep: LoRA rank <= 16");
+  qkv_grad_prep_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(
+      dq, dk, dv, h, head_dim, rope, reinterpret_cast<const float2*>(rope_tab), pos, Bq, Bv, r,
+      reinterpret_cast<__nv_bfloat16*>(dqkv), u, ldu);
+  LEMO_CHECK_LAUNCH("lemo_qkv_grad_prep");
+  return 0;
+}
+
+int lemo_lora_grads(const void* xg, const float* inv, const float* w, const float* t,
+                    const float* u, int ld, const float* g0, const float* g1, int M, int h, int r,
+                    float scale, int lda, float* dA0, float* dB0, float* dA1, float* dB1,
+                    void* stream) {
+  if (M <= 0) return 0;
+  LEMO_ARG_CHECK(r <= 16, "lemo_lora_grads: LoRA rank <= 16");
+  dim3 grid((h + 127) / 128, (M + kLoraRows - 1) / kLoraRows);
+  lora_grads_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(xg), inv, w, t, u, ld, g0, g1, M, h, r, scale, lda,
+      dA0, dB0, dA1, dB1);
+  LEMO_CHECK_LAUNCH("lemo_lora_grads");
+  return 0;
+}
+
+int lemo_ce_rows(const float* logits, int ldl, const int* targets, int n, int V, int ignore,
+                 float inv_count, void* dlogits, int ldd, float* row_loss, int* bad,
+                 void* stream) {
+  if (n <= 0) return 0;
+  ce_rows_kernel<<<n, 256, 0, (cudaStream_t)stream>>>(logits, ldl, targets, V, ignore, inv_count,
+                                                      reinterpret_cast<__nv_bfloat16*>(dlogits),
+                                                      ldd, row_loss, bad);
+  LEMO_CHECK_LAUNCH("lemo_ce_rows");
+  return 0;
+}
+
+int lemo_sum_f64(const float* x, int n, double* out, int accumulate, void* stream) {
+  sum_f64_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(x, n, out, accumulate);
+  LEMO_CHECK_LAUNCH("lemo_sum_f64");
+  return 0;
+}
+
+int lemo_adam(float* p, const float* g, float* m, float* v, long long n, float lr, float b1,
+              float b2, float eps, float wd, float bc1, float bc2, void* stream) {
+  if (n <= 0) return 0;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  adam_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(p, g, m, v, n, lr, b1, b2, eps, wd,
+                                                             bc1, bc2);
+  LEMO_CHECK_LAUNCH("lemo_adam");
+  return 0;
+}
+
+}  // extern "C"

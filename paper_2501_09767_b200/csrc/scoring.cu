@@ -1,0 +1,354 @@
+// Pattern scoring and selection kernels (K1/K2 of the design):
+//   block_embed      predictor.py:117-123 (block mean of the residual stream)
+//   sgemm            Predictor.predict (predictor.py:83-89) and Eq. 3 eq·ekᵀ
+//                    (predictor.py:176-186), fp32 so predicted scores track
+//                    the fp32 reference to ~1e-6 (mask parity)
+//   colsum_clamped   model.py:575-578 + sparsity.py:253-260 (clamp ≥ 0, f64
+//                    column sums accumulated in ascending query block)
+//   mlp_block_scores sparsity.py:284-305 (mean |inner| per token, block max)
+//   select           sparsity.py:263-281 + 95-104 (>= threshold, sink force,
+//                    block → token compaction; k stays on device)
+//   quantile_lower   model.py:545-563 (np.quantile method="lower" as a radix
+//                    select over order-preserving 64-bit keys)
+#include "common.cuh"
+#include "lemo_internal.h"
+
+namespace lemo {
+
+// --------------------------------------------------------------------------
+// block mean: one thread per (block, 4 columns); b independent float4 loads in
+// flight per thread, sequential f32 sum in row order then / b — the same
+// arithmetic numpy uses for mean over a non-contiguous axis.
+__global__ void __launch_bounds__(256) block_embed_kernel(const float* __restrict__ x, int ldx,
+                                                          int nb, int h, int b,
+                                                          float* __restrict__ xb) {
+  const int nv = h >> 2;
+  const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gid >= (long long)nb * nv) return;
+  const int n = (int)(gid / nv), c = (int)(gid - (long long)n * nv);
+  const float4* src = reinterpret_cast<const float4*>(x + (size_t)n * b * ldx) + c;
+  const size_t stride = (size_t)ldx >> 2;
+  float4 acc = __ldg(src);
+#pragma unroll 8
+  for (int i = 1; i < b; ++i) {
+    const float4 v = __ldg(src + i * stride);
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  const float fb = (float)b;
+  acc.x /= fb; acc.y /= fb; acc.z /= fb; acc.w /= fb;
+  reinterpret_cast<float4*>(xb + (size_t)n * h)[c] = acc;
+}
+
+// --------------------------------------------------------------------------
+// fp32 SIMT GEMM, 128x128x8 tiles, 8x8 per thread.  C = act(A·op(B))·mask.
+template <bool kBT>
+__global__ void __launch_bounds__(256) sgemm_kernel(const float* __restrict__ A, int lda,
+                                                    const float* __restrict__ B, int ldb,
+                                                    float* __restrict__ C, int ldc, int M, int N,
+                                                    int K, int relu,
+                                                    const unsigned char* __restrict__ mask) {
+  __shared__ float As[2][8][132];
+  __shared__ float Bs[2][8][132];
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.y * 128, n0 = blockIdx.x * 128;
+  const int tx = tid & 15, ty = tid >> 4;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+  // loader mapping: A: row = tid>>1, k4 = (tid&1)*4 ; B (kBT): n = tid>>1, k4 = (tid&1)*4
+  //                 B (!kBT): k = tid>>5, n4 = (tid&31)*4
+  float ra[4], rb[4];
+  auto load = [&](int k0) {
+    {
+      const int row = m0 + (tid >> 1), kk = k0 + (tid & 1) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        ra[e] = (row < M && kk + e < K) ? __ldg(A + (size_t)row * lda + kk + e) : 0.f;
+    }
+    if (kBT) {
+      const int n = n0 + (tid >> 1), kk = k0 + (tid & 1) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        rb[e] = (n < N && kk + e < K) ? __ldg(B + (size_t)n * ldb + kk + e) : 0.f;
+    } else {
+      const int kk = k0 + (tid >> 5), n = n0 + (tid & 31) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        rb[e] = (kk < K && n + e < N) ? __ldg(B + (size_t)kk * ldb + n + e) : 0.f;
+    }
+  };
+  auto store = [&](int buf) {
+    {
+      const int r = tid >> 1, k4 = (tid & 1) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) As[buf][k4 + e][r] = ra[e];
+    }
+    if (kBT) {
+      const int n = tid >> 1, k4 = (tid & 1) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) Bs[buf][k4 + e][n] = rb[e];
+    } else {
+      const int k = tid >> 5, n4 = (tid & 31) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) Bs[buf][k][n4 + e] = rb[e];
+    }
+  };
+  load(0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < K; k0 += 8) {
+    const bool more = k0 + 8 < K;
+    if (more) load(k0 + 8);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      float a[8], bv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = As[buf][kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bv[j] = Bs[buf][kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], bv[j], acc[i][j]);
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = m0 + ty + 16 * i;
+    if (row >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int col = n0 + tx + 16 * j;
+      if (col >= N) continue;
+      float v = acc[i][j];
+      if (relu) v = fmaxf(v, 0.f);
+      if (mask) v = mask[col] ? v : 0.f;
+      C[(size_t)row * ldc + col] = v;
+    }
+  }
+}
+
+// vec[n] = Σ_{m=n}^{nb-1} (double)max(S[m,n], 0), ascending m (sparsity.py:256-259)
+__global__ void colsum_clamped_kernel(const float* __restrict__ S, int lds, int nb,
+                                      double* __restrict__ vec) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= nb) return;
+  double acc = 0.0;
+  int m = n;
+  for (; m + 4 <= nb; m += 4) {
+    const float a = S[(size_t)m * lds + n], b = S[(size_t)(m + 1) * lds + n];
+    const float c = S[(size_t)(m + 2) * lds + n], d = S[(size_t)(m + 3) * lds + n];
+    acc += (double)fmaxf(a, 0.f);
+    acc += (double)fmaxf(b, 0.f);
+    acc += (double)fmaxf(c, 0.f);
+    acc += (double)fmaxf(d, 0.f);
+  }
+  for (; m < nb; ++m) acc += (double)fmaxf(S[(size_t)m * lds + n], 0.f);
+  vec[n] = acc;
+}
+
+__global__ void mlp_block_scores_kernel(const float* __restrict__ partial, int n_tiles, int s,
+                                        int n_valid, int b, float m_real,
+                                        double* __restrict__ vec) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nb = (s + b - 1) / b;
+  if (n >= nb) return;
+  const int t0 = n * b;
+  const int t1 = min(min(t0 + b, s), n_valid);
+  double best = 0.0;
+  bool any = false;
+  for (int row = t0; row < t1; ++row) {
+    float acc = 0.f;
+    for (int t = 0; t < n_tiles; ++t) acc += partial[(size_t)t * s + row];
+    const double tok = (double)(acc / m_real);
+    best = any ? fmax(best, tok) : tok;
+    any = true;
+  }
+  vec[n] = any ? best : 0.0;
+}
+
+// --------------------------------------------------------------------------
+// selection: one CTA; keep n iff vec[n] >= T (or forced sink block 0);
+// blocks/tokens compacted in ascending order via a block-wide scan.
+constexpr int kSelThreads = 1024;
+__global__ void __launch_bounds__(kSelThreads) select_kernel(
+    const double* __restrict__ vec, int nb, double thr, const double* __restrict__ thr_dev,
+    const unsigned char* __restrict__ force, int b, int n_tokens, unsigned char* __restrict__ mask, int* __restrict__ blocks,
+    int* __restrict__ tokens, int* __restrict__ counts, double* __restrict__ thr_out) {
+  __shared__ int scan[kSelThreads];
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  if (tid == 0) bad = 0;
+  const double T = thr_dev ? *thr_dev : thr;
+  const int per = (nb + kSelThreads - 1) / kSelThreads;
+  const int start = min(tid * per, nb), end = min(start + per, nb);
+  int cnt = 0;
+  bool nonfinite = false;
+  for (int n = start; n < end; ++n) {
+    const double v = vec[n];
+    if (!isfinite(v)) nonfinite = true;
+    const bool keep = (v >= T) || (force && force[n]);
+    mask[n] = keep ? 1 : 0;
+    cnt += keep;
+  }
+  __syncthreads();
+  if (nonfinite) atomicOr(&bad, 1);
+  scan[tid] = cnt;
+  __syncthreads();
+  for (int o = 1; o < kSelThreads; o <<= 1) {
+    const int v = tid >= o ? scan[tid - o] : 0;
+    __syncthreads();
+    scan[tid] += v;
+    __syncthreads();
+  }
+  int off = scan[tid] - cnt;
+  for (int n = start; n < end; ++n) {
+    if (!mask[n]) continue;
+    blocks[off] = n;
+    const int t0 = n * b, t1 = min(t0 + b, n_tokens);
+    for (int t = t0; t < t1; ++t) tokens[off * b + (t - t0)] = t;
+    ++off;
+  }
+  if (tid == kSelThreads - 1) {
+    const int total = scan[tid];
+    const int short_tail = (nb > 0 && mask[nb - 1]) ? nb * b - n_tokens : 0;
+    counts[0] = total * b - short_tail;
+    counts[1] = total;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    counts[2] = bad;
+    if (thr_out) *thr_out = T;
+  }
+}
+
+__device__ __forceinline__ unsigned long long f64_key(double x) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_f64(unsigned long long k) {
+  const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+__global__ void __launch_bounds__(1024) quantile_kernel(const double* __restrict__ data, int n,
+                                                        long long rank, int plus_one,
+                                                        double* __restrict__ out) {
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned long long s_prefix, s_mask;
+  __shared__ long long s_rank;
+  if (threadIdx.x == 0) {
+    s_prefix = 0;
+    s_mask = 0;
+    s_rank = rank;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 56 - 8 * pass;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const unsigned long long prefix = s_prefix, msk = s_mask;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned long long k = f64_key(data[i]);
+      if ((k & msk) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long r = s_rank;
+      int d = 0;
+      for (; d < 256; ++d) {
+        if (r < (long long)hist[d]) break;
+        r -= hist[d];
+      }
+      if (d > 255) d = 255;
+      s_rank = r;
+      s_prefix = prefix | ((unsigned long long)d << shift);
+      s_mask = msk | (255ull << shift);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double v = key_f64(s_prefix);
+    if (plus_one) v += 1.0;
+    *out = v;
+  }
+}
+
+}  // namespace lemo
+
+using namespace lemo;
+
+extern "C" {
+
+int lemo_block_embed(const float* x, int ldx, int s, int h, int b, float* xb, void* stream) {
+  LEMO_ARG_CHECK(b > 0 && s % b == 0, "lemo_block_embed: s must be a multiple of the block size");
+  LEMO_ARG_CHECK(h % 4 == 0 && ldx % 4 == 0, "lemo_block_embed: h, ldx multiples of 4");
+  const int nb = s / b;
+  const long long total = (long long)nb * (h / 4);
+  if (total == 0) return 0;
+  block_embed_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      x, ldx, nb, h, b, xb);
+  LEMO_CHECK_LAUNCH("lemo_block_embed");
+  return 0;
+}
+
+int lemo_sgemm(const float* A, int lda, const float* B, int ldb, int b_trans, float* C, int ldc,
+               int M, int N, int K, int relu, const unsigned char* col_mask, void* stream) {
+  if (M <= 0 || N <= 0) return 0;
+  dim3 grid((N + 127) / 128, (M + 127) / 128);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (b_trans)
+    sgemm_kernel<true><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, relu, col_mask);
+  else
+    sgemm_kernel<false><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, relu, col_mask);
+  LEMO_CHECK_LAUNCH("lemo_sgemm");
+  return 0;
+}
+
+int lemo_colsum_clamped(const float* S, int lds, int nb, double* vec, void* stream) {
+  if (nb <= 0) return 0;
+  colsum_clamped_kernel<<<(nb + 127) / 128, 128, 0, (cudaStream_t)stream>>>(S, lds, nb, vec);
+  LEMO_CHECK_LAUNCH("lemo_colsum_clamped");
+  return 0;
+}
+
+int lemo_mlp_block_scores(const float* partial, int n_tiles, int s, int n_valid, int b, int m_real,
+                          double* vec, void* stream) {
+  const int nb = (s + b - 1) / b;
+  if (nb <= 0) return 0;
+  mlp_block_scores_kernel<<<(nb + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+      partial, n_tiles, s, n_valid, b, (float)m_real, vec);
+  LEMO_CHECK_LAUNCH("lemo_mlp_block_scores");
+  return 0;
+}
+
+int lemo_select(const double* vec, int nb, double thr, const double* thr_dev,
+                const unsigned char* force, int b,
+                int n_tokens, unsigned char* mask, int* blocks, int* tokens, int* counts,
+                double* thr_out, void* stream) {
+  LEMO_ARG_CHECK(nb == (n_tokens + b - 1) / b, "lemo_select: nb must equal ceil(n_tokens / b)");
+  select_kernel<<<1, kSelThreads, 0, (cudaStream_t)stream>>>(vec, nb, thr, thr_dev, force, b,
+                                                            n_tokens, mask, blocks, tokens,
+                                                            counts, thr_out);
+  LEMO_CHECK_LAUNCH("lemo_select");
+  return 0;
+}
+
+int lemo_quantile_lower(const double* data, int n, long long rank, int plus_one, double* out,
+                        void* stream) {
+  LEMO_ARG_CHECK(n > 0 && rank >= 0 && rank < n, "lemo_quantile_lower: rank out of range");
+  quantile_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(data, n, rank, plus_one, out);
+  LEMO_CHECK_LAUNCH("lemo_quantile_lower");
+  return 0;
+}
+
+}  // extern "C"

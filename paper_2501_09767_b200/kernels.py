@@ -1,0 +1,322 @@
+"""Permutation-free sparse execution and segment-based loss on the GPU.
+
+Mirrors ``sparsetune.kernels`` (kernels.py:25-288).  The reference gathers
+retained rows, runs the block on them and scatter-adds the result into a
+copy of the residual stream; here every step is a liblemo kernel:
+
+  attention block  gather+RMSNorm(+LoRA x·A)  → tcgen05 q/k/v GEMM with the
+                   LoRA side term and RoPE at the ORIGINAL positions in its
+                   epilogue → causal flash attention on the compact sequence
+                   → tcgen05 output projection whose epilogue adds each row
+                   into the residual at idx[row] (in place, no atomics)
+  MLP block        gather+RMSNorm → tcgen05 gate/up GEMM (SwiGLU in the
+                   epilogue) → tcgen05 down projection with the same
+                   index-remapped residual epilogue; when the MLP scorer has
+                   already produced gate/up for every row, the retained rows
+                   are compacted instead of recomputed
+  backward         only compact retained-row buffers are saved (tensor.py:
+                   578-597 semantics); gradients are gathered from the
+                   residual gradient, pushed through dX-only GEMMs (frozen
+                   weights get no dW) and RMSNorm backward scatter-adds them
+                   back at idx.
+
+The block functions operate IN PLACE on a float32 residual stream `x`
+[n_tokens, h]; the reference-named wrappers at the bottom keep the
+reference's value semantics (they return a new tensor).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import ops
+from .errors import ContractError
+
+BF16, F32 = torch.bfloat16, torch.float32
+
+
+class GatherPlan:
+    """Sorted retained token indices within a sequence of n_tokens
+    (kernels.py:25-55); indices live on the device as int32."""
+
+    __slots__ = ("indices", "n_tokens", "k")
+
+    def __init__(self, indices, n_tokens: int, *, device=None, _trusted: bool = False):
+        if isinstance(indices, torch.Tensor) and indices.is_cuda and _trusted:
+            self.indices = indices
+            self.k = int(indices.shape[0])
+            self.n_tokens = n_tokens
+            return
+        idx = np.asarray(indices.cpu() if isinstance(indices, torch.Tensor) else indices,
+                         dtype=np.int64)
+        if idx.ndim != 1:
+            raise ContractError("plan indices must be one-dimensional")
+        if idx.size:
+            if (np.diff(idx) <= 0).any():
+                raise ContractError("plan indices must be strictly increasing")
+            if idx[0] < 0 or idx[-1] >= n_tokens:
+                raise ContractError(f"plan indices out of range [0, {n_tokens})")
+        dev = device or (indices.device if isinstance(indices, torch.Tensor) and indices.is_cuda
+                         else torch.device("cuda"))
+        self.indices = torch.as_tensor(idx.astype(np.int32)).to(dev)
+        self.k = int(idx.size)
+        self.n_tokens = n_tokens
+
+    @staticmethod
+    def full(n_tokens: int, device=None) -> "GatherPlan":
+        dev = device or torch.device("cuda")
+        return GatherPlan(torch.arange(n_tokens, dtype=torch.int32, device=dev), n_tokens,
+                          _trusted=True)
+
+    @staticmethod
+    def empty(n_tokens: int, device=None) -> "GatherPlan":
+        dev = device or torch.device("cuda")
+        return GatherPlan(torch.empty(0, dtype=torch.int32, device=dev), n_tokens, _trusted=True)
+
+    @staticmethod
+    def from_pattern(pattern, n_tokens: int, device) -> "GatherPlan":
+        """Device indices straight from the select kernel (already sorted)."""
+        return GatherPlan(pattern.device_token_indices(device), n_tokens, _trusted=True)
+
+
+@dataclass(frozen=True)
+class SegmentPlan:
+    """Contiguous partition of [0, n_tokens) into non-empty segments (kernels.py:58-88)."""
+
+    n_tokens: int
+    boundaries: tuple
+
+    def __post_init__(self):
+        b = tuple(int(x) for x in self.boundaries)
+        object.__setattr__(self, "boundaries", b)
+        if len(b) < 2 or b[0] != 0 or b[-1] != self.n_tokens:
+            raise ContractError(f"boundaries must span [0, {self.n_tokens}], got {b}")
+        if any(b[i + 1] <= b[i] for i in range(len(b) - 1)):
+            raise ContractError(f"every segment must be non-empty, got {b}")
+
+    @property
+    def n_segments(self) -> int:
+        return len(self.boundaries) - 1
+
+    @property
+    def segments(self):
+        return [(self.boundaries[i], self.boundaries[i + 1]) for i in range(self.n_segments)]
+
+    @staticmethod
+    def even(n_tokens: int, n_segments: int) -> "SegmentPlan":
+        if n_segments < 1 or n_segments > n_tokens:
+            raise ContractError(f"cannot split {n_tokens} tokens into {n_segments} non-empty "
+                                "segments")
+        return SegmentPlan(n_tokens, tuple(round(i * n_tokens / n_segments)
+                                           for i in range(n_segments + 1)))
+
+
+# ---------------------------------------------------------------------------
+# attention block
+
+
+def attention_forward(x: torch.Tensor, plan: GatherPlan, layer, *, save: bool = True):
+    """x[idx] += attention_core(gather_rmsnorm(x, idx)) in place; returns the
+    compact saved state (or None when save=False / k == 0)."""
+    if plan.k == 0:
+        return None
+    k, h = plan.k, x.shape[1]
+    dev = x.device
+    idx = plan.indices
+    r = layer.lora_rank
+    xn = torch.empty(k, h, dtype=BF16, device=dev)
+    xg = torch.empty(k, h, dtype=BF16, device=dev) if save else None
+    inv = torch.empty(k, dtype=F32, device=dev) if save else None
+    t = torch.empty(k, 2 * r, dtype=F32, device=dev) if r else None
+    ops.rmsnorm_gather(x, layer.attn_norm_w, idx, xn=xn, xg=xg, inv=inv,
+                       A=layer.lora_A if r else None, r=r, t=t)
+    q, kk, v = ops.gemm_qkv(xn, layer.w_qkv_t, h=h, head_dim=layer.head_dim, rope=layer.rope,
+                            rope_tab=layer.rope_tab, pos=idx, t=t, r=r,
+                            Bq=layer.lora_Bq if r else None, Bv=layer.lora_Bv if r else None,
+                            scale=layer.lora_scaling)
+    del xn
+    o, lse = ops.flash_fwd(q, kk, v, head_dim=layer.head_dim, scale=1.0 / math.sqrt(layer.head_dim))
+    ops.gemm_scatter_add(o, layer.w_o_t, x, idx)
+    if not save:
+        return None
+    return dict(idx=idx, xg=xg, inv=inv, t=t, q=q, k=kk, v=v, o=o, lse=lse)
+
+
+def attention_backward(dx: torch.Tensor, saved: dict, layer, grads) -> None:
+    """dx[idx] += d(attention block)/dx (in place); LoRA grads accumulated
+    into grads = (dA_qv, dBq, dBv) views of the flat gradient buffer."""
+    idx = saved["idx"]
+    k, h = idx.shape[0], dx.shape[1]
+    dev = dx.device
+    r = layer.lora_rank
+    dy = ops.gather_rows_bf16(dx, idx)
+    d_o = ops.gemm_bf16(dy, layer.w_o)
+    del dy
+    dq, dk, dv = ops.flash_bwd(saved["q"], saved["k"], saved["v"], saved["o"], d_o, saved["lse"],
+                               head_dim=layer.head_dim, scale=1.0 / math.sqrt(layer.head_dim))
+    del d_o
+    dqkv = torch.empty(k, 3 * h, dtype=BF16, device=dev)
+    u = torch.empty(k, 2 * r, dtype=F32, device=dev) if r else None
+    ops.qkv_grad_prep(dq, dk, dv, head_dim=layer.head_dim, rope=layer.rope,
+                      rope_tab=layer.rope_tab, pos=idx, Bq=layer.lora_Bq if r else None,
+                      Bv=layer.lora_Bv if r else None, r=r, dqkv=dqkv, u=u)
+    if r and grads is not None:
+        dA, dBq, dBv = grads
+        ops.lora_grads(saved["xg"], saved["inv"], layer.attn_norm_w, saved["t"], u, dq, dv, r=r,
+                       scale=layer.lora_scaling, dA=dA, dB0=dBq, dB1=dBv)
+    del dq, dk, dv
+    dxn = ops.gemm_f32(dqkv, layer.w_qkv, side_u=u, side_s=layer.lora_A if r else None,
+                       side_strides=(1, 2 * r), scale=layer.lora_scaling)
+    ops.rmsnorm_bwd(dxn, saved["xg"], saved["inv"], layer.attn_norm_w, dx, idx, accumulate=True)
+
+
+# ---------------------------------------------------------------------------
+# MLP block
+
+
+def mlp_forward(x: torch.Tensor, plan: GatherPlan, layer, *, scored=None, save: bool = True):
+    """x[idx] += mlp_core(gather_rmsnorm(x, idx)) in place.  `scored` =
+    (gu_all, inv_all) from the MLP scorer over every row of this same x:
+    retained rows are then compacted instead of recomputed."""
+    if plan.k == 0:
+        return None
+    k, h = plan.k, x.shape[1]
+    dev = x.device
+    idx = plan.indices
+    N = layer.w_gu_t.shape[0]
+    gu = torch.empty(k, N, dtype=BF16, device=dev)
+    inner = torch.empty(k, layer.m_pad, dtype=BF16, device=dev)
+    xg = torch.empty(k, h, dtype=BF16, device=dev)
+    inv = torch.empty(k, dtype=F32, device=dev)
+    if scored is not None:
+        gu_all, inv_all = scored
+        ops.mlp_compact(gu_all, x, inv_all, idx, m_pad=layer.m_pad, relu=layer.relu, gu_out=gu,
+                        inner_out=inner, xg_out=xg, inv_out=inv)
+    else:
+        xn = ops.rmsnorm_gather(x, layer.mlp_norm_w, idx, xg=xg, inv=inv)
+        ops.gemm_gateup(xn, layer.w_gu_t, gu=gu, inner=inner, relu=layer.relu)
+        del xn
+    ops.gemm_scatter_add(inner, layer.w_down_t, x, idx)
+    if not save:
+        return None
+    return dict(idx=idx, xg=xg, inv=inv, gu=gu)
+
+
+def mlp_backward(dx: torch.Tensor, saved: dict, layer) -> None:
+    idx = saved["idx"]
+    k = idx.shape[0]
+    dy = ops.gather_rows_bf16(dx, idx)
+    dgu = torch.empty(k, layer.w_gu_t.shape[0], dtype=BF16, device=dx.device)
+    ops.gemm_dgateup(dy, layer.w_down, saved["gu"], dgu, m_pad=layer.m_pad, relu=layer.relu)
+    del dy
+    dxn = ops.gemm_f32(dgu, layer.w_gu)
+    del dgu
+    ops.rmsnorm_bwd(dxn, saved["xg"], saved["inv"], layer.mlp_norm_w, dx, idx, accumulate=True)
+
+
+# ---------------------------------------------------------------------------
+# segment-based loss (kernels.py:229-288): logits of one segment at a time,
+# CE + dlogits + grad_hidden computed in the forward pass.
+
+
+def segmented_loss_forward(hidden: torch.Tensor, lm_head_t: torch.Tensor, lm_head: torch.Tensor,
+                           targets_dev: torch.Tensor, count: int, plan: SegmentPlan,
+                           ignore_index: int = -1, need_grad: bool = True):
+    """Returns (loss device scalar f64, grad_hidden f32 [n, h] or None)."""
+    n, h = hidden.shape
+    V = lm_head_t.shape[0]
+    dev = hidden.device
+    if count == 0:
+        raise ContractError("segmented loss: no valid targets")
+    grad_hidden = torch.empty(n, h, dtype=F32, device=dev) if need_grad else None
+    row_loss = torch.empty(n, dtype=F32, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    inv_count = 1.0 / count
+    for a, b in plan.segments:
+        logits = ops.gemm_f32(hidden[a:b], lm_head_t)
+        dlog = torch.empty(b - a, V, dtype=BF16, device=dev)
+        ops.ce_rows(logits, targets_dev[a:b], V=V, ignore=ignore_index, inv_count=inv_count,
+                    dlogits=dlog, row_loss=row_loss[a:b], bad=bad)
+        del logits
+        if need_grad:
+            ops.gemm_f32(dlog, lm_head, out=grad_hidden[a:b])
+        del dlog
+    loss_sum = torch.empty(1, dtype=torch.float64, device=dev)
+    ops.sum_f64(row_loss, loss_sum)
+    return loss_sum / count, grad_hidden
+
+
+def check_targets(targets: np.ndarray, vocab: int, ignore_index: int = -1) -> int:
+    """IndexError for out-of-range targets (tensor.py:452-457); returns the
+    number of valid targets."""
+    valid = targets != ignore_index
+    chk = targets[valid]
+    if chk.size and (chk.min() < 0 or chk.max() >= vocab):
+        raise IndexError(f"target index out of range [0, {vocab}): min={chk.min()}, "
+                         f"max={chk.max()}")
+    return int(valid.sum())
+
+
+# ---------------------------------------------------------------------------
+# reference-named entry points (value semantics: inputs are not modified)
+
+
+class _SparseBlock(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, lora_flat, plan, layer, kind):
+        out = x.detach().clone()
+        if kind == "attention":
+            saved = attention_forward(out, plan, layer)
+        else:
+            saved = mlp_forward(out, plan, layer)
+        ctx.saved_state = saved
+        ctx.plan, ctx.layer, ctx.kind = plan, layer, kind
+        ctx.lora_shape = lora_flat.shape
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        dx = g.detach().to(F32).clone().contiguous()
+        dlora = torch.zeros(ctx.lora_shape, dtype=F32, device=dx.device)
+        if ctx.saved_state is not None:
+            if ctx.kind == "attention":
+                attention_backward(dx, ctx.saved_state, ctx.layer,
+                                   ctx.layer.grad_views(dlora))
+            else:
+                mlp_backward(dx, ctx.saved_state, ctx.layer)
+        ctx.saved_state = None
+        return dx, dlora, None, None, None
+
+
+def _check_plan(x, plan):
+    if plan.n_tokens != x.shape[0]:
+        raise ContractError(f"plan covers {plan.n_tokens} tokens, input has {x.shape[0]}")
+
+
+def sparse_attention_fused(x: torch.Tensor, plan: GatherPlan, layer,
+                           fuse_projections: bool = True) -> torch.Tensor:
+    """kernels.py:153-177: k == 0 returns x itself; otherwise a new residual
+    tensor with the attention output added at the retained rows."""
+    _check_plan(x, plan)
+    if plan.k == 0:
+        return x
+    return _SparseBlock.apply(x, layer.lora_param, plan, layer, "attention")
+
+
+def sparse_mlp_fused(x: torch.Tensor, plan: GatherPlan, layer,
+                     fuse_projections: bool = True) -> torch.Tensor:
+    """kernels.py:201-222"""
+    _check_plan(x, plan)
+    if plan.k == 0:
+        return x
+    return _SparseBlock.apply(x, layer.lora_param, plan, layer, "mlp")
+
+
+# The reference's naive variants (kernels.py:131-150, 180-198) differ only in
+# their transient buffers; on the GPU both names run the fused kernels.
+sparse_attention_naive = sparse_attention_fused
+sparse_mlp_naive = sparse_mlp_fused

@@ -1,0 +1,746 @@
+"""Decoder model with LoRA adapters and the per-layer token-elimination hook.
+
+Mirrors ``sparsetune.model`` (model.py:23-590): ModelConfig, LoraAdapter,
+LayerState, DecoderModel.forward_step and the pattern sources.  Frozen
+weights live on the GPU in bf16 in the two K-major layouts the tcgen05 GEMMs
+need (forward: [out, in]; backward dX: [in, out]); the residual stream is
+fp32; all LoRA parameters share one flat fp32 buffer (one Adam launch, one
+NCCL all-reduce bucket).
+
+`forward_step` runs the whole step through liblemo kernels and returns a
+loss whose `.backward()` runs the sparse backward sweep (saved activations
+are compact retained-row buffers only) and fills `model.lora_param.grad`.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels, ops, predictor as predictor_mod, sparsity
+from .errors import ContractError, DimensionError
+
+PAD_TOKEN = 0
+IGNORE_INDEX = -1
+BF16, F32 = torch.bfloat16, torch.float32
+
+
+@dataclass
+class ModelConfig:
+    """Geometry, model.py:23-64 (same fields and validation)."""
+
+    n_layers: int = 4
+    hidden_dim: int = 64
+    n_heads: int = 4
+    vocab_size: int = 256
+    max_seq_len: int = 2048
+    mlp_variant: str = "silu"  # "relu" | "silu"
+    mlp_dim: int = 256
+    lora_rank: int = 8
+    lora_alpha: float = 16.0
+    block_size: int = 16
+    positions: str = "rope"  # "rope" | "learned"
+    rope_base: float = 10000.0
+    dtype: str = "float32"
+
+    def __post_init__(self):
+        if self.hidden_dim % self.n_heads != 0:
+            raise DimensionError(f"hidden_dim {self.hidden_dim} not divisible by {self.n_heads} heads")
+        if self.positions == "rope" and self.head_dim % 2 != 0:
+            raise DimensionError("rotary positions need an even head dim")
+        if self.max_seq_len % self.block_size != 0:
+            raise ContractError(f"max_seq_len {self.max_seq_len} must be a multiple of block "
+                                f"size {self.block_size}")
+        if self.mlp_variant not in ("relu", "silu"):
+            raise ContractError(f"unknown mlp variant {self.mlp_variant!r}")
+        if self.positions not in ("rope", "learned"):
+            raise ContractError(f"unknown position mode {self.positions!r}")
+        if self.dtype not in ("float32", "float64", "bfloat16"):
+            raise ContractError(f"unsupported dtype {self.dtype!r}")
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden_dim // self.n_heads
+
+    @property
+    def mlp_pad(self) -> int:
+        return -(-self.mlp_dim // 128) * 128
+
+    def check_gpu_geometry(self) -> None:
+        """Tile constraints of the B200 kernels (reported, never silently padded)."""
+        if self.head_dim not in (64, 128):
+            raise ContractError(f"GPU kernels support head_dim 64 or 128, got {self.head_dim}")
+        if self.hidden_dim % 128:
+            raise ContractError("GPU kernels need hidden_dim % 128 == 0")
+        if self.vocab_size % 32:
+            raise ContractError("GPU kernels need vocab_size % 32 == 0")
+        if self.lora_rank > 16:
+            raise ContractError("GPU kernels support LoRA rank <= 16")
+
+
+def llama2_7b(**kw) -> ModelConfig:
+    """Llama2-7B geometry (BASELINE configs[1], north star at 16K)."""
+    base = dict(n_layers=32, hidden_dim=4096, n_heads=32, vocab_size=32000, max_seq_len=16384,
+                mlp_dim=11008, lora_rank=8, lora_alpha=16.0, block_size=16)
+    base.update(kw)
+    return ModelConfig(**base)
+
+
+def tiny_t(**kw) -> ModelConfig:
+    """Config T of SURVEY §8 (BASELINE configs[0])."""
+    base = dict(n_layers=2, hidden_dim=256, n_heads=4, vocab_size=256, max_seq_len=2048,
+                mlp_dim=688, lora_rank=8, lora_alpha=16.0, block_size=16)
+    base.update(kw)
+    return ModelConfig(**base)
+
+
+# ---------------------------------------------------------------------------
+# weights
+
+
+def _interleave_gate_up(w_gate, w_up, m_pad):
+    """[h, m] gate/up → [h, 2·m_pad] with 128-column chunks interleaved
+    (gate chunk i, up chunk i, …); padded columns are zero (exact no-ops)."""
+    h, m = w_up.shape
+    out = torch.zeros(h, 2 * m_pad, dtype=w_up.dtype, device=w_up.device)
+    g = torch.zeros(h, m_pad, dtype=w_up.dtype, device=w_up.device)
+    u = torch.zeros_like(g)
+    g[:, :m] = w_gate
+    u[:, :m] = w_up
+    out.view(h, m_pad // 128, 2, 128)[:, :, 0, :] = g.view(h, m_pad // 128, 128)
+    out.view(h, m_pad // 128, 2, 128)[:, :, 1, :] = u.view(h, m_pad // 128, 128)
+    return out
+
+
+def rope_table(max_pos: int, head_dim: int, base: float, device) -> torch.Tensor:
+    """(cos, sin) per (position, frequency) computed in float64 then cast —
+    the table of tensor.py:604-607."""
+    half = head_dim // 2
+    inv_freq = base ** (-np.arange(half, dtype=np.float64) / half)
+    ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv_freq[None, :]
+    tab = np.stack([np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)], axis=-1)
+    return torch.as_tensor(np.ascontiguousarray(tab)).to(device)
+
+
+class LoraAdapter:
+    """Views of one adapter inside the model's flat LoRA buffer (model.py:67-80).
+    a: [h, r] (strided view), b: [r, h]."""
+
+    def __init__(self, a: torch.Tensor, b: torch.Tensor, scaling: float, grad_a, grad_b):
+        self.a = a
+        self.b = b
+        self.rank = a.shape[1]
+        self.scaling = scaling
+        self._ga, self._gb = grad_a, grad_b
+
+    @property
+    def a_grad(self):
+        return self._ga()
+
+    @property
+    def b_grad(self):
+        return self._gb()
+
+    def parameters(self):
+        return [self.a, self.b]
+
+
+class LayerState:
+    """Frozen bf16 weights in GEMM layouts + LoRA views for one layer (model.py:83-130)."""
+
+    def __init__(self, model: "DecoderModel", layer_id: int, arrays: dict):
+        cfg = model.config
+        dev = model.device
+        h, m = cfg.hidden_dim, cfg.mlp_dim
+        self.layer_id = layer_id
+        self.n_heads = cfg.n_heads
+        self.head_dim = cfg.head_dim
+        self.rope = cfg.positions == "rope"
+        self.rope_base = cfg.rope_base
+        self.mlp_variant = cfg.mlp_variant
+        self.relu = cfg.mlp_variant == "relu"
+        self.m = m
+        self.m_pad = cfg.mlp_pad
+        self.rope_tab = model.rope_tab
+
+        def g(name):
+            a = arrays[name]
+            t = a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a))
+            return t.to(device=dev, dtype=F32)
+
+        wq, wk, wv, wo = g("wq"), g("wk"), g("wv"), g("wo")
+        w_qkv = torch.cat([wq, wk, wv], dim=1)  # [h, 3h]   (x·W layout)
+        self.w_qkv = w_qkv.to(BF16).contiguous()
+        self.w_qkv_t = w_qkv.t().contiguous().to(BF16)
+        self.w_o = wo.to(BF16).contiguous()
+        self.w_o_t = wo.t().contiguous().to(BF16)
+        w_up = g("w_up")
+        if self.relu:
+            gu = torch.zeros(h, self.m_pad, device=dev)
+            gu[:, :m] = w_up
+        else:
+            gu = _interleave_gate_up(g("w_gate"), w_up, self.m_pad)
+        self.w_gu = gu.to(BF16).contiguous()
+        self.w_gu_t = gu.t().contiguous().to(BF16)
+        wd = torch.zeros(self.m_pad, h, device=dev)
+        wd[:m] = g("w_down")
+        self.w_down = wd.to(BF16).contiguous()
+        self.w_down_t = wd.t().contiguous().to(BF16)
+        del w_qkv, gu, wd
+        self.attn_norm_w = g("attn_norm").contiguous()
+        self.mlp_norm_w = g("mlp_norm").contiguous()
+        # LoRA: views into the model's flat buffer
+        r = cfg.lora_rank
+        self.lora_rank = r
+        self.lora_scaling = cfg.lora_alpha / r if r else 0.0
+        self.lora_param = model.lora_param
+        self.predictor_q: predictor_mod.Predictor | None = None
+        self.predictor_k: predictor_mod.Predictor | None = None
+        if r:
+            self._off = model._lora_offset(layer_id)
+            A, Bq, Bv = self._views(model.lora_param.data)
+            self.lora_A, self.lora_Bq, self.lora_Bv = A, Bq, Bv
+            self.lora_q = LoraAdapter(A[:, :r], Bq, self.lora_scaling,
+                                      lambda: self._grad("Aq"), lambda: self._grad("Bq"))
+            self.lora_v = LoraAdapter(A[:, r:], Bv, self.lora_scaling,
+                                      lambda: self._grad("Av"), lambda: self._grad("Bv"))
+        else:
+            self.lora_q = self.lora_v = None
+
+    def _views(self, flat):
+        h, r = self.head_dim * self.n_heads, self.lora_rank
+        o = self._off
+        A = flat[o:o + 2 * h * r].view(h, 2 * r)
+        Bq = flat[o + 2 * h * r:o + 3 * h * r].view(r, h)
+        Bv = flat[o + 3 * h * r:o + 4 * h * r].view(r, h)
+        return A, Bq, Bv
+
+    def grad_views(self, flat_grad):
+        return self._views(flat_grad) if self.lora_rank else None
+
+    def _grad(self, which):
+        gr = self.lora_param.grad
+        if gr is None:
+            return None
+        A, Bq, Bv = self._views(gr)
+        r = self.lora_rank
+        return {"Aq": A[:, :r], "Av": A[:, r:], "Bq": Bq, "Bv": Bv}[which]
+
+
+def reference_init_arrays(cfg: ModelConfig, seed: int) -> dict:
+    """Host arrays with the reference's exact draw order (model.py:86-153)."""
+    rng = np.random.default_rng(seed)
+    h, m = cfg.hidden_dim, cfg.mlp_dim
+    std = 1.0 / np.sqrt(h)
+    out = {"embed": (rng.standard_normal((cfg.vocab_size, h)) * std).astype(np.float32)}
+    if cfg.positions == "learned":
+        out["pos_embed"] = (rng.standard_normal((cfg.max_seq_len, h)) * std).astype(np.float32)
+    for i in range(cfg.n_layers):
+        p = f"layer{i}"
+
+        def w(rows, cols):
+            return (rng.standard_normal((rows, cols)) * std).astype(np.float32)
+        out[f"{p}.wq"], out[f"{p}.wk"], out[f"{p}.wv"], out[f"{p}.wo"] = (w(h, h) for _ in range(4))
+        out[f"{p}.attn_norm"] = np.ones(h, np.float32)
+        out[f"{p}.mlp_norm"] = np.ones(h, np.float32)
+        out[f"{p}.w_up"] = w(h, m)
+        out[f"{p}.w_down"] = w(m, h)
+        if cfg.mlp_variant == "silu":
+            out[f"{p}.w_gate"] = w(h, m)
+        if cfg.lora_rank > 0:
+            for tag in ("lora_q", "lora_v"):
+                out[f"{p}.{tag}.a"] = (rng.standard_normal((h, cfg.lora_rank)) /
+                                       np.sqrt(h)).astype(np.float32)
+                out[f"{p}.{tag}.b"] = np.zeros((cfg.lora_rank, h), np.float32)
+    out["final_norm"] = np.ones(h, np.float32)
+    out["lm_head"] = (rng.standard_normal((h, cfg.vocab_size)) * std).astype(np.float32)
+    return out
+
+
+class _TorchInit:
+    """Lazy on-device random init for large models (same distributions as the
+    reference: N(0, 1/h) frozen weights, norms 1, LoRA A ~ N(0, 1/h), B = 0)."""
+
+    def __init__(self, cfg: ModelConfig, seed: int, device):
+        self.cfg, self.dev = cfg, device
+        self.gen = torch.Generator(device=device)
+        self.gen.manual_seed(seed)
+
+    def normal(self, rows, cols, std):
+        return torch.randn(rows, cols, generator=self.gen, device=self.dev) * std
+
+    def layer(self, i):
+        cfg = self.cfg
+        h, m = cfg.hidden_dim, cfg.mlp_dim
+        std = 1.0 / math.sqrt(h)
+        d = {n: self.normal(h, h, std) for n in ("wq", "wk", "wv", "wo")}
+        d["w_up"] = self.normal(h, m, std)
+        d["w_down"] = self.normal(m, h, std)
+        if cfg.mlp_variant == "silu":
+            d["w_gate"] = self.normal(h, m, std)
+        d["attn_norm"] = torch.ones(h, device=self.dev)
+        d["mlp_norm"] = torch.ones(h, device=self.dev)
+        if cfg.lora_rank:
+            for tag in ("lora_q", "lora_v"):
+                d[f"{tag}.a"] = self.normal(h, cfg.lora_rank, std)
+                d[f"{tag}.b"] = torch.zeros(cfg.lora_rank, h, device=self.dev)
+        return d
+
+
+class DecoderModel:
+    """model.py:133-326 on the GPU.
+
+    init="reference": numpy draws in the reference's order (bit-identical
+    weights to sparsetune.DecoderModel(cfg, seed)); init="torch": on-device
+    generator with the same distributions (for 7B-scale benches).
+    """
+
+    def __init__(self, cfg: ModelConfig, seed: int = 0, *, device=None, init: str = "torch",
+                 arrays: dict | None = None):
+        cfg.check_gpu_geometry()
+        self.config = cfg
+        self.seed = seed
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        dev = self.device
+        h, r, L = cfg.hidden_dim, cfg.lora_rank, cfg.n_layers
+        self.rope_tab = rope_table(cfg.max_seq_len, cfg.head_dim, cfg.rope_base, dev) \
+            if cfg.positions == "rope" else None
+        self.lora_param = torch.zeros(max(4 * h * r * L, 1), dtype=F32, device=dev)
+        if arrays is None and init == "reference":
+            arrays = reference_init_arrays(cfg, seed)
+        if arrays is not None:
+            get = lambda n: arrays[n]  # noqa: E731
+            layer_arrays = lambda i: {k.split(".", 1)[1]: v for k, v in arrays.items()  # noqa
+                                      if k.startswith(f"layer{i}.")}
+        else:
+            ti = _TorchInit(cfg, seed, dev)
+            std = 1.0 / math.sqrt(h)
+            glob = {"embed": ti.normal(cfg.vocab_size, h, std)}
+            if cfg.positions == "learned":
+                glob["pos_embed"] = ti.normal(cfg.max_seq_len, h, std)
+            get = glob.__getitem__
+            layer_arrays = ti.layer
+        f32 = lambda a: (a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a))  # noqa
+                         ).to(device=dev, dtype=F32).contiguous()
+        self.embed = f32(get("embed"))
+        self.pos_embed = f32(get("pos_embed")) if cfg.positions == "learned" else None
+        self.layers = []
+        for i in range(L):
+            la = layer_arrays(i)
+            layer = LayerState(self, i, la)
+            if r:
+                for tag, ad in (("lora_q", layer.lora_q), ("lora_v", layer.lora_v)):
+                    ad.a.copy_(f32(la[f"{tag}.a"]))
+                    ad.b.copy_(f32(la[f"{tag}.b"]))
+            self.layers.append(layer)
+            del la
+        if arrays is not None:
+            final, lm = arrays["final_norm"], arrays["lm_head"]
+        else:
+            final = torch.ones(h, device=dev)
+            lm = ti.normal(h, cfg.vocab_size, 1.0 / math.sqrt(h))
+        self.final_norm_w = f32(final)
+        lm = f32(lm)
+        self.lm_head = lm.to(BF16).contiguous()           # [h, V]  (dhidden GEMM)
+        self.lm_head_t = lm.t().contiguous().to(BF16)      # [V, h]  (logits GEMM)
+        del lm
+        self.lora_param.requires_grad_(cfg.lora_rank > 0)
+        self._mlp_scored = {}
+        self.last_stats: dict = {}
+
+    # -- parameters -------------------------------------------------------------
+
+    def _lora_offset(self, layer_id: int) -> int:
+        return 4 * self.config.hidden_dim * self.config.lora_rank * layer_id
+
+    def adapter_parameters(self):
+        out = []
+        for layer in self.layers:
+            for ad in (layer.lora_q, layer.lora_v):
+                if ad is not None:
+                    out.extend(ad.parameters())
+        return out
+
+    def adapter_state(self) -> dict:
+        """name -> host array of every adapter tensor (reference names)."""
+        out = {}
+        for layer in self.layers:
+            for tag, ad in (("lora_q", layer.lora_q), ("lora_v", layer.lora_v)):
+                if ad is not None:
+                    out[f"layer{layer.layer_id}.{tag}.a"] = ad.a.cpu().numpy()
+                    out[f"layer{layer.layer_id}.{tag}.b"] = ad.b.cpu().numpy()
+        return out
+
+    def adapter_grads(self) -> dict:
+        out = {}
+        for layer in self.layers:
+            for tag, ad in (("lora_q", layer.lora_q), ("lora_v", layer.lora_v)):
+                if ad is not None and ad.a_grad is not None:
+                    out[f"layer{layer.layer_id}.{tag}.a"] = ad.a_grad.cpu().numpy()
+                    out[f"layer{layer.layer_id}.{tag}.b"] = ad.b_grad.cpu().numpy()
+        return out
+
+    def load_adapter_state(self, state: dict) -> None:
+        for layer in self.layers:
+            for tag, ad in (("lora_q", layer.lora_q), ("lora_v", layer.lora_v)):
+                if ad is None:
+                    continue
+                for ab, t in (("a", ad.a), ("b", ad.b)):
+                    key = f"layer{layer.layer_id}.{tag}.{ab}"
+                    if key in state:
+                        t.copy_(torch.as_tensor(np.asarray(state[key], np.float32)))
+
+    def attach_predictors(self, pairs: dict) -> None:
+        for layer_id, (p_q, p_k) in pairs.items():
+            self.layers[layer_id].predictor_q = p_q
+            self.layers[layer_id].predictor_k = p_k
+
+    # -- padding ------------------------------------------------------------------
+
+    def pad_tokens(self, tokens, targets):
+        """model.py:218-236 (host)."""
+        tokens = np.asarray(tokens, dtype=np.int64)
+        n = tokens.shape[0]
+        if n == 0:
+            raise ContractError("empty token sequence")
+        if n > self.config.max_seq_len:
+            raise ContractError(f"sequence length {n} exceeds max {self.config.max_seq_len}")
+        if targets is None:
+            targets = np.concatenate([tokens[1:], [IGNORE_INDEX]])
+        else:
+            targets = np.asarray(targets, dtype=np.int64)
+            if targets.shape != tokens.shape:
+                raise ContractError("targets must match token count")
+        b = self.config.block_size
+        n_pad = -(-n // b) * b
+        if n_pad > n:
+            tokens = np.concatenate([tokens, np.full(n_pad - n, PAD_TOKEN, dtype=np.int64)])
+            targets = np.concatenate([targets, np.full(n_pad - n, IGNORE_INDEX, dtype=np.int64)])
+        return tokens, targets, n
+
+    # -- forward --------------------------------------------------------------------
+
+    def forward_step(self, tokens, targets=None, *, pattern_source=None, segments: int = 1,
+                     fused: bool = True, fuse_projections: bool = True):
+        """model.py:246-297.  Returns (loss, hidden): loss is a CUDA scalar whose
+        backward() runs the sparse backward sweep into lora_param.grad;
+        hidden is the final normalised hidden state (bf16)."""
+        step = _Step(self, tokens, targets, pattern_source, segments)
+        if torch.is_grad_enabled():
+            loss = _StepFn.apply(self.lora_param, step)
+        else:
+            with torch.no_grad():
+                loss = step.forward(need_grad=False)
+        return loss, step.hidden
+
+    @staticmethod
+    def _plan_from(pattern, n_pad: int, device) -> kernels.GatherPlan:
+        if pattern is None:
+            return kernels.GatherPlan.full(n_pad, device)
+        return kernels.GatherPlan.from_pattern(pattern, n_pad, device)
+
+
+class _Step:
+    """Saved state of one training step (the reference's tape, compacted)."""
+
+    def __init__(self, model: DecoderModel, tokens, targets, source, segments):
+        self.model = model
+        self.source = source
+        ids, tgts, n_valid = model.pad_tokens(tokens, targets)
+        cfg = model.config
+        if ids.min() < 0 or ids.max() >= cfg.vocab_size:
+            raise IndexError(f"token id out of range [0, {cfg.vocab_size}): min={ids.min()}, "
+                             f"max={ids.max()}")
+        self.count = kernels.check_targets(tgts, cfg.vocab_size, IGNORE_INDEX)
+        if self.count == 0:
+            raise ContractError("segmented loss: no valid targets")
+        self.n_valid = n_valid
+        self.n_pad = len(ids)
+        self.segments = max(1, segments)
+        dev = model.device
+        host = torch.empty(2, self.n_pad, dtype=torch.int32, pin_memory=True)
+        host[0].copy_(torch.from_numpy(ids.astype(np.int32)))
+        host[1].copy_(torch.from_numpy(tgts.astype(np.int32)))
+        both = host.to(dev, non_blocking=True)
+        self.ids, self.tgts = both[0], both[1]
+        self.h2d_bytes = host.numel() * 4
+        self.hidden = None
+
+    def forward(self, need_grad: bool = True):
+        m = self.model
+        cfg = m.config
+        dev = m.device
+        mem0 = torch.cuda.memory_allocated(dev)
+        x = ops.embed(self.ids, m.embed,
+                      m.pos_embed[: self.n_pad].contiguous() if m.pos_embed is not None else None)
+        saved = []
+        src = self.source
+        for layer in m.layers:
+            pat = src.pattern(layer.layer_id, sparsity.ATTENTION, x, self.n_valid) \
+                if src is not None else None
+            plan = DecoderModel._plan_from(pat, self.n_pad, dev)
+            sa = kernels.attention_forward(x, plan, layer, save=need_grad)
+            pat = src.pattern(layer.layer_id, sparsity.MLP, x, self.n_valid) \
+                if src is not None else None
+            plan = DecoderModel._plan_from(pat, self.n_pad, dev)
+            scored = m._mlp_scored.pop(layer.layer_id, None)
+            sm = kernels.mlp_forward(x, plan, layer, scored=scored, save=need_grad)
+            del scored
+            saved.append((sa, sm))
+        inv_f = torch.empty(self.n_pad, dtype=F32, device=dev)
+        hidden = ops.rmsnorm_gather(x, m.final_norm_w, None, inv=inv_f)
+        plan = kernels.SegmentPlan.even(self.n_pad, self.segments)
+        loss, grad_hidden = kernels.segmented_loss_forward(
+            hidden, m.lm_head_t, m.lm_head, self.tgts, self.count, plan, IGNORE_INDEX,
+            need_grad=need_grad)
+        self.hidden = hidden
+        # post_forward mark (model.py:296): activation bytes = everything still
+        # allocated by this step that backward needs
+        mark = torch.cuda.memory_allocated(dev)
+        m.last_stats = {"activation_bytes_post_forward": mark - mem0,
+                        "retained": dict(src.last_fractions) if src is not None else {}}
+        if need_grad:
+            self.saved, self.x, self.inv_f, self.grad_hidden = saved, x, inv_f, grad_hidden
+        return loss.to(F32).reshape(())
+
+    def backward(self, g: torch.Tensor) -> torch.Tensor:
+        m = self.model
+        gval = float(g.item()) if isinstance(g, torch.Tensor) else float(g)
+        grad = torch.zeros_like(m.lora_param)
+        dx = torch.empty_like(self.x)
+        ops.rmsnorm_bwd(self.grad_hidden, self.x, self.inv_f, m.final_norm_w, dx, None,
+                        gscale=gval, accumulate=False)
+        self.grad_hidden = self.x = self.inv_f = None
+        for layer, (sa, sm) in zip(reversed(m.layers), reversed(self.saved)):
+            if sm is not None:
+                kernels.mlp_backward(dx, sm, layer)
+            if sa is not None:
+                kernels.attention_backward(dx, sa, layer, layer.grad_views(grad))
+            self.saved.pop()
+        self.saved = None
+        return grad
+
+
+class _StepFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, lora_param, step):
+        ctx.step = step
+        return step.forward(need_grad=True)
+
+    @staticmethod
+    def backward(ctx, g):
+        step = ctx.step
+        ctx.step = None
+        return step.backward(g), None
+
+
+# ---------------------------------------------------------------------------
+# scoring helpers (model.py:356-396)
+
+
+def mlp_block_score_vector(layer: LayerState, x: torch.Tensor, block_size: int, n_valid: int,
+                           *, keep_rows: bool = False):
+    """Exact MLP block scores (model.py:371-396): RMSNorm of every row, the
+    tcgen05 gate/up GEMM with |silu(g)·u| row sums in its epilogue, then
+    mean/max per block.  With keep_rows=True also returns (gu_all, inv_all)
+    so the sparse MLP can compact retained rows instead of recomputing."""
+    s, h = x.shape
+    dev = x.device
+    N = layer.w_gu_t.shape[0]
+    inv_all = torch.empty(s, dtype=F32, device=dev)
+    xn_all = ops.rmsnorm_gather(x, layer.mlp_norm_w, None, inv=inv_all)
+    gu_all = torch.empty(s, N, dtype=BF16, device=dev) if keep_rows else None
+    partial = torch.empty(N // 256, s, dtype=F32, device=dev)
+    ops.gemm_gateup(xn_all, layer.w_gu_t, gu=gu_all, partial=partial, relu=layer.relu)
+    del xn_all
+    vec = ops.mlp_block_scores(partial, s=s, n_valid=n_valid, b=block_size, m_real=layer.m)
+    if keep_rows:
+        return vec, (gu_all, inv_all)
+    return vec
+
+
+def layer_qk(layer: LayerState, x: torch.Tensor):
+    """model.py:356-368: post-rotation Q (with LoRA) and K (without), [s, h] bf16."""
+    s, h = x.shape
+    r = layer.lora_rank
+    t = torch.empty(s, 2 * r, dtype=F32, device=x.device) if r else None
+    xn = ops.rmsnorm_gather(x, layer.attn_norm_w, None, A=layer.lora_A if r else None, r=r, t=t)
+    pos = torch.arange(s, dtype=torch.int32, device=x.device)
+    q, k = ops.gemm_qkv(xn, layer.w_qkv_t, h=h, head_dim=layer.head_dim, rope=layer.rope,
+                        rope_tab=layer.rope_tab, pos=pos, t=t, r=r,
+                        Bq=layer.lora_Bq if r else None, Bv=None, scale=layer.lora_scaling,
+                        nmat=2)
+    return q, k
+
+
+# ---------------------------------------------------------------------------
+# pattern sources (model.py:403-590)
+
+
+class PatternSourceBase:
+    """Interleaves scoring with the layer loop; records retained fractions."""
+
+    def __init__(self):
+        self.last_fractions: dict = {}
+
+    def pattern(self, layer_id, component, x, n_valid):
+        raise NotImplementedError
+
+    def _note(self, layer_id, component, pattern):
+        self.last_fractions[(layer_id, component)] = (
+            1.0 if pattern is None else pattern.retained_fraction)
+        return pattern
+
+
+class AllRetainSource(PatternSourceBase):
+    def pattern(self, layer_id, component, x, n_valid):
+        return self._note(layer_id, component, None)
+
+
+class FixedPatternSource(PatternSourceBase):
+    """Serves pre-built patterns keyed by (layer, component)."""
+
+    def __init__(self, patterns: dict):
+        super().__init__()
+        self.patterns = patterns
+
+    def pattern(self, layer_id, component, x, n_valid):
+        return self._note(layer_id, component, self.patterns.get((layer_id, component)))
+
+
+class FractionSource(PatternSourceBase):
+    """Evenly spaced fraction of blocks (model.py:437-451)."""
+
+    def __init__(self, fraction: float, block_size: int):
+        super().__init__()
+        self.fraction = fraction
+        self.block_size = block_size
+
+    def pattern(self, layer_id, component, x, n_valid):
+        s = x.shape[0]
+        nb = sparsity.n_blocks_for(s, self.block_size)
+        keep = max(1, int(round(nb * self.fraction)))
+        blocks = tuple(np.unique(np.linspace(0, nb - 1, keep).round().astype(int)).tolist())
+        return self._note(layer_id, component,
+                          sparsity.SparsityPattern(layer_id, component, blocks, self.block_size, s))
+
+
+class PredictedPatternSource(PatternSourceBase):
+    """model.py:516-590 on the GPU: attention blocks from the predictor pair
+    (fused block-pool → predictors → Eq. 3 → clamp → column sums), optional
+    periodic re-derivation of the threshold as an order statistic over the
+    last `history` score vectors (radix select), MLP blocks from the exact
+    fused MLP scorer; selection by the liblemo select kernel."""
+
+    def __init__(self, model: DecoderModel, pred_thresholds: sparsity.ThresholdSet, *,
+                 mlp_scoring: bool = True, sink_first_block: bool = False, pooling: str = "mean",
+                 target_retention: dict | None = None, recalibrate_every: int = 0,
+                 history: int = 8, record: bool = False):
+        super().__init__()
+        self.model = model
+        self.thresholds = pred_thresholds
+        self.mlp_scoring = mlp_scoring
+        self.sink_first_block = sink_first_block
+        self.pooling = pooling
+        self.target_retention = target_retention or {}
+        self.recalibrate_every = recalibrate_every
+        self.history = history
+        self.record = record
+        self.recorded_vectors: dict = {}
+        self._recent: dict = {}
+        self._calls: dict = {}
+
+    def _maybe_recalibrate(self, layer_id, vec):
+        """model.py:545-563; returns a device threshold or None."""
+        if not self.recalibrate_every or layer_id not in self.target_retention:
+            return None
+        recent = self._recent.setdefault(layer_id, [])
+        recent.append(vec)
+        if len(recent) > self.history:
+            recent.pop(0)
+        self._calls[layer_id] = self._calls.get(layer_id, 0) + 1
+        if self._calls[layer_id] % self.recalibrate_every != 0:
+            return None
+        retained = min(max(self.target_retention[layer_id], 0.0), 1.0)
+        out = torch.empty(1, dtype=torch.float64, device=vec.device)
+        if retained >= 1.0:
+            out.fill_(float("-inf"))
+            return out
+        pooled = torch.cat(recent) if len(recent) > 1 else recent[0]
+        if retained <= 0.0:
+            return ops.quantile_lower(pooled, 1.0, out, plus_one=True)
+        return ops.quantile_lower(pooled, 1.0 - retained, out)
+
+    def pattern(self, layer_id, component, x, n_valid):
+        b = self.model.config.block_size
+        layer = self.model.layers[layer_id]
+        thr_dev = None
+        if component == sparsity.ATTENTION:
+            if layer.predictor_q is None or layer.predictor_k is None:
+                raise ContractError(f"layer {layer_id} has no attached predictors")
+            vec = predictor_mod.predicted_block_vector(layer.predictor_q, layer.predictor_k, x, b,
+                                                       self.pooling)
+            thr_dev = self._maybe_recalibrate(layer_id, vec)
+            thr = None if thr_dev is not None else self.thresholds.get(layer_id, component)
+        else:
+            if not self.mlp_scoring:
+                return self._note(layer_id, component, None)
+            vec, rows = mlp_block_score_vector(layer, x, b, n_valid, keep_rows=True)
+            self.model._mlp_scored[layer_id] = rows
+            thr = self.thresholds.get(layer_id, component)
+        if self.record:
+            self.recorded_vectors.setdefault((layer_id, component), []).append(vec)
+        force = (0,) if self.sink_first_block else ()
+        pat, used = sparsity.select_device(vec, thr, thr_dev=thr_dev, layer_id=layer_id,
+                                           component=component, block_size=b,
+                                           n_tokens=x.shape[0], force_blocks=force)
+        if thr_dev is not None:
+            self.thresholds.set(layer_id, sparsity.ATTENTION, used)
+        return self._note(layer_id, component, pat)
+
+
+class ExactPatternSource(PatternSourceBase):
+    """model.py:454-513: exact attention scores from the layer's actual Q/K
+    (tcgen05 projections + fused exact block scorer) and exact MLP scores;
+    thresholds=None profiles only (retain all)."""
+
+    def __init__(self, model: DecoderModel, thresholds: sparsity.ThresholdSet | None, *,
+                 mlp_scoring: bool = True, sink_first_block: bool = False, record: bool = False):
+        super().__init__()
+        self.model = model
+        self.thresholds = thresholds
+        self.mlp_scoring = mlp_scoring
+        self.sink_first_block = sink_first_block
+        self.record = record
+        self.recorded_vectors: dict = {}
+
+    def pattern(self, layer_id, component, x, n_valid):
+        from . import exact  # noqa: WPS433 (kernel module)
+
+        b = self.model.config.block_size
+        layer = self.model.layers[layer_id]
+        if component == sparsity.ATTENTION:
+            q, k = layer_qk(layer, x)
+            vec = exact.exact_block_vector(q, k, b, n_heads=layer.n_heads, n_valid=n_valid)
+        else:
+            if not self.mlp_scoring:
+                return self._note(layer_id, component, None)
+            keep = self.thresholds is not None
+            res = mlp_block_score_vector(layer, x, b, n_valid, keep_rows=keep)
+            if keep:
+                vec, rows = res
+                self.model._mlp_scored[layer_id] = rows
+            else:
+                vec = res
+        if self.record:
+            self.recorded_vectors.setdefault((layer_id, component), []).append(vec)
+        if self.thresholds is None:
+            return self._note(layer_id, component, None)
+        force = (0,) if self.sink_first_block else ()
+        pat, _ = sparsity.select_device(vec, self.thresholds.get(layer_id, component),
+                                        layer_id=layer_id, component=component, block_size=b,
+                                        n_tokens=x.shape[0], force_blocks=force)
+        return self._note(layer_id, component, pat)

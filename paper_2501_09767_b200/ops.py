@@ -1,11 +1,14 @@
-"""Thin torch-tensor wrappers over the liblemo C ABI.
+"""Thin torch-tensor wrappers over the liblemo C ABI (include/lemo.h).
 
-Each wrapper validates shapes/dtypes/devices on the host (raising the
-reference's exception types), then calls the corresponding ``lemo_*`` entry
-point on torch's current stream.  No wrapper has a non-CUDA path.
+Each wrapper checks devices/dtypes/shapes on the host (raising the
+reference's exception types) and calls the corresponding ``lemo_*`` entry
+point on torch's current stream.  There is no non-CUDA path: a CPU tensor is
+a ContractError and a missing library is a LemoError.
 """
 
 from __future__ import annotations
+
+import math
 
 import torch
 
@@ -14,18 +17,16 @@ from .errors import ContractError, DimensionError
 
 BF16 = torch.bfloat16
 F32 = torch.float32
+F64 = torch.float64
+I32 = torch.int32
 
 
-def _cuda(*ts):
+def _check(*ts):
     for t in ts:
-        if t is not None and not t.is_cuda:
-            raise ContractError("liblemo operands must be CUDA tensors (no CPU fallback)")
-
-
-def _contig(*ts):
-    for t in ts:
-        if t is not None and not t.is_contiguous():
-            raise ContractError("liblemo operands must be contiguous")
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise ContractError("liblemo operands must be CUDA tensors (there is no CPU path)")
 
 
 def _dt(t, dtype, name):
@@ -33,53 +34,291 @@ def _dt(t, dtype, name):
         raise ContractError(f"{name} must be {dtype}, got {t.dtype}")
 
 
+def _rowmajor(t, name):
+    if t is not None and (t.dim() != 2 or t.stride(1) != 1):
+        raise ContractError(f"{name} must be a row-major 2-D tensor")
+
+
+def _s():
+    return stream_ptr()
+
+
 # ---------------------------------------------------------------------------
-# GEMMs  (C = A · Bᵀ, B given as [N, K])
+# tcgen05 GEMMs   C = A · Bᵀ  (B given as [N, K])
 
 
-def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-    _cuda(a, b)
-    _dt(a, BF16, "a")
-    _dt(b, BF16, "b")
+def _mnk(a, b):
+    _check(a, b)
+    _dt(a, BF16, "A")
+    _dt(b, BF16, "B")
+    _rowmajor(a, "A")
+    _rowmajor(b, "B")
     M, K = a.shape
     N, K2 = b.shape
     if K != K2:
-        raise DimensionError(f"gemm inner extents differ: {tuple(a.shape)} vs {tuple(b.shape)}")
+        raise DimensionError(f"matmul inner extents differ: {tuple(a.shape)} vs {tuple(b.shape)}")
+    return M, N, K
+
+
+def gemm_bf16(a, b, out=None):
+    M, N, K = _mnk(a, b)
     if out is None:
         out = torch.empty(M, N, dtype=BF16, device=a.device)
-    call("lemo_gemm_bf16", ptr(a), a.stride(0), ptr(b), b.stride(0), ptr(out), out.stride(0),
-         M, N, K, stream_ptr())
+    call("lemo_gemm_bf16", ptr(a), a.stride(0), ptr(b), b.stride(0), ptr(out), out.stride(0), M, N,
+         K, _s())
     return out
 
 
 def gemm_f32(a, b, out=None, *, side_u=None, side_s=None, side_strides=(0, 0), scale=1.0,
              accumulate=False):
-    """out (+)= a·bᵀ + scale·side_u·S, S(j, col) = side_s[j*s_rs + col*s_cs]."""
-    _cuda(a, b, out, side_u, side_s)
-    _dt(a, BF16, "a")
-    _dt(b, BF16, "b")
-    M, K = a.shape
-    N, K2 = b.shape
-    if K != K2:
-        raise DimensionError(f"gemm inner extents differ: {tuple(a.shape)} vs {tuple(b.shape)}")
+    """out (+)= a·bᵀ + scale·side_u·S with S(j, col) = side_s[j*s_rs + col*s_cs]."""
+    M, N, K = _mnk(a, b)
+    _check(out, side_u, side_s)
     if out is None:
         out = torch.empty(M, N, dtype=F32, device=a.device)
     R = 0 if side_u is None else side_u.shape[1]
     ldu = 0 if side_u is None else side_u.stride(0)
     call("lemo_gemm_f32", ptr(a), a.stride(0), ptr(b), b.stride(0), ptr(out), out.stride(0), M, N,
          K, ptr(side_u), ldu, R, ptr(side_s), int(side_strides[0]), int(side_strides[1]),
-         float(scale), int(bool(accumulate)), stream_ptr())
+         float(scale), int(bool(accumulate)), _s())
     return out
 
 
 def gemm_scatter_add(a, b, resid, idx=None):
-    """resid[idx] += a·bᵀ (in place)."""
-    _cuda(a, b, resid, idx)
+    """resid[idx] += a·bᵀ in place (idx None = identity rows)."""
+    M, N, K = _mnk(a, b)
+    _check(resid, idx)
     _dt(resid, F32, "resid")
-    M, K = a.shape
-    N = b.shape[0]
     if idx is not None and idx.shape[0] != M:
         raise DimensionError("scatter index length must equal the GEMM row count")
     call("lemo_gemm_scatter_add", ptr(a), a.stride(0), ptr(b), b.stride(0), ptr(resid),
-         resid.stride(0), ptr(idx), M, N, K, stream_ptr())
+         resid.stride(0), ptr(idx), M, N, K, _s())
     return resid
+
+
+def gemm_qkv(xn, w_qkv_t, *, h, head_dim, rope, rope_tab, pos, t=None, r=0, Bq=None, Bv=None,
+             scale=1.0, nmat=3, out=None):
+    """q, k(, v) = rope(xn·W (+LoRA)) at positions pos — see lemo_gemm_qkv."""
+    M = xn.shape[0]
+    _check(xn, w_qkv_t, pos, t, Bq, Bv)
+    if out is None:
+        out = [torch.empty(M, h, dtype=BF16, device=xn.device) for _ in range(nmat)]
+    q, k = out[0], out[1]
+    v = out[2] if nmat == 3 else None
+    tq = t
+    tv = None if t is None else t[:, r:]
+    call("lemo_gemm_qkv", ptr(xn), ptr(w_qkv_t), M, h, nmat, ptr(q), ptr(k), ptr(v), head_dim,
+         int(bool(rope)), ptr(rope_tab), ptr(pos), ptr(tq), ptr(tv),
+         0 if t is None else t.stride(0), r if t is not None else 0, ptr(Bq), ptr(Bv),
+         float(scale), _s())
+    return out
+
+
+def gemm_gateup(xn, w_gu_t, *, gu=None, inner=None, partial=None, relu=False):
+    M, K = xn.shape
+    N = w_gu_t.shape[0]
+    _check(xn, w_gu_t, gu, inner, partial)
+    call("lemo_gemm_gateup", ptr(xn), xn.stride(0), ptr(w_gu_t), M, N, K, ptr(gu), ptr(inner),
+         ptr(partial), int(bool(relu)), _s())
+
+
+def gemm_dgateup(dy, w_down, gu, dgu, *, m_pad, relu=False):
+    M, h = dy.shape
+    _check(dy, w_down, gu, dgu)
+    call("lemo_gemm_dgateup", ptr(dy), ptr(w_down), M, m_pad, h, ptr(gu), ptr(dgu),
+         int(bool(relu)), _s())
+
+
+# ---------------------------------------------------------------------------
+# row kernels
+
+
+def rmsnorm_gather(x, w, idx=None, *, xn=None, xg=None, inv=None, A=None, r=0, t=None):
+    """Fused gather + RMSNorm (+LoRA factors t = xn·[A0|A1], A = [h, 2r] interleaved)."""
+    _check(x, w, idx, A, t)
+    _dt(x, F32, "x")
+    M = x.shape[0] if idx is None else idx.shape[0]
+    h = x.shape[1]
+    if xn is None:
+        xn = torch.empty(M, h, dtype=BF16, device=x.device)
+    A0 = A1 = None
+    lda = 0
+    if A is not None:
+        A0 = A
+        A1 = A[:, r:]
+        lda = A.stride(0)
+    call("lemo_rmsnorm_gather", ptr(x), x.stride(0), ptr(idx), M, h, ptr(w), ptr(xn), ptr(xg),
+         ptr(inv), ptr(A0), ptr(A1), lda, r, ptr(t), 0 if t is None else t.stride(0), _s())
+    return xn
+
+
+def gather_rows_bf16(src, idx, out=None):
+    _check(src, idx)
+    M = src.shape[0] if idx is None else idx.shape[0]
+    h = src.shape[1]
+    if out is None:
+        out = torch.empty(M, h, dtype=BF16, device=src.device)
+    call("lemo_gather_rows_bf16", ptr(src), src.stride(0), ptr(idx), M, h, ptr(out), _s())
+    return out
+
+
+def rmsnorm_bwd(g, x, inv, w, dx, idx=None, *, gscale=1.0, accumulate=True):
+    _check(g, x, inv, w, dx, idx)
+    M, h = g.shape
+    call("lemo_rmsnorm_bwd", ptr(g), g.stride(0), ptr(x), int(x.dtype == BF16), x.stride(0),
+         ptr(inv), ptr(w), ptr(idx), M, h, float(gscale), ptr(dx), dx.stride(0),
+         int(bool(accumulate)), _s())
+    return dx
+
+
+def embed(ids, table, pos_table=None, out=None):
+    _check(ids, table, pos_table)
+    n = ids.shape[0]
+    h = table.shape[1]
+    if out is None:
+        out = torch.empty(n, h, dtype=F32, device=table.device)
+    call("lemo_embed", ptr(ids), n, ptr(table), h, ptr(pos_table), ptr(out), _s())
+    return out
+
+
+def mlp_compact(gu_all, x, inv_all, idx, *, m_pad, relu, gu_out, inner_out, xg_out, inv_out):
+    _check(gu_all, x, inv_all, idx, gu_out, inner_out, xg_out, inv_out)
+    M = idx.shape[0]
+    h = x.shape[1]
+    call("lemo_mlp_compact", ptr(gu_all), ptr(x), x.stride(0), ptr(inv_all), ptr(idx), M, h, m_pad,
+         int(bool(relu)), ptr(gu_out), ptr(inner_out), ptr(xg_out), ptr(inv_out), _s())
+
+
+def qkv_grad_prep(dq, dk, dv, *, head_dim, rope, rope_tab, pos, Bq, Bv, r, dqkv, u):
+    _check(dq, dk, dv, rope_tab, pos, Bq, Bv, dqkv, u)
+    M, h = dq.shape
+    call("lemo_qkv_grad_prep", ptr(dq), ptr(dk), ptr(dv), M, h, head_dim, int(bool(rope)),
+         ptr(rope_tab), ptr(pos), ptr(Bq), ptr(Bv), r, ptr(dqkv), ptr(u),
+         0 if u is None else u.stride(0), _s())
+
+
+def lora_grads(xg, inv, w, t, u, g0, g1, *, r, scale, dA, dB0, dB1):
+    """dA (= [h, 2r] interleaved q|v), dB0, dB1 accumulated in place."""
+    _check(xg, inv, w, t, u, g0, g1, dA, dB0, dB1)
+    M, h = xg.shape
+    call("lemo_lora_grads", ptr(xg), ptr(inv), ptr(w), ptr(t), ptr(u), t.stride(0), ptr(g0),
+         ptr(g1), M, h, r, float(scale), dA.stride(0), ptr(dA), ptr(dB0), ptr(dA[:, r:]),
+         ptr(dB1), _s())
+
+
+def ce_rows(logits, targets, *, V, ignore, inv_count, dlogits, row_loss, bad):
+    _check(logits, targets, dlogits, row_loss, bad)
+    n = logits.shape[0]
+    call("lemo_ce_rows", ptr(logits), logits.stride(0), ptr(targets), n, V, ignore,
+         float(inv_count), ptr(dlogits), dlogits.stride(0), ptr(row_loss), ptr(bad), _s())
+
+
+def sum_f64(x, out, accumulate=False):
+    _check(x, out)
+    call("lemo_sum_f64", ptr(x), x.numel(), ptr(out), int(bool(accumulate)), _s())
+    return out
+
+
+def adam(p, g, m, v, *, lr, b1, b2, eps, wd, bc1, bc2):
+    _check(p, g, m, v)
+    call("lemo_adam", ptr(p), ptr(g), ptr(m), ptr(v), p.numel(), float(lr), float(b1), float(b2),
+         float(eps), float(wd), float(bc1), float(bc2), _s())
+
+
+# ---------------------------------------------------------------------------
+# scoring / selection
+
+
+def block_embed(x, b, out=None):
+    _check(x)
+    _dt(x, F32, "x")
+    s, h = x.shape
+    if s % b != 0:
+        raise ContractError(f"sequence length {s} not a multiple of block size {b}")
+    if out is None:
+        out = torch.empty(s // b, h, dtype=F32, device=x.device)
+    call("lemo_block_embed", ptr(x), x.stride(0), s, h, b, ptr(out), _s())
+    return out
+
+
+def sgemm(a, b, *, b_trans=False, relu=False, col_mask=None, out=None):
+    """fp32 C = act(a·op(b))·col_mask; op(b) = b ([K,N]) or bᵀ (b is [N,K])."""
+    _check(a, b, col_mask, out)
+    _dt(a, F32, "a")
+    _dt(b, F32, "b")
+    M, K = a.shape
+    N = b.shape[0] if b_trans else b.shape[1]
+    Kb = b.shape[1] if b_trans else b.shape[0]
+    if K != Kb:
+        raise DimensionError(f"matmul inner extents differ: {tuple(a.shape)} vs {tuple(b.shape)}")
+    if out is None:
+        out = torch.empty(M, N, dtype=F32, device=a.device)
+    call("lemo_sgemm", ptr(a), a.stride(0), ptr(b), b.stride(0), int(bool(b_trans)), ptr(out),
+         out.stride(0), M, N, K, int(bool(relu)), ptr(col_mask), _s())
+    return out
+
+
+def colsum_clamped(S, out=None):
+    _check(S)
+    nb = S.shape[0]
+    if out is None:
+        out = torch.empty(nb, dtype=F64, device=S.device)
+    call("lemo_colsum_clamped", ptr(S), S.stride(0), nb, ptr(out), _s())
+    return out
+
+
+def mlp_block_scores(partial, *, s, n_valid, b, m_real, out=None):
+    _check(partial)
+    nb = -(-s // b)
+    if out is None:
+        out = torch.empty(nb, dtype=F64, device=partial.device)
+    call("lemo_mlp_block_scores", ptr(partial), partial.shape[0], s, n_valid, b, m_real, ptr(out),
+         _s())
+    return out
+
+
+def select(vec, *, b, n_tokens, thr=0.0, thr_dev=None, force=None, mask, blocks, tokens, counts,
+           thr_out=None):
+    _check(vec, thr_dev, force, mask, blocks, tokens, counts, thr_out)
+    _dt(vec, F64, "scores")
+    nb = vec.shape[0]
+    call("lemo_select", ptr(vec), nb, float(thr), ptr(thr_dev), ptr(force), b, n_tokens, ptr(mask),
+         ptr(blocks), ptr(tokens), ptr(counts), ptr(thr_out), _s())
+
+
+def quantile_lower(data, q, out, *, plus_one=False):
+    """out = np.quantile(data, q, method='lower') (rank computed exactly like numpy)."""
+    _check(data, out)
+    n = data.numel()
+    rank = n - 1 if plus_one else int(math.floor((n - 1) * q))
+    call("lemo_quantile_lower", ptr(data), n, rank, int(bool(plus_one)), ptr(out), _s())
+    return out
+
+
+# ---------------------------------------------------------------------------
+# attention
+
+
+def flash_fwd(q, k, v, *, head_dim, scale, o=None, lse=None):
+    _check(q, k, v)
+    n, h = q.shape
+    if o is None:
+        o = torch.empty(n, h, dtype=BF16, device=q.device)
+    if lse is None:
+        lse = torch.empty(h // head_dim, n, dtype=F32, device=q.device)
+    call("lemo_flash_fwd", ptr(q), ptr(k), ptr(v), ptr(o), ptr(lse), n, h, head_dim, float(scale),
+         _s())
+    return o, lse
+
+
+def flash_bwd(q, k, v, o, dout, lse, *, head_dim, scale, dq=None, dk=None, dv=None):
+    _check(q, k, v, o, dout, lse)
+    n, h = q.shape
+    dev = q.device
+    delta = torch.empty(h // head_dim, n, dtype=F32, device=dev)
+    dq = torch.empty(n, h, dtype=F32, device=dev) if dq is None else dq
+    dk = torch.empty(n, h, dtype=F32, device=dev) if dk is None else dk
+    dv = torch.empty(n, h, dtype=F32, device=dev) if dv is None else dv
+    call("lemo_flash_bwd", ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(delta), ptr(dq),
+         ptr(dk), ptr(dv), n, h, head_dim, float(scale), _s())
+    return dq, dk, dv

@@ -1,0 +1,295 @@
+"""Per-kernel parity of liblemo against the oracle / a plain fp32 torch reference."""
+
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lemo_oracle as O
+from paper_2501_09767_b200 import ops, predictor as P, sparsity as S
+from paper_2501_09767_b200.model import DecoderModel, ModelConfig, mlp_block_score_vector, layer_qk
+from paper_2501_09767_b200 import exact
+
+pytestmark = pytest.mark.gpu
+G = Path(__file__).resolve().parent / "golden"
+
+
+def _split(flat, lens):
+    out, o = [], 0
+    for n in lens:
+        out.append(flat[o:o + n])
+        o += n
+    return out
+
+
+# ------------------------------------------------------------------ selection
+
+
+def test_select_bit_exact_on_reference_scores(cuda):
+    """Given the reference's own score vectors and thresholds, retained blocks
+    and token indices are bit-identical (sparsity.py:263-281, 95-104)."""
+    z = np.load(G / "select.npz")
+    vecs = _split(z["vec"], z["vec_len"])
+    masks = _split(z["mask"], z["vec_len"])
+    toks = _split(z["tok"], z["tok_len"])
+    for v, thr, sink, n, b, m, t in zip(vecs, z["thr"], z["sink"], z["n_tokens"], z["block"],
+                                        masks, toks):
+        pat = S.eliminate(v, float(thr), block_size=int(b), n_tokens=int(n),
+                          force_blocks=(0,) if sink else ())
+        assert pat.retained_blocks == tuple(np.nonzero(m)[0].tolist())
+        np.testing.assert_array_equal(pat.token_indices, t)
+        assert pat.k == len(t)
+
+
+def test_select_rejects_nonfinite(cuda):
+    from paper_2501_09767_b200.errors import ContractError
+    with pytest.raises(ContractError):
+        S.eliminate(np.array([1.0, np.nan, 2.0]), 0.5, block_size=4, n_tokens=12)
+    with pytest.raises(ContractError):
+        S.eliminate(np.array([1.0, np.inf]), 0.5, block_size=4, n_tokens=8)
+
+
+def test_select_large_random(cuda):
+    rng = np.random.default_rng(3)
+    for nb in (1, 1023, 1024, 1025, 4096, 5000):
+        v = rng.integers(0, 50, nb).astype(np.float64) * 0.25
+        thr = float(np.quantile(v, 0.5, method="lower"))
+        pat = S.eliminate(v, thr, block_size=16, n_tokens=nb * 16 - 5)
+        assert pat.retained_blocks == O.eliminate(v, thr)
+        np.testing.assert_array_equal(pat.token_indices,
+                                      O.token_indices(O.eliminate(v, thr), 16, nb * 16 - 5))
+
+
+def test_quantile_recalibration_bit_exact(cuda):
+    z = np.load(G / "quantile.npz")
+    flat, o = z["vecs"], 0
+    for nb, thr_seq, ret in zip(z["nb"], z["thr"], z["ret"]):
+        recent = []
+        for call in range(len(thr_seq)):
+            v = flat[o:o + nb]
+            o += nb
+            recent.append(v)
+            recent = recent[-8:]
+            got = P.quantile_threshold(torch.as_tensor(np.concatenate(recent)).cuda(), float(ret))
+            assert got == thr_seq[call] or (np.isinf(got) and np.isinf(thr_seq[call]))
+
+
+def test_colsum_golden(cuda):
+    z = np.load(G / "colsum.npz")
+    nbs = list(z["nb"])
+    for nb, p, v in zip(nbs, _split(z["packed"], [O.tri_size(n) for n in nbs]), _split(z["vec"], nbs)):
+        d = np.zeros((nb, nb), np.float32)
+        r, c = np.tril_indices(nb)
+        d[r, c] = p
+        got = ops.colsum_clamped(torch.as_tensor(d).cuda()).cpu().numpy()
+        np.testing.assert_array_equal(got, v)  # same f64 order: bitwise
+
+
+# ------------------------------------------------------------------ predictor
+
+
+def test_block_embed_bitwise(cuda):
+    z = np.load(G / "predictor.npz")
+    got = ops.block_embed(torch.as_tensor(z["x"]).cuda(), int(z["b"])).cpu().numpy()
+    np.testing.assert_array_equal(got, z["block_embed"])
+
+
+def test_predictor_golden(cuda):
+    z = np.load(G / "predictor.npz")
+    pq = P.Predictor(z["q_w1"], z["q_w2"], z["q_w3"])
+    pq.set_masks(z["q_m1"], z["q_m2"])
+    pk = P.Predictor(z["k_w1"], z["k_w2"], z["k_w3"])
+    pk.set_masks(z["k_m1"], z["k_m2"])
+    x = torch.as_tensor(z["x"]).cuda()
+    b = int(z["b"])
+    np.testing.assert_allclose(P.predicted_triangle(pq, pk, x, b).cpu().numpy(), z["packed"],
+                               rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(P.predicted_triangle(pq, pk, x, b, "token").cpu().numpy(),
+                               z["packed_token"], rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(P.predicted_block_vector(pq, pk, x, b).cpu().numpy(), z["vec"],
+                               rtol=1e-5, atol=1e-6)
+
+
+def test_sgemm_vs_torch(cuda):
+    g = torch.Generator(device=cuda).manual_seed(0)
+    for M, N, K in ((1, 1, 1), (130, 257, 70), (1024, 1024, 4096)):
+        a = torch.randn(M, K, device=cuda, generator=g)
+        b = torch.randn(K, N, device=cuda, generator=g)
+        torch.testing.assert_close(ops.sgemm(a, b), a @ b, rtol=1e-4, atol=1e-4 * math.sqrt(K))
+        bt = b.t().contiguous()
+        torch.testing.assert_close(ops.sgemm(a, bt, b_trans=True, relu=True),
+                                   torch.relu(a @ b), rtol=1e-4, atol=1e-4 * math.sqrt(K))
+
+
+# ------------------------------------------------------------------ scorers
+
+
+def _scorer_model(seed, **kw):
+    cfg = ModelConfig(n_layers=1, hidden_dim=128, n_heads=2, vocab_size=64, max_seq_len=256,
+                      block_size=16, **kw)
+    ocfg = O.Config(n_layers=1, hidden_dim=128, n_heads=2, vocab_size=64, max_seq_len=256,
+                    block_size=16, **kw)
+    om = O.init_model(ocfg, seed=seed)
+    return DecoderModel(cfg, seed, init="reference"), om
+
+
+def test_mlp_scores_golden(cuda):
+    z = np.load(G / "scorers.npz")
+    m, _ = _scorer_model(3, mlp_dim=344, lora_rank=4, lora_alpha=8.0)
+    x = torch.as_tensor(z["x"]).cuda()
+    got = mlp_block_score_vector(m.layers[0], x, 16, int(z["n_valid"])).cpu().numpy()
+    # bf16 GEMM operands: token scores are means over m products -> ~1e-3 relative
+    np.testing.assert_allclose(got, z["mlp_vec"], rtol=2e-2)
+    zr = np.load(G / "scorers_relu.npz")
+    mr, _ = _scorer_model(4, mlp_dim=256, mlp_variant="relu")
+    got = mlp_block_score_vector(mr.layers[0], x, 16, int(zr["n_valid"])).cpu().numpy()
+    np.testing.assert_allclose(got, zr["mlp_vec"], rtol=2e-2)
+
+
+def test_exact_scores_golden(cuda):
+    z = np.load(G / "scorers.npz")
+    H, s, d = z["q"].shape
+    q = torch.as_tensor(z["q"].transpose(1, 0, 2).reshape(s, H * d)).cuda().bfloat16()
+    k = torch.as_tensor(z["k"].transpose(1, 0, 2).reshape(s, H * d)).cuda().bfloat16()
+    nv = int(z["n_valid"])
+    bsm = exact.exact_block_scores(q, k, 16, n_heads=H, n_valid=nv)
+    ref = z["exact_packed"]
+    np.testing.assert_allclose(bsm.scores.cpu().numpy(), ref, rtol=2e-2, atol=2e-2 * ref.max())
+    vec = exact.exact_block_vector(q, k, 16, n_heads=H, n_valid=nv).cpu().numpy()
+    np.testing.assert_allclose(vec, z["exact_vec"], rtol=2e-2)
+
+
+def test_layer_qk_matches_oracle(cuda):
+    z = np.load(G / "scorers.npz")
+    m, om = _scorer_model(3, mlp_dim=344, lora_rank=4, lora_alpha=8.0)
+    m.layers[0].lora_q.b.copy_(torch.as_tensor(z["lora_q_b"]))
+    x = torch.as_tensor(z["x"]).cuda()
+    q, k = layer_qk(m.layers[0], x)
+    H, s, d = z["q"].shape
+    qref = z["q"].transpose(1, 0, 2).reshape(s, H * d)
+    kref = z["k"].transpose(1, 0, 2).reshape(s, H * d)
+    np.testing.assert_allclose(q.float().cpu().numpy(), qref, rtol=3e-2, atol=3e-2)
+    np.testing.assert_allclose(k.float().cpu().numpy(), kref, rtol=3e-2, atol=3e-2)
+
+
+# ------------------------------------------------------------------ attention
+
+
+def _torch_attn(q, k, v, H):
+    n, h = q.shape
+    d = h // H
+    qh = q.float().view(n, H, d).transpose(0, 1)
+    kh = k.float().view(n, H, d).transpose(0, 1)
+    vh = v.float().view(n, H, d).transpose(0, 1)
+    s = qh @ kh.transpose(1, 2) / math.sqrt(d)
+    mask = torch.ones(n, n, dtype=torch.bool, device=q.device).tril()
+    s = s.masked_fill(~mask, float("-inf"))
+    p = torch.softmax(s, -1)
+    lse = torch.logsumexp(s, -1)
+    return (p @ vh).transpose(0, 1).reshape(n, h), lse
+
+
+@pytest.mark.parametrize("n,H,d", [(1, 2, 64), (17, 2, 64), (64, 4, 128), (100, 2, 128),
+                                   (257, 4, 64), (1000, 2, 128)])
+def test_flash_fwd_bwd_vs_torch(cuda, n, H, d):
+    g = torch.Generator(device=cuda).manual_seed(n)
+    h = H * d
+    q, k, v = (torch.randn(n, h, device=cuda, generator=g).bfloat16() for _ in range(3))
+    o, lse = ops.flash_fwd(q, k, v, head_dim=d, scale=1 / math.sqrt(d))
+    qr, kr, vr = (t.float().requires_grad_(True) for t in (q, k, v))
+    oref, lref = _torch_attn(qr, kr, vr, H)
+    torch.testing.assert_close(o.float(), oref, rtol=2e-2, atol=2e-2)
+    torch.testing.assert_close(lse, lref, rtol=1e-3, atol=1e-3)
+    dout = torch.randn(n, h, device=cuda, generator=g).bfloat16()
+    oref.backward(dout.float())
+    dq, dk, dv = ops.flash_bwd(q, k, v, o, dout, lse, head_dim=d, scale=1 / math.sqrt(d))
+    floor = 1e-2 * dout.float().norm()  # dq = dk = 0 exactly for a single token
+    for got, ref in ((dq, qr.grad), (dk, kr.grad), (dv, vr.grad)):
+        err = (got - ref).norm() / torch.maximum(ref.norm(), floor)
+        assert err < 2e-2, float(err)
+
+
+# ------------------------------------------------------------------ rows
+
+
+def test_rmsnorm_gather_lora(cuda):
+    g = torch.Generator(device=cuda).manual_seed(1)
+    s, h, r = 300, 512, 8
+    x = torch.randn(s, h, device=cuda, generator=g)
+    w = torch.rand(h, device=cuda, generator=g) + 0.5
+    A = torch.randn(h, 2 * r, device=cuda, generator=g) / math.sqrt(h)
+    idx = torch.arange(0, s, 3, device=cuda, dtype=torch.int32)
+    k = idx.numel()
+    xg = torch.empty(k, h, dtype=torch.bfloat16, device=cuda)
+    inv = torch.empty(k, device=cuda)
+    t = torch.empty(k, 2 * r, device=cuda)
+    xn = ops.rmsnorm_gather(x, w, idx, xg=xg, inv=inv, A=A, r=r, t=t)
+    xr = x[idx.long()]
+    invr = 1 / torch.sqrt((xr * xr).mean(-1, keepdim=True) + 1e-6)
+    xnr = xr * invr * w
+    torch.testing.assert_close(xn.float(), xnr, rtol=1e-2, atol=1e-2)
+    torch.testing.assert_close(inv, invr[:, 0], rtol=1e-5, atol=1e-6)
+    torch.testing.assert_close(t, xnr @ A, rtol=1e-4, atol=1e-4)
+    torch.testing.assert_close(xg.float(), xr, rtol=1e-2, atol=1e-2)
+
+
+def test_gateup_and_dgateup_vs_torch(cuda):
+    g = torch.Generator(device=cuda).manual_seed(2)
+    M, h, m = 200, 256, 344
+    cfg = ModelConfig(n_layers=1, hidden_dim=h, n_heads=4, vocab_size=64, mlp_dim=m)
+    model = DecoderModel(cfg, 0)
+    L = model.layers[0]
+    xn = torch.randn(M, h, device=cuda, generator=g).bfloat16()
+    N = L.w_gu_t.shape[0]
+    gu = torch.empty(M, N, dtype=torch.bfloat16, device=cuda)
+    inner = torch.empty(M, L.m_pad, dtype=torch.bfloat16, device=cuda)
+    part = torch.empty(N // 256, M, device=cuda)
+    ops.gemm_gateup(xn, L.w_gu_t, gu=gu, inner=inner, partial=part)
+    full = xn.float() @ L.w_gu_t.float().t()
+    gate = full.view(M, L.m_pad // 128, 2, 128)[:, :, 0].reshape(M, -1)
+    up = full.view(M, L.m_pad // 128, 2, 128)[:, :, 1].reshape(M, -1)
+    innr = torch.nn.functional.silu(gate) * up
+    torch.testing.assert_close(inner.float(), innr, rtol=3e-2, atol=3e-2)
+    torch.testing.assert_close(part.sum(0) / m, innr.abs().sum(-1) / m, rtol=1e-2, atol=1e-3)
+    dy = torch.randn(M, h, device=cuda, generator=g).bfloat16()
+    dgu = torch.empty_like(gu)
+    ops.gemm_dgateup(dy, L.w_down, gu, dgu, m_pad=L.m_pad)
+    dinner = dy.float() @ L.w_down.float().t()
+    gb = gu.float().view(M, L.m_pad // 128, 2, 128)
+    gg, uu = gb[:, :, 0].reshape(M, -1), gb[:, :, 1].reshape(M, -1)
+    sg = torch.sigmoid(gg)
+    dg = dinner * uu * sg * (1 + gg * (1 - sg))
+    du = dinner * gg * sg
+    got = dgu.float().view(M, L.m_pad // 128, 2, 128)
+    torch.testing.assert_close(got[:, :, 0].reshape(M, -1), dg, rtol=3e-2, atol=3e-2)
+    torch.testing.assert_close(got[:, :, 1].reshape(M, -1), du, rtol=3e-2, atol=3e-2)
+
+
+def test_qkv_rope_lora_vs_oracle(cuda):
+    """q/k/v projection epilogue = _project + rope_rotate at original positions."""
+    rng = np.random.default_rng(0)
+    h, H, r, M = 256, 4, 8, 96
+    d = h // H
+    cfg = ModelConfig(n_layers=1, hidden_dim=h, n_heads=H, vocab_size=64, mlp_dim=256, lora_rank=r)
+    model = DecoderModel(cfg, 0)
+    L = model.layers[0]
+    L.lora_q.b.copy_(torch.randn(r, h, device=cuda) * 0.1)
+    L.lora_v.b.copy_(torch.randn(r, h, device=cuda) * 0.1)
+    xn = torch.as_tensor(rng.standard_normal((M, h)).astype(np.float32)).cuda().bfloat16()
+    pos_np = np.sort(rng.choice(1000, M, replace=False))
+    pos = torch.as_tensor(pos_np.astype(np.int32)).cuda()
+    t = (xn.float() @ L.lora_A).contiguous()
+    q, k, v = ops.gemm_qkv(xn, L.w_qkv_t, h=h, head_dim=d, rope=True, rope_tab=L.rope_tab, pos=pos,
+                           t=t, r=r, Bq=L.lora_Bq, Bv=L.lora_Bv, scale=L.lora_scaling)
+    xf = xn.float().cpu().numpy()
+    W = L.w_qkv.float().cpu().numpy()
+    s = L.lora_scaling
+    qr = xf @ W[:, :h] + (t[:, :r].cpu().numpy() @ L.lora_Bq.cpu().numpy()) * s
+    kr = xf @ W[:, h:2 * h]
+    vr = xf @ W[:, 2 * h:] + (t[:, r:].cpu().numpy() @ L.lora_Bv.cpu().numpy()) * s
+    qr = O.rope_fwd(qr.astype(np.float32), pos_np, H, 10000.0)
+    kr = O.rope_fwd(kr.astype(np.float32), pos_np, H, 10000.0)
+    for got, ref in ((q, qr), (k, kr), (v, vr)):
+        np.testing.assert_allclose(got.float().cpu().numpy(), ref, rtol=2e-2, atol=2e-2)

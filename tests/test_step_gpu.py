@@ -1,0 +1,167 @@
+"""Whole-step parity: GPU forward_step + sparse backward vs the reference.
+
+The golden fixtures hold the reference's own loss / LoRA gradients / masks
+for a 2-layer model (tests/golden/make_golden.py); the oracle (pinned to the
+same fixtures by test_oracle.py) supplies extra cases at full Llama width.
+
+Tolerances (bf16 GEMM operands, fp32 accumulation, fp32 residual stream):
+  loss       relative error <= 1e-2
+  LoRA grads relative L2 error (per tensor) <= 5e-2
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lemo_oracle as O
+from paper_2501_09767_b200 import model as M, predictor as P, sparsity as S
+from paper_2501_09767_b200.optim import Adam
+
+pytestmark = pytest.mark.gpu
+G = Path(__file__).resolve().parent / "golden"
+
+STEP_CFG = dict(n_layers=2, hidden_dim=128, n_heads=2, vocab_size=128, max_seq_len=256,
+                mlp_dim=344, block_size=16, lora_rank=8, lora_alpha=16.0)
+LOSS_RTOL = 1e-2
+GRAD_RL2 = 5e-2
+
+
+def _model_and_oracle():
+    om = O.init_model(O.Config(**STEP_CFG), seed=17)
+    O.perturb_lora_b(om, 23)
+    arrays = M.reference_init_arrays(M.ModelConfig(**STEP_CFG), 17)
+    for name in om.adapter_names():
+        arrays[name] = om.adapter(name)
+    return M.DecoderModel(M.ModelConfig(**STEP_CFG), 17, arrays=arrays), om
+
+
+def _rl2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _source(mode, model, z):
+    if mode == "dense":
+        return None
+    if mode == "fraction":
+        return M.FractionSource(0.5, 16)
+    thr = S.ThresholdSet({(l, c): float(z[f"thr_{l}_{c}"]) for l in range(2)
+                          for c in (S.ATTENTION, S.MLP)})
+    if mode == "exact":
+        return M.ExactPatternSource(model, thr)
+    pairs = {l: (P.Predictor(z[f"pred{l}_q_w1"], z[f"pred{l}_q_w2"], z[f"pred{l}_q_w3"], "q", l),
+                 P.Predictor(z[f"pred{l}_k_w1"], z[f"pred{l}_k_w2"], z[f"pred{l}_k_w3"], "k", l))
+             for l in range(2)}
+    model.attach_predictors(pairs)
+    return M.PredictedPatternSource(model, thr, target_retention={0: 0.5, 1: 0.5},
+                                    recalibrate_every=1)
+
+
+@pytest.mark.parametrize("mode", ["dense", "fraction", "predicted", "exact"])
+def test_step_matches_reference(cuda, mode):
+    z = np.load(G / f"step_{mode}.npz")
+    model, _ = _model_and_oracle()
+    src = _source(mode, model, z)
+    loss, hidden = model.forward_step(z["tokens"], pattern_source=src, segments=2)
+    loss.backward()
+    got = float(loss)
+    assert abs(got - z["losses"][0]) <= LOSS_RTOL * abs(z["losses"][0]), (got, z["losses"][0])
+    grads = model.adapter_grads()
+    for name, g in grads.items():
+        ref = z[f"grad__{name}"]
+        assert _rl2(g, ref) <= GRAD_RL2, (name, _rl2(g, ref))
+    if src is not None and mode in ("fraction",):
+        frac = json.loads(str(z["fractions"]))
+        for key, f in frac.items():
+            l, c = key.split(":")
+            assert src.last_fractions[(int(l), c)] == pytest.approx(f)
+    # one Adam step (lr 1e-2), then the second loss of the reference trajectory
+    opt = Adam(model.lora_param, lr=1e-2)
+    opt.step()
+    opt.zero_grad()
+    with torch.no_grad():
+        loss2, _ = model.forward_step(z["tokens"], pattern_source=src, segments=2)
+    assert abs(float(loss2) - z["losses"][1]) <= LOSS_RTOL * abs(z["losses"][1])
+
+
+@pytest.mark.parametrize("mode", ["predicted", "exact"])
+def test_layer_masks_teacher_forced(cuda, mode):
+    """Feeding the reference's own per-layer input x_l to the GPU hook gives
+    the reference's retained blocks (scores computed on the GPU)."""
+    z = np.load(G / f"patterns_{mode}.npz")
+    zs = np.load(G / f"step_{mode}.npz")
+    model, _ = _model_and_oracle()
+    src = _source(mode, model, zs)
+    flips = 0
+    for l in range(2):
+        for c in (S.ATTENTION, S.MLP):
+            x = torch.as_tensor(z[f"x_{l}_{c}"]).cuda()
+            pat = src.pattern(l, c, x, 150)
+            model._mlp_scored.clear()
+            want = set(z[f"blocks_{l}_{c}"].tolist())
+            flips += len(set(pat.retained_blocks) ^ want)
+    assert flips == 0
+
+
+def test_all_retain_equals_dense_bitwise(cuda):
+    """tests/test_model.py:186-191: all-retain patterns ≡ dense, bitwise."""
+    z = np.load(G / "step_dense.npz")
+    m1, _ = _model_and_oracle()
+    l1, _ = m1.forward_step(z["tokens"], segments=2)
+    l1.backward()
+    m2, _ = _model_and_oracle()
+    l2, _ = m2.forward_step(z["tokens"], pattern_source=M.AllRetainSource(), segments=2)
+    l2.backward()
+    assert float(l1) == float(l2)
+    assert torch.equal(m1.lora_param.grad, m2.lora_param.grad)
+
+
+def test_segment_count_invariance(cuda):
+    """tests/test_kernels.py:190-211: N in {1,2,4,8} within 1e-6 (here: bf16 GEMM, fp32 CE)."""
+    z = np.load(G / "step_dense.npz")
+    losses = []
+    for seg in (1, 2, 4, 8):
+        m, _ = _model_and_oracle()
+        with torch.no_grad():
+            loss, _ = m.forward_step(z["tokens"], segments=seg)
+        losses.append(float(loss))
+    assert max(losses) - min(losses) <= 1e-5 * abs(losses[0])
+
+
+def test_empty_pattern_is_identity(cuda):
+    """k == 0 leaves the residual untouched (kernels.py:161-162)."""
+    z = np.load(G / "step_dense.npz")
+    m, om = _model_and_oracle()
+    pats = {(l, c): S.SparsityPattern.empty(160, 16, l, c) for l in range(2)
+            for c in (S.ATTENTION, S.MLP)}
+    loss, _ = m.forward_step(z["tokens"], pattern_source=M.FixedPatternSource(pats), segments=2)
+    ores = O.train_step(om, z["tokens"], source=O.FixedSource({k: () for k in pats}), segments=2)
+    assert abs(float(loss) - ores["loss"]) <= 1e-3 * abs(ores["loss"])
+
+
+@pytest.mark.parametrize("frac", [0.25, 0.5, 1.0])
+def test_full_width_layer_vs_oracle(cuda, frac):
+    """One Llama2-7B-width layer (h=4096, 32 heads, m=11008) at s=512 against
+    the oracle with identical weights and patterns."""
+    cfg = dict(n_layers=1, hidden_dim=4096, n_heads=32, vocab_size=512, max_seq_len=512,
+               mlp_dim=11008, block_size=16, lora_rank=8, lora_alpha=16.0)
+    om = O.init_model(O.Config(**cfg), seed=5)
+    O.perturb_lora_b(om, 6)
+    arrays = M.reference_init_arrays(M.ModelConfig(**cfg), 5)
+    for name in om.adapter_names():
+        arrays[name] = om.adapter(name)
+    model = M.DecoderModel(M.ModelConfig(**cfg), 5, arrays=arrays)
+    tokens = np.random.default_rng(7).integers(0, 512, 512)
+    nb = 32
+    keep = max(1, int(round(nb * frac)))
+    blocks = tuple(np.unique(np.linspace(0, nb - 1, keep).round().astype(int)).tolist())
+    oref = O.train_step(om, tokens, source=O.FixedSource({(0, c): blocks for c in ("attention", "mlp")}),
+                        segments=2)
+    src = M.FractionSource(frac, 16)
+    loss, _ = model.forward_step(tokens, pattern_source=src, segments=2)
+    loss.backward()
+    assert abs(float(loss) - oref["loss"]) <= LOSS_RTOL * abs(oref["loss"])
+    for name, g in model.adapter_grads().items():
+        assert _rl2(g, oref["grads"][name]) <= GRAD_RL2, (name, _rl2(g, oref["grads"][name]))
