@@ -93,10 +93,56 @@ def ptr(t) -> int | None:
     return int(t.data_ptr())
 
 
+# kernels launched per entry point (everything else launches exactly one)
+_LAUNCHES = {"lemo_flash_bwd": 3}
+
+
+class Instrument:
+    """Launch counting and per-entry-point CUDA-event timing (bench.py).
+
+    counting: launches[name] += kernels launched by each call.
+    timing:   for names in `timed`, a (start, end) event pair is recorded on
+              the current stream around every call.
+    """
+
+    def __init__(self):
+        self.enabled = False
+        self.launches: dict[str, int] = {}
+        self.timed: set[str] = set()
+        self.events: dict[str, list] = {}
+
+    def reset(self, timed=()):
+        self.launches = {}
+        self.timed = set(timed)
+        self.events = {n: [] for n in self.timed}
+
+    def total_launches(self) -> int:
+        return sum(self.launches.values())
+
+    def elapsed_ms(self, name: str) -> list[float]:
+        return [a.elapsed_time(b) for a, b in self.events.get(name, [])]
+
+
+INSTRUMENT = Instrument()
+
+
 def call(name: str, *args):
     """Invoke a status-returning entry point; raise LemoError on failure."""
     fn = getattr(lib(), name)
-    rc = fn(*args)
+    ins = INSTRUMENT
+    if ins.enabled:
+        ins.launches[name] = ins.launches.get(name, 0) + _LAUNCHES.get(name, 1)
+        if name in ins.timed:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            rc = fn(*args)
+            b.record()
+            ins.events[name].append((a, b))
+        else:
+            rc = fn(*args)
+    else:
+        rc = fn(*args)
     if rc != 0:
         msg = lib().lemo_last_error().decode(errors="replace")
         raise LemoError(f"{name} failed ({rc}): {msg}")

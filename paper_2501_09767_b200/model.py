@@ -423,6 +423,9 @@ class DecoderModel:
 
     # -- forward --------------------------------------------------------------------
 
+    def stage_tokens(self, tokens, targets=None) -> "StagedBatch":
+        return StagedBatch(self, tokens, targets)
+
     def forward_step(self, tokens, targets=None, *, pattern_source=None, segments: int = 1,
                      fused: bool = True, fuse_projections: bool = True):
         """model.py:246-297.  Returns (loss, hidden): loss is a CUDA scalar whose
@@ -443,12 +446,12 @@ class DecoderModel:
         return kernels.GatherPlan.from_pattern(pattern, n_pad, device)
 
 
-class _Step:
-    """Saved state of one training step (the reference's tape, compacted)."""
+class StagedBatch:
+    """A padded, validated token/target pair resident on the device
+    (DecoderModel.stage_tokens); forward_step accepts it in place of host
+    arrays so a caller can keep inputs in HBM across steps."""
 
-    def __init__(self, model: DecoderModel, tokens, targets, source, segments):
-        self.model = model
-        self.source = source
+    def __init__(self, model: "DecoderModel", tokens, targets=None):
         ids, tgts, n_valid = model.pad_tokens(tokens, targets)
         cfg = model.config
         if ids.min() < 0 or ids.max() >= cfg.vocab_size:
@@ -459,14 +462,27 @@ class _Step:
             raise ContractError("segmented loss: no valid targets")
         self.n_valid = n_valid
         self.n_pad = len(ids)
-        self.segments = max(1, segments)
-        dev = model.device
         host = torch.empty(2, self.n_pad, dtype=torch.int32, pin_memory=True)
         host[0].copy_(torch.from_numpy(ids.astype(np.int32)))
         host[1].copy_(torch.from_numpy(tgts.astype(np.int32)))
-        both = host.to(dev, non_blocking=True)
+        both = host.to(model.device, non_blocking=True)
         self.ids, self.tgts = both[0], both[1]
         self.h2d_bytes = host.numel() * 4
+
+
+class _Step:
+    """Saved state of one training step (the reference's tape, compacted)."""
+
+    def __init__(self, model: DecoderModel, tokens, targets, source, segments):
+        self.model = model
+        self.source = source
+        batch = tokens if isinstance(tokens, StagedBatch) else StagedBatch(model, tokens, targets)
+        self.count = batch.count
+        self.n_valid = batch.n_valid
+        self.n_pad = batch.n_pad
+        self.ids, self.tgts = batch.ids, batch.tgts
+        self.h2d_bytes = 0 if batch is tokens else batch.h2d_bytes
+        self.segments = max(1, segments)
         self.hidden = None
 
     def forward(self, need_grad: bool = True):
