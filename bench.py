@@ -164,6 +164,19 @@ def run_reference(args):
 # B200 arm
 
 
+def _mlp_only_profile(src, S):
+    """ExactPatternSource restricted to MLP scoring (attention retained in the
+    profile pass; its thresholds are set by the predicted calibration pass)."""
+    orig = src.pattern
+
+    def pattern(layer_id, component, x, n_valid):
+        if component == S.ATTENTION:
+            return src._note(layer_id, component, None)
+        return orig(layer_id, component, x, n_valid)
+
+    return pattern
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -204,21 +217,28 @@ def main():
     tokens = rng.integers(0, cfg.vocab_size, size=seq)
     segments = 8 if seq >= 1024 else 1
 
-    # thresholds: profiling pass (retain all, record scores) -> MLP pooled mean,
-    # attention re-derived at 50% retention on the first call
+    # thresholds (the reference pipeline's order: profile -> init -> predicted init):
+    #  pass 1  retain-all profile of exact MLP scores -> MLP thresholds = pooled
+    #          mean (init_thresholds, sparsity.py:360-376)
+    #  pass 2  with those MLP thresholds, attention thresholds re-derived at 50%
+    #          retention from the predicted scores (model.py:545-563)
     retention = {l: 0.5 for l in range(cfg.n_layers)}
-    prof = M.PredictedPatternSource(
-        model, S.ThresholdSet({(l, S.MLP): float("-inf") for l in range(cfg.n_layers)}),
-        target_retention=retention, recalibrate_every=1, record=True)
+    prof = M.ExactPatternSource(model, None, record=True)
+    prof.pattern = _mlp_only_profile(prof, S)
     with torch.no_grad():
         model.forward_step(tokens, pattern_source=prof, segments=segments)
-    thr = S.init_thresholds({k: v for k, v in prof.recorded_vectors.items() if k[1] == S.MLP})
-    for l in range(cfg.n_layers):
-        thr.set(l, S.ATTENTION, prof.thresholds.get(l, S.ATTENTION))
-    del prof
+    thr = S.init_thresholds(prof.recorded_vectors)
     model._mlp_scored.clear()
-    source = M.PredictedPatternSource(model, thr.copy(), target_retention=retention,
+    for l in range(cfg.n_layers):
+        thr.set(l, S.ATTENTION, 0.0)
+    cal = M.PredictedPatternSource(model, thr.copy(), target_retention=retention,
+                                   recalibrate_every=1)
+    with torch.no_grad():
+        model.forward_step(tokens, pattern_source=cal, segments=segments)
+    model._mlp_scored.clear()
+    source = M.PredictedPatternSource(model, cal.thresholds.copy(), target_retention=retention,
                                       recalibrate_every=50)
+    del prof, cal
     opt = Adam(model.lora_param, lr=1e-4)
 
     def step(src, batch, read_loss=False):
@@ -228,7 +248,7 @@ def main():
             dist.all_reduce(model.lora_param.grad, op=dist.ReduceOp.AVG)
         opt.step()
         opt.zero_grad()
-        return float(loss) if read_loss else loss
+        return float(loss.detach()) if read_loss else loss
 
     def timed(src, batch_fn, steps, read_loss=False, timed_names=()):
         ins = _lib.INSTRUMENT

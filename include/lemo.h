@@ -81,13 +81,15 @@ int lemo_gemm_dgateup(const void* dy, const void* w_down, int M, int m_pad, int 
 
 /* ---- row kernels (HBM-bound) --------------------------------------------- */
 
-/* Fused gather + RMSNorm (tensor.py:578-597; idx NULL = all rows): xn (bf16),
- * optional saved raw rows xg (bf16) and inv (fp32), and optional LoRA factors
- * t[i, 0:r] = xn_i·A0, t[i, r:2r] = xn_i·A1 (kernels.py:97-98; A: [h, r] fp32
- * with row stride lda). */
+/* Fused gather + RMSNorm (tensor.py:578-597; idx NULL = all rows): xn (bf16)
+ * plus optional saved raw rows xg (bf16) and inv (fp32). */
 int lemo_rmsnorm_gather(const float* x, int ldx, const int* idx, int M, int h, const float* w,
-                        void* xn, void* xg, float* inv, const float* A0, const float* A1, int lda,
-                        int r, float* t, int ldt, void* stream);
+                        void* xn, void* xg, float* inv, void* stream);
+
+/* LoRA down-projection operand: out[j, c] = bf16(A[c*lda + j]) for j < r2,
+ * zero for r2 <= j < 32 (out: [32, h] bf16), so t = xn·[A_q|A_v]
+ * (kernels.py:97-98) is one tcgen05 GEMM with N = 32. */
+int lemo_lora_pack(const float* A, int lda, int h, int r2, void* out, void* stream);
 
 /* dst[i] = bf16(src[idx[i]]) — gradient rows for the output-projection
  * backward (the g[idx] of scatter_add_rows backward, tensor.py:547-548). */
@@ -150,6 +152,20 @@ int lemo_block_embed(const float* x, int ldx, int s, int h, int b, float* xb, vo
  * (predictor.py:83-89) and Eq. 3 eq·ekᵀ (predictor.py:186). */
 int lemo_sgemm(const float* A, int lda, const float* B, int ldb, int b_trans, float* C, int ldc,
                int M, int N, int K, int relu, const unsigned char* col_mask, void* stream);
+
+/* fp32-faithful bf16 tensor-core GEMMs ("bf16x3"): a fp32 matrix is carried
+ * as hi = bf16(v), lo = bf16(v - hi) and A·B ≈ Ahi·Bhi + Ahi·Blo + Alo·Bhi is
+ * one GEMM over K' = 3K with A' = [hi|hi|lo] (pattern 0) and B' = [hi|lo|hi]
+ * (pattern 1).  lemo_split_bf16x3 builds an operand [M, 3K] from fp32 A. */
+int lemo_split_bf16x3(const float* A, int lda, int M, int K, int pattern, void* out,
+                      void* stream);
+
+/* C = act(A'·B'ᵀ)·mask over K' = K3 (= 3K): writes the split form of C
+ * (out [M, 3N], pattern as above) and/or fp32 C (f32 [M, N]); act = relu if
+ * relu.  One Predictor layer (predictor.py:83-89) per call. */
+int lemo_gemm_split3(const void* A, int lda, const void* B, int ldb, int M, int N, int K3,
+                     int relu, const unsigned char* mask, int pattern, void* out, int ldo,
+                     float* f32, int ldf, void* stream);
 
 /* vec[n] = Σ_{m>=n} max(S[m,n], 0) in float64, ascending m
  * (model.py:575-578 + sparsity.py:253-260). */

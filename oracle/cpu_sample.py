@@ -31,7 +31,7 @@ class CpuSample:
         cfg = O.Config(n_layers=1, hidden_dim=hidden, n_heads=heads, vocab_size=vocab,
                        max_seq_len=sample_tokens, mlp_dim=mlp, block_size=block,
                        lora_rank=lora_rank, lora_alpha=2.0 * lora_rank)
-        self.model = O.init_model(cfg, seed=seed)
+        self.model = O.init_model(cfg, seed=seed, fast=True)
         rng = np.random.default_rng(seed + 1)
         L = self.model.layers[0]
         r = hidden // 4

@@ -313,10 +313,19 @@ class Model:
         return ad[0] if ab == "a" else ad[1]
 
 
-def init_model(cfg: Config, seed: int = 0, dtype=np.float32) -> Model:
+def init_model(cfg: Config, seed: int = 0, dtype=np.float32, fast: bool = False) -> Model:
     """Same draw order as DecoderModel.__init__ / LayerState / LoraAdapter
-    (model.py:67-153)."""
+    (model.py:67-153).  fast=True draws float32 normals directly (different
+    values, same distribution) — used only for the timed CPU sample."""
     rng = np.random.default_rng(seed)
+    if fast:
+        gen = rng
+
+        class _R:
+            @staticmethod
+            def standard_normal(shape):
+                return gen.standard_normal(shape, dtype=np.float32)
+        rng = _R()
     h, m = cfg.hidden_dim, cfg.mlp_dim
     std = 1.0 / np.sqrt(h)
     embed = (rng.standard_normal((cfg.vocab_size, h)) * std).astype(dtype)
@@ -483,17 +492,22 @@ def mlp_block_score_vector(L: Layer, x: np.ndarray, block_size: int, n_valid: in
     s = x.shape[0]
     nb = n_blocks_for(s, block_size)
     out = np.zeros(nb)
-    for blk in range(nb):
-        t0, t1 = blk * block_size, min((blk + 1) * block_size, s, n_valid)
-        if t1 <= t0:
-            continue
-        xn, _ = rmsnorm_fwd(x[t0:t1], L.mlp_norm)
+    lim = min(s, n_valid)
+    # rows are independent: stream a few blocks per GEMM (same per-row math as
+    # the reference's one-block-at-a-time loop, better BLAS efficiency)
+    per = block_size * max(1, 256 // block_size)
+    for c0 in range(0, lim, per):
+        c1 = min(c0 + per, lim)
+        xn, _ = rmsnorm_fwd(x[c0:c1], L.mlp_norm)
         if L.mlp_variant == "silu":
             gate = xn @ L.w_gate
             inner = gate * sigmoid(gate) * (xn @ L.w_up)
         else:
             inner = np.maximum(xn @ L.w_up, 0)
-        out[blk] = np.abs(inner).mean(axis=-1).astype(np.float64).max()
+        tok = np.abs(inner).mean(axis=-1).astype(np.float64)
+        for blk in range(c0 // block_size, n_blocks_for(c1, block_size)):
+            t0, t1 = blk * block_size, min((blk + 1) * block_size, c1)
+            out[blk] = tok[t0 - c0:t1 - c0].max()
     return out
 
 

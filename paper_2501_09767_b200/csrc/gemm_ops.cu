@@ -109,15 +109,23 @@ struct EpiStoreF32 {
       load_chunk(taddr + c, v);
       if (valid && col0 + c < N) {
         add_side(v, u, R, S, s_rs, s_cs, col0 + c, scale);
-        float4* d = reinterpret_cast<float4*>(C + (size_t)row * ldc + col0 + c);
+        const int n = min(32, N - col0 - c);
+        float* dst = C + (size_t)row * ldc + col0 + c;
+        if (n == 32 && (ldc & 3) == 0) {
+          float4* d = reinterpret_cast<float4*>(dst);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          if (accumulate) {
-            float4 p = d[q];
-            o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+          for (int q = 0; q < 8; ++q) {
+            float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            if (accumulate) {
+              float4 p = d[q];
+              o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+            }
+            d[q] = o;
           }
-          d[q] = o;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < n) dst[i] = accumulate ? dst[i] + v[i] : v[i];
         }
       }
     }
@@ -304,6 +312,63 @@ struct EpiDGateUp {
   }
 };
 
+// fp32-faithful GEMM chains on bf16 tensor cores ("bf16x3"): a fp32 value v
+// is carried as hi = bf16(v), lo = bf16(v - hi); A·B ≈ Ahi·Bhi + Ahi·Blo +
+// Alo·Bhi, realised as ONE GEMM over K' = 3K with A' = [hi|hi|lo] (pattern 0)
+// and B' = [hi|lo|hi] (pattern 1).  This epilogue applies relu·mask (the
+// Predictor hidden layers, predictor.py:83-89) and writes the split form of
+// the result for the next GEMM of the chain, and/or the fp32 value.
+struct EpiSplit3 {
+  __nv_bfloat16* out;  // [M, 3N] (or null)
+  int ldo;
+  float* f32;  // [M, N] (or null)
+  int ldf, N, pattern, relu;
+  const unsigned char* mask;
+  template <int BN>
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      load_chunk(taddr + c, v);
+      if (!valid || col0 + c >= N) continue;
+      float hi[32], lo[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        float x = v[i];
+        if (relu) x = fmaxf(x, 0.f);
+        if (mask && !mask[col0 + c + i]) x = 0.f;
+        v[i] = x;
+        hi[i] = round_bf16(x);
+        lo[i] = x - hi[i];
+      }
+      const int n = min(32, N - col0 - c);
+      if (out) {
+        __nv_bfloat16* o = out + (size_t)row * ldo + col0 + c;
+        if (n == 32 && (ldo & 7) == 0 && (N & 7) == 0) {
+          store_bf16x32(o, hi);
+          store_bf16x32(o + N, pattern ? lo : hi);
+          store_bf16x32(o + 2 * N, pattern ? hi : lo);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (i < n) {
+              o[i] = __float2bfloat16_rn(hi[i]);
+              o[N + i] = __float2bfloat16_rn(pattern ? lo[i] : hi[i]);
+              o[2 * N + i] = __float2bfloat16_rn(pattern ? hi[i] : lo[i]);
+            }
+          }
+        }
+      }
+      if (f32) {
+        float* d = f32 + (size_t)row * ldf + col0 + c;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < n) d[i] = v[i];
+      }
+    }
+  }
+};
+
 }  // namespace lemo
 
 // The kernel template calls epi(row, valid, col0, taddr); wrap run<BN>.
@@ -345,7 +410,6 @@ int lemo_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int 
 int lemo_gemm_f32(const void* A, int lda, const void* B, int ldb, float* C, int ldc, int M, int N,
                   int K, const float* U, int ldu, int R, const float* S, int s_rs, int s_cs,
                   float scale, int accumulate, void* stream) {
-  LEMO_ARG_CHECK(N % 32 == 0 && ldc % 4 == 0, "lemo_gemm_f32: N and ldc must be multiples of 32/4");
   LEMO_ARG_CHECK(R >= 0 && R <= kMaxSideRank, "lemo_gemm_f32: side rank out of range");
   EpiStoreF32 e{C, ldc, N, U, ldu, R, S, s_rs, s_cs, scale, accumulate};
   LEMO_RETURN_RC("lemo_gemm_f32", gemm_auto(A, lda, B, ldb, M, N, K, e, (cudaStream_t)stream));
@@ -389,6 +453,16 @@ int lemo_gemm_gateup(const void* xn, int ldx, const void* w_gu_t, int M, int N, 
               relu ? N : N / 2, partial, M, relu};
   LEMO_RETURN_RC("lemo_gemm_gateup",
                  gemm<256>(xn, ldx, w_gu_t, K, M, N, K, e, (cudaStream_t)stream));
+}
+
+int lemo_gemm_split3(const void* A, int lda, const void* B, int ldb, int M, int N, int K3,
+                     int relu, const unsigned char* mask, int pattern, void* out, int ldo,
+                     float* f32, int ldf, void* stream) {
+  LEMO_ARG_CHECK(K3 % 3 == 0, "lemo_gemm_split3: K' must be 3K");
+  EpiSplit3 e{reinterpret_cast<__nv_bfloat16*>(out), ldo, f32, ldf, N, pattern, relu, mask};
+  // BN = 128: these GEMMs are small in M (n_blocks) — twice the CTAs of BN = 256
+  LEMO_RETURN_RC("lemo_gemm_split3",
+                 gemm<128>(A, lda, B, ldb, M, N, K3, e, (cudaStream_t)stream));
 }
 
 int lemo_gemm_dgateup(const void* dy, const void* w_down, int M, int m_pad, int h, const void* gu,

@@ -25,17 +25,16 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 // ---------------------------------------------------------------------------
-// gather_rmsnorm (tensor.py:578-597) fused with the LoRA down-projection
-// t = xn · [A0 | A1] (kernels.py:97-98).  idx == null: every row.
+// gather_rmsnorm (tensor.py:578-597).  idx == null: every row.  (The LoRA
+// down-projection t = xn·[A_q|A_v] runs as a tcgen05 GEMM on the bf16 xn;
+// see lemo_lora_pack.)
 
 template <int VPT>
 __global__ void __launch_bounds__(128) gather_rmsnorm_kernel(
     const float* __restrict__ x, int ldx, const int* __restrict__ idx, int h,
     const float* __restrict__ w, __nv_bfloat16* __restrict__ xn, __nv_bfloat16* __restrict__ xg,
-    float* __restrict__ inv_out, const float* __restrict__ A0, const float* __restrict__ A1, int lda,
-    int r, float* __restrict__ t, int ldt) {
+    float* __restrict__ inv_out) {
   __shared__ float red[4];
-  __shared__ float tred[4][32];
   const int row = blockIdx.x;
   const int src = idx ? __ldg(idx + row) : row;
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)src * ldx);
@@ -52,9 +51,6 @@ __global__ void __launch_bounds__(128) gather_rmsnorm_kernel(
   const float inv = 1.f / sqrtf(ss / (float)h + kEps);
   if (threadIdx.x == 0 && inv_out) inv_out[row] = inv;
   const float4* w4 = reinterpret_cast<const float4*>(w);
-  float tacc[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) tacc[j] = 0.f;
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int c = threadIdx.x + i * blockDim.x;
@@ -71,36 +67,18 @@ __global__ void __launch_bounds__(128) gather_rmsnorm_kernel(
       reinterpret_cast<uint2*>(xg + (size_t)row * h)[c] =
           make_uint2(pack_bf16x2(v[i].x, v[i].y), pack_bf16x2(v[i].z, v[i].w));
     }
-    if (A0) {
-      const float oc[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float* a0 = A0 + (size_t)(4 * c + e) * lda;
-        const float* a1 = A1 + (size_t)(4 * c + e) * lda;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if (j < r) {
-            tacc[j] = fmaf(oc[e], __ldg(a0 + j), tacc[j]);
-            tacc[16 + j] = fmaf(oc[e], __ldg(a1 + j), tacc[16 + j]);
-          }
-        }
-      }
-    }
   }
-  if (A0) {
-    const int wid = threadIdx.x >> 5, l = threadIdx.x & 31;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      float s = warp_sum(tacc[j]);
-      if (l == 0) tred[wid][j] = s;
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      const int j = threadIdx.x;
-      const float s = tred[0][j] + tred[1][j] + tred[2][j] + tred[3][j];
-      if ((j & 15) < r) t[(size_t)row * ldt + (j >> 4) * r + (j & 15)] = s;
-    }
-  }
+}
+
+// LoRA down-projection operand for the tcgen05 GEMM: out[j, c] = bf16(A[c*lda + j])
+// for j < 2r (A = [A_q | A_v] interleaved [h, 2r]), zero rows up to 32.
+__global__ void lora_pack_kernel(const float* __restrict__ A, int lda, int h, int r2,
+                                 __nv_bfloat16* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= h) return;
+#pragma unroll 4
+  for (int j = 0; j < 32; ++j)
+    out[(size_t)j * h + c] = __float2bfloat16_rn(j < r2 ? A[(size_t)c * lda + j] : 0.f);
 }
 
 // dst[i] = bf16(src[idx[i]])
@@ -421,20 +399,16 @@ using namespace lemo;
 extern "C" {
 
 int lemo_rmsnorm_gather(const float* x, int ldx, const int* idx, int M, int h, const float* w,
-                        void* xn, void* xg, float* inv, const float* A0, const float* A1, int lda,
-                        int r, float* t, int ldt, void* stream) {
+                        void* xn, void* xg, float* inv, void* stream) {
   if (M <= 0) return 0;
   LEMO_ARG_CHECK(h % 4 == 0 && ldx % 4 == 0, "lemo_rmsnorm_gather: h, ldx must be multiples of 4");
   LEMO_ARG_CHECK(h <= 4 * 128 * 16, "lemo_rmsnorm_gather: h too large");
-  LEMO_ARG_CHECK(!A0 || (r > 0 && r <= 16 && A1 && t), "lemo_rmsnorm_gather: LoRA rank <= 16");
   const int nv = h / 4;
   const int vpt = (nv + 127) / 128;
   cudaStream_t st = (cudaStream_t)stream;
   auto* xnp = reinterpret_cast<__nv_bfloat16*>(xn);
   auto* xgp = reinterpret_cast<__nv_bfloat16*>(xg);
-#define LAUNCH(V)                                                                              \
-  gather_rmsnorm_kernel<V><<<M, 128, 0, st>>>(x, ldx, idx, h, w, xnp, xgp, inv, A0, A1, lda, r, \
-                                              t, ldt)
+#define LAUNCH(V) gather_rmsnorm_kernel<V><<<M, 128, 0, st>>>(x, ldx, idx, h, w, xnp, xgp, inv)
   if (vpt <= 1) LAUNCH(1);
   else if (vpt <= 2) LAUNCH(2);
   else if (vpt <= 4) LAUNCH(4);
@@ -442,6 +416,14 @@ int lemo_rmsnorm_gather(const float* x, int ldx, const int* idx, int M, int h, c
   else LAUNCH(16);
 #undef LAUNCH
   LEMO_CHECK_LAUNCH("lemo_rmsnorm_gather");
+  return 0;
+}
+
+int lemo_lora_pack(const float* A, int lda, int h, int r2, void* out, void* stream) {
+  LEMO_ARG_CHECK(r2 <= 32, "lemo_lora_pack: 2r must be <= 32");
+  lora_pack_kernel<<<(h + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      A, lda, h, r2, reinterpret_cast<__nv_bfloat16*>(out));
+  LEMO_CHECK_LAUNCH("lemo_lora_pack");
   return 0;
 }
 

@@ -283,6 +283,21 @@ __global__ void __launch_bounds__(1024) quantile_kernel(const double* __restrict
   }
 }
 
+// fp32 -> bf16x3 operand ([hi|hi|lo] pattern 0, [hi|lo|hi] pattern 1), see EpiSplit3.
+__global__ void split_bf16x3_kernel(const float* __restrict__ A, int lda, int M, int K,
+                                    int pattern, __nv_bfloat16* __restrict__ out) {
+  const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gid >= (long long)M * K) return;
+  const int row = (int)(gid / K), c = (int)(gid - (long long)row * K);
+  const float v = A[(size_t)row * lda + c];
+  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+  const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+  __nv_bfloat16* o = out + (size_t)row * 3 * K;
+  o[c] = hi;
+  o[K + c] = pattern ? lo : hi;
+  o[2 * K + c] = pattern ? hi : lo;
+}
+
 }  // namespace lemo
 
 using namespace lemo;
@@ -311,6 +326,16 @@ int lemo_sgemm(const float* A, int lda, const float* B, int ldb, int b_trans, fl
   else
     sgemm_kernel<false><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, relu, col_mask);
   LEMO_CHECK_LAUNCH("lemo_sgemm");
+  return 0;
+}
+
+int lemo_split_bf16x3(const float* A, int lda, int M, int K, int pattern, void* out,
+                      void* stream) {
+  const long long total = (long long)M * K;
+  if (total == 0) return 0;
+  split_bf16x3_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      A, lda, M, K, pattern, reinterpret_cast<__nv_bfloat16*>(out));
+  LEMO_CHECK_LAUNCH("lemo_split_bf16x3");
   return 0;
 }
 

@@ -131,9 +131,8 @@ def attention_forward(x: torch.Tensor, plan: GatherPlan, layer, *, save: bool = 
     xn = torch.empty(k, h, dtype=BF16, device=dev)
     xg = torch.empty(k, h, dtype=BF16, device=dev) if save else None
     inv = torch.empty(k, dtype=F32, device=dev) if save else None
-    t = torch.empty(k, 2 * r, dtype=F32, device=dev) if r else None
-    ops.rmsnorm_gather(x, layer.attn_norm_w, idx, xn=xn, xg=xg, inv=inv,
-                       A=layer.lora_A if r else None, r=r, t=t)
+    ops.rmsnorm_gather(x, layer.attn_norm_w, idx, xn=xn, xg=xg, inv=inv)
+    t = ops.lora_down(xn, layer.lora_A_packed()) if r else None
     q, kk, v = ops.gemm_qkv(xn, layer.w_qkv_t, h=h, head_dim=layer.head_dim, rope=layer.rope,
                             rope_tab=layer.rope_tab, pos=idx, t=t, r=r,
                             Bq=layer.lora_Bq if r else None, Bv=layer.lora_Bv if r else None,
@@ -160,7 +159,7 @@ def attention_backward(dx: torch.Tensor, saved: dict, layer, grads) -> None:
                                head_dim=layer.head_dim, scale=1.0 / math.sqrt(layer.head_dim))
     del d_o
     dqkv = torch.empty(k, 3 * h, dtype=BF16, device=dev)
-    u = torch.empty(k, 2 * r, dtype=F32, device=dev) if r else None
+    u = torch.empty(k, ops.LORA_T_COLS, dtype=F32, device=dev) if r else None
     ops.qkv_grad_prep(dq, dk, dv, head_dim=layer.head_dim, rope=layer.rope,
                       rope_tab=layer.rope_tab, pos=idx, Bq=layer.lora_Bq if r else None,
                       Bv=layer.lora_Bv if r else None, r=r, dqkv=dqkv, u=u)
@@ -169,8 +168,9 @@ def attention_backward(dx: torch.Tensor, saved: dict, layer, grads) -> None:
         ops.lora_grads(saved["xg"], saved["inv"], layer.attn_norm_w, saved["t"], u, dq, dv, r=r,
                        scale=layer.lora_scaling, dA=dA, dB0=dBq, dB1=dBv)
     del dq, dk, dv
-    dxn = ops.gemm_f32(dqkv, layer.w_qkv, side_u=u, side_s=layer.lora_A if r else None,
-                       side_strides=(1, 2 * r), scale=layer.lora_scaling)
+    dxn = ops.gemm_f32(dqkv, layer.w_qkv, side_u=u[:, :2 * r] if r else None,
+                       side_s=layer.lora_A if r else None, side_strides=(1, 2 * r),
+                       scale=layer.lora_scaling)
     ops.rmsnorm_bwd(dxn, saved["xg"], saved["inv"], layer.attn_norm_w, dx, idx, accumulate=True)
 
 

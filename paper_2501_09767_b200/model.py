@@ -218,6 +218,11 @@ class LayerState:
         Bv = flat[o + 3 * h * r:o + 4 * h * r].view(r, h)
         return A, Bq, Bv
 
+    def lora_A_packed(self) -> torch.Tensor:
+        """[32, h] bf16 copy of [A_q | A_v] for the t = xn·A GEMM (re-packed each
+        call: the adapters change every optimizer step)."""
+        return ops.lora_pack(self.lora_A, self.lora_rank)
+
     def grad_views(self, flat_grad):
         return self._views(flat_grad) if self.lora_rank else None
 
@@ -582,8 +587,8 @@ def layer_qk(layer: LayerState, x: torch.Tensor):
     """model.py:356-368: post-rotation Q (with LoRA) and K (without), [s, h] bf16."""
     s, h = x.shape
     r = layer.lora_rank
-    t = torch.empty(s, 2 * r, dtype=F32, device=x.device) if r else None
-    xn = ops.rmsnorm_gather(x, layer.attn_norm_w, None, A=layer.lora_A if r else None, r=r, t=t)
+    xn = ops.rmsnorm_gather(x, layer.attn_norm_w, None)
+    t = ops.lora_down(xn, layer.lora_A_packed()) if r else None
     pos = torch.arange(s, dtype=torch.int32, device=x.device)
     q, k = ops.gemm_qkv(xn, layer.w_qkv_t, h=h, head_dim=layer.head_dim, rope=layer.rope,
                         rope_tab=layer.rope_tab, pos=pos, t=t, r=r,

@@ -133,23 +133,35 @@ def gemm_dgateup(dy, w_down, gu, dgu, *, m_pad, relu=False):
 # row kernels
 
 
-def rmsnorm_gather(x, w, idx=None, *, xn=None, xg=None, inv=None, A=None, r=0, t=None):
-    """Fused gather + RMSNorm (+LoRA factors t = xn·[A0|A1], A = [h, 2r] interleaved)."""
-    _check(x, w, idx, A, t)
+def rmsnorm_gather(x, w, idx=None, *, xn=None, xg=None, inv=None):
+    """Fused gather + RMSNorm."""
+    _check(x, w, idx)
     _dt(x, F32, "x")
     M = x.shape[0] if idx is None else idx.shape[0]
     h = x.shape[1]
     if xn is None:
         xn = torch.empty(M, h, dtype=BF16, device=x.device)
-    A0 = A1 = None
-    lda = 0
-    if A is not None:
-        A0 = A
-        A1 = A[:, r:]
-        lda = A.stride(0)
     call("lemo_rmsnorm_gather", ptr(x), x.stride(0), ptr(idx), M, h, ptr(w), ptr(xn), ptr(xg),
-         ptr(inv), ptr(A0), ptr(A1), lda, r, ptr(t), 0 if t is None else t.stride(0), _s())
+         ptr(inv), _s())
     return xn
+
+
+LORA_T_COLS = 32  # t / u buffers are [k, 32] (2r <= 32, zero-padded)
+
+
+def lora_pack(A, r, out=None):
+    """[h, 2r] interleaved LoRA A (fp32) -> [32, h] bf16 GEMM operand."""
+    _check(A, out)
+    h = A.shape[0]
+    if out is None:
+        out = torch.empty(LORA_T_COLS, h, dtype=BF16, device=A.device)
+    call("lemo_lora_pack", ptr(A), A.stride(0), h, 2 * r, ptr(out), _s())
+    return out
+
+
+def lora_down(xn, A_packed, t=None):
+    """t = xn · [A_q | A_v]  ([k, 32] fp32, columns >= 2r are zero)."""
+    return gemm_f32(xn, A_packed, out=t)
 
 
 def gather_rows_bf16(src, idx, out=None):
@@ -256,6 +268,32 @@ def sgemm(a, b, *, b_trans=False, relu=False, col_mask=None, out=None):
     call("lemo_sgemm", ptr(a), a.stride(0), ptr(b), b.stride(0), int(bool(b_trans)), ptr(out),
          out.stride(0), M, N, K, int(bool(relu)), ptr(col_mask), _s())
     return out
+
+
+def split_bf16x3(a, pattern, out=None):
+    """fp32 [M, K] -> bf16 [M, 3K] operand ([hi|hi|lo] pattern 0, [hi|lo|hi] pattern 1)."""
+    _check(a, out)
+    _dt(a, F32, "a")
+    M, K = a.shape
+    if out is None:
+        out = torch.empty(M, 3 * K, dtype=BF16, device=a.device)
+    call("lemo_split_bf16x3", ptr(a), a.stride(0), M, K, int(pattern), ptr(out), _s())
+    return out
+
+
+def gemm_split3(a3, b3, *, relu=False, mask=None, pattern=0, split_out=True, f32_out=False):
+    """C = act(A·Bᵀ)·mask in fp32-faithful bf16x3; returns (split C or None, fp32 C or None)."""
+    _check(a3, b3, mask)
+    M, K3 = a3.shape
+    N = b3.shape[0]
+    if b3.shape[1] != K3:
+        raise DimensionError(f"bf16x3 inner extents differ: {tuple(a3.shape)} vs {tuple(b3.shape)}")
+    out = torch.empty(M, 3 * N, dtype=BF16, device=a3.device) if split_out else None
+    f32 = torch.empty(M, N, dtype=F32, device=a3.device) if f32_out else None
+    call("lemo_gemm_split3", ptr(a3), a3.stride(0), ptr(b3), b3.stride(0), M, N, K3,
+         int(bool(relu)), ptr(mask), int(pattern), ptr(out), 0 if out is None else out.stride(0),
+         ptr(f32), 0 if f32 is None else f32.stride(0), _s())
+    return out, f32
 
 
 def colsum_clamped(S, out=None):

@@ -36,6 +36,23 @@ class Predictor:
         self.layer_id = layer_id
         self.mask1 = torch.ones(self.w1.shape[1], dtype=torch.uint8, device=dev)
         self.mask2 = torch.ones(self.w2.shape[1], dtype=torch.uint8, device=dev)
+        self._split = None
+
+    def _weights3(self):
+        """bf16x3 B-operands [N, 3K] (pattern 1) of W1ᵀ, W2ᵀ, W3ᵀ — rebuilt only
+        when the weights change (predictors are frozen during fine-tuning)."""
+        key = tuple(int(w._version) for w in (self.w1, self.w2, self.w3))
+        if self._split is None or self._split[0] != key:
+            ws = tuple(ops.split_bf16x3(w.t().contiguous(), 1) for w in (self.w1, self.w2, self.w3))
+            self._split = (key, ws)
+        return self._split[1]
+
+    def hidden3(self, x3: torch.Tensor) -> torch.Tensor:
+        """relu/mask hidden layers on a bf16x3 input; returns split h2 [M, 3 r2]."""
+        w1, w2, _ = self._weights3()
+        h1, _ = ops.gemm_split3(x3, w1, relu=True, mask=self.mask1, pattern=0)
+        h2, _ = ops.gemm_split3(h1, w2, relu=True, mask=self.mask2, pattern=0)
+        return h2
 
     @staticmethod
     def create(rng: np.random.Generator, h: int, r1: int, r2: int, d_pred: int, role: str,
@@ -63,11 +80,18 @@ class Predictor:
         return h * a1 + a1 * a2 + a2 * self.d_pred
 
     def predict(self, x: torch.Tensor) -> torch.Tensor:
-        """h1 = relu(x·W1)·m1; h2 = relu(h1·W2)·m2; out = h2·W3 (predictor.py:83-89)."""
+        """h1 = relu(x·W1)·m1; h2 = relu(h1·W2)·m2; out = h2·W3 (predictor.py:83-89),
+        fp32-faithful on bf16 tensor cores (bf16x3 tcgen05 GEMMs)."""
         x = _dev_f32(x, self.w1.device)
-        h1 = ops.sgemm(x, self.w1, relu=True, col_mask=self.mask1)
-        h2 = ops.sgemm(h1, self.w2, relu=True, col_mask=self.mask2)
-        return ops.sgemm(h2, self.w3)
+        h2 = self.hidden3(ops.split_bf16x3(x, 0))
+        _, out = ops.gemm_split3(h2, self._weights3()[2], split_out=False, f32_out=True)
+        return out
+
+    def predict3(self, x3: torch.Tensor, pattern: int) -> torch.Tensor:
+        """Predictor output in split form (pattern 0: A-side, 1: B-side of Eq. 3)."""
+        h2 = self.hidden3(x3)
+        out, _ = ops.gemm_split3(h2, self._weights3()[2], pattern=pattern)
+        return out
 
     forward = predict
 
@@ -113,9 +137,18 @@ def pair_block_outputs(p_q: Predictor, p_k: Predictor, x, block_size: int, pooli
 
 
 def predicted_dense(p_q, p_k, x, block_size: int, pooling: str = "mean") -> torch.Tensor:
-    """Dense eq·ekᵀ [nb, nb] (unclamped)."""
-    eq, ek = pair_block_outputs(p_q, p_k, x, block_size, pooling)
-    return ops.sgemm(eq, ek, b_trans=True)
+    """Dense eq·ekᵀ [nb, nb] fp32 (unclamped), every product on tcgen05 in
+    fp32-faithful bf16x3 form.  mean pooling: block_embed → split → 2×3
+    predictor GEMMs → Eq. 3 GEMM, no fp32 round trip between them."""
+    if pooling == "mean":
+        xb = block_embed(x, block_size)
+        x3 = ops.split_bf16x3(xb, 0)
+        eq3 = p_q.predict3(x3, 0)
+        ek3 = p_k.predict3(x3, 1)
+    else:
+        eq, ek = pair_block_outputs(p_q, p_k, x, block_size, pooling)
+        eq3, ek3 = ops.split_bf16x3(eq, 0), ops.split_bf16x3(ek, 1)
+    return ops.gemm_f32(eq3, ek3)
 
 
 def predicted_triangle(p_q, p_k, x, block_size: int, pooling: str = "mean") -> torch.Tensor:
@@ -138,7 +171,7 @@ def predict_scores(p_q: Predictor, p_k: Predictor, x_blocks, *, layer_id=None) -
         raise ContractError(f"predictor output dims differ: {p_q.d_pred} vs {p_k.d_pred}")
     eq = p_q.predict(x_blocks)
     ek = p_k.predict(x_blocks)
-    full = ops.sgemm(eq, ek, b_trans=True)
+    full = ops.gemm_f32(ops.split_bf16x3(eq, 0), ops.split_bf16x3(ek, 1))
     nb = full.shape[0]
     r, c = torch.tril_indices(nb, nb, device=full.device)
     packed = torch.clamp_min(full[r, c], 0.0)

@@ -104,12 +104,14 @@ def test_predictor_golden(cuda):
     pk.set_masks(z["k_m1"], z["k_m2"])
     x = torch.as_tensor(z["x"]).cuda()
     b = int(z["b"])
+    # fp32-faithful bf16x3 products: |err| <= 1e-5 of the output scale
+    scale = np.abs(z["packed"]).max()
     np.testing.assert_allclose(P.predicted_triangle(pq, pk, x, b).cpu().numpy(), z["packed"],
-                               rtol=1e-5, atol=1e-6)
+                               rtol=1e-5, atol=1e-5 * scale)
     np.testing.assert_allclose(P.predicted_triangle(pq, pk, x, b, "token").cpu().numpy(),
-                               z["packed_token"], rtol=1e-5, atol=1e-6)
+                               z["packed_token"], rtol=1e-5, atol=1e-5 * scale)
     np.testing.assert_allclose(P.predicted_block_vector(pq, pk, x, b).cpu().numpy(), z["vec"],
-                               rtol=1e-5, atol=1e-6)
+                               rtol=1e-5, atol=1e-5 * np.abs(z["vec"]).max())
 
 
 def test_sgemm_vs_torch(cuda):
@@ -224,14 +226,16 @@ def test_rmsnorm_gather_lora(cuda):
     k = idx.numel()
     xg = torch.empty(k, h, dtype=torch.bfloat16, device=cuda)
     inv = torch.empty(k, device=cuda)
-    t = torch.empty(k, 2 * r, device=cuda)
-    xn = ops.rmsnorm_gather(x, w, idx, xg=xg, inv=inv, A=A, r=r, t=t)
+    xn = ops.rmsnorm_gather(x, w, idx, xg=xg, inv=inv)
+    t = ops.lora_down(xn, ops.lora_pack(A, r))
     xr = x[idx.long()]
     invr = 1 / torch.sqrt((xr * xr).mean(-1, keepdim=True) + 1e-6)
     xnr = xr * invr * w
     torch.testing.assert_close(xn.float(), xnr, rtol=1e-2, atol=1e-2)
     torch.testing.assert_close(inv, invr[:, 0], rtol=1e-5, atol=1e-6)
-    torch.testing.assert_close(t, xnr @ A, rtol=1e-4, atol=1e-4)
+    assert t.shape == (k, 32) and float(t[:, 2 * r:].abs().max()) == 0.0
+    torch.testing.assert_close(t[:, :2 * r], xn.float() @ A.bfloat16().float(), rtol=1e-3,
+                               atol=1e-3)
     torch.testing.assert_close(xg.float(), xr, rtol=1e-2, atol=1e-2)
 
 
