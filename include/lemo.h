@@ -53,16 +53,26 @@ int lemo_gemm_scatter_add(const void* A, int lda, const void* B, int ldb, float*
                           const int* idx, int M, int N, int K, void* stream);
 
 /* Fused q/k/v projection of attention_core (kernels.py:103-114):
- *   [q|k|v] = xn · W_qkv  (+ scale·(xn·A_q)·B_q on q, + scale·(xn·A_v)·B_v on v)
- *   then rope_rotate (tensor.py:610-634) at pos[i] (original token positions).
- * w_qkv_t: [3h, h] bf16 (rows = output features; nmat = 2 computes q, k only,
- * as layer_qk does, model.py:356-368); tq/tv: [M, ldt] fp32 = xn·A;
- * Bq/Bv: [r, h] fp32; rope_tab: [max_pos, head_dim/2] float2 (cos, sin). */
-int lemo_gemm_qkv(const void* xn, const void* w_qkv_t, int M, int h, int nmat, void* q, void* k,
-                  void* v,
-                  int head_dim, int rope, const void* rope_tab, const int* pos, const float* tq,
-                  const float* tv, int ldt, int r, const float* Bq, const float* Bv, float scale,
-                  void* stream);
+ *   [q|k|v] = xn_ext · w_qkv_tᵀ over K columns, then rope_rotate
+ *   (tensor.py:610-634) of q, k at pos[i] (original token positions).
+ * With LoRA, K = h + 64: xn_ext = [xn | s·(xn·A_q) | s·(xn·A_v) | 0]
+ * (lemo_lora_qkv_prep) and w_qkv_t = [W_qkvᵀ | B_qᵀ, B_vᵀ | 0]
+ * (lemo_lora_pack_b), so q = xn·Wq + s·(xn·A_q)·B_q (kernels.py:95-100) is
+ * accumulated by the tensor core itself.  Without LoRA, K = h.
+ * w_qkv_t: [nmat·h, ldw] bf16 (nmat = 2: q, k only, as layer_qk does,
+ * model.py:356-368); inv_freq: [head_dim/2] float64 = base^(-j/half). */
+int lemo_gemm_qkv(const void* xn, int ldx, const void* w_qkv_t, int ldw, int M, int h, int K,
+                  int nmat, void* q, void* k, void* v, int head_dim, int rope,
+                  const double* inv_freq, const int* pos, void* stream);
+
+/* A-side LoRA K-extension: xn_ext[i, h+j] = bf16(scale·t[i, j]) (j < r2), 0 up to 64. */
+int lemo_lora_qkv_prep(const float* t, int ldt, int M, int r2, float scale, void* xn_ext, int ldx,
+                       int h, void* stream);
+
+/* B-side LoRA K-extension of w_qkv_t [3h, ldw]: columns h..h+63 ← B_qᵀ (q rows),
+ * B_vᵀ (v rows, offset r), zeros elsewhere.  Re-run after every optimizer step. */
+int lemo_lora_pack_b(const float* Bq, const float* Bv, int h, int r, void* w_ext, int ldw,
+                     void* stream);
 
 /* Gate/up half of mlp_core (kernels.py:119-124) with the MLP token
  * informativeness (model.py:371-396, sparsity.py:284-290) in the epilogue.
@@ -84,7 +94,7 @@ int lemo_gemm_dgateup(const void* dy, const void* w_down, int M, int m_pad, int 
 /* Fused gather + RMSNorm (tensor.py:578-597; idx NULL = all rows): xn (bf16)
  * plus optional saved raw rows xg (bf16) and inv (fp32). */
 int lemo_rmsnorm_gather(const float* x, int ldx, const int* idx, int M, int h, const float* w,
-                        void* xn, void* xg, float* inv, void* stream);
+                        void* xn, int ldxn, void* xg, float* inv, void* stream);
 
 /* LoRA down-projection operand: out[j, c] = bf16(A[c*lda + j]) for j < r2,
  * zero for r2 <= j < 32 (out: [32, h] bf16), so t = xn·[A_q|A_v]

@@ -157,29 +157,24 @@ struct EpiScatterAdd {
   }
 };
 
-// Fused q/k/v projection epilogue: + LoRA side term (q, v) then rotary
-// rotation at the retained tokens' ORIGINAL positions pos[row]
-// (kernels.py:109-114, tensor.py:604-634).  Tile never straddles q/k/v.
+// Fused q/k/v projection epilogue (kernels.py:103-114).  The LoRA terms are
+// already inside the accumulator: the GEMM runs over K = h + 64 with
+// A = [xn | s·t_q | s·t_v | 0] and B = [W | B_qᵀ / B_vᵀ | 0] (lemo_lora_qkv_prep,
+// lemo_lora_pack_b), so the epilogue only rotates q and k at the retained
+// tokens' ORIGINAL positions (tensor.py:604-634).  cos/sin are computed on the
+// fly: angle = pos · inv_freq in float64 (the reference's precision), reduced
+// mod 2π in float64, then fp32 sincos of the reduced angle — no table gathers.
 struct EpiQKV {
   __nv_bfloat16 *q, *k, *v;
   int h, head_dim, rope;
-  const float2* rope_tab;  // [max_pos, head_dim/2] (cos, sin), f64-derived
+  const double* inv_freq;  // [head_dim/2]
   const int* pos;
-  const float *tq, *tv;  // [M, ldt] LoRA x·A factors
-  int ldt, r;
-  const float *Bq, *Bv;  // [r, h]
-  float scale;
   template <int BN>
   __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
     const int which = col0 / h;
     const int cbase = col0 - which * h;
     __nv_bfloat16* out = which == 0 ? q : (which == 1 ? k : v);
-    const float* U = which == 0 ? tq : (which == 2 ? tv : nullptr);
-    const float* S = which == 0 ? Bq : Bv;
-    const int R = U ? r : 0;
-    float u[kMaxSideRank];
-    load_side_u(u, U, ldt, R, row, valid);
-    const int p = valid && rope ? __ldg(pos + row) : 0;
+    const double dp = (valid && rope) ? (double)__ldg(pos + row) : 0.0;
     const int half = head_dim >> 1;
 #pragma unroll 1
     for (int hd = 0; hd < BN; hd += head_dim) {
@@ -190,16 +185,17 @@ struct EpiQKV {
         load_chunk(taddr + hd + half + cp, b);
         if (!valid) continue;
         const int ca = cbase + hd + cp, cb = ca + half;
-        add_side(a, u, R, S, h, 1, ca, scale);
-        add_side(b, u, R, S, h, 1, cb, scale);
         if (rope && which < 2) {  // only q and k are rotated (kernels.py:112-114)
-          const float2* tab = rope_tab + (size_t)p * half + cp;
-#pragma unroll
+#pragma unroll 4
           for (int i = 0; i < 32; ++i) {
-            const float2 cs = __ldg(tab + i);
+            const double ang = dp * __ldg(inv_freq + cp + i);
+            const double kq = rint(ang * 0.15915494309189535);
+            const float red = (float)fma(-kq, 6.283185307179586476925, ang);
+            float sn, cs;
+            sincosf(red, &sn, &cs);
             const float xa = a[i], xb = b[i];
-            a[i] = xa * cs.x - xb * cs.y;
-            b[i] = xa * cs.y + xb * cs.x;
+            a[i] = xa * cs - xb * sn;
+            b[i] = xa * sn + xb * cs;
           }
         }
         store_bf16x32(out + (size_t)row * h + ca, a);
@@ -423,22 +419,18 @@ int lemo_gemm_scatter_add(const void* A, int lda, const void* B, int ldb, float*
                  gemm_auto(A, lda, B, ldb, M, N, K, e, (cudaStream_t)stream));
 }
 
-int lemo_gemm_qkv(const void* xn, const void* w_qkv_t, int M, int h, int nmat, void* q, void* k,
-                  void* v,
-                  int head_dim, int rope, const void* rope_tab, const int* pos, const float* tq,
-                  const float* tv, int ldt, int r, const float* Bq, const float* Bv, float scale,
-                  void* stream) {
+int lemo_gemm_qkv(const void* xn, int ldx, const void* w_qkv_t, int ldw, int M, int h, int K,
+                  int nmat, void* q, void* k, void* v, int head_dim, int rope,
+                  const double* inv_freq, const int* pos, void* stream) {
   LEMO_ARG_CHECK(head_dim % 64 == 0, "lemo_gemm_qkv: head_dim must be a multiple of 64");
   LEMO_ARG_CHECK(nmat == 2 || nmat == 3, "lemo_gemm_qkv: nmat must be 2 (q,k) or 3 (q,k,v)");
-  LEMO_ARG_CHECK(r >= 0 && r <= kMaxSideRank, "lemo_gemm_qkv: LoRA rank too large");
   EpiQKV e{reinterpret_cast<__nv_bfloat16*>(q), reinterpret_cast<__nv_bfloat16*>(k),
-           reinterpret_cast<__nv_bfloat16*>(v), h, head_dim, rope,
-           reinterpret_cast<const float2*>(rope_tab), pos, tq, tv, ldt, r, Bq, Bv, scale};
+           reinterpret_cast<__nv_bfloat16*>(v), h, head_dim, rope, inv_freq, pos};
   int rc;
   if (h % 256 == 0 && 256 % head_dim == 0)
-    rc = gemm<256>(xn, h, w_qkv_t, h, M, nmat * h, h, e, (cudaStream_t)stream);
+    rc = gemm<256>(xn, ldx, w_qkv_t, ldw, M, nmat * h, K, e, (cudaStream_t)stream);
   else if (h % 128 == 0 && 128 % head_dim == 0)
-    rc = gemm<128>(xn, h, w_qkv_t, h, M, nmat * h, h, e, (cudaStream_t)stream);
+    rc = gemm<128>(xn, ldx, w_qkv_t, ldw, M, nmat * h, K, e, (cudaStream_t)stream);
   else {
     set_error_msg("lemo_gemm_qkv: hidden dim must be a multiple of 128 and of head_dim");
     return LEMO_ERR_REPORTED;

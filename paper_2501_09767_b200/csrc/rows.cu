@@ -32,8 +32,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 template <int VPT>
 __global__ void __launch_bounds__(128) gather_rmsnorm_kernel(
     const float* __restrict__ x, int ldx, const int* __restrict__ idx, int h,
-    const float* __restrict__ w, __nv_bfloat16* __restrict__ xn, __nv_bfloat16* __restrict__ xg,
-    float* __restrict__ inv_out) {
+    const float* __restrict__ w, __nv_bfloat16* __restrict__ xn, int ldxn,
+    __nv_bfloat16* __restrict__ xg, float* __restrict__ inv_out) {
   __shared__ float red[4];
   const int row = blockIdx.x;
   const int src = idx ? __ldg(idx + row) : row;
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(128) gather_rmsnorm_kernel(
     o.z = v[i].z * inv * ww.z;
     o.w = v[i].w * inv * ww.w;
     uint2 ob = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
-    reinterpret_cast<uint2*>(xn + (size_t)row * h)[c] = ob;
+    reinterpret_cast<uint2*>(xn + (size_t)row * ldxn)[c] = ob;
     if (xg) {
       reinterpret_cast<uint2*>(xg + (size_t)row * h)[c] =
           make_uint2(pack_bf16x2(v[i].x, v[i].y), pack_bf16x2(v[i].z, v[i].w));
@@ -79,6 +79,29 @@ __global__ void lora_pack_kernel(const float* __restrict__ A, int lda, int h, in
 #pragma unroll 4
   for (int j = 0; j < 32; ++j)
     out[(size_t)j * h + c] = __float2bfloat16_rn(j < r2 ? A[(size_t)c * lda + j] : 0.f);
+}
+
+// LoRA as a K-extension of the q/k/v GEMM (64 extra K columns):
+//   A-side: xn_ext[i, h + j] = bf16(scale · t[i, j]) for j < 2r, 0 for 2r <= j < 64
+//   B-side: w_ext[c, h + j]          = bf16(Bq[j, c])   (q rows, j < r)
+//           w_ext[2h + c, h + r + j] = bf16(Bv[j, c])   (v rows, j < r), all else 0
+__global__ void lora_qkv_prep_kernel(const float* __restrict__ t, int ldt, int M, int r2,
+                                     float scale, __nv_bfloat16* __restrict__ xn, int ldx,
+                                     int h) {
+  const int i = blockIdx.x * 4 + (threadIdx.x >> 6), j = threadIdx.x & 63;
+  if (i >= M) return;
+  xn[(size_t)i * ldx + h + j] = __float2bfloat16_rn(j < r2 ? scale * t[(size_t)i * ldt + j] : 0.f);
+}
+
+__global__ void lora_pack_b_kernel(const float* __restrict__ Bq, const float* __restrict__ Bv,
+                                   int h, int r, __nv_bfloat16* __restrict__ w, int ldw) {
+  const int row = blockIdx.x;  // 0 .. 3h-1
+  const int j = threadIdx.x;   // 0 .. 63
+  const int which = row / h, c = row - which * h;
+  float val = 0.f;
+  if (which == 0 && j < r) val = Bq[(size_t)j * h + c];
+  if (which == 2 && j >= r && j < 2 * r) val = Bv[(size_t)(j - r) * h + c];
+  w[(size_t)row * ldw + h + j] = __float2bfloat16_rn(val);
 }
 
 // dst[i] = bf16(src[idx[i]])
@@ -399,7 +422,8 @@ using namespace lemo;
 extern "C" {
 
 int lemo_rmsnorm_gather(const float* x, int ldx, const int* idx, int M, int h, const float* w,
-                        void* xn, void* xg, float* inv, void* stream) {
+                        void* xn, int ldxn, void* xg, float* inv, void* stream) {
+  LEMO_ARG_CHECK(ldxn % 4 == 0 && ldxn >= h, "lemo_rmsnorm_gather: bad xn row stride");
   if (M <= 0) return 0;
   LEMO_ARG_CHECK(h % 4 == 0 && ldx % 4 == 0, "lemo_rmsnorm_gather: h, ldx must be multiples of 4");
   LEMO_ARG_CHECK(h <= 4 * 128 * 16, "lemo_rmsnorm_gather: h too large");
@@ -408,7 +432,8 @@ int lemo_rmsnorm_gather(const float* x, int ldx, const int* idx, int M, int h, c
   cudaStream_t st = (cudaStream_t)stream;
   auto* xnp = reinterpret_cast<__nv_bfloat16*>(xn);
   auto* xgp = reinterpret_cast<__nv_bfloat16*>(xg);
-#define LAUNCH(V) gather_rmsnorm_kernel<V><<<M, 128, 0, st>>>(x, ldx, idx, h, w, xnp, xgp, inv)
+#define LAUNCH(V) \
+  gather_rmsnorm_kernel<V><<<M, 128, 0, st>>>(x, ldx, idx, h, w, xnp, ldxn, xgp, inv)
   if (vpt <= 1) LAUNCH(1);
   else if (vpt <= 2) LAUNCH(2);
   else if (vpt <= 4) LAUNCH(4);
@@ -416,6 +441,25 @@ int lemo_rmsnorm_gather(const float* x, int ldx, const int* idx, int M, int h, c
   else LAUNCH(16);
 #undef LAUNCH
   LEMO_CHECK_LAUNCH("lemo_rmsnorm_gather");
+  return 0;
+}
+
+int lemo_lora_qkv_prep(const float* t, int ldt, int M, int r2, float scale, void* xn_ext, int ldx,
+                       int h, void* stream) {
+  if (M <= 0) return 0;
+  LEMO_ARG_CHECK(r2 <= 64 && ldx >= h + 64, "lemo_lora_qkv_prep: need 64 extension columns");
+  lora_qkv_prep_kernel<<<(M + 3) / 4, 256, 0, (cudaStream_t)stream>>>(
+      t, ldt, M, r2, scale, reinterpret_cast<__nv_bfloat16*>(xn_ext), ldx, h);
+  LEMO_CHECK_LAUNCH("lemo_lora_qkv_prep");
+  return 0;
+}
+
+int lemo_lora_pack_b(const float* Bq, const float* Bv, int h, int r, void* w_ext, int ldw,
+                     void* stream) {
+  LEMO_ARG_CHECK(2 * r <= 64 && ldw >= h + 64, "lemo_lora_pack_b: need 64 extension columns");
+  lora_pack_b_kernel<<<3 * h, 64, 0, (cudaStream_t)stream>>>(
+      Bq, Bv, h, r, reinterpret_cast<__nv_bfloat16*>(w_ext), ldw);
+  LEMO_CHECK_LAUNCH("lemo_lora_pack_b");
   return 0;
 }
 

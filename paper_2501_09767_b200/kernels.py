@@ -128,15 +128,13 @@ def attention_forward(x: torch.Tensor, plan: GatherPlan, layer, *, save: bool = 
     dev = x.device
     idx = plan.indices
     r = layer.lora_rank
-    xn = torch.empty(k, h, dtype=BF16, device=dev)
+    xn = torch.empty(k, layer.w_qkv_t.shape[1], dtype=BF16, device=dev)  # [xn | LoRA ext]
     xg = torch.empty(k, h, dtype=BF16, device=dev) if save else None
     inv = torch.empty(k, dtype=F32, device=dev) if save else None
     ops.rmsnorm_gather(x, layer.attn_norm_w, idx, xn=xn, xg=xg, inv=inv)
-    t = ops.lora_down(xn, layer.lora_A_packed()) if r else None
+    t = layer.qkv_input(xn) if r else None
     q, kk, v = ops.gemm_qkv(xn, layer.w_qkv_t, h=h, head_dim=layer.head_dim, rope=layer.rope,
-                            rope_tab=layer.rope_tab, pos=idx, t=t, r=r,
-                            Bq=layer.lora_Bq if r else None, Bv=layer.lora_Bv if r else None,
-                            scale=layer.lora_scaling)
+                            inv_freq=layer.inv_freq, pos=idx)
     del xn
     o, lse = ops.flash_fwd(q, kk, v, head_dim=layer.head_dim, scale=1.0 / math.sqrt(layer.head_dim))
     ops.gemm_scatter_add(o, layer.w_o_t, x, idx)

@@ -174,7 +174,11 @@ class LayerState:
         wq, wk, wv, wo = g("wq"), g("wk"), g("wv"), g("wo")
         w_qkv = torch.cat([wq, wk, wv], dim=1)  # [h, 3h]   (x·W layout)
         self.w_qkv = w_qkv.to(BF16).contiguous()
-        self.w_qkv_t = w_qkv.t().contiguous().to(BF16)
+        # forward operand [3h, h (+64 LoRA K-extension columns, see lemo_gemm_qkv)]
+        kext = ops.LORA_K_EXT if cfg.lora_rank else 0
+        self.w_qkv_t = torch.zeros(3 * h, h + kext, dtype=BF16, device=dev)
+        self.w_qkv_t[:, :h] = w_qkv.t().to(BF16)
+        self.inv_freq = model.inv_freq
         self.w_o = wo.to(BF16).contiguous()
         self.w_o_t = wo.t().contiguous().to(BF16)
         w_up = g("w_up")
@@ -222,6 +226,16 @@ class LayerState:
         """[32, h] bf16 copy of [A_q | A_v] for the t = xn·A GEMM (re-packed each
         call: the adapters change every optimizer step)."""
         return ops.lora_pack(self.lora_A, self.lora_rank)
+
+    def qkv_input(self, xn_ext: torch.Tensor) -> torch.Tensor:
+        """Complete the q/k/v GEMM operands for LoRA (kernels.py:95-100): t = xn·A
+        (fp32, saved for backward), s·t into xn_ext's 64 extension columns and
+        the current B_q/B_v into the weight's extension columns.  Returns t."""
+        h, r = self.w_qkv.shape[0], self.lora_rank
+        t = ops.lora_down(xn_ext[:, :h], self.lora_A_packed())
+        ops.lora_qkv_prep(t, r, self.lora_scaling, xn_ext, h)
+        ops.lora_pack_b(self.lora_Bq, self.lora_Bv, r, self.w_qkv_t, h)
+        return t
 
     def grad_views(self, flat_grad):
         return self._views(flat_grad) if self.lora_rank else None
@@ -313,6 +327,9 @@ class DecoderModel:
         h, r, L = cfg.hidden_dim, cfg.lora_rank, cfg.n_layers
         self.rope_tab = rope_table(cfg.max_seq_len, cfg.head_dim, cfg.rope_base, dev) \
             if cfg.positions == "rope" else None
+        half = cfg.head_dim // 2
+        self.inv_freq = torch.as_tensor(
+            cfg.rope_base ** (-np.arange(half, dtype=np.float64) / half)).to(dev)
         self.lora_param = torch.zeros(max(4 * h * r * L, 1), dtype=F32, device=dev)
         if arrays is None and init == "reference":
             arrays = reference_init_arrays(cfg, seed)
@@ -587,13 +604,13 @@ def layer_qk(layer: LayerState, x: torch.Tensor):
     """model.py:356-368: post-rotation Q (with LoRA) and K (without), [s, h] bf16."""
     s, h = x.shape
     r = layer.lora_rank
-    xn = ops.rmsnorm_gather(x, layer.attn_norm_w, None)
-    t = ops.lora_down(xn, layer.lora_A_packed()) if r else None
+    xn = torch.empty(s, layer.w_qkv_t.shape[1], dtype=BF16, device=x.device)
+    ops.rmsnorm_gather(x, layer.attn_norm_w, None, xn=xn)
+    if r:
+        layer.qkv_input(xn)
     pos = torch.arange(s, dtype=torch.int32, device=x.device)
     q, k = ops.gemm_qkv(xn, layer.w_qkv_t, h=h, head_dim=layer.head_dim, rope=layer.rope,
-                        rope_tab=layer.rope_tab, pos=pos, t=t, r=r,
-                        Bq=layer.lora_Bq if r else None, Bv=None, scale=layer.lora_scaling,
-                        nmat=2)
+                        inv_freq=layer.inv_freq, pos=pos, nmat=2)
     return q, k
 
 

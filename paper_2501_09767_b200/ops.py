@@ -96,21 +96,19 @@ def gemm_scatter_add(a, b, resid, idx=None):
     return resid
 
 
-def gemm_qkv(xn, w_qkv_t, *, h, head_dim, rope, rope_tab, pos, t=None, r=0, Bq=None, Bv=None,
-             scale=1.0, nmat=3, out=None):
-    """q, k(, v) = rope(xn·W (+LoRA)) at positions pos — see lemo_gemm_qkv."""
-    M = xn.shape[0]
-    _check(xn, w_qkv_t, pos, t, Bq, Bv)
+def gemm_qkv(xn, w_qkv_t, *, h, head_dim, rope, inv_freq, pos, nmat=3, out=None):
+    """q, k(, v) = rope(xn·Wᵀ) at positions pos over K = xn.shape[1] columns
+    (h, or h + 64 with the LoRA K-extension) — see lemo_gemm_qkv."""
+    M, K = xn.shape
+    _check(xn, w_qkv_t, pos, inv_freq)
+    if w_qkv_t.shape[1] < K or w_qkv_t.shape[0] < nmat * h:
+        raise DimensionError("q/k/v weight does not cover the requested output")
     if out is None:
         out = [torch.empty(M, h, dtype=BF16, device=xn.device) for _ in range(nmat)]
     q, k = out[0], out[1]
     v = out[2] if nmat == 3 else None
-    tq = t
-    tv = None if t is None else t[:, r:]
-    call("lemo_gemm_qkv", ptr(xn), ptr(w_qkv_t), M, h, nmat, ptr(q), ptr(k), ptr(v), head_dim,
-         int(bool(rope)), ptr(rope_tab), ptr(pos), ptr(tq), ptr(tv),
-         0 if t is None else t.stride(0), r if t is not None else 0, ptr(Bq), ptr(Bv),
-         float(scale), _s())
+    call("lemo_gemm_qkv", ptr(xn), xn.stride(0), ptr(w_qkv_t), w_qkv_t.stride(0), M, h, K, nmat,
+         ptr(q), ptr(k), ptr(v), head_dim, int(bool(rope)), ptr(inv_freq), ptr(pos), _s())
     return out
 
 
@@ -141,9 +139,25 @@ def rmsnorm_gather(x, w, idx=None, *, xn=None, xg=None, inv=None):
     h = x.shape[1]
     if xn is None:
         xn = torch.empty(M, h, dtype=BF16, device=x.device)
-    call("lemo_rmsnorm_gather", ptr(x), x.stride(0), ptr(idx), M, h, ptr(w), ptr(xn), ptr(xg),
-         ptr(inv), _s())
+    call("lemo_rmsnorm_gather", ptr(x), x.stride(0), ptr(idx), M, h, ptr(w), ptr(xn),
+         xn.stride(0), ptr(xg), ptr(inv), _s())
     return xn
+
+
+LORA_K_EXT = 64  # extra K columns of the q/k/v GEMM carrying the LoRA terms
+
+
+def lora_qkv_prep(t, r, scale, xn_ext, h):
+    """xn_ext[:, h:h+64] = [s·t_q | s·t_v | 0] (bf16)."""
+    _check(t, xn_ext)
+    call("lemo_lora_qkv_prep", ptr(t), t.stride(0), xn_ext.shape[0], 2 * r, float(scale),
+         ptr(xn_ext), xn_ext.stride(0), h, _s())
+
+
+def lora_pack_b(Bq, Bv, r, w_ext, h):
+    """w_ext[:, h:h+64] = [B_qᵀ | B_vᵀ | 0] on the q / v rows (bf16)."""
+    _check(Bq, Bv, w_ext)
+    call("lemo_lora_pack_b", ptr(Bq), ptr(Bv), h, r, ptr(w_ext), w_ext.stride(0), _s())
 
 
 LORA_T_COLS = 32  # t / u buffers are [k, 32] (2r <= 32, zero-padded)

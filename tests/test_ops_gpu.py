@@ -281,18 +281,22 @@ def test_qkv_rope_lora_vs_oracle(cuda):
     L = model.layers[0]
     L.lora_q.b.copy_(torch.randn(r, h, device=cuda) * 0.1)
     L.lora_v.b.copy_(torch.randn(r, h, device=cuda) * 0.1)
-    xn = torch.as_tensor(rng.standard_normal((M, h)).astype(np.float32)).cuda().bfloat16()
+    xn_ext = torch.empty(M, h + 64, dtype=torch.bfloat16, device=cuda)
+    xn_ext[:, :h] = torch.as_tensor(rng.standard_normal((M, h)).astype(np.float32)).cuda().bfloat16()
+    xn = xn_ext[:, :h]
     pos_np = np.sort(rng.choice(1000, M, replace=False))
     pos = torch.as_tensor(pos_np.astype(np.int32)).cuda()
-    t = (xn.float() @ L.lora_A).contiguous()
-    q, k, v = ops.gemm_qkv(xn, L.w_qkv_t, h=h, head_dim=d, rope=True, rope_tab=L.rope_tab, pos=pos,
-                           t=t, r=r, Bq=L.lora_Bq, Bv=L.lora_Bv, scale=L.lora_scaling)
+    t = L.qkv_input(xn_ext)
+    q, k, v = ops.gemm_qkv(xn_ext, L.w_qkv_t, h=h, head_dim=d, rope=True, inv_freq=L.inv_freq,
+                           pos=pos)
     xf = xn.float().cpu().numpy()
     W = L.w_qkv.float().cpu().numpy()
     s = L.lora_scaling
+    np.testing.assert_allclose(t[:, :2 * r].cpu().numpy(),
+                               xf @ L.lora_A.bfloat16().float().cpu().numpy(), rtol=1e-3, atol=1e-3)
     qr = xf @ W[:, :h] + (t[:, :r].cpu().numpy() @ L.lora_Bq.cpu().numpy()) * s
     kr = xf @ W[:, h:2 * h]
-    vr = xf @ W[:, 2 * h:] + (t[:, r:].cpu().numpy() @ L.lora_Bv.cpu().numpy()) * s
+    vr = xf @ W[:, 2 * h:] + (t[:, r:2 * r].cpu().numpy() @ L.lora_Bv.cpu().numpy()) * s
     qr = O.rope_fwd(qr.astype(np.float32), pos_np, H, 10000.0)
     kr = O.rope_fwd(kr.astype(np.float32), pos_np, H, 10000.0)
     for got, ref in ((q, qr), (k, kr), (v, vr)):
