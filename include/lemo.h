@@ -39,6 +39,10 @@ void lemo_clear_descriptor_cache(void);
 int lemo_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N,
                    int K, void* stream);
 
+/* C(bf16) = A·B with B [K, N] row-major (MN-major tcgen05 B operand). */
+int lemo_gemm_nn_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M,
+                      int N, int K, void* stream);
+
 /* C(f32) (+)= A·Bᵀ + scale · U[M,R] · S  where S(j, col) = S[j*s_rs + col*s_cs]
  * (rank-R side product = the LoRA term of kernels.py:95-100; R = 0 disables it). */
 int lemo_gemm_f32(const void* A, int lda, const void* B, int ldb, float* C, int ldc, int M, int N,
@@ -212,6 +216,22 @@ int lemo_exact_block_scores(const void* q, const void* k, int s, int h, int head
  * side by side); o [n, h] bf16, lse [h/head_dim, n] fp32 (natural log). */
 int lemo_flash_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int n, int h,
                    int head_dim, float scale, void* stream);
+
+/* Same contract as lemo_flash_fwd on the tcgen05 path (TMA, TMEM S/O
+ * accumulators, single-thread MMA issue); head_dim must be 128. */
+int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float* lse, int n,
+                      int h, int head_dim, float scale, void* stream);
+
+/* delta[hd, i] = Σ_d dO[i, hd·D + d] · O[i, hd·D + d]  (tensor.py:696). */
+int lemo_attn_delta(const void* o, const void* dout, float* delta, int n, int h, int head_dim,
+                    void* stream);
+
+/* Attention backward on the tcgen05 path (head_dim 128): an atomic-free dK/dV
+ * kernel (transposed formulation, dK/dV resident in TMEM) and a dQ kernel,
+ * both recomputing P from lse.  Same contract as lemo_flash_bwd. */
+int lemo_flash_bwd_tc(const void* q, const void* k, const void* v, const void* o,
+                      const void* dout, const float* lse, float* delta, float* dq, float* dk,
+                      float* dv, int n, int h, int head_dim, float scale, void* stream);
 
 /* Attention backward (tensor.py:693-722): dq/dk/dv fp32 [n, h]; delta is a
  * caller workspace [h/head_dim, n] fp32. */

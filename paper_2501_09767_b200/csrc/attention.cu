@@ -483,6 +483,16 @@ int lemo_flash_fwd(const void* q, const void* k, const void* v, void* o, float* 
   return 0;
 }
 
+int lemo_attn_delta(const void* o, const void* dout, float* delta, int n, int h, int head_dim,
+                    void* stream) {
+  if (n <= 0) return 0;
+  flash_bwd_delta_kernel<<<n, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout),
+      delta, n, h, head_dim);
+  LEMO_CHECK_LAUNCH("lemo_attn_delta");
+  return 0;
+}
+
 int lemo_flash_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
                    const float* lse, float* delta, float* dq, float* dk, float* dv, int n, int h,
                    int head_dim, float scale, void* stream) {

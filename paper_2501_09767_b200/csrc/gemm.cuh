@@ -59,7 +59,7 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int num_m, int num_n) {
 // address of (this warp's lane base, first accumulator column of the tile).
 // The functor must issue the same sequence of tcgen05.ld for every lane of
 // the warp (they are warp-collective) and only store when `valid`.
-template <int BN, class Epi>
+template <int BN, class Epi, bool kBMN = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int M, int N, int K, Epi epi) {
@@ -114,8 +114,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
           tma_load_2d(&tmA, &full_bar[stage], smem_a + stage * Cfg::kABytes, kb * kBlockK,
                       tc.m * kBlockM);
-          tma_load_2d(&tmB, &full_bar[stage], smem_b + stage * Cfg::kBBytes, kb * kBlockK,
-                      tc.n * BN);
+          if constexpr (!kBMN) {
+            tma_load_2d(&tmB, &full_bar[stage], smem_b + stage * Cfg::kBBytes, kb * kBlockK,
+                        tc.n * BN);
+          } else {  // B is [K, N] (N contiguous): BN/64 MN-atoms of 64 N x 64 K
+#pragma unroll
+            for (int a = 0; a < BN / 64; ++a)
+              tma_load_2d(&tmB, &full_bar[stage], smem_b + stage * Cfg::kBBytes + a * 8192,
+                          tc.n * BN + a * 64, kb * kBlockK);
+          }
           if (++stage == Cfg::kStages) {
             stage = 0;
             phase ^= 1;
@@ -125,7 +132,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread) ----------------
-    constexpr uint32_t idesc = umma_idesc_bf16(kBlockM, BN);
+    constexpr uint32_t idesc = umma_idesc_bf16(kBlockM, BN, 0, kBMN ? 1 : 0);
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
@@ -145,7 +152,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int k = 0; k < kBlockK / kUmmaK; ++k) {
             // advancing K inside the 128-B swizzle atom = +32 B on the start address
             const uint64_t da = umma_desc_k_sw128(a_addr + k * kUmmaK * 2);
-            const uint64_t db = umma_desc_k_sw128(b_addr + k * kUmmaK * 2);
+            const uint64_t db = kBMN ? umma_desc_mn_sw128(b_addr + k * 2048, 8192)
+                                     : umma_desc_k_sw128(b_addr + k * kUmmaK * 2);
             umma_bf16_ss(d_tmem, da, db, idesc, (kb | k) != 0 ? 1u : 0u);
           }
           umma_commit(&empty_bar[stage]);
@@ -197,7 +205,7 @@ int make_tma_bf16_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t
 
 int gemm_num_sms();
 
-template <int BN, class Epi>
+template <int BN, class Epi, bool kBMN = false>
 int launch_gemm_tn(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
                    const Epi& epi, cudaStream_t stream) {
   if (M <= 0 || N <= 0) return 0;
@@ -205,11 +213,14 @@ int launch_gemm_tn(const void* A, int lda, const void* B, int ldb, int M, int N,
   CUtensorMap ta, tb;
   int rc = make_tma_bf16_2d(&ta, A, (uint64_t)M, (uint64_t)K, (uint64_t)lda, kBlockM);
   if (rc) return rc;
-  rc = make_tma_bf16_2d(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, BN);
+  if constexpr (kBMN)
+    rc = make_tma_bf16_2d(&tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, 64);
+  else
+    rc = make_tma_bf16_2d(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, BN);
   if (rc) return rc;
   static bool attr_set = false;  // one per template instantiation
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN, Epi>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN, Epi, kBMN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::kSmemBytes);
     if (e != cudaSuccess) return (int)e;
@@ -217,7 +228,8 @@ int launch_gemm_tn(const void* A, int lda, const void* B, int ldb, int M, int N,
   }
   const int tiles = ((M + kBlockM - 1) / kBlockM) * ((N + BN - 1) / BN);
   const int grid = tiles < gemm_num_sms() ? tiles : gemm_num_sms();
-  gemm_tn_kernel<BN, Epi><<<grid, kGemmThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, epi);
+  gemm_tn_kernel<BN, Epi, kBMN><<<grid, kGemmThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K,
+                                                                               epi);
   return (int)cudaGetLastError();
 }
 

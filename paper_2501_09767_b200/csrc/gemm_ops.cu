@@ -403,6 +403,14 @@ int lemo_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int 
   LEMO_RETURN_RC("lemo_gemm_bf16", gemm_auto(A, lda, B, ldb, M, N, K, e, (cudaStream_t)stream));
 }
 
+int lemo_gemm_nn_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M,
+                      int N, int K, void* stream) {
+  LEMO_ARG_CHECK(N % 32 == 0 && ldc % 8 == 0, "lemo_gemm_nn_bf16: N%32, ldc%8");
+  Bound<256, EpiStoreBF16> b{EpiStoreBF16{reinterpret_cast<__nv_bfloat16*>(C), ldc, N}};
+  LEMO_RETURN_RC("lemo_gemm_nn_bf16", (launch_gemm_tn<256, Bound<256, EpiStoreBF16>, true>(
+                                          A, lda, B, ldb, M, N, K, b, (cudaStream_t)stream)));
+}
+
 int lemo_gemm_f32(const void* A, int lda, const void* B, int ldb, float* C, int ldc, int M, int N,
                   int K, const float* U, int ldu, int R, const float* S, int s_rs, int s_cs,
                   float scale, int accumulate, void* stream) {

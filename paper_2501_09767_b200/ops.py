@@ -351,19 +351,23 @@ def quantile_lower(data, q, out, *, plus_one=False):
 # attention
 
 
-def flash_fwd(q, k, v, *, head_dim, scale, o=None, lse=None):
+def flash_fwd(q, k, v, *, head_dim, scale, o=None, lse=None, impl=None):
+    """Causal attention forward; impl None = tcgen05 kernel when head_dim == 128."""
     _check(q, k, v)
     n, h = q.shape
     if o is None:
         o = torch.empty(n, h, dtype=BF16, device=q.device)
     if lse is None:
         lse = torch.empty(h // head_dim, n, dtype=F32, device=q.device)
-    call("lemo_flash_fwd", ptr(q), ptr(k), ptr(v), ptr(o), ptr(lse), n, h, head_dim, float(scale),
-         _s())
+    if impl is None:
+        impl = "tc" if head_dim == 128 else "mma"
+    name = "lemo_flash_fwd_tc" if impl == "tc" else "lemo_flash_fwd"
+    call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(lse), n, h, head_dim, float(scale), _s())
     return o, lse
 
 
-def flash_bwd(q, k, v, o, dout, lse, *, head_dim, scale, dq=None, dk=None, dv=None):
+def flash_bwd(q, k, v, o, dout, lse, *, head_dim, scale, dq=None, dk=None, dv=None, impl=None):
+    """Causal attention backward; impl None = tcgen05 kernels when head_dim == 128."""
     _check(q, k, v, o, dout, lse)
     n, h = q.shape
     dev = q.device
@@ -371,6 +375,9 @@ def flash_bwd(q, k, v, o, dout, lse, *, head_dim, scale, dq=None, dk=None, dv=No
     dq = torch.empty(n, h, dtype=F32, device=dev) if dq is None else dq
     dk = torch.empty(n, h, dtype=F32, device=dev) if dk is None else dk
     dv = torch.empty(n, h, dtype=F32, device=dev) if dv is None else dv
-    call("lemo_flash_bwd", ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(delta), ptr(dq),
+    if impl is None:
+        impl = "tc" if head_dim == 128 else "mma"
+    name = "lemo_flash_bwd_tc" if impl == "tc" else "lemo_flash_bwd"
+    call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(delta), ptr(dq),
          ptr(dk), ptr(dv), n, h, head_dim, float(scale), _s())
     return dq, dk, dv

@@ -1,0 +1,27 @@
+"""Micro-benchmark of the attention kernels (CUDA events, warm)."""
+import math, sys, torch
+sys.path.insert(0, '.')
+from paper_2501_09767_b200 import ops
+
+def bench(fn, it=10):
+    for _ in range(3): fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(it): fn()
+    b.record(); torch.cuda.synchronize()
+    return a.elapsed_time(b) / it
+
+for n in (4096, 8192, 16384):
+    H, d = 32, 128
+    q, k, v = (torch.randn(n, H * d, device='cuda').bfloat16() for _ in range(3))
+    fl = 2 * n * n * d * H  # causal fwd flops (QK^T + PV, half)
+    for impl in ("mma", "tc"):
+        t = bench(lambda: ops.flash_fwd(q, k, v, head_dim=d, scale=1 / math.sqrt(d), impl=impl))
+        print(f"fwd n={n} {impl}: {t:.3f} ms  {fl / t / 1e9:.0f} TFLOP/s")
+    o, lse = ops.flash_fwd(q, k, v, head_dim=d, scale=1 / math.sqrt(d))
+    do = torch.randn_like(o)
+    for impl in ("mma",) + (("tc",) if "impl" in ops.flash_bwd.__code__.co_varnames else ()):
+        kw = {} if impl == "mma" else {"impl": "tc"}
+        t = bench(lambda: ops.flash_bwd(q, k, v, o, do, lse, head_dim=d, scale=1 / math.sqrt(d), **kw))
+        print(f"bwd n={n} {impl}: {t:.3f} ms  {2.5 * fl / t / 1e9:.0f} TFLOP/s (2.5x fwd flops)")

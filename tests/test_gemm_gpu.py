@@ -57,3 +57,18 @@ def test_gemm_scatter_add(cuda):
     ops.gemm_scatter_add(a, b, resid, idx)
     torch.cuda.synchronize()
     assert torch.allclose(resid, ref, atol=1e-3, rtol=1e-3)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 512, 4096), (1000, 768, 320)])
+def test_gemm_nn_mn_major_b(cuda, M, N, K):
+    """MN-major B operand descriptors (used by the attention kernels)."""
+    from paper_2501_09767_b200._lib import call, ptr, stream_ptr
+    g = torch.Generator(device=cuda).manual_seed(11)
+    a = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    b = torch.randn(K, N, device=cuda, generator=g).bfloat16()
+    c = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    call("lemo_gemm_nn_bf16", ptr(a), K, ptr(b), N, ptr(c), N, M, N, K, stream_ptr())
+    torch.cuda.synchronize()
+    ref = a.float() @ b.float()
+    err = (c.float() - ref).abs().max().item()
+    assert err <= 1e-2 * ref.abs().max().item() + 1e-3, err

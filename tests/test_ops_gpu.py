@@ -301,3 +301,37 @@ def test_qkv_rope_lora_vs_oracle(cuda):
     kr = O.rope_fwd(kr.astype(np.float32), pos_np, H, 10000.0)
     for got, ref in ((q, qr), (k, kr), (v, vr)):
         np.testing.assert_allclose(got.float().cpu().numpy(), ref, rtol=2e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("n,H", [(1, 1), (100, 2), (128, 1), (129, 2), (1000, 4), (4096, 2)])
+def test_flash_fwd_tc_vs_torch_and_mma(cuda, n, H):
+    """tcgen05 attention forward vs fp32 torch and vs the mma.sync kernel."""
+    d = 128
+    g = torch.Generator(device=cuda).manual_seed(n + 7)
+    h = H * d
+    q, k, v = (torch.randn(n, h, device=cuda, generator=g).bfloat16() for _ in range(3))
+    o, lse = ops.flash_fwd(q, k, v, head_dim=d, scale=1 / math.sqrt(d), impl="tc")
+    oref, lref = _torch_attn(q, k, v, H)
+    torch.testing.assert_close(o.float(), oref, rtol=2e-2, atol=2e-2)
+    torch.testing.assert_close(lse, lref, rtol=1e-3, atol=1e-3)
+    o2, lse2 = ops.flash_fwd(q, k, v, head_dim=d, scale=1 / math.sqrt(d), impl="mma")
+    torch.testing.assert_close(o.float(), o2.float(), rtol=2e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("n,H", [(1, 1), (100, 2), (128, 1), (257, 2), (1000, 2)])
+def test_flash_bwd_tc_vs_torch(cuda, n, H):
+    d = 128
+    g = torch.Generator(device=cuda).manual_seed(n + 11)
+    h = H * d
+    q, k, v = (torch.randn(n, h, device=cuda, generator=g).bfloat16() for _ in range(3))
+    o, lse = ops.flash_fwd(q, k, v, head_dim=d, scale=1 / math.sqrt(d), impl="tc")
+    qr, kr, vr = (t.float().requires_grad_(True) for t in (q, k, v))
+    oref, _ = _torch_attn(qr, kr, vr, H)
+    dout = torch.randn(n, h, device=cuda, generator=g).bfloat16()
+    oref.backward(dout.float())
+    dq, dk, dv = ops.flash_bwd(q, k, v, o, dout, lse, head_dim=d, scale=1 / math.sqrt(d),
+                               impl="tc")
+    floor = 1e-2 * dout.float().norm()
+    for name, got, ref in (("dq", dq, qr.grad), ("dk", dk, kr.grad), ("dv", dv, vr.grad)):
+        err = (got - ref).norm() / torch.maximum(ref.norm(), floor)
+        assert err < 2e-2, (name, float(err))
