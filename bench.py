@@ -193,7 +193,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    from paper_2501_09767_b200 import _lib, model as M, predictor as P, sparsity as S
+    from paper_2501_09767_b200 import _lib, model as M, parallel, predictor as P, sparsity as S
     from paper_2501_09767_b200.optim import Adam
 
     wl = CONFIGS[args.config]
@@ -244,8 +244,8 @@ def main():
     def step(src, batch, read_loss=False):
         loss, _ = model.forward_step(batch, pattern_source=src, segments=segments)
         loss.backward()
-        if world > 1:
-            dist.all_reduce(model.lora_param.grad, op=dist.ReduceOp.AVG)
+        if world > 1:  # the path's only exchange: mean of the LoRA gradients (§8e)
+            parallel.allreduce_mean_(model.lora_param.grad)
         opt.step()
         opt.zero_grad()
         return float(loss.detach()) if read_loss else loss
