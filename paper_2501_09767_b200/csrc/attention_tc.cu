@@ -154,27 +154,29 @@ __global__ void __launch_bounds__(256, 1)
       }
       const int kv0 = j * kB;
       const bool edge = (j == qb) || (kv0 + kB > n);
-      float mx = m;
+      float mraw = -INFINITY;
 #pragma unroll
       for (int i = 0; i < kB; ++i) {
-        float v = s[i] * sl2;
         if (edge) {
           const int key = kv0 + i;
-          if (key > grow || key >= n) v = -INFINITY;
+          if (key > grow || key >= n) s[i] = -INFINITY;
         }
-        s[i] = v;
-        mx = fmaxf(mx, v);
+        mraw = fmaxf(mraw, s[i]);
       }
-      const float corr = (m == -INFINITY) ? 0.f : exp2f(m - mx);
+      // lazy rescaling: keep the running max unless it grew by > 8 (log2
+      // units); O / l / lse stay exact because they share the stale max
+      const float mx = mraw * sl2;
+      const float m_new = (m == -INFINITY || mx > m + 8.f) ? fmaxf(mx, m) : m;
+      const float corr = (m == -INFINITY) ? 0.f : ex2_approx(m - m_new);
       float sum = 0.f;
 #pragma unroll
       for (int i = 0; i < kB; ++i) {
-        const float p = exp2f(s[i] - mx);
+        const float p = ex2_approx(fmaf(s[i], sl2, -m_new));
         s[i] = p;
         sum += p;
       }
       l = l * corr + sum;
-      m = mx;
+      m = m_new;
       if (j > 0) {
         // P_{j-1}·V_{j-1} finished: P buffer is free and O is stable; rescale O
         mbar_wait(o_full, (j - 1) & 1);
@@ -405,7 +407,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int i = 0; i < kB; ++i) {
         const int key = kv0 + i;
-        float e = exp2f(p[i] * sl2 - lse2);
+        float e = ex2_approx(fmaf(p[i], sl2, -lse2));
         if (key > grow || key >= n || grow >= n) e = 0.f;
         p[i] = e;
       }
@@ -567,7 +569,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int c = 0; c < kB; ++c) {
         const int qr = qrow0 + c;
-        float e = exp2f(p[c] * sl2 - sL[buf * 128 + c]);
+        float e = ex2_approx(fmaf(p[c], sl2, -sL[buf * 128 + c]));
         if (key > qr || qr >= n || key >= n) e = 0.f;
         p[c] = e;
       }

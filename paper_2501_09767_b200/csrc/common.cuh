@@ -55,6 +55,13 @@ __device__ __forceinline__ float round_bf16(float x) {
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 
+// 2^x on the SFU (MUFU.EX2), flush-to-zero; ex2(-inf) = +0.
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Stable logistic, same branch structure as the reference sigmoid_np
 // (tensor.py:368-374); expf on the negative magnitude never overflows.
 __device__ __forceinline__ float sigmoid_stable(float x) {

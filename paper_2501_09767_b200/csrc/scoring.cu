@@ -10,6 +10,8 @@
 //                    block → token compaction; k stays on device)
 //   quantile_lower   model.py:545-563 (np.quantile method="lower" as a radix
 //                    select over order-preserving 64-bit keys)
+#include <algorithm>
+
 #include "common.cuh"
 #include "lemo_internal.h"
 
@@ -19,9 +21,34 @@ namespace lemo {
 // block mean: one thread per (block, 4 columns); b independent float4 loads in
 // flight per thread, sequential f32 sum in row order then / b — the same
 // arithmetic numpy uses for mean over a non-contiguous axis.
-__global__ void __launch_bounds__(256) block_embed_kernel(const float* __restrict__ x, int ldx,
-                                                          int nb, int h, int b,
-                                                          float* __restrict__ xb) {
+// One CTA per token block: the b rows of the block are contiguous in HBM
+// (b·h·4 bytes), so every CTA streams one contiguous region; each thread
+// keeps b independent 16-B loads in flight (first batch issued before any add).
+template <int B>
+__global__ void __launch_bounds__(1024) block_embed_kernel(const float* __restrict__ x, int ldx,
+                                                           int h, float* __restrict__ xb) {
+  const int n = blockIdx.x;
+  const int nv = h >> 2;
+  const float4* base = reinterpret_cast<const float4*>(x + (size_t)n * B * ldx);
+  const size_t stride = (size_t)ldx >> 2;
+  for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+    float4 v[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) v[i] = __ldcs(base + i * stride + c);
+    float4 acc = v[0];
+#pragma unroll
+    for (int i = 1; i < B; ++i) {
+      acc.x += v[i].x; acc.y += v[i].y; acc.z += v[i].z; acc.w += v[i].w;
+    }
+    const float fb = (float)B;
+    acc.x /= fb; acc.y /= fb; acc.z /= fb; acc.w /= fb;
+    reinterpret_cast<float4*>(xb + (size_t)n * h)[c] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) block_embed_generic_kernel(const float* __restrict__ x,
+                                                                  int ldx, int nb, int h, int b,
+                                                                  float* __restrict__ xb) {
   const int nv = h >> 2;
   const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (gid >= (long long)nb * nv) return;
@@ -29,7 +56,6 @@ __global__ void __launch_bounds__(256) block_embed_kernel(const float* __restric
   const float4* src = reinterpret_cast<const float4*>(x + (size_t)n * b * ldx) + c;
   const size_t stride = (size_t)ldx >> 2;
   float4 acc = __ldg(src);
-#pragma unroll 8
   for (int i = 1; i < b; ++i) {
     const float4 v = __ldg(src + i * stride);
     acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
@@ -310,8 +336,15 @@ int lemo_block_embed(const float* x, int ldx, int s, int h, int b, float* xb, vo
   const int nb = s / b;
   const long long total = (long long)nb * (h / 4);
   if (total == 0) return 0;
-  block_embed_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      x, ldx, nb, h, b, xb);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int threads = std::min(1024, std::max(32, ((h / 4 + 31) / 32) * 32));
+  if (b == 16)
+    block_embed_kernel<16><<<nb, threads, 0, st>>>(x, ldx, h, xb);
+  else if (b == 8)
+    block_embed_kernel<8><<<nb, threads, 0, st>>>(x, ldx, h, xb);
+  else
+    block_embed_generic_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(x, ldx, nb, h, b,
+                                                                               xb);
   LEMO_CHECK_LAUNCH("lemo_block_embed");
   return 0;
 }
