@@ -129,11 +129,21 @@ int lemo_mlp_compact(const void* gu_all, const float* x, int ldx, const float* i
                      void* inner_out, void* xg_out, float* inv_out, void* stream);
 
 /* After attention backward: RoPE backward of dq/dk (tensor.py:627-632; dq is
- * rewritten in place pre-rotation), packed bf16 [dq|dk|dv] rows for the dX
- * GEMM, and u = [dq·Bqᵀ | dv·Bvᵀ] (LoRA backward factors). */
+ * rewritten in place pre-rotation) and packed bf16 [dq|dk|dv] rows (row stride
+ * ldo >= 3h) for the dX GEMM. */
 int lemo_qkv_grad_prep(float* dq, const float* dk, const float* dv, int M, int h, int head_dim,
-                       int rope, const void* rope_tab, const int* pos, const float* Bq,
-                       const float* Bv, int r, void* dqkv, float* u, int ldu, void* stream);
+                       int rope, const void* rope_tab, const int* pos, void* dqkv, int ldo,
+                       void* stream);
+
+/* out [32, 3h] bf16: row j < r = [Bq[j] | 0 | 0], r <= j < 2r = [0 | 0 | Bv[j-r]];
+ * u = dqkv·outᵀ gives [dq·Bqᵀ | dv·Bvᵀ] (the LoRA backward factors of
+ * kernels.py:95-100) as one tcgen05 GEMM. */
+int lemo_lora_pack_bt(const float* Bq, const float* Bv, int h, int r, void* out, void* stream);
+
+/* w[c, col0 + j] = bf16(A[c*lda + j]) for j < r2, 0 up to 64 — the LoRA
+ * K-extension of the dX weight, so dxn += s·u·Aᵀ runs inside the GEMM. */
+int lemo_lora_pack_a_ext(const float* A, int lda, int h, int r2, void* w, int ldw, int col0,
+                         void* stream);
 
 /* LoRA weight gradients accumulated (+=) into dA0/dB0/dA1/dB1:
  * dA[c,j] = s·Σ xn[i,c]u[i,j], dB[j,c] = s·Σ t[i,j]g[i,c] (tensor.py:324-325). */

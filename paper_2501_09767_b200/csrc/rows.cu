@@ -222,120 +222,132 @@ __global__ void mlp_compact_kernel(const __nv_bfloat16* __restrict__ gu_all, int
 }
 
 // After FlashAttention backward: rotate dq/dk back (tensor.py:627-632), pack
-// [dq|dk|dv] as bf16 for the dX GEMM, keep fp32 pre-rotation dq (in place)
-// for the LoRA grads, and form u = [dq·Bqᵀ | dv·Bvᵀ] (kernels.py:97-99 bwd).
+// [dq|dk|dv] as bf16 rows (row stride ldo; the LoRA K-extension columns
+// after 3h are filled separately) for the dX GEMM, and keep the fp32
+// pre-rotation dq (in place) for the LoRA gradients.  Pure streaming.
 __global__ void __launch_bounds__(256) qkv_grad_prep_kernel(
     float* __restrict__ dq, const float* __restrict__ dk, const float* __restrict__ dv, int h,
     int head_dim, int rope, const float2* __restrict__ rope_tab, const int* __restrict__ pos,
-    const float* __restrict__ Bq, const float* __restrict__ Bv, int r,
-    __nv_bfloat16* __restrict__ dqkv, float* __restrict__ u, int ldu) {
-  __shared__ float red[8][32];
+    __nv_bfloat16* __restrict__ dqkv, int ldo) {
   const int row = blockIdx.x;
   const int half = head_dim >> 1;
   const int p = rope ? __ldg(pos + row) : 0;
   float* dqr = dq + (size_t)row * h;
   const float* dkr = dk + (size_t)row * h;
   const float* dvr = dv + (size_t)row * h;
-  __nv_bfloat16* o = dqkv + (size_t)row * 3 * h;
-  float acc[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-  // each thread handles pairs (c, c+half) inside a head
-  for (int e = threadIdx.x; e < (h >> 1); e += blockDim.x) {
+  __nv_bfloat16* o = dqkv + (size_t)row * ldo;
+  // each thread: two consecutive rotation pairs (ca, ca+1) / (cb, cb+1) of one head
+  for (int e2 = threadIdx.x; e2 < (h >> 2); e2 += blockDim.x) {
+    const int e = e2 * 2;
     const int hd = e / half, j = e - hd * half;
     const int ca = hd * head_dim + j, cb = ca + half;
-    float qa = dqr[ca], qb = dqr[cb], ka = dkr[ca], kb = dkr[cb];
+    float2 qa = *reinterpret_cast<const float2*>(dqr + ca);
+    float2 qb = *reinterpret_cast<const float2*>(dqr + cb);
+    float2 ka = *reinterpret_cast<const float2*>(dkr + ca);
+    float2 kb = *reinterpret_cast<const float2*>(dkr + cb);
+    const float2 va = *reinterpret_cast<const float2*>(dvr + ca);
+    const float2 vb = *reinterpret_cast<const float2*>(dvr + cb);
     if (rope) {
-      const float2 cs = rope_tab[(size_t)p * half + j];
-      const float nqa = qa * cs.x + qb * cs.y, nqb = -qa * cs.y + qb * cs.x;
-      const float nka = ka * cs.x + kb * cs.y, nkb = -ka * cs.y + kb * cs.x;
-      qa = nqa; qb = nqb; ka = nka; kb = nkb;
+      const float4 cs = *reinterpret_cast<const float4*>(rope_tab + (size_t)p * half + j);
+      // (cs.x, cs.y) = (cos, sin) of pair j, (cs.z, cs.w) of pair j+1
+      float t0 = qa.x * cs.x + qb.x * cs.y, t1 = -qa.x * cs.y + qb.x * cs.x;
+      float u0 = qa.y * cs.z + qb.y * cs.w, u1 = -qa.y * cs.w + qb.y * cs.z;
+      qa = make_float2(t0, u0);
+      qb = make_float2(t1, u1);
+      t0 = ka.x * cs.x + kb.x * cs.y; t1 = -ka.x * cs.y + kb.x * cs.x;
+      u0 = ka.y * cs.z + kb.y * cs.w; u1 = -ka.y * cs.w + kb.y * cs.z;
+      ka = make_float2(t0, u0);
+      kb = make_float2(t1, u1);
     }
-    dqr[ca] = qa;
-    dqr[cb] = qb;
-    const float va = dvr[ca], vb = dvr[cb];
-    o[ca] = __float2bfloat16_rn(qa);
-    o[cb] = __float2bfloat16_rn(qb);
-    o[h + ca] = __float2bfloat16_rn(ka);
-    o[h + cb] = __float2bfloat16_rn(kb);
-    o[2 * h + ca] = __float2bfloat16_rn(va);
-    o[2 * h + cb] = __float2bfloat16_rn(vb);
-    if (Bq) {
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) {
-        if (jj < r) {
-          acc[jj] += qa * __ldg(Bq + (size_t)jj * h + ca) + qb * __ldg(Bq + (size_t)jj * h + cb);
-          acc[16 + jj] += va * __ldg(Bv + (size_t)jj * h + ca) + vb * __ldg(Bv + (size_t)jj * h + cb);
-        }
-      }
-    }
+    *reinterpret_cast<float2*>(dqr + ca) = qa;
+    *reinterpret_cast<float2*>(dqr + cb) = qb;
+    *reinterpret_cast<uint32_t*>(o + ca) = pack_bf16x2(qa.x, qa.y);
+    *reinterpret_cast<uint32_t*>(o + cb) = pack_bf16x2(qb.x, qb.y);
+    *reinterpret_cast<uint32_t*>(o + h + ca) = pack_bf16x2(ka.x, ka.y);
+    *reinterpret_cast<uint32_t*>(o + h + cb) = pack_bf16x2(kb.x, kb.y);
+    *reinterpret_cast<uint32_t*>(o + 2 * h + ca) = pack_bf16x2(va.x, va.y);
+    *reinterpret_cast<uint32_t*>(o + 2 * h + cb) = pack_bf16x2(vb.x, vb.y);
   }
-  if (Bq) {
-    const int wid = threadIdx.x >> 5, l = threadIdx.x & 31;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float s = warp_sum(acc[j]);
-      if (l == 0) red[wid][j] = s;
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      const int j = threadIdx.x;
-      float s = 0.f;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][j];
-      if ((j & 15) < r) u[(size_t)row * ldu + (j >> 4) * r + (j & 15)] = s;
-    }
-  }
+}
+
+// LoRA operands of the backward GEMMs:
+//  Bt [32, 3h]:  row j < r: [Bq[j] | 0 | 0];  r <= j < 2r: [0 | 0 | Bv[j-r]]  (u = dqkv·Btᵀ)
+//  A-extension of the dX weight: w[c, col0 + j] = A[c, j] (j < 2r), 0 up to 64.
+__global__ void lora_pack_bt_kernel(const float* __restrict__ Bq, const float* __restrict__ Bv,
+                                    int h, int r, __nv_bfloat16* __restrict__ out) {
+  const int j = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= 3 * h) return;
+  const int which = c / h, cc = c - which * h;
+  float val = 0.f;
+  if (which == 0 && j < r) val = Bq[(size_t)j * h + cc];
+  if (which == 2 && j >= r && j < 2 * r) val = Bv[(size_t)(j - r) * h + cc];
+  out[(size_t)j * 3 * h + c] = __float2bfloat16_rn(val);
+}
+
+__global__ void lora_pack_a_ext_kernel(const float* __restrict__ A, int lda, int h, int r2,
+                                       __nv_bfloat16* __restrict__ w, int ldw, int col0) {
+  const int c = blockIdx.x * 4 + (threadIdx.x >> 6), j = threadIdx.x & 63;
+  if (c >= h) return;
+  w[(size_t)c * ldw + col0 + j] = __float2bfloat16_rn(j < r2 ? A[(size_t)c * lda + j] : 0.f);
 }
 
 // LoRA weight gradients (kernels.py:95-100 through tensor.py:324-325):
 //   dA0[c,j] += s Σ_i xn[i,c] u0[i,j]     dB0[j,c] += s Σ_i t0[i,j] g0[i,c]
 // (same for adapter 1), xn recomputed from the saved bf16 rows, inv, w.
 constexpr int kLoraRows = 64;
+template <int R>
 __global__ void __launch_bounds__(128) lora_grads_kernel(
     const __nv_bfloat16* __restrict__ xg, const float* __restrict__ inv, const float* __restrict__ w,
     const float* __restrict__ t, const float* __restrict__ u, int ld, const float* __restrict__ g0,
-    const float* __restrict__ g1, int M, int h, int r, float scale, int lda, float* __restrict__ dA0,
+    const float* __restrict__ g1, int M, int h, float scale, int lda, float* __restrict__ dA0,
     float* __restrict__ dB0, float* __restrict__ dA1, float* __restrict__ dB1) {
-  __shared__ float st[kLoraRows][32];
-  __shared__ float su[kLoraRows][32];
+  // per row: [t_q (R) | t_v (R)] and [u_q (R) | u_v (R)], read as float4 broadcasts
+  __shared__ __align__(16) float st[kLoraRows][2 * R];
+  __shared__ __align__(16) float su[kLoraRows][2 * R];
   __shared__ float sinv[kLoraRows];
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int r0 = blockIdx.y * kLoraRows;
   const int nrow = min(kLoraRows, M - r0);
-  for (int e = threadIdx.x; e < nrow * 2 * r; e += blockDim.x) {
-    const int i = e / (2 * r), j = e - i * 2 * r;
+  for (int e = threadIdx.x; e < nrow * 2 * R; e += blockDim.x) {
+    const int i = e / (2 * R), j = e - i * 2 * R;
     st[i][j] = t[(size_t)(r0 + i) * ld + j];
     su[i][j] = u[(size_t)(r0 + i) * ld + j];
   }
   for (int i = threadIdx.x; i < nrow; i += blockDim.x) sinv[i] = inv[r0 + i];
   __syncthreads();
   if (c >= h) return;
-  float a0[16], b0[16], a1[16], b1[16];
+  float a0[R], b0[R], a1[R], b1[R];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) a0[j] = b0[j] = a1[j] = b1[j] = 0.f;
+  for (int j = 0; j < R; ++j) a0[j] = b0[j] = a1[j] = b1[j] = 0.f;
   const float wc = w[c];
+#pragma unroll 2
   for (int i = 0; i < nrow; ++i) {
     const size_t off = (size_t)(r0 + i) * h + c;
     const float xn = __bfloat162float(xg[off]) * sinv[i] * wc;
     const float q = g0[off], v = g1[off];
+    float tv[2 * R], uv[2 * R];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (j < r) {
-        a0[j] = fmaf(xn, su[i][j], a0[j]);
-        a1[j] = fmaf(xn, su[i][r + j], a1[j]);
-        b0[j] = fmaf(st[i][j], q, b0[j]);
-        b1[j] = fmaf(st[i][r + j], v, b1[j]);
-      }
+    for (int j = 0; j < 2 * R; j += 4) {
+      const float4 a = *reinterpret_cast<const float4*>(&st[i][j]);
+      const float4 b = *reinterpret_cast<const float4*>(&su[i][j]);
+      tv[j] = a.x; tv[j + 1] = a.y; tv[j + 2] = a.z; tv[j + 3] = a.w;
+      uv[j] = b.x; uv[j + 1] = b.y; uv[j + 2] = b.z; uv[j + 3] = b.w;
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      a0[j] = fmaf(xn, uv[j], a0[j]);
+      a1[j] = fmaf(xn, uv[R + j], a1[j]);
+      b0[j] = fmaf(tv[j], q, b0[j]);
+      b1[j] = fmaf(tv[R + j], v, b1[j]);
     }
   }
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    if (j < r) {
-      atomicAdd(dA0 + (size_t)c * lda + j, scale * a0[j]);
-      atomicAdd(dA1 + (size_t)c * lda + j, scale * a1[j]);
-      atomicAdd(dB0 + (size_t)j * h + c, scale * b0[j]);
-      atomicAdd(dB1 + (size_t)j * h + c, scale * b1[j]);
-    }
+  for (int j = 0; j < R; ++j) {
+    atomicAdd(dA0 + (size_t)c * lda + j, scale * a0[j]);
+    atomicAdd(dA1 + (size_t)c * lda + j, scale * a1[j]);
+    atomicAdd(dB0 + (size_t)j * h + c, scale * b0[j]);
+    atomicAdd(dB1 + (size_t)j * h + c, scale * b1[j]);
   }
 }
 
@@ -520,14 +532,33 @@ int lemo_mlp_compact(const void* gu_all, const float* x, int ldx, const float* i
 }
 
 int lemo_qkv_grad_prep(float* dq, const float* dk, const float* dv, int M, int h, int head_dim,
-                       int rope, const void* rope_tab, const int* pos, const float* Bq,
-                       const float* Bv, int r, void* dqkv, float* u, int ldu, void* stream) {
+                       int rope, const void* rope_tab, const int* pos, void* dqkv, int ldo,
+                       void* stream) {
   if (M <= 0) return 0;
-  LEMO_ARG_CHECK(r <= 16, "lemo_qkv_grad_prep: LoRA rank <= 16");
+  LEMO_ARG_CHECK(head_dim % 4 == 0 && ldo >= 3 * h && ldo % 2 == 0,
+                 "lemo_qkv_grad_prep: bad geometry");
   qkv_grad_prep_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(
-      dq, dk, dv, h, head_dim, rope, reinterpret_cast<const float2*>(rope_tab), pos, Bq, Bv, r,
-      reinterpret_cast<__nv_bfloat16*>(dqkv), u, ldu);
+      dq, dk, dv, h, head_dim, rope, reinterpret_cast<const float2*>(rope_tab), pos,
+      reinterpret_cast<__nv_bfloat16*>(dqkv), ldo);
   LEMO_CHECK_LAUNCH("lemo_qkv_grad_prep");
+  return 0;
+}
+
+int lemo_lora_pack_bt(const float* Bq, const float* Bv, int h, int r, void* out, void* stream) {
+  LEMO_ARG_CHECK(2 * r <= 32, "lemo_lora_pack_bt: 2r <= 32");
+  dim3 grid((3 * h + 255) / 256, 32);
+  lora_pack_bt_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      Bq, Bv, h, r, reinterpret_cast<__nv_bfloat16*>(out));
+  LEMO_CHECK_LAUNCH("lemo_lora_pack_bt");
+  return 0;
+}
+
+int lemo_lora_pack_a_ext(const float* A, int lda, int h, int r2, void* w, int ldw, int col0,
+                         void* stream) {
+  LEMO_ARG_CHECK(r2 <= 64 && ldw >= col0 + 64, "lemo_lora_pack_a_ext: need 64 columns");
+  lora_pack_a_ext_kernel<<<(h + 3) / 4, 256, 0, (cudaStream_t)stream>>>(
+      A, lda, h, r2, reinterpret_cast<__nv_bfloat16*>(w), ldw, col0);
+  LEMO_CHECK_LAUNCH("lemo_lora_pack_a_ext");
   return 0;
 }
 
@@ -538,9 +569,19 @@ int lemo_lora_grads(const void* xg, const float* inv, const float* w, const floa
   if (M <= 0) return 0;
   LEMO_ARG_CHECK(r <= 16, "lemo_lora_grads: LoRA rank <= 16");
   dim3 grid((h + 127) / 128, (M + kLoraRows - 1) / kLoraRows);
-  lora_grads_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(xg), inv, w, t, u, ld, g0, g1, M, h, r, scale, lda,
-      dA0, dB0, dA1, dB1);
+  cudaStream_t st = (cudaStream_t)stream;
+  auto* xgp = reinterpret_cast<const __nv_bfloat16*>(xg);
+#define LG(RR)                                                                                 \
+  lora_grads_kernel<RR><<<grid, 128, 0, st>>>(xgp, inv, w, t, u, ld, g0, g1, M, h, scale, lda, \
+                                              dA0, dB0, dA1, dB1)
+  switch (r) {
+    case 2: LG(2); break;
+    case 4: LG(4); break;
+    case 8: LG(8); break;
+    case 16: LG(16); break;
+    default: set_error_msg("lemo_lora_grads: LoRA rank must be 2, 4, 8 or 16"); return LEMO_ERR_REPORTED;
+  }
+#undef LG
   LEMO_CHECK_LAUNCH("lemo_lora_grads");
   return 0;
 }

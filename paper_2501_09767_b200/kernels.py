@@ -156,19 +156,17 @@ def attention_backward(dx: torch.Tensor, saved: dict, layer, grads) -> None:
     dq, dk, dv = ops.flash_bwd(saved["q"], saved["k"], saved["v"], saved["o"], d_o, saved["lse"],
                                head_dim=layer.head_dim, scale=1.0 / math.sqrt(layer.head_dim))
     del d_o
-    dqkv = torch.empty(k, 3 * h, dtype=BF16, device=dev)
-    u = torch.empty(k, ops.LORA_T_COLS, dtype=F32, device=dev) if r else None
+    dqkv = torch.empty(k, layer.w_qkv.shape[1], dtype=BF16, device=dev)  # [dq|dk|dv|LoRA ext]
     ops.qkv_grad_prep(dq, dk, dv, head_dim=layer.head_dim, rope=layer.rope,
-                      rope_tab=layer.rope_tab, pos=idx, Bq=layer.lora_Bq if r else None,
-                      Bv=layer.lora_Bv if r else None, r=r, dqkv=dqkv, u=u)
-    if r and grads is not None:
-        dA, dBq, dBv = grads
-        ops.lora_grads(saved["xg"], saved["inv"], layer.attn_norm_w, saved["t"], u, dq, dv, r=r,
-                       scale=layer.lora_scaling, dA=dA, dB0=dBq, dB1=dBv)
+                      rope_tab=layer.rope_tab, pos=idx, dqkv=dqkv)
+    if r:
+        u = layer.qkv_grad_input(dqkv)
+        if grads is not None:
+            dA, dBq, dBv = grads
+            ops.lora_grads(saved["xg"], saved["inv"], layer.attn_norm_w, saved["t"], u, dq, dv,
+                           r=r, scale=layer.lora_scaling, dA=dA, dB0=dBq, dB1=dBv)
     del dq, dk, dv
-    dxn = ops.gemm_f32(dqkv, layer.w_qkv, side_u=u[:, :2 * r] if r else None,
-                       side_s=layer.lora_A if r else None, side_strides=(1, 2 * r),
-                       scale=layer.lora_scaling)
+    dxn = ops.gemm_f32(dqkv, layer.w_qkv)  # LoRA term inside the K-extension
     ops.rmsnorm_bwd(dxn, saved["xg"], saved["inv"], layer.attn_norm_w, dx, idx, accumulate=True)
 
 

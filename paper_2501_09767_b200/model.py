@@ -173,9 +173,11 @@ class LayerState:
 
         wq, wk, wv, wo = g("wq"), g("wk"), g("wv"), g("wo")
         w_qkv = torch.cat([wq, wk, wv], dim=1)  # [h, 3h]   (x·W layout)
-        self.w_qkv = w_qkv.to(BF16).contiguous()
-        # forward operand [3h, h (+64 LoRA K-extension columns, see lemo_gemm_qkv)]
         kext = ops.LORA_K_EXT if cfg.lora_rank else 0
+        # backward dX operand [h, 3h (+64: A_q|A_v, the LoRA term of dxn)]
+        self.w_qkv = torch.zeros(h, 3 * h + kext, dtype=BF16, device=dev)
+        self.w_qkv[:, :3 * h] = w_qkv.to(BF16)
+        # forward operand [3h, h (+64 LoRA K-extension columns, see lemo_gemm_qkv)]
         self.w_qkv_t = torch.zeros(3 * h, h + kext, dtype=BF16, device=dev)
         self.w_qkv_t[:, :h] = w_qkv.t().to(BF16)
         self.inv_freq = model.inv_freq
@@ -236,6 +238,16 @@ class LayerState:
         ops.lora_qkv_prep(t, r, self.lora_scaling, xn_ext, h)
         ops.lora_pack_b(self.lora_Bq, self.lora_Bv, r, self.w_qkv_t, h)
         return t
+
+    def qkv_grad_input(self, dqkv_ext: torch.Tensor) -> torch.Tensor:
+        """Backward counterpart: u = [dq·Bqᵀ | dv·Bvᵀ] (fp32 [k, 32], one GEMM),
+        s·u into dqkv_ext's extension columns and A_q|A_v into the dX weight's,
+        so dxn = dqkv·W_qkvᵀ + s·u·Aᵀ (kernels.py:95-100 backward) is one GEMM."""
+        h, r = self.w_qkv.shape[0], self.lora_rank
+        u = ops.gemm_f32(dqkv_ext[:, :3 * h], ops.lora_pack_bt(self.lora_Bq, self.lora_Bv, r, h))
+        ops.lora_qkv_prep(u, r, self.lora_scaling, dqkv_ext, 3 * h)
+        ops.lora_pack_a_ext(self.lora_A, r, self.w_qkv, 3 * h)
+        return u
 
     def grad_views(self, flat_grad):
         return self._views(flat_grad) if self.lora_rank else None

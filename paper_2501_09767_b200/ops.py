@@ -215,12 +215,28 @@ def mlp_compact(gu_all, x, inv_all, idx, *, m_pad, relu, gu_out, inner_out, xg_o
          int(bool(relu)), ptr(gu_out), ptr(inner_out), ptr(xg_out), ptr(inv_out), _s())
 
 
-def qkv_grad_prep(dq, dk, dv, *, head_dim, rope, rope_tab, pos, Bq, Bv, r, dqkv, u):
-    _check(dq, dk, dv, rope_tab, pos, Bq, Bv, dqkv, u)
+def qkv_grad_prep(dq, dk, dv, *, head_dim, rope, rope_tab, pos, dqkv):
+    """RoPE backward of dq/dk (dq rewritten in place) + bf16 [dq|dk|dv] rows."""
+    _check(dq, dk, dv, rope_tab, pos, dqkv)
     M, h = dq.shape
     call("lemo_qkv_grad_prep", ptr(dq), ptr(dk), ptr(dv), M, h, head_dim, int(bool(rope)),
-         ptr(rope_tab), ptr(pos), ptr(Bq), ptr(Bv), r, ptr(dqkv), ptr(u),
-         0 if u is None else u.stride(0), _s())
+         ptr(rope_tab), ptr(pos), ptr(dqkv), dqkv.stride(0), _s())
+
+
+def lora_pack_bt(Bq, Bv, r, h, out=None):
+    """[32, 3h] bf16 with B_q (q block) / B_v (v block) rows for u = dqkv·outᵀ."""
+    _check(Bq, Bv, out)
+    if out is None:
+        out = torch.empty(LORA_T_COLS, 3 * h, dtype=BF16, device=Bq.device)
+    call("lemo_lora_pack_bt", ptr(Bq), ptr(Bv), h, r, ptr(out), _s())
+    return out
+
+
+def lora_pack_a_ext(A, r, w_ext, col0):
+    """w_ext[:, col0:col0+64] = [A_q | A_v | 0] (bf16): LoRA K-extension of a dX weight."""
+    _check(A, w_ext)
+    call("lemo_lora_pack_a_ext", ptr(A), A.stride(0), A.shape[0], 2 * r, ptr(w_ext),
+         w_ext.stride(0), col0, _s())
 
 
 def lora_grads(xg, inv, w, t, u, g0, g1, *, r, scale, dA, dB0, dB1):
