@@ -43,11 +43,11 @@ int lemo_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int 
 int lemo_gemm_nn_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M,
                       int N, int K, void* stream);
 
-/* C(f32) (+)= A·Bᵀ + scale · U[M,R] · S  where S(j, col) = S[j*s_rs + col*s_cs]
- * (rank-R side product = the LoRA term of kernels.py:95-100; R = 0 disables it). */
+/* C(f32) (+)= A·Bᵀ (accumulate != 0 adds into C).  Any N; partial column
+ * chunks are stored element-wise.  (LoRA terms of the dX GEMMs ride in a
+ * K-extension of the operands — lemo_lora_pack_a_ext — not in the epilogue.) */
 int lemo_gemm_f32(const void* A, int lda, const void* B, int ldb, float* C, int ldc, int M, int N,
-                  int K, const float* U, int ldu, int R, const float* S, int s_rs, int s_cs,
-                  float scale, int accumulate, void* stream);
+                  int K, int accumulate, void* stream);
 
 /* R[idx[i], :] += (A·Bᵀ)[i, :]  — index-remapped in-place residual update,
  * replaces T.scatter_add_rows (tensor.py:536-550) after the output projections

@@ -5,8 +5,9 @@
 //   accumulator: fp32 in TMEM, two BN-column stages (MMA of tile i+1
 //   overlaps the epilogue of tile i).
 //
-// Warp roles (256 threads):  w0 TMA producer · w1 MMA issuer · w2 TMEM
-// allocator · w3 idle · w4..w7 epilogue (warp w%4 owns TMEM lanes 32·(w%4)…).
+// Warp roles (384 threads):  w0 TMA producer · w1 MMA issuer · w2 TMEM
+// allocator · w3 idle · w4..w11 epilogue (warp w owns TMEM lanes 32·(w%4)…
+// and column half (w-4)/4 of the tile).
 // Every epilogue thread owns one output row of the 128-row tile and pulls
 // its accumulator row out of TMEM in 32-column chunks; the epilogue functor
 // decides what to do with it (plain store, scatter-add into the residual
@@ -23,7 +24,7 @@ namespace lemo {
 constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int kUmmaK = 16;
-constexpr int kGemmThreads = 256;
+constexpr int kGemmThreads = 384;
 constexpr int kGroupM = 16;  // rasterisation group (L2 reuse of B tiles)
 
 template <int BN>
@@ -54,7 +55,7 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int num_m, int num_n) {
 }
 
 // Epilogue contract:
-//   __device__ void operator()(int row, bool valid, int col0, uint32_t taddr) const
+//   __device__ void operator()(int row, bool valid, int col0, uint32_t taddr, int part) const
 // called by each epilogue thread for its row of the tile; `taddr` is the TMEM
 // address of (this warp's lane base, first accumulator column of the tile).
 // The functor must issue the same sequence of tcgen05.ld for every lane of
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 4);  // one elected lane per epilogue warp
+      mbar_init(&tempty_bar[s], 8);  // one elected lane per epilogue warp
     }
     fence_barrier_init();
   }
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
     const int wq = warp & 3;
+    const int part = (warp - 4) >> 2;
     int local = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
       const TileCoord tc = tile_coord(t, num_m, num_n);
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const int row = tc.m * kBlockM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
-      epi(row, row < M, tc.n * BN, taddr);
+      epi(row, row < M, tc.n * BN, taddr, part);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);

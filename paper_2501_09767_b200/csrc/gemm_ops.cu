@@ -2,20 +2,22 @@
 // C ABI declared in include/lemo.h.
 //
 // Reference semantics each epilogue reproduces:
-//   EpiQKV        kernels.py:95-116 (_project + rope_rotate at positions idx)
+//   EpiQKV        kernels.py:95-116 (_project + rope_rotate at positions idx;
+//                 the LoRA term rides in a 64-column K-extension of the GEMM)
 //   EpiScatterAdd tensor.py:536-550 (scatter_add_rows, in place, no atomics:
 //                 retained rows are disjoint)
 //   EpiGateUp     model.py:371-396 + sparsity.py:284-290 (SwiGLU inner and
 //                 mean |inner| token informativeness, fused in the epilogue)
 //   EpiDGateUp    tensor.py:283-292,377-384 (mul / silu backward)
-//   EpiStoreF32   matmul forward/backward (tensor.py:316-327) plus an optional
-//                 rank-R side term (the LoRA path of _project, kernels.py:95-100)
+//   EpiStoreF32   matmul forward/backward (tensor.py:316-327)
+//   EpiSplit3     predictor layers in fp32-faithful bf16x3 form (predictor.py:83-89)
+//
+// Every epilogue runs on 8 warps: warp (4 + 4·part + q) owns TMEM lanes
+// 32q..32q+31 (= output rows) and the `part`-th half of the tile's columns.
 #include "gemm.cuh"
 #include "lemo_internal.h"
 
 namespace lemo {
-
-constexpr int kMaxSideRank = 32;
 
 __device__ __forceinline__ void load_chunk(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
@@ -51,27 +53,10 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float (&v
   }
 }
 
-// v[i] += scale * sum_j U[j] * S[j*s_rs + (col0+i)*s_cs]  (rank-R side product)
-__device__ __forceinline__ void add_side(float (&v)[32], const float (&u)[kMaxSideRank], int R,
-                                         const float* __restrict__ S, int s_rs, int s_cs,
-                                         int col0, float scale) {
-  if (R == 0) return;
-#pragma unroll 4
-  for (int i = 0; i < 32; ++i) {
-    const float* sp = S + (size_t)(col0 + i) * s_cs;
-    float acc = 0.f;
-#pragma unroll
-    for (int j = 0; j < kMaxSideRank; ++j) {
-      if (j < R) acc = fmaf(u[j], __ldg(sp + (size_t)j * s_rs), acc);
-    }
-    v[i] = fmaf(scale, acc, v[i]);
-  }
-}
-
-__device__ __forceinline__ void load_side_u(float (&u)[kMaxSideRank], const float* U, int ldu,
-                                            int R, int row, bool valid) {
-#pragma unroll
-  for (int j = 0; j < kMaxSideRank; ++j) u[j] = (valid && j < R) ? U[(size_t)row * ldu + j] : 0.f;
+// Branch-free logistic on the SFU: 1 / (1 + 2^(-x·log2 e)).  Saturates
+// correctly at both ends (2^(+big) = inf -> 0, 2^(-big) = 0 -> 1).
+__device__ __forceinline__ float sigmoid_fast(float x) {
+  return __frcp_rn(1.f + ex2_approx(-1.4426950408889634f * x));
 }
 
 // ---------------------------------------------------------------------------
@@ -80,9 +65,9 @@ struct EpiStoreBF16 {
   __nv_bfloat16* C;
   int ldc, N;
   template <int BN>
-  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr, int part) const {
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = part * (BN / 2); c < (part + 1) * (BN / 2); c += 32) {
       float v[32];
       load_chunk(taddr + c, v);
       if (valid && col0 + c < N) store_bf16x32(C + (size_t)row * ldc + col0 + c, v);
@@ -92,41 +77,31 @@ struct EpiStoreBF16 {
 
 struct EpiStoreF32 {
   float* C;
-  int ldc, N;
-  const float* U;  // [M, ldu] side factors (rank R) or null
-  int ldu, R;
-  const float* S;  // side matrix, element (j, col) at S[j*s_rs + col*s_cs]
-  int s_rs, s_cs;
-  float scale;
-  int accumulate;
+  int ldc, N, accumulate;
   template <int BN>
-  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
-    float u[kMaxSideRank];
-    load_side_u(u, U, ldu, R, row, valid);
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr, int part) const {
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = part * (BN / 2); c < (part + 1) * (BN / 2); c += 32) {
       float v[32];
       load_chunk(taddr + c, v);
-      if (valid && col0 + c < N) {
-        add_side(v, u, R, S, s_rs, s_cs, col0 + c, scale);
-        const int n = min(32, N - col0 - c);
-        float* dst = C + (size_t)row * ldc + col0 + c;
-        if (n == 32 && (ldc & 3) == 0) {
-          float4* d = reinterpret_cast<float4*>(dst);
+      if (!valid || col0 + c >= N) continue;
+      const int n = min(32, N - col0 - c);
+      float* dst = C + (size_t)row * ldc + col0 + c;
+      if (n == 32 && (ldc & 3) == 0) {
+        float4* d = reinterpret_cast<float4*>(dst);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            if (accumulate) {
-              float4 p = d[q];
-              o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
-            }
-            d[q] = o;
+        for (int q = 0; q < 8; ++q) {
+          float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          if (accumulate) {
+            const float4 p = d[q];
+            o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
           }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < n) dst[i] = accumulate ? dst[i] + v[i] : v[i];
+          d[q] = o;
         }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < n) dst[i] = accumulate ? dst[i] + v[i] : v[i];
       }
     }
   }
@@ -138,10 +113,10 @@ struct EpiScatterAdd {
   int ldr, N;
   const int* idx;
   template <int BN>
-  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr, int part) const {
     const int dst_row = valid ? (idx ? __ldg(idx + row) : row) : 0;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = part * (BN / 2); c < (part + 1) * (BN / 2); c += 32) {
       float v[32];
       load_chunk(taddr + c, v);
       if (valid && col0 + c < N) {
@@ -170,37 +145,37 @@ struct EpiQKV {
   const double* inv_freq;  // [head_dim/2]
   const int* pos;
   template <int BN>
-  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr, int part) const {
     const int which = col0 / h;
     const int cbase = col0 - which * h;
     __nv_bfloat16* out = which == 0 ? q : (which == 1 ? k : v);
     const double dp = (valid && rope) ? (double)__ldg(pos + row) : 0.0;
     const int half = head_dim >> 1;
+    const int per_head = half >> 5;  // 32-column rotation chunks per head
+    const int items = (BN / head_dim) * per_head;
 #pragma unroll 1
-    for (int hd = 0; hd < BN; hd += head_dim) {
-#pragma unroll 1
-      for (int cp = 0; cp < half; cp += 32) {
-        float a[32], b[32];
-        load_chunk(taddr + hd + cp, a);
-        load_chunk(taddr + hd + half + cp, b);
-        if (!valid) continue;
-        const int ca = cbase + hd + cp, cb = ca + half;
-        if (rope && which < 2) {  // only q and k are rotated (kernels.py:112-114)
-#pragma unroll 4
-          for (int i = 0; i < 32; ++i) {
-            const double ang = dp * __ldg(inv_freq + cp + i);
-            const double kq = rint(ang * 0.15915494309189535);
-            const float red = (float)fma(-kq, 6.283185307179586476925, ang);
-            float sn, cs;
-            sincosf(red, &sn, &cs);
-            const float xa = a[i], xb = b[i];
-            a[i] = xa * cs - xb * sn;
-            b[i] = xa * sn + xb * cs;
-          }
+    for (int it = part; it < items; it += 2) {
+      const int hd = (it / per_head) * head_dim, cp = (it % per_head) * 32;
+      float a[32], b[32];
+      load_chunk(taddr + hd + cp, a);
+      load_chunk(taddr + hd + half + cp, b);
+      if (!valid) continue;
+      const int ca = cbase + hd + cp, cb = ca + half;
+      if (rope && which < 2) {  // only q and k are rotated (kernels.py:112-114)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const double ang = dp * __ldg(inv_freq + cp + i);
+          const double kq = rint(ang * 0.15915494309189535);
+          const float red = (float)fma(-kq, 6.283185307179586476925, ang);
+          float sn, cs;
+          __sincosf(red, &sn, &cs);  // |red| <= pi: abs err < 2^-21
+          const float xa = a[i], xb = b[i];
+          a[i] = xa * cs - xb * sn;
+          b[i] = xa * sn + xb * cs;
         }
-        store_bf16x32(out + (size_t)row * h + ca, a);
-        store_bf16x32(out + (size_t)row * h + cb, b);
       }
+      store_bf16x32(out + (size_t)row * h + ca, a);
+      store_bf16x32(out + (size_t)row * h + cb, b);
     }
   }
 };
@@ -211,7 +186,7 @@ struct EpiQKV {
 // so one BN=256 tile holds matching gate/up columns.
 //   gu      : [M, N] bf16, same interleaved column order (saved for backward)
 //   inner   : [M, N/2] bf16 (silu) or [M, N] (relu), optional
-//   partial : [num_n_tiles, M] fp32 row sums of |inner| per tile, optional
+//   partial : [N/128, M] fp32 row sums of |inner| per half tile, optional
 struct EpiGateUp {
   __nv_bfloat16* gu;
   int ldgu;
@@ -220,12 +195,12 @@ struct EpiGateUp {
   float* partial;
   int M, relu;
   template <int BN>
-  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr, int part) const {
     static_assert(BN == 256, "gate/up interleave assumes 256-column tiles");
     float score = 0.f;
     if (!relu) {
 #pragma unroll 1
-      for (int c = 0; c < 128; c += 32) {
+      for (int c = part * 64; c < part * 64 + 64; c += 32) {
         float g[32], u[32];
         load_chunk(taddr + c, g);
         load_chunk(taddr + 128 + c, u);
@@ -237,7 +212,7 @@ struct EpiGateUp {
         for (int i = 0; i < 32; ++i) {
           g[i] = round_bf16(g[i]);
           u[i] = round_bf16(u[i]);
-          in[i] = g[i] * sigmoid_stable(g[i]) * u[i];
+          in[i] = g[i] * sigmoid_fast(g[i]) * u[i];
           score += fabsf(in[i]);
         }
         if (gu) {
@@ -248,7 +223,7 @@ struct EpiGateUp {
       }
     } else {
 #pragma unroll 1
-      for (int c = 0; c < 256; c += 32) {
+      for (int c = part * 128; c < part * 128 + 128; c += 32) {
         float u[32];
         load_chunk(taddr + c, u);
         if (!valid) continue;
@@ -263,7 +238,7 @@ struct EpiGateUp {
         if (inner) store_bf16x32(inner + (size_t)row * ldi + col0 + c, in);
       }
     }
-    if (valid && partial) partial[(size_t)(col0 / 256) * M + row] = score;
+    if (valid && partial) partial[(size_t)((col0 / 256) * 2 + part) * M + row] = score;
   }
 };
 
@@ -276,33 +251,34 @@ struct EpiDGateUp {
   __nv_bfloat16* dgu;
   int relu;
   template <int BN>
-  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr, int part) const {
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = part * (BN / 2); c < (part + 1) * (BN / 2); c += 32) {
+      const int mc = col0 + c;
+      const int gcol = relu ? mc : (mc >> 7) * 256 + (mc & 127);
+      // issue the saved-activation loads before the TMEM load
+      float g[32], u[32];
+      if (valid) {
+        load_bf16x32(gu + (size_t)row * ldgu + gcol, g);
+        if (!relu) load_bf16x32(gu + (size_t)row * ldgu + gcol + 128, u);
+      }
       float d[32];
       load_chunk(taddr + c, d);
       if (!valid) continue;
-      const int mc = col0 + c;
       if (!relu) {
-        const int gcol = (mc >> 7) * 256 + (mc & 127);
-        float g[32], u[32];
-        load_bf16x32(gu + (size_t)row * ldgu + gcol, g);
-        load_bf16x32(gu + (size_t)row * ldgu + gcol + 128, u);
         float dg[32], du[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const float s = sigmoid_stable(g[i]);
+          const float s = sigmoid_fast(g[i]);
           du[i] = d[i] * (g[i] * s);
           dg[i] = d[i] * u[i] * (s * (1.f + g[i] * (1.f - s)));
         }
         store_bf16x32(dgu + (size_t)row * ldgu + gcol, dg);
         store_bf16x32(dgu + (size_t)row * ldgu + gcol + 128, du);
       } else {
-        float u[32];
-        load_bf16x32(gu + (size_t)row * ldgu + mc, u);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) u[i] = u[i] > 0.f ? d[i] : 0.f;
-        store_bf16x32(dgu + (size_t)row * ldgu + mc, u);
+        for (int i = 0; i < 32; ++i) g[i] = g[i] > 0.f ? d[i] : 0.f;
+        store_bf16x32(dgu + (size_t)row * ldgu + mc, g);
       }
     }
   }
@@ -321,9 +297,9 @@ struct EpiSplit3 {
   int ldf, N, pattern, relu;
   const unsigned char* mask;
   template <int BN>
-  __device__ void run(int row, bool valid, int col0, uint32_t taddr) const {
+  __device__ void run(int row, bool valid, int col0, uint32_t taddr, int part) const {
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = part * (BN / 2); c < (part + 1) * (BN / 2); c += 32) {
       float v[32];
       load_chunk(taddr + c, v);
       if (!valid || col0 + c >= N) continue;
@@ -332,7 +308,7 @@ struct EpiSplit3 {
       for (int i = 0; i < 32; ++i) {
         float x = v[i];
         if (relu) x = fmaxf(x, 0.f);
-        if (mask && !mask[col0 + c + i]) x = 0.f;
+        if (mask && !mask[min(col0 + c + i, N - 1)]) x = 0.f;
         v[i] = x;
         hi[i] = round_bf16(x);
         lo[i] = x - hi[i];
@@ -365,15 +341,12 @@ struct EpiSplit3 {
   }
 };
 
-}  // namespace lemo
-
-// The kernel template calls epi(row, valid, col0, taddr); wrap run<BN>.
-namespace lemo {
+// The kernel template calls epi(row, valid, col0, taddr, part); wrap run<BN>.
 template <int BN, class Epi>
 struct Bound {
   Epi e;
-  __device__ void operator()(int row, bool valid, int col0, uint32_t taddr) const {
-    e.template run<BN>(row, valid, col0, taddr);
+  __device__ void operator()(int row, bool valid, int col0, uint32_t taddr, int part) const {
+    e.template run<BN>(row, valid, col0, taddr, part);
   }
 };
 
@@ -390,6 +363,7 @@ static int gemm_auto(const void* A, int lda, const void* B, int ldb, int M, int 
   if (N % 256 == 0 || N > 256) return gemm<256>(A, lda, B, ldb, M, N, K, e, st);
   return gemm<128>(A, lda, B, ldb, M, N, K, e, st);
 }
+
 }  // namespace lemo
 
 using namespace lemo;
@@ -412,10 +386,8 @@ int lemo_gemm_nn_bf16(const void* A, int lda, const void* B, int ldb, void* C, i
 }
 
 int lemo_gemm_f32(const void* A, int lda, const void* B, int ldb, float* C, int ldc, int M, int N,
-                  int K, const float* U, int ldu, int R, const float* S, int s_rs, int s_cs,
-                  float scale, int accumulate, void* stream) {
-  LEMO_ARG_CHECK(R >= 0 && R <= kMaxSideRank, "lemo_gemm_f32: side rank out of range");
-  EpiStoreF32 e{C, ldc, N, U, ldu, R, S, s_rs, s_cs, scale, accumulate};
+                  int K, int accumulate, void* stream) {
+  EpiStoreF32 e{C, ldc, N, accumulate};
   LEMO_RETURN_RC("lemo_gemm_f32", gemm_auto(A, lda, B, ldb, M, N, K, e, (cudaStream_t)stream));
 }
 

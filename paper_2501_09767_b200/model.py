@@ -603,7 +603,7 @@ def mlp_block_score_vector(layer: LayerState, x: torch.Tensor, block_size: int, 
     inv_all = torch.empty(s, dtype=F32, device=dev)
     xn_all = ops.rmsnorm_gather(x, layer.mlp_norm_w, None, inv=inv_all)
     gu_all = torch.empty(s, N, dtype=BF16, device=dev) if keep_rows else None
-    partial = torch.empty(N // 256, s, dtype=F32, device=dev)
+    partial = torch.empty(N // 128, s, dtype=F32, device=dev)
     ops.gemm_gateup(xn_all, layer.w_gu_t, gu=gu_all, partial=partial, relu=layer.relu)
     del xn_all
     vec = ops.mlp_block_scores(partial, s=s, n_valid=n_valid, b=block_size, m_real=layer.m)

@@ -69,18 +69,14 @@ def gemm_bf16(a, b, out=None):
     return out
 
 
-def gemm_f32(a, b, out=None, *, side_u=None, side_s=None, side_strides=(0, 0), scale=1.0,
-             accumulate=False):
-    """out (+)= a·bᵀ + scale·side_u·S with S(j, col) = side_s[j*s_rs + col*s_cs]."""
+def gemm_f32(a, b, out=None, *, accumulate=False):
+    """out (+)= a·bᵀ in fp32."""
     M, N, K = _mnk(a, b)
-    _check(out, side_u, side_s)
+    _check(out)
     if out is None:
         out = torch.empty(M, N, dtype=F32, device=a.device)
-    R = 0 if side_u is None else side_u.shape[1]
-    ldu = 0 if side_u is None else side_u.stride(0)
     call("lemo_gemm_f32", ptr(a), a.stride(0), ptr(b), b.stride(0), ptr(out), out.stride(0), M, N,
-         K, ptr(side_u), ldu, R, ptr(side_s), int(side_strides[0]), int(side_strides[1]),
-         float(scale), int(bool(accumulate)), _s())
+         K, int(bool(accumulate)), _s())
     return out
 
 

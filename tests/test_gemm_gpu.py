@@ -27,20 +27,17 @@ def test_gemm_bf16(cuda, M, N, K):
     assert err <= 1e-2 * scale + 1e-3, (err, scale)
 
 
-@pytest.mark.parametrize("M,N,K,R", [(256, 512, 256, 0), (333, 256, 512, 16), (128, 4096, 4096, 8)])
-def test_gemm_f32_side(cuda, M, N, K, R):
+@pytest.mark.parametrize("M,N,K,acc", [(256, 512, 256, True), (333, 250, 512, False),
+                                       (128, 4096, 4096, True), (1024, 10, 3072, False)])
+def test_gemm_f32(cuda, M, N, K, acc):
     g = torch.Generator(device=cuda).manual_seed(3)
     a = torch.randn(M, K, device=cuda, generator=g).bfloat16()
     b = torch.randn(N, K, device=cuda, generator=g).bfloat16()
     out = torch.randn(M, N, device=cuda, generator=g)
     base = out.clone()
-    u = torch.randn(M, max(R, 1), device=cuda, generator=g)[:, :R].contiguous() if R else None
-    s = torch.randn(N, max(R, 1), device=cuda, generator=g).contiguous() if R else None  # S(j,col)=s[col*R+j]
-    ops.gemm_f32(a, b, out, side_u=u, side_s=s, side_strides=(1, R), scale=0.5, accumulate=True)
+    ops.gemm_f32(a, b, out, accumulate=acc)
     torch.cuda.synchronize()
-    ref = base + _ref(a, b)
-    if R:
-        ref = ref + 0.5 * u @ s.T
+    ref = (base if acc else 0) + _ref(a, b)
     err = (out - ref).abs().max().item()
     assert err <= 1e-3 * ref.abs().max().item() + 1e-3
 

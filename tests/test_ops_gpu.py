@@ -249,7 +249,7 @@ def test_gateup_and_dgateup_vs_torch(cuda):
     N = L.w_gu_t.shape[0]
     gu = torch.empty(M, N, dtype=torch.bfloat16, device=cuda)
     inner = torch.empty(M, L.m_pad, dtype=torch.bfloat16, device=cuda)
-    part = torch.empty(N // 256, M, device=cuda)
+    part = torch.empty(N // 128, M, device=cuda)
     ops.gemm_gateup(xn, L.w_gu_t, gu=gu, inner=inner, partial=part)
     full = xn.float() @ L.w_gu_t.float().t()
     gate = full.view(M, L.m_pad // 128, 2, 128)[:, :, 0].reshape(M, -1)
