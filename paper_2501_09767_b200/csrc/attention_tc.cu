@@ -144,37 +144,48 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&s_full[st], (j >> 1) & 1);
       tc_fence_after();
       float s[kB];
+      {
+        uint32_t raw[kB];
 #pragma unroll
-      for (int c = 0; c < kB / 32; ++c) {
-        uint32_t raw[32];
-        tmem_ld_32x32b_x32(tS[st] + lane_off + c * 32, raw);
-        tmem_ld_wait();
+        for (int c = 0; c < kB / 32; ++c)
+          tmem_ld_32x32b_x32(tS[st] + lane_off + c * 32,
+                             *reinterpret_cast<uint32_t(*)[32]>(raw + c * 32));
+        tmem_ld_wait();  // one wait for all four loads
 #pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(raw[i]);
+        for (int i = 0; i < kB; ++i) s[i] = __uint_as_float(raw[i]);
       }
       const int kv0 = j * kB;
       const bool edge = (j == qb) || (kv0 + kB > n);
-      float mraw = -INFINITY;
+      if (edge) {
 #pragma unroll
-      for (int i = 0; i < kB; ++i) {
-        if (edge) {
+        for (int i = 0; i < kB; ++i) {
           const int key = kv0 + i;
           if (key > grow || key >= n) s[i] = -INFINITY;
         }
-        mraw = fmaxf(mraw, s[i]);
       }
+      // row max / row sum with 8 independent chains (ILP; one warp per SMSP)
+      float mr[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mr[t] = s[t];
+#pragma unroll
+      for (int i = 8; i < kB; ++i) mr[i & 7] = fmaxf(mr[i & 7], s[i]);
+      const float mraw = fmaxf(fmaxf(fmaxf(mr[0], mr[1]), fmaxf(mr[2], mr[3])),
+                               fmaxf(fmaxf(mr[4], mr[5]), fmaxf(mr[6], mr[7])));
       // lazy rescaling: keep the running max unless it grew by > 8 (log2
       // units); O / l / lse stay exact because they share the stale max
       const float mx = mraw * sl2;
       const float m_new = (m == -INFINITY || mx > m + 8.f) ? fmaxf(mx, m) : m;
       const float corr = (m == -INFINITY) ? 0.f : ex2_approx(m - m_new);
-      float sum = 0.f;
+      float sm[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) sm[t] = 0.f;
 #pragma unroll
       for (int i = 0; i < kB; ++i) {
         const float p = ex2_approx(fmaf(s[i], sl2, -m_new));
         s[i] = p;
-        sum += p;
+        sm[i & 7] += p;
       }
+      const float sum = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
       l = l * corr + sum;
       m = m_new;
       if (j > 0) {
@@ -263,14 +274,13 @@ __device__ __forceinline__ void store_row_sw128(uint8_t* tile, int r, const floa
 }
 
 __device__ __forceinline__ void tmem_row_load(uint32_t taddr, float (&v)[kB]) {
+  uint32_t raw[kB];
 #pragma unroll
-  for (int c = 0; c < kB / 32; ++c) {
-    uint32_t raw[32];
-    tmem_ld_32x32b_x32(taddr + c * 32, raw);
-    tmem_ld_wait();
+  for (int c = 0; c < kB / 32; ++c)
+    tmem_ld_32x32b_x32(taddr + c * 32, *reinterpret_cast<uint32_t(*)[32]>(raw + c * 32));
+  tmem_ld_wait();
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[c * 32 + i] = __uint_as_float(raw[i]);
-  }
+  for (int i = 0; i < kB; ++i) v[i] = __uint_as_float(raw[i]);
 }
 
 // Issue D (+)= A·B over K = 128 with A K-major SW128 (two 64-col boxes) and B
