@@ -154,6 +154,57 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(
   }
 }
 
+// Vectorised variant: the row of g, x and w stays in registers between the
+// dot product and the output pass (one read of each, 16-B accesses).
+template <bool kXBf16, int VPT>
+__global__ void __launch_bounds__(256) rmsnorm_bwd_vec_kernel(
+    const float* __restrict__ g, int ldg, const void* __restrict__ xv, int ldx,
+    const float* __restrict__ inv_in, const float* __restrict__ w, const int* __restrict__ idx,
+    int h, float gscale, float* __restrict__ dx, int lddx, int accumulate) {
+  __shared__ float red[8];
+  const int row = blockIdx.x;
+  const float inv = inv_in[row];
+  const int nv = h >> 2;
+  float4 gw[VPT], xr[VPT];
+  float dot = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * 256;
+    if (c < nv) {
+      const float4 gg = reinterpret_cast<const float4*>(g + (size_t)row * ldg)[c];
+      const float4 ww = __ldg(reinterpret_cast<const float4*>(w) + c);
+      if (kXBf16) {
+        const uint2 u = reinterpret_cast<const uint2*>(
+            reinterpret_cast<const __nv_bfloat16*>(xv) + (size_t)row * ldx)[c];
+        xr[i] = make_float4(bf16_lo(u.x), bf16_hi(u.x), bf16_lo(u.y), bf16_hi(u.y));
+      } else {
+        xr[i] = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(xv) +
+                                                (size_t)row * ldx)[c];
+      }
+      gw[i] = make_float4(gscale * gg.x * ww.x, gscale * gg.y * ww.y, gscale * gg.z * ww.z,
+                          gscale * gg.w * ww.w);
+      dot += gw[i].x * xr[i].x + gw[i].y * xr[i].y + gw[i].z * xr[i].z + gw[i].w * xr[i].w;
+    }
+  }
+  dot = block_sum<256>(dot, red);
+  const float coef = inv * inv * inv * dot / (float)h;
+  const int dst = idx ? __ldg(idx + row) : row;
+  float4* d = reinterpret_cast<float4*>(dx + (size_t)dst * lddx);
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * 256;
+    if (c < nv) {
+      float4 val = make_float4(gw[i].x * inv - xr[i].x * coef, gw[i].y * inv - xr[i].y * coef,
+                               gw[i].z * inv - xr[i].z * coef, gw[i].w * inv - xr[i].w * coef);
+      if (accumulate) {
+        const float4 o = d[c];
+        val.x += o.x; val.y += o.y; val.z += o.z; val.w += o.w;
+      }
+      d[c] = val;
+    }
+  }
+}
+
 __global__ void embed_kernel(const int* __restrict__ ids, const float* __restrict__ table, int h,
                              const float* __restrict__ pos_table, float* __restrict__ x) {
   const int row = blockIdx.x;
@@ -498,12 +549,28 @@ int lemo_rmsnorm_bwd(const float* g, int ldg, const void* x, int x_bf16, int ldx
                      float* dx, int lddx, int accumulate, void* stream) {
   if (M <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  if (x_bf16)
+  const bool vec_ok = (h % 4 == 0) && (ldg % 4 == 0) && (ldx % 4 == 0) && (lddx % 4 == 0) &&
+                      h <= 4 * 256 * 8;
+  if (vec_ok) {
+    const int vpt = (h / 4 + 255) / 256;
+#define RB(XB, V)                                                                       \
+  rmsnorm_bwd_vec_kernel<XB, V><<<M, 256, 0, st>>>(g, ldg, x, ldx, inv, w, idx, h, gscale, dx, \
+                                                   lddx, accumulate)
+    if (x_bf16) {
+      if (vpt <= 1) RB(true, 1); else if (vpt <= 2) RB(true, 2); else if (vpt <= 4) RB(true, 4);
+      else RB(true, 8);
+    } else {
+      if (vpt <= 1) RB(false, 1); else if (vpt <= 2) RB(false, 2); else if (vpt <= 4) RB(false, 4);
+      else RB(false, 8);
+    }
+#undef RB
+  } else if (x_bf16) {
     rmsnorm_bwd_kernel<true><<<M, 256, 0, st>>>(g, ldg, x, ldx, inv, w, idx, h, gscale, dx, lddx,
                                                 accumulate);
-  else
+  } else {
     rmsnorm_bwd_kernel<false><<<M, 256, 0, st>>>(g, ldg, x, ldx, inv, w, idx, h, gscale, dx, lddx,
                                                  accumulate);
+  }
   LEMO_CHECK_LAUNCH("lemo_rmsnorm_bwd");
   return 0;
 }

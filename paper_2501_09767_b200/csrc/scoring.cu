@@ -164,22 +164,49 @@ __global__ void __launch_bounds__(256) sgemm_kernel(const float* __restrict__ A,
 }
 
 // vec[n] = Σ_{m=n}^{nb-1} (double)max(S[m,n], 0), ascending m (sparsity.py:256-259)
+// One warp per column: the 32 lanes fetch 32 consecutive query blocks at once
+// (all loads in flight), then the warp adds them in ascending m order through
+// shuffles — the reference's exact f64 summation order, without its latency.
 __global__ void colsum_clamped_kernel(const float* __restrict__ S, int lds, int nb,
                                       double* __restrict__ vec) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (n >= nb) return;
   double acc = 0.0;
-  int m = n;
-  for (; m + 4 <= nb; m += 4) {
-    const float a = S[(size_t)m * lds + n], b = S[(size_t)(m + 1) * lds + n];
-    const float c = S[(size_t)(m + 2) * lds + n], d = S[(size_t)(m + 3) * lds + n];
-    acc += (double)fmaxf(a, 0.f);
-    acc += (double)fmaxf(b, 0.f);
-    acc += (double)fmaxf(c, 0.f);
-    acc += (double)fmaxf(d, 0.f);
+  int m0 = n;
+  float cur = m0 + lane < nb ? S[(size_t)(m0 + lane) * lds + n] : 0.f;
+  while (m0 < nb) {
+    const int m1 = m0 + 32;
+    const float nxt = m1 + lane < nb ? S[(size_t)(m1 + lane) * lds + n] : 0.f;  // prefetch
+    const double v = (double)fmaxf(cur, 0.f);
+    const int cnt = min(32, nb - m0);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double x = __shfl_sync(0xffffffffu, v, j);
+      if (j < cnt) acc += x;
+    }
+    cur = nxt;
+    m0 = m1;
   }
-  for (; m < nb; ++m) acc += (double)fmaxf(S[(size_t)m * lds + n], 0.f);
-  vec[n] = acc;
+  if (lane == 0) vec[n] = acc;
+}
+
+// Token scores (one thread per row, coalesced over the per-tile partials, the
+// same sequential tile order as before) and the block max via segmented warp
+// shuffles (b a power of two <= 32).
+__global__ void mlp_block_scores_warp_kernel(const float* __restrict__ partial, int n_tiles,
+                                             int s, int n_valid, int b, float m_real,
+                                             double* __restrict__ vec) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lim = min(s, n_valid);
+  float best = -INFINITY;
+  if (row < lim) {
+    float acc = 0.f;
+    for (int t = 0; t < n_tiles; ++t) acc += partial[(size_t)t * s + row];
+    best = acc / m_real;
+  }
+  for (int o = b >> 1; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((row % b) == 0 && row < s) vec[row / b] = best == -INFINITY ? 0.0 : (double)best;
 }
 
 __global__ void mlp_block_scores_kernel(const float* __restrict__ partial, int n_tiles, int s,
@@ -374,7 +401,7 @@ int lemo_split_bf16x3(const float* A, int lda, int M, int K, int pattern, void* 
 
 int lemo_colsum_clamped(const float* S, int lds, int nb, double* vec, void* stream) {
   if (nb <= 0) return 0;
-  colsum_clamped_kernel<<<(nb + 127) / 128, 128, 0, (cudaStream_t)stream>>>(S, lds, nb, vec);
+  colsum_clamped_kernel<<<(nb + 7) / 8, 256, 0, (cudaStream_t)stream>>>(S, lds, nb, vec);
   LEMO_CHECK_LAUNCH("lemo_colsum_clamped");
   return 0;
 }
@@ -383,8 +410,14 @@ int lemo_mlp_block_scores(const float* partial, int n_tiles, int s, int n_valid,
                           double* vec, void* stream) {
   const int nb = (s + b - 1) / b;
   if (nb <= 0) return 0;
-  mlp_block_scores_kernel<<<(nb + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
-      partial, n_tiles, s, n_valid, b, (float)m_real, vec);
+  if (b <= 32 && (b & (b - 1)) == 0) {
+    const long long rows = (long long)nb * b;
+    mlp_block_scores_warp_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        partial, n_tiles, s, n_valid, b, (float)m_real, vec);
+  } else {
+    mlp_block_scores_kernel<<<(nb + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+        partial, n_tiles, s, n_valid, b, (float)m_real, vec);
+  }
   LEMO_CHECK_LAUNCH("lemo_mlp_block_scores");
   return 0;
 }
