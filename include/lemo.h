@@ -146,11 +146,14 @@ int lemo_lora_pack_a_ext(const float* A, int lda, int h, int r2, void* w, int ld
                          void* stream);
 
 /* LoRA weight gradients accumulated (+=) into dA0/dB0/dA1/dB1:
- * dA[c,j] = s·Σ xn[i,c]u[i,j], dB[j,c] = s·Σ t[i,j]g[i,c] (tensor.py:324-325). */
+ * dA[c,j] = s·Σ xn[i,c]u[i,j], dB[j,c] = s·Σ t[i,j]g[i,c] (tensor.py:324-325).
+ * Row-group partial sums go to `workspace` (lemo_lora_grads_workspace floats)
+ * and are reduced in a fixed order: deterministic, no atomics. */
+int lemo_lora_grads_workspace(int M, int h, int r); /* floats; not a status */
 int lemo_lora_grads(const void* xg, const float* inv, const float* w, const float* t,
                     const float* u, int ld, const float* g0, const float* g1, int M, int h, int r,
                     float scale, int lda, float* dA0, float* dB0, float* dA1, float* dB1,
-                    void* stream);
+                    float* workspace, void* stream);
 
 /* Cross-entropy rows of segmented_loss_and_grad (kernels.py:256-273): per-row
  * loss terms and dlogits = (softmax - onehot)·inv_count (bf16); ignore rows

@@ -94,7 +94,7 @@ def ptr(t) -> int | None:
 
 
 # kernels launched per entry point (everything else launches exactly one)
-_LAUNCHES = {"lemo_flash_bwd": 3}
+_LAUNCHES = {"lemo_flash_bwd": 3, "lemo_lora_grads": 2}
 
 
 class Instrument:

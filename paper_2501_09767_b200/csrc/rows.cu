@@ -347,19 +347,25 @@ __global__ void lora_pack_a_ext_kernel(const float* __restrict__ A, int lda, int
 //   dA0[c,j] += s Σ_i xn[i,c] u0[i,j]     dB0[j,c] += s Σ_i t0[i,j] g0[i,c]
 // (same for adapter 1), xn recomputed from the saved bf16 rows, inv, w.
 constexpr int kLoraRows = 64;
+constexpr int kLoraGroups = 32;  // row groups = partial sums reduced in fixed order
 template <int R>
 __global__ void __launch_bounds__(128) lora_grads_kernel(
     const __nv_bfloat16* __restrict__ xg, const float* __restrict__ inv, const float* __restrict__ w,
     const float* __restrict__ t, const float* __restrict__ u, int ld, const float* __restrict__ g0,
-    const float* __restrict__ g1, int M, int h, float scale, int lda, float* __restrict__ dA0,
-    float* __restrict__ dB0, float* __restrict__ dA1, float* __restrict__ dB1) {
+    const float* __restrict__ g1, int M, int h, float* __restrict__ part) {
   // per row: [t_q (R) | t_v (R)] and [u_q (R) | u_v (R)], read as float4 broadcasts
   __shared__ __align__(16) float st[kLoraRows][2 * R];
   __shared__ __align__(16) float su[kLoraRows][2 * R];
   __shared__ float sinv[kLoraRows];
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r0 = blockIdx.y * kLoraRows;
+  float a0[R], b0[R], a1[R], b1[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) a0[j] = b0[j] = a1[j] = b1[j] = 0.f;
+  const float wc = c < h ? w[c] : 0.f;
+  // row-group g owns slabs g, g+G, g+2G, ... (fixed order: deterministic)
+  for (int r0 = blockIdx.y * kLoraRows; r0 < M; r0 += gridDim.y * kLoraRows) {
   const int nrow = min(kLoraRows, M - r0);
+  __syncthreads();
   for (int e = threadIdx.x; e < nrow * 2 * R; e += blockDim.x) {
     const int i = e / (2 * R), j = e - i * 2 * R;
     st[i][j] = t[(size_t)(r0 + i) * ld + j];
@@ -367,11 +373,7 @@ __global__ void __launch_bounds__(128) lora_grads_kernel(
   }
   for (int i = threadIdx.x; i < nrow; i += blockDim.x) sinv[i] = inv[r0 + i];
   __syncthreads();
-  if (c >= h) return;
-  float a0[R], b0[R], a1[R], b1[R];
-#pragma unroll
-  for (int j = 0; j < R; ++j) a0[j] = b0[j] = a1[j] = b1[j] = 0.f;
-  const float wc = w[c];
+  if (c < h) {
 #pragma unroll 2
   for (int i = 0; i < nrow; ++i) {
     const size_t off = (size_t)(r0 + i) * h + c;
@@ -393,13 +395,38 @@ __global__ void __launch_bounds__(128) lora_grads_kernel(
       b1[j] = fmaf(tv[R + j], v, b1[j]);
     }
   }
+  }
+  }
+  if (c >= h) return;
+  // partials part[g][q][j][c], q = A0, A1, B0, B1 (coalesced over c)
+  float* pg = part + (size_t)blockIdx.y * 4 * R * h + c;
 #pragma unroll
   for (int j = 0; j < R; ++j) {
-    atomicAdd(dA0 + (size_t)c * lda + j, scale * a0[j]);
-    atomicAdd(dA1 + (size_t)c * lda + j, scale * a1[j]);
-    atomicAdd(dB0 + (size_t)j * h + c, scale * b0[j]);
-    atomicAdd(dB1 + (size_t)j * h + c, scale * b1[j]);
+    pg[(size_t)(0 * R + j) * h] = a0[j];
+    pg[(size_t)(1 * R + j) * h] = a1[j];
+    pg[(size_t)(2 * R + j) * h] = b0[j];
+    pg[(size_t)(3 * R + j) * h] = b1[j];
   }
+}
+
+// Fixed-order sum of the row-group partials (g ascending), scaled and added
+// into the gradients: no atomics, so all-retain ≡ dense bitwise
+// (tests/test_model.py:186-191) and repeated steps are reproducible.
+__global__ void __launch_bounds__(256) lora_grads_reduce_kernel(
+    const float* __restrict__ part, int G, int R, int h, float scale, int lda,
+    float* __restrict__ dA0, float* __restrict__ dB0, float* __restrict__ dA1,
+    float* __restrict__ dB1) {
+  const int n = 4 * R * h;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  float acc = 0.f;
+  for (int g = 0; g < G; ++g) acc += part[(size_t)g * n + e];
+  const int q = e / (R * h), rem = e - q * R * h, j = rem / h, c = rem - j * h;
+  float* dst = q == 0 ? dA0 + (size_t)c * lda + j
+             : q == 1 ? dA1 + (size_t)c * lda + j
+             : q == 2 ? dB0 + (size_t)j * h + c
+                      : dB1 + (size_t)j * h + c;
+  *dst += scale * acc;
 }
 
 // Cross-entropy rows of segmented_loss_and_grad (kernels.py:256-273,
@@ -629,18 +656,29 @@ int lemo_lora_pack_a_ext(const float* A, int lda, int h, int r2, void* w, int ld
   return 0;
 }
 
+static int lora_row_groups(int M) {
+  const int slabs = (M + kLoraRows - 1) / kLoraRows;
+  return slabs < kLoraGroups ? slabs : kLoraGroups;
+}
+
+int lemo_lora_grads_workspace(int M, int h, int r) {
+  if (M <= 0) return 0;
+  return lora_row_groups(M) * 4 * r * h;
+}
+
 int lemo_lora_grads(const void* xg, const float* inv, const float* w, const float* t,
                     const float* u, int ld, const float* g0, const float* g1, int M, int h, int r,
                     float scale, int lda, float* dA0, float* dB0, float* dA1, float* dB1,
-                    void* stream) {
+                    float* workspace, void* stream) {
   if (M <= 0) return 0;
   LEMO_ARG_CHECK(r <= 16, "lemo_lora_grads: LoRA rank <= 16");
-  dim3 grid((h + 127) / 128, (M + kLoraRows - 1) / kLoraRows);
+  LEMO_ARG_CHECK(workspace != nullptr, "lemo_lora_grads: workspace required");
+  const int G = lora_row_groups(M);
+  dim3 grid((h + 127) / 128, G);
   cudaStream_t st = (cudaStream_t)stream;
   auto* xgp = reinterpret_cast<const __nv_bfloat16*>(xg);
-#define LG(RR)                                                                                 \
-  lora_grads_kernel<RR><<<grid, 128, 0, st>>>(xgp, inv, w, t, u, ld, g0, g1, M, h, scale, lda, \
-                                              dA0, dB0, dA1, dB1)
+#define LG(RR) \
+  lora_grads_kernel<RR><<<grid, 128, 0, st>>>(xgp, inv, w, t, u, ld, g0, g1, M, h, workspace)
   switch (r) {
     case 2: LG(2); break;
     case 4: LG(4); break;
@@ -649,6 +687,9 @@ int lemo_lora_grads(const void* xg, const float* inv, const float* w, const floa
     default: set_error_msg("lemo_lora_grads: LoRA rank must be 2, 4, 8 or 16"); return LEMO_ERR_REPORTED;
   }
 #undef LG
+  const int n = 4 * r * h;
+  lora_grads_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(workspace, G, r, h, scale, lda, dA0,
+                                                            dB0, dA1, dB1);
   LEMO_CHECK_LAUNCH("lemo_lora_grads");
   return 0;
 }

@@ -12,7 +12,7 @@ import math
 
 import torch
 
-from ._lib import call, ptr, stream_ptr
+from ._lib import call, lib, ptr, stream_ptr
 from .errors import ContractError, DimensionError
 
 BF16 = torch.bfloat16
@@ -239,9 +239,11 @@ def lora_grads(xg, inv, w, t, u, g0, g1, *, r, scale, dA, dB0, dB1):
     """dA (= [h, 2r] interleaved q|v), dB0, dB1 accumulated in place."""
     _check(xg, inv, w, t, u, g0, g1, dA, dB0, dB1)
     M, h = xg.shape
+    ws = torch.empty(max(1, lib().lemo_lora_grads_workspace(M, h, r)), dtype=torch.float32,
+                     device=xg.device)
     call("lemo_lora_grads", ptr(xg), ptr(inv), ptr(w), ptr(t), ptr(u), t.stride(0), ptr(g0),
          ptr(g1), M, h, r, float(scale), dA.stride(0), ptr(dA), ptr(dB0), ptr(dA[:, r:]),
-         ptr(dB1), _s())
+         ptr(dB1), ptr(ws), _s())
 
 
 def ce_rows(logits, targets, *, V, ignore, inv_count, dlogits, row_loss, bad):
