@@ -240,8 +240,9 @@ int lemo_attn_delta(const void* o, const void* dout, float* delta, int n, int h,
                     void* stream);
 
 /* Attention backward on the tcgen05 path (head_dim 128): an atomic-free dK/dV
- * kernel (transposed formulation, dK/dV resident in TMEM) and a dQ kernel,
- * both recomputing P from lse.  Same contract as lemo_flash_bwd. */
+ * kernel (transposed formulation, dK/dV resident in TMEM, Pᵀ/dSᵀ as bf16 TMEM
+ * A operands) and a dQ kernel, both recomputing P from lse and pipelined so
+ * the element-wise phases overlap the MMAs.  Same contract as lemo_flash_bwd. */
 int lemo_flash_bwd_tc(const void* q, const void* k, const void* v, const void* o,
                       const void* dout, const float* lse, float* delta, float* dq, float* dk,
                       float* dv, int n, int h, int head_dim, float scale, void* stream);

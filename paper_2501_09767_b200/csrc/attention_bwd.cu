@@ -1,0 +1,555 @@
+// tcgen05 FlashAttention backward over the compact retained sequence
+// (tensor.py:693-722: P recomputed from the saved log-sum-exp,
+// Δ = Σ dO∘O, dS = P∘(dP − Δ)), head_dim 128, atomic-free and deterministic.
+//
+// Two kernels on 128 x 128 tiles (tcgen05 reaches its full rate only for
+// N >= 128: an M128·N64 MMA costs 48 cycles instead of 32, measured by
+// scripts/probes/mma_probe.cu), 384 threads: w0 TMA producer, w1 MMA issuer,
+// w2 TMEM allocator, w4-w7 / w8-w11 two element-wise warpgroups that split the
+// 128 columns of every score tile (WG w owns columns 64w..64w+63).
+//
+//   dK/dV  CTA = one 128-key tile of one head, thread = key row.  Per
+//          128-query tile t (diagonal first):
+//            Sᵀ = K·Q_tᵀ, dPᵀ = V·dO_tᵀ                     (TMEM, fp32)
+//            phase A: Pᵀ = exp2(Sᵀ·c − lse₂) → bf16 over the Sᵀ columns
+//            phase B: dSᵀ = Pᵀ∘(dPᵀ − Δ)     → bf16 over the dPᵀ columns
+//            dV += Pᵀ·dO_t, dK += dSᵀ·Q_t  (A operand read from TMEM)
+//          issue order  S(0) dP(0) | dV(t) S(t+1) dK(t) dP(t+1) | …  so the
+//          tensor core computes S(t+1) while phase B(t) runs and dP(t+1) while
+//          phase A(t+1) runs.  dV, dK stay in TMEM (4 × 128 columns in all).
+//   dQ     CTA = one 128-query tile, thread = query row.  Per key tile j:
+//            S_j = Q·K_jᵀ (double-buffered), dP_j = dO·V_jᵀ,
+//            phase A: P = exp2(S·c − lse₂) (registers), phase B: dS = P∘(dP − Δ)
+//            → bf16 over the dP columns, dQ += dS·K_j (A from TMEM)
+//          issue order  S(0) S(1) dP(0) | dQ(j) dP(j+1) S(j+2) | …
+//
+// A later MMA that overwrites TMEM columns still read (as bf16 A operand) by
+// an earlier one is safe without a wait: tcgen05.mma executes in issue order.
+#include "gemm.cuh"
+#include "lemo_internal.h"
+
+namespace lemo {
+namespace fab {
+
+constexpr int kT = 128;                // rows per tile (keys or queries)
+constexpr int kD = 128;                // head dim
+constexpr int kBox = kT * 64 * 2;      // [128 x 64] bf16 SW128 box = 16 KB
+constexpr int kTile = 2 * kBox;        // [128 x 128] = 32 KB
+constexpr int kThreads = 384;
+constexpr float kLog2e = 1.4426950408889634f;
+
+// D (+)= A·Bᵀ with A, B [128 x 128] K-major tiles (two 16 KB boxes each).
+template <uint32_t kIdesc>
+__device__ __forceinline__ void mma_kk(uint32_t d, uint32_t a, uint32_t b) {
+#pragma unroll
+  for (int kk = 0; kk < kD / 16; ++kk) {
+    const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
+    umma_bf16_ss(d, umma_desc_k_sw128(a + off), umma_desc_k_sw128(b + off), kIdesc,
+                 kk > 0 ? 1u : 0u);
+  }
+}
+
+// D (+)= A·B, A = bf16 [128 x 128] in TMEM, packed as two 32-column groups at
+// a_tmem and a_tmem + 64 (columns 64w..64w+31 hold WG w's 64 values); B =
+// smem [128 (K) x 128 (N)] row-major tile = MN-major, two 16 KB 64-col atoms.
+template <uint32_t kIdesc>
+__device__ __forceinline__ void mma_tk(uint32_t d, uint32_t a_tmem, uint32_t b, bool acc) {
+#pragma unroll
+  for (int kk = 0; kk < kT / 16; ++kk)
+    umma_bf16_ts(d, a_tmem + (kk >> 2) * 64 + (kk & 3) * 8,
+                 umma_desc_mn_sw128(b + kk * 2048, kBox), kIdesc, (acc || kk > 0) ? 1u : 0u);
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// 32 values → 16 packed bf16x2 TMEM columns (element 2j in the low half).
+__device__ __forceinline__ void st_bf16x32(uint32_t taddr, const float* v) {
+  uint32_t p[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) p[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+  tmem_st_32x32b_x16(taddr, p);
+}
+
+// This thread's TMEM row segment [0, kCols) × scale → fp32 dst.
+template <int kCols>
+__device__ __forceinline__ void store_row_f32(uint32_t taddr, float* dst, float scale, bool ok) {
+#pragma unroll 1
+  for (int c = 0; c < kCols / 32; ++c) {
+    uint32_t raw[32];
+    tmem_ld_32x32b_x32(taddr + c * 32, raw);
+    tmem_ld_wait();
+    if (ok) {
+      float4* p = reinterpret_cast<float4*>(dst + c * 32);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        p[q] = make_float4(__uint_as_float(raw[4 * q]) * scale, __uint_as_float(raw[4 * q + 1]) * scale,
+                           __uint_as_float(raw[4 * q + 2]) * scale,
+                           __uint_as_float(raw[4 * q + 3]) * scale);
+    }
+  }
+}
+
+// The 227 KB budget leaves no room for a 1 KB alignment pad: the dynamic
+// window must already be 1024-B aligned (it is when no static smem precedes it).
+__device__ __forceinline__ uint8_t* aligned_smem(uint8_t* raw) {
+  if (smem_u32(raw) & 1023u) __trap();
+  return raw;
+}
+
+// ---------------------------------------------------------------------------
+// dK / dV
+
+constexpr int kQStages = 3, kOStages = 2;
+constexpr int kSmemKV = (2 + kQStages + kOStages) * kTile + 2 * 2 * kT * 4 + 256;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    flash_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmQ,
+                          const __grid_constant__ CUtensorMap tmK,
+                          const __grid_constant__ CUtensorMap tmV,
+                          const __grid_constant__ CUtensorMap tmO,
+                          const float* __restrict__ lse, const float* __restrict__ delta,
+                          float* __restrict__ dk, float* __restrict__ dv, int n, int h, float sl2,
+                          float scale) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = aligned_smem(smem_raw);
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + kTile;
+  uint8_t* sQ = smem + 2 * kTile;              // [kQStages]
+  uint8_t* sO = sQ + kQStages * kTile;         // [kOStages]
+  float* sLD = reinterpret_cast<float*>(sO + kOStages * kTile);  // [wg][buf][lse₂ 64 | Δ 64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + 2 * 2 * kT);
+  uint64_t* kv_full = bars;
+  uint64_t* q_full = bars + 1;              // [kQStages]
+  uint64_t* q_empty = q_full + kQStages;    // [kQStages]
+  uint64_t* o_full = q_empty + kQStages;    // [kOStages]
+  uint64_t* o_empty = o_full + kOStages;    // [kOStages]
+  uint64_t* s_full = o_empty + kOStages;
+  uint64_t* dp_full = s_full + 1;
+  uint64_t* p_full = dp_full + 1;
+  uint64_t* ds_full = p_full + 1;
+  uint64_t* mm_done = ds_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mm_done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x, hd = blockIdx.y;
+  const int k0 = kb * kT, c0 = hd * kD;
+  const int T = (n - k0 + kT - 1) / kT;  // query tiles from the diagonal on
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmO);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < kQStages; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+    }
+    for (int s = 0; s < kOStages; ++s) {
+      mbar_init(&o_full[s], 1);
+      mbar_init(&o_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(p_full, 8);
+    mbar_init(ds_full, 8);
+    mbar_init(mm_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tP = tmem + 128, tdV = tmem + 256, tdK = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * kTile);
+      tma_load_2d(&tmK, kv_full, sK, c0, k0);
+      tma_load_2d(&tmK, kv_full, sK + kBox, c0 + 64, k0);
+      tma_load_2d(&tmV, kv_full, sV, c0, k0);
+      tma_load_2d(&tmV, kv_full, sV + kBox, c0 + 64, k0);
+      for (int t = 0; t < T; ++t) {
+        const int q0 = k0 + t * kT;
+        const int sq = t % kQStages, so = t % kOStages;
+        mbar_wait(&q_empty[sq], ((t / kQStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[sq], kTile);
+        tma_load_2d(&tmQ, &q_full[sq], sQ + sq * kTile, c0, q0);
+        tma_load_2d(&tmQ, &q_full[sq], sQ + sq * kTile + kBox, c0 + 64, q0);
+        mbar_wait(&o_empty[so], ((t / kOStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&o_full[so], kTile);
+        tma_load_2d(&tmO, &o_full[so], sO + so * kTile, c0, q0);
+        tma_load_2d(&tmO, &o_full[so], sO + so * kTile + kBox, c0 + 64, q0);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(kT, kT, 0, 0);
+    constexpr uint32_t idesc_g = umma_idesc_bf16(kT, kD, 0, 1);
+    const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+    const uint32_t aQ = smem_u32(sQ), aO = smem_u32(sO);
+    mbar_wait(kv_full, 0);
+    auto issue_s = [&](int t) {
+      const int sq = t % kQStages;
+      mbar_wait(&q_full[sq], (t / kQStages) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        mma_kk<idesc_s>(tS, aK, aQ + sq * kTile);
+        umma_commit(s_full);
+      }
+      __syncwarp();
+    };
+    auto issue_dp = [&](int t) {
+      const int so = t % kOStages;
+      mbar_wait(&o_full[so], (t / kOStages) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        mma_kk<idesc_s>(tP, aV, aO + so * kTile);
+        umma_commit(dp_full);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    issue_dp(0);
+    for (int t = 0; t < T; ++t) {
+      mbar_wait(p_full, t & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        mma_tk<idesc_g>(tdV, tS, aO + (t % kOStages) * kTile, t > 0);
+        umma_commit(&o_empty[t % kOStages]);
+      }
+      __syncwarp();
+      if (t + 1 < T) issue_s(t + 1);
+      mbar_wait(ds_full, t & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        mma_tk<idesc_g>(tdK, tP, aQ + (t % kQStages) * kTile, t > 0);
+        umma_commit(&q_empty[t % kQStages]);
+        if (t == T - 1) umma_commit(mm_done);
+      }
+      __syncwarp();
+      if (t + 1 < T) issue_dp(t + 1);
+    }
+  } else if (warp >= 4) {
+    const int wg = (warp - 4) >> 2;  // columns 64·wg … 64·wg + 63 of every query tile
+    const int wq = warp & 3;
+    const int r = wq * 32 + lane;    // key row within the tile == TMEM lane
+    const int key = k0 + r;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const uint32_t tSw = tS + lane_off + 64 * wg, tPw = tP + lane_off + 64 * wg;
+    for (int t = 0; t < T; ++t) {
+      const int qw = k0 + t * kT + 64 * wg;  // first query of this WG's columns
+      float* L = sLD + (wg * 2 + (t & 1)) * kT;
+      {
+        const int c = r & 63, q = qw + c;
+        L[r] = q < n ? (r < 64 ? lse[(size_t)hd * n + q] * kLog2e : delta[(size_t)hd * n + q])
+                     : 0.f;
+      }
+      named_bar_sync(1 + wg, 128);
+      const bool edge = (t == 0) || (qw + 64 > n) || (key >= n);
+      float p[64];
+      // phase A: Pᵀ
+      mbar_wait(s_full, t & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t raw[32];
+        tmem_ld_32x32b_x32(tSw + 32 * hf, raw);
+        tmem_ld_wait();
+        float* ph = p + 32 * hf;
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          ph[c] = ex2_approx(fmaf(__uint_as_float(raw[c]), sl2, -L[32 * hf + c]));
+        if (edge) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int q = qw + 32 * hf + c;
+            if (key > q || q >= n || key >= n) ph[c] = 0.f;
+          }
+        }
+        st_bf16x32(tSw + 16 * hf, ph);  // packed half lands below the fp32 half still unread
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      // phase B: dSᵀ
+      mbar_wait(dp_full, t & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t raw[32];
+        tmem_ld_32x32b_x32(tPw + 32 * hf, raw);
+        tmem_ld_wait();
+        float* ph = p + 32 * hf;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) ph[c] *= (__uint_as_float(raw[c]) - L[64 + 32 * hf + c]);
+        st_bf16x32(tPw + 16 * hf, ph);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+    }
+    mbar_wait(mm_done, 0);
+    tc_fence_after();
+    const bool ok = key < n;
+    if (wg == 0)
+      store_row_f32<kD>(tdV + lane_off, dv + (size_t)key * h + c0, 1.f, ok);
+    else
+      store_row_f32<kD>(tdK + lane_off, dk + (size_t)key * h + c0, scale, ok);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dQ
+
+constexpr int kKStages = 3, kVStages = 2;
+constexpr int kSmemQ = (2 + kKStages + kVStages) * kTile + 256;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    flash_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ,
+                        const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV,
+                        const __grid_constant__ CUtensorMap tmO,
+                        const float* __restrict__ lse, const float* __restrict__ delta,
+                        float* __restrict__ dq, int n, int h, float sl2, float scale) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = aligned_smem(smem_raw);
+  uint8_t* sQ = smem;
+  uint8_t* sO = smem + kTile;
+  uint8_t* sK = smem + 2 * kTile;              // [kKStages]
+  uint8_t* sV = sK + kKStages * kTile;         // [kVStages]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVStages * kTile);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;               // [kKStages]
+  uint64_t* k_empty = k_full + kKStages;     // [kKStages]
+  uint64_t* v_full = k_empty + kKStages;     // [kVStages]
+  uint64_t* v_empty = v_full + kVStages;     // [kVStages]
+  uint64_t* s_full = v_empty + kVStages;     // [2]
+  uint64_t* s_free = s_full + 2;             // [2]
+  uint64_t* dp_full = s_free + 2;
+  uint64_t* ds_full = dp_full + 1;
+  uint64_t* dq_done = ds_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qb = (int)(gridDim.x - 1 - blockIdx.x);  // heavy tiles first
+  const int hd = blockIdx.y;
+  const int q0 = qb * kT, c0 = hd * kD;
+  const int T = qb + 1;  // key tiles 0 … diagonal
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmO);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kKStages; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < kVStages; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_free[b], 8);
+    }
+    mbar_init(dp_full, 1);
+    mbar_init(ds_full, 8);
+    mbar_init(dq_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tP = tmem + 256, tdQ = tmem + 384;  // S[b] at 128·b
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, 2 * kTile);
+      tma_load_2d(&tmQ, q_full, sQ, c0, q0);
+      tma_load_2d(&tmQ, q_full, sQ + kBox, c0 + 64, q0);
+      tma_load_2d(&tmO, q_full, sO, c0, q0);
+      tma_load_2d(&tmO, q_full, sO + kBox, c0 + 64, q0);
+      for (int j = 0; j < T; ++j) {
+        const int sk = j % kKStages, sv = j % kVStages;
+        mbar_wait(&k_empty[sk], ((j / kKStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[sk], kTile);
+        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile, c0, j * kT);
+        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile + kBox, c0 + 64, j * kT);
+        mbar_wait(&v_empty[sv], ((j / kVStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&v_full[sv], kTile);
+        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile, c0, j * kT);
+        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile + kBox, c0 + 64, j * kT);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(kT, kT, 0, 0);
+    constexpr uint32_t idesc_g = umma_idesc_bf16(kT, kD, 0, 1);
+    const uint32_t aQ = smem_u32(sQ), aO = smem_u32(sO);
+    const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+    mbar_wait(q_full, 0);
+    auto issue_s = [&](int j) {
+      const int sk = j % kKStages, b = j & 1;
+      if (j >= 2) mbar_wait(&s_free[b], ((j - 2) >> 1) & 1);  // phase A of j-2 read it
+      mbar_wait(&k_full[sk], (j / kKStages) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        mma_kk<idesc_s>(tmem + 128 * b, aQ, aK + sk * kTile);
+        umma_commit(&s_full[b]);
+      }
+      __syncwarp();
+    };
+    auto issue_dp = [&](int j) {
+      const int sv = j % kVStages;
+      mbar_wait(&v_full[sv], (j / kVStages) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        mma_kk<idesc_s>(tP, aO, aV + sv * kTile);
+        umma_commit(dp_full);
+        umma_commit(&v_empty[sv]);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    if (T > 1) issue_s(1);
+    issue_dp(0);
+    for (int j = 0; j < T; ++j) {
+      mbar_wait(ds_full, j & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        mma_tk<idesc_g>(tdQ, tP, aK + (j % kKStages) * kTile, j > 0);
+        umma_commit(&k_empty[j % kKStages]);
+        if (j == T - 1) umma_commit(dq_done);
+      }
+      __syncwarp();
+      if (j + 1 < T) issue_dp(j + 1);
+      if (j + 2 < T) issue_s(j + 2);
+    }
+  } else if (warp >= 4) {
+    const int wg = (warp - 4) >> 2;
+    const int wq = warp & 3;
+    const int r = wq * 32 + lane;  // query row within the tile == TMEM lane
+    const int qr = q0 + r;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const uint32_t tPw = tP + lane_off + 64 * wg;
+    const float lse2 = qr < n ? lse[(size_t)hd * n + qr] * kLog2e : 0.f;
+    const float dl = qr < n ? delta[(size_t)hd * n + qr] : 0.f;
+    for (int j = 0; j < T; ++j) {
+      const int b = j & 1;
+      const int kw = j * kT + 64 * wg;  // first key of this WG's columns
+      const bool edge = (j == qb) || (kw + 64 > n) || (qr >= n);
+      float p[64];
+      // phase A: P (registers only)
+      mbar_wait(&s_full[b], (j >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t raw[32];
+        tmem_ld_32x32b_x32(tmem + 128 * b + lane_off + 64 * wg + 32 * hf, raw);
+        tmem_ld_wait();
+        float* ph = p + 32 * hf;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) ph[c] = ex2_approx(fmaf(__uint_as_float(raw[c]), sl2, -lse2));
+        if (edge) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int key = kw + 32 * hf + c;
+            if (key > qr || key >= n || qr >= n) ph[c] = 0.f;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[b]);
+      // phase B: dS
+      mbar_wait(dp_full, j & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t raw[32];
+        tmem_ld_32x32b_x32(tPw + 32 * hf, raw);
+        tmem_ld_wait();
+        float* ph = p + 32 * hf;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) ph[c] *= (__uint_as_float(raw[c]) - dl);
+        st_bf16x32(tPw + 16 * hf, ph);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+    }
+    mbar_wait(dq_done, 0);
+    tc_fence_after();
+    store_row_f32<64>(tdQ + lane_off + 64 * wg, dq + (size_t)qr * h + c0 + 64 * wg, scale,
+                      qr < n);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace fab
+}  // namespace lemo
+
+using namespace lemo;
+
+extern "C" {
+
+int lemo_attn_delta(const void* o, const void* dout, float* delta, int n, int h, int head_dim,
+                    void* stream);
+
+int lemo_flash_bwd_tc(const void* q, const void* k, const void* v, const void* o,
+                      const void* dout, const float* lse, float* delta, float* dq, float* dk,
+                      float* dv, int n, int h, int head_dim, float scale, void* stream) {
+  if (n <= 0) return 0;
+  LEMO_ARG_CHECK(head_dim == fab::kD, "lemo_flash_bwd_tc: head_dim must be 128");
+  LEMO_ARG_CHECK(h % head_dim == 0, "lemo_flash_bwd_tc: h % head_dim");
+  int rc = lemo_attn_delta(o, dout, delta, n, h, head_dim, stream);
+  if (rc) return rc;
+  CUtensorMap tq, tk, tv, to;
+  rc = make_tma_bf16_2d(&tq, q, (uint64_t)n, (uint64_t)h, (uint64_t)h, fab::kT);
+  if (!rc) rc = make_tma_bf16_2d(&tk, k, (uint64_t)n, (uint64_t)h, (uint64_t)h, fab::kT);
+  if (!rc) rc = make_tma_bf16_2d(&tv, v, (uint64_t)n, (uint64_t)h, (uint64_t)h, fab::kT);
+  if (!rc) rc = make_tma_bf16_2d(&to, dout, (uint64_t)n, (uint64_t)h, (uint64_t)h, fab::kT);
+  if (rc) LEMO_RETURN_RC("lemo_flash_bwd_tc", rc);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fab::flash_bwd_dkdv_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         fab::kSmemKV);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fab::flash_bwd_dq_kernel,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, fab::kSmemQ);
+    if (e != cudaSuccess) LEMO_RETURN_RC("lemo_flash_bwd_tc", (int)e);
+    attr = true;
+  }
+  const float sl2 = scale * fab::kLog2e;
+  dim3 grid((n + fab::kT - 1) / fab::kT, h / head_dim);
+  cudaStream_t st = (cudaStream_t)stream;
+  fab::flash_bwd_dkdv_kernel<<<grid, fab::kThreads, fab::kSmemKV, st>>>(
+      tq, tk, tv, to, lse, delta, dk, dv, n, h, sl2, scale);
+  fab::flash_bwd_dq_kernel<<<grid, fab::kThreads, fab::kSmemQ, st>>>(tq, tk, tv, to, lse, delta,
+                                                                     dq, n, h, sl2, scale);
+  LEMO_CHECK_LAUNCH("lemo_flash_bwd_tc");
+  return 0;
+}
+
+}  // extern "C"

@@ -318,7 +318,8 @@ def test_flash_fwd_tc_vs_torch_and_mma(cuda, n, H):
     torch.testing.assert_close(o.float(), o2.float(), rtol=2e-2, atol=2e-2)
 
 
-@pytest.mark.parametrize("n,H", [(1, 1), (100, 2), (128, 1), (257, 2), (1000, 2)])
+@pytest.mark.parametrize("n,H", [(1, 1), (63, 1), (65, 2), (100, 2), (128, 1), (191, 1), (257, 2),
+                                 (1000, 2), (2049, 1)])
 def test_flash_bwd_tc_vs_torch(cuda, n, H):
     d = 128
     g = torch.Generator(device=cuda).manual_seed(n + 11)
