@@ -230,8 +230,9 @@ int lemo_exact_block_scores(const void* q, const void* k, int s, int h, int head
 int lemo_flash_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int n, int h,
                    int head_dim, float scale, void* stream);
 
-/* Same contract as lemo_flash_fwd on the tcgen05 path (TMA, TMEM S/O
- * accumulators, single-thread MMA issue); head_dim must be 128. */
+/* Same contract as lemo_flash_fwd on the tcgen05 path: two query tiles per
+ * CTA ping-ponging two softmax warpgroups, S/O in TMEM, P as a bf16 TMEM A
+ * operand, single-thread MMA issue; head_dim must be 128. */
 int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float* lse, int n,
                       int h, int head_dim, float scale, void* stream);
 

@@ -1,0 +1,317 @@
+// tcgen05 FlashAttention forward over the compact retained sequence
+// (tensor.py:646-691: causal by compact index, q pre-scaled by 1/√d, online
+// softmax, saves lse), head_dim 128.
+//
+// One CTA = two adjacent 128-query tiles (Q0, Q1) of one head sharing every
+// K/V tile load; 320 threads:
+//   w0-w3  softmax warpgroup 0 (rows of Q0),  w4-w7 softmax warpgroup 1 (Q1)
+//   w8     TMA producer (Q0/Q1 once, K_j into a 3-deep ring, V_j into 2)
+//   w9     MMA issuer + TMEM allocator (512 columns: S0 | S1 | O0 | O1)
+// Per KV tile j the tensor core runs  S0(j) S1(j) | PV0(j) S0(j+1) PV1(j)
+// S1(j+1) | …  so softmax WG0 works on S0 while the tensor core serves WG1 and
+// vice versa (ping-pong).  P is written back as bf16 over its own S columns
+// and read as the TMEM A operand of O += P·V (V_j as an MN-major B operand);
+// a later S MMA overwriting those columns is ordered after the PV MMA that
+// reads them because tcgen05.mma executes in issue order.  O rescales are
+// lazy (only when the running max grows by > 8 in log2 units) and need no
+// extra wait: when S_g(j) is complete, PV_g(j-1) is complete too.
+#include "gemm.cuh"
+#include "lemo_internal.h"
+
+namespace lemo {
+namespace faf {
+
+constexpr int kT = 128;
+constexpr int kD = 128;
+constexpr int kBox = kT * 64 * 2;   // [128 x 64] bf16 SW128 box = 16 KB
+constexpr int kTile = 2 * kBox;     // [128 x 128] = 32 KB
+constexpr int kKStages = 3, kVStages = 2;
+constexpr int kThreads = 320;
+constexpr int kSmem = (2 + kKStages + kVStages) * kTile + 256;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ uint8_t* aligned_smem(uint8_t* raw) {
+  if (smem_u32(raw) & 1023u) __trap();
+  return raw;
+}
+
+template <uint32_t kIdesc>
+__device__ __forceinline__ void mma_qk(uint32_t d, uint32_t a, uint32_t b) {
+#pragma unroll
+  for (int kk = 0; kk < kD / 16; ++kk) {
+    const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
+    umma_bf16_ss(d, umma_desc_k_sw128(a + off), umma_desc_k_sw128(b + off), kIdesc,
+                 kk > 0 ? 1u : 0u);
+  }
+}
+
+// O (+)= P·V: P = bf16 [128 x 128] packed in TMEM columns [p, p+64), V_j smem
+// [128 keys x 128 d] = MN-major B.
+template <uint32_t kIdesc>
+__device__ __forceinline__ void mma_pv(uint32_t d, uint32_t p, uint32_t b, bool acc) {
+#pragma unroll
+  for (int kk = 0; kk < kT / 16; ++kk)
+    umma_bf16_ts(d, p + kk * 8, umma_desc_mn_sw128(b + kk * 2048, kBox), kIdesc,
+                 (acc || kk > 0) ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ o,
+                     float* __restrict__ lse, int n, int h, float sl2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = aligned_smem(smem_raw);
+  uint8_t* sQ = smem;                          // Q0 | Q1
+  uint8_t* sK = smem + 2 * kTile;              // [kKStages]
+  uint8_t* sV = sK + kKStages * kTile;         // [kVStages]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVStages * kTile);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;               // [kKStages]
+  uint64_t* k_empty = k_full + kKStages;     // [kKStages]
+  uint64_t* v_full = k_empty + kKStages;     // [kVStages]
+  uint64_t* v_empty = v_full + kVStages;     // [kVStages]
+  uint64_t* s_full = v_empty + kVStages;     // [2] per query tile
+  uint64_t* p_full = s_full + 2;             // [2]
+  uint64_t* o_done = p_full + 2;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = (n + kT - 1) / kT;
+  const int pair = (int)(gridDim.x - 1 - blockIdx.x);  // heavy pairs first
+  const int hd = blockIdx.y, c0 = hd * kD;
+  const int qt0 = 2 * pair;
+  const bool two = qt0 + 1 < nt;
+  const int T = two ? qt0 + 2 : qt0 + 1;  // KV tiles; Q0 uses [0, qt0], Q1 uses [0, qt0+1]
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kKStages; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < kVStages; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&s_full[g], 1);
+      mbar_init(&p_full[g], 4);
+      mbar_init(&o_done[g], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S_g at 128·g, O_g at 256 + 128·g
+
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, (two ? 2 : 1) * kTile);
+      for (int g = 0; g < (two ? 2 : 1); ++g) {
+        tma_load_2d(&tmQ, q_full, sQ + g * kTile, c0, (qt0 + g) * kT);
+        tma_load_2d(&tmQ, q_full, sQ + g * kTile + kBox, c0 + 64, (qt0 + g) * kT);
+      }
+      for (int j = 0; j < T; ++j) {
+        const int sk = j % kKStages, sv = j % kVStages;
+        mbar_wait(&k_empty[sk], ((j / kKStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[sk], kTile);
+        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile, c0, j * kT);
+        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile + kBox, c0 + 64, j * kT);
+        mbar_wait(&v_empty[sv], ((j / kVStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&v_full[sv], kTile);
+        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile, c0, j * kT);
+        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile + kBox, c0 + 64, j * kT);
+      }
+    }
+  } else if (warp == 9) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(kT, kT, 0, 0);
+    constexpr uint32_t idesc_o = umma_idesc_bf16(kT, kD, 0, 1);
+    const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV);
+    // tile g takes part in KV tile j iff j <= qt0 + g
+    auto uses = [&](int g, int j) { return (g == 0 || two) && j <= qt0 + g; };
+    auto last_k_user = [&](int j) { return uses(1, j) ? 1 : 0; };
+    mbar_wait(q_full, 0);
+    auto issue_s = [&](int g, int j) {
+      const int sk = j % kKStages;
+      if (g == 0) mbar_wait(&k_full[sk], (j / kKStages) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        mma_qk<idesc_s>(tmem + 128 * g, aQ + g * kTile, aK + sk * kTile);
+        umma_commit(&s_full[g]);
+        if (g == last_k_user(j)) umma_commit(&k_empty[sk]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int g, int j) {
+      const int sv = j % kVStages;
+      mbar_wait(&p_full[g], j & 1);
+      if (g == 0 || !uses(0, j)) mbar_wait(&v_full[sv], (j / kVStages) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        mma_pv<idesc_o>(tmem + 256 + 128 * g, tmem + 128 * g, aV + sv * kTile, j > 0);
+        if (g == last_k_user(j)) umma_commit(&v_empty[sv]);
+        if (j == qt0 + g) umma_commit(&o_done[g]);
+      }
+      __syncwarp();
+    };
+    issue_s(0, 0);
+    if (two) issue_s(1, 0);
+    for (int j = 0; j < T; ++j) {
+      if (uses(0, j)) {
+        issue_pv(0, j);
+        if (uses(0, j + 1)) issue_s(0, j + 1);
+      }
+      if (uses(1, j)) {
+        if (!uses(0, j + 1) && j + 1 < T) {  // Q0 is done: Q1 now waits for K itself
+          const int sk = (j + 1) % kKStages;
+          mbar_wait(&k_full[sk], ((j + 1) / kKStages) & 1);
+        }
+        issue_pv(1, j);
+        if (j + 1 < T) issue_s(1, j + 1);
+      }
+    }
+  } else {
+    // softmax warpgroup g = warp / 4, thread = query row of tile g
+    const int g = warp >> 2;
+    if (g == 0 || two) {
+      const int wq = warp & 3;
+      const int r = wq * 32 + lane;
+      const int qt = qt0 + g;
+      const int qr = qt * kT + r;
+      const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+      const uint32_t tS = tmem + 128 * g + lane_off, tO = tmem + 256 + 128 * g + lane_off;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j <= qt; ++j) {
+        mbar_wait(&s_full[g], j & 1);
+        tc_fence_after();
+        float s[kT];
+        {
+          uint32_t raw[kT];
+#pragma unroll
+          for (int c = 0; c < kT / 32; ++c)
+            tmem_ld_32x32b_x32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(raw + c * 32));
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < kT; ++i) s[i] = __uint_as_float(raw[i]);
+        }
+        const int kv0 = j * kT;
+        if (j == qt || kv0 + kT > n) {
+#pragma unroll
+          for (int i = 0; i < kT; ++i)
+            if (kv0 + i > qr || kv0 + i >= n) s[i] = -INFINITY;
+        }
+        float mr[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) mr[t] = s[t];
+#pragma unroll
+        for (int i = 8; i < kT; ++i) mr[i & 7] = fmaxf(mr[i & 7], s[i]);
+        const float mraw = fmaxf(fmaxf(fmaxf(mr[0], mr[1]), fmaxf(mr[2], mr[3])),
+                                 fmaxf(fmaxf(mr[4], mr[5]), fmaxf(mr[6], mr[7])));
+        const float mx = mraw * sl2;
+        const float m_new = (m == -INFINITY || mx > m + 8.f) ? fmaxf(mx, m) : m;
+        const float corr = (m == -INFINITY) ? 0.f : ex2_approx(m - m_new);
+        if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
+          // PV_g(j-1) completed before S_g(j) did (issue order): O is stable
+#pragma unroll 1
+          for (int c = 0; c < kD / 32; ++c) {
+            uint32_t raw[32];
+            tmem_ld_32x32b_x32(tO + c * 32, raw);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) raw[i] = __float_as_uint(__uint_as_float(raw[i]) * corr);
+            tmem_st_32x32b_x32(tO + c * 32, raw);
+          }
+        }
+        float sm[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) sm[t] = 0.f;
+#pragma unroll
+        for (int c = 0; c < kT / 32; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float a = ex2_approx(fmaf(s[32 * c + 2 * i], sl2, -m_new));
+            const float b = ex2_approx(fmaf(s[32 * c + 2 * i + 1], sl2, -m_new));
+            sm[(2 * i) & 7] += a;
+            sm[(2 * i + 1) & 7] += b;
+            pk[i] = pack_bf16x2(a, b);
+          }
+          tmem_st_32x32b_x16(tS + 16 * c, pk);  // P over the already-read S columns
+        }
+        const float sum = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
+        l = l * corr + sum;
+        m = m_new;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[g]);
+      }
+      mbar_wait(&o_done[g], 0);
+      tc_fence_after();
+      const float inv_l = 1.f / l;
+#pragma unroll 1
+      for (int c = 0; c < kD / 32; ++c) {
+        uint32_t raw[32];
+        tmem_ld_32x32b_x32(tO + c * 32, raw);
+        tmem_ld_wait();
+        if (qr < n) {
+          uint4* dst = reinterpret_cast<uint4*>(o + (size_t)qr * h + c0 + c * 32);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            dst[q] = make_uint4(
+                pack_bf16x2(__uint_as_float(raw[8 * q + 0]) * inv_l, __uint_as_float(raw[8 * q + 1]) * inv_l),
+                pack_bf16x2(__uint_as_float(raw[8 * q + 2]) * inv_l, __uint_as_float(raw[8 * q + 3]) * inv_l),
+                pack_bf16x2(__uint_as_float(raw[8 * q + 4]) * inv_l, __uint_as_float(raw[8 * q + 5]) * inv_l),
+                pack_bf16x2(__uint_as_float(raw[8 * q + 6]) * inv_l, __uint_as_float(raw[8 * q + 7]) * inv_l));
+        }
+      }
+      if (qr < n) lse[(size_t)hd * n + qr] = (m + log2f(l)) * kLn2;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace faf
+}  // namespace lemo
+
+using namespace lemo;
+
+extern "C" {
+
+int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float* lse, int n,
+                      int h, int head_dim, float scale, void* stream) {
+  if (n <= 0) return 0;
+  LEMO_ARG_CHECK(head_dim == faf::kD, "lemo_flash_fwd_tc: head_dim must be 128");
+  LEMO_ARG_CHECK(h % head_dim == 0, "lemo_flash_fwd_tc: h % head_dim");
+  CUtensorMap tq, tk, tv;
+  int rc = make_tma_bf16_2d(&tq, q, (uint64_t)n, (uint64_t)h, (uint64_t)h, faf::kT);
+  if (!rc) rc = make_tma_bf16_2d(&tk, k, (uint64_t)n, (uint64_t)h, (uint64_t)h, faf::kT);
+  if (!rc) rc = make_tma_bf16_2d(&tv, v, (uint64_t)n, (uint64_t)h, (uint64_t)h, faf::kT);
+  if (rc) LEMO_RETURN_RC("lemo_flash_fwd_tc", rc);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(faf::flash_fwd_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, faf::kSmem);
+    if (e != cudaSuccess) LEMO_RETURN_RC("lemo_flash_fwd_tc", (int)e);
+    attr = true;
+  }
+  const int nt = (n + faf::kT - 1) / faf::kT;
+  dim3 grid((nt + 1) / 2, h / head_dim);
+  faf::flash_fwd_kernel<<<grid, faf::kThreads, faf::kSmem, (cudaStream_t)stream>>>(
+      tq, tk, tv, reinterpret_cast<__nv_bfloat16*>(o), lse, n, h, scale * faf::kLog2e);
+  LEMO_CHECK_LAUNCH("lemo_flash_fwd_tc");
+  return 0;
+}
+
+}  // extern "C"

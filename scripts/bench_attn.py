@@ -17,8 +17,13 @@ for n in (4096, 8192, 16384):
     H, d = 32, 128
     q, k, v = (torch.randn(n, H * d, device='cuda').bfloat16() for _ in range(3))
     fl = 2 * n * n * d * H  # causal fwd flops (QK^T + PV, half)
-    t = bench(lambda: ops.flash_fwd(q, k, v, head_dim=d, scale=1 / math.sqrt(d), impl="tc"))
-    print(f"fwd n={n} tc: {t:.3f} ms  {fl / t / 1e9:.0f} TFLOP/s")
+    o1, l1 = ops.flash_fwd(q, k, v, head_dim=d, scale=1 / math.sqrt(d), impl="tc")
+    for fi in ("tc",):
+        t = bench(lambda: ops.flash_fwd(q, k, v, head_dim=d, scale=1 / math.sqrt(d), impl=fi))
+        o2, l2 = ops.flash_fwd(q, k, v, head_dim=d, scale=1 / math.sqrt(d), impl=fi)
+        e = float((o2.float() - o1.float()).norm() / o1.float().norm())
+        print(f"fwd n={n} {fi}: {t:.3f} ms  {fl / t / 1e9:.0f} TFLOP/s  rel-vs-tc {e:.2e} "
+              f"lse-maxdiff {float((l2 - l1).abs().max()):.2e}")
     o, lse = ops.flash_fwd(q, k, v, head_dim=d, scale=1 / math.sqrt(d))
     do = torch.randn_like(o)
     ref = None

@@ -303,7 +303,8 @@ def test_qkv_rope_lora_vs_oracle(cuda):
         np.testing.assert_allclose(got.float().cpu().numpy(), ref, rtol=2e-2, atol=2e-2)
 
 
-@pytest.mark.parametrize("n,H", [(1, 1), (100, 2), (128, 1), (129, 2), (1000, 4), (4096, 2)])
+@pytest.mark.parametrize("n,H", [(1, 1), (100, 2), (128, 1), (129, 2), (255, 1), (256, 2),
+                                 (257, 1), (1000, 4), (4096, 2)])
 def test_flash_fwd_tc_vs_torch_and_mma(cuda, n, H):
     """tcgen05 attention forward vs fp32 torch and vs the mma.sync kernel."""
     d = 128
@@ -336,3 +337,4 @@ def test_flash_bwd_tc_vs_torch(cuda, n, H):
     for name, got, ref in (("dq", dq, qr.grad), ("dk", dk, kr.grad), ("dv", dv, vr.grad)):
         err = (got - ref).norm() / torch.maximum(ref.norm(), floor)
         assert err < 2e-2, (name, float(err))
+
