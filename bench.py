@@ -282,12 +282,22 @@ def main():
     clocks = Clocks(local)
     clocks.start()
     gemm_name, embed_name = "lemo_gemm_gateup", "lemo_block_embed"
-    ms = timed(source, lambda: staged, args.steps, timed_names=(gemm_name, embed_name))
+    fa_f, fa_b = "lemo_flash_fwd_tc", "lemo_flash_bwd_tc"
+    ms = timed(source, lambda: staged, args.steps,
+               timed_names=(gemm_name, embed_name, fa_f, fa_b))
     ck = clocks.stop()
     ins = _lib.INSTRUMENT
     launches_per_step = ins.total_launches() / args.steps
     gemm_ms = ins.elapsed_ms(gemm_name)
     embed_ms = ins.elapsed_ms(embed_name)
+    # attention (causal, compact retained rows): fwd 2·n²·h, bwd 5·n²·h algorithmic flops
+    attn = {}
+    for nm, mult in ((fa_f, 2.0), (fa_b, 5.0)):
+        tms, ns = ins.elapsed_ms(nm), ins.notes.get(nm, [])
+        if tms and len(ns) == len(tms):
+            fl = sum(mult * float(nn) * nn * cfg.hidden_dim for nn in ns)
+            attn[nm] = {"tflops": fl / (sum(tms) / 1e3) / 1e12, "launches": len(tms),
+                        "avg_ms": sum(tms) / len(tms), "avg_rows": sum(ns) / len(ns)}
     lemo_stats = dict(model.last_stats)
     peak_step = torch.cuda.max_memory_allocated(dev) - base_mem
     ms_step = ms / args.steps
@@ -328,7 +338,9 @@ def main():
     roofline = {"kernel": "gemm_tn_kernel<256,EpiGateUp> (lemo_gemm_gateup, MLP scoring)",
                 "bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops_sustained"],
                 "unit": "TFLOP/s", "frac": (ach / pk["bf16_tflops_sustained"]) if ach else None,
-                "traffic": traffic, "peak_source": f"{pk_src} bf16_tflops_sustained",
+                "frac_burst": (ach / pk["bf16_tflops"]) if ach else None,
+                "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
+                "peak_source": f"{pk_src} bf16_tflops_sustained (kernel timed inside the step)",
                 "algorithmic_per_launch": flops_gemm, "launches_timed": len(gemm_ms),
                 "avg_launch_ms": avg_gemm_s * 1e3}
     nb = seq // cfg.block_size
@@ -385,6 +397,9 @@ def main():
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "roofline": roofline,
         "roofline_scoring": roofline_scoring,
+        "attention": {k: dict(v, bound="tensor", peak=pk["bf16_tflops"],
+                              frac_burst=v["tflops"] / pk["bf16_tflops"])
+                      for k, v in attn.items()},
         "cpu_baseline": cpu,
         "clocks": ck,
     }

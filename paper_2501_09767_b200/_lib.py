@@ -110,11 +110,18 @@ class Instrument:
         self.launches: dict[str, int] = {}
         self.timed: set[str] = set()
         self.events: dict[str, list] = {}
+        self.notes: dict[str, list] = {}
 
     def reset(self, timed=()):
         self.launches = {}
         self.timed = set(timed)
         self.events = {n: [] for n in self.timed}
+        self.notes = {n: [] for n in self.timed}
+
+    def note(self, name: str, value) -> None:
+        """Per-call metadata (e.g. the row count) for timed entry points."""
+        if self.enabled and name in self.notes:
+            self.notes[name].append(value)
 
     def total_launches(self) -> int:
         return sum(self.launches.values())

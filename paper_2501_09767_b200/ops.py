@@ -12,7 +12,7 @@ import math
 
 import torch
 
-from ._lib import call, lib, ptr, stream_ptr
+from ._lib import INSTRUMENT, call, lib, ptr, stream_ptr
 from .errors import ContractError, DimensionError
 
 BF16 = torch.bfloat16
@@ -376,6 +376,7 @@ def flash_fwd(q, k, v, *, head_dim, scale, o=None, lse=None, impl=None):
     if impl is None:
         impl = "tc" if head_dim == 128 else "mma"
     name = "lemo_flash_fwd_tc" if impl == "tc" else "lemo_flash_fwd"
+    INSTRUMENT.note(name, n)
     call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(lse), n, h, head_dim, float(scale), _s())
     return o, lse
 
@@ -392,6 +393,7 @@ def flash_bwd(q, k, v, o, dout, lse, *, head_dim, scale, dq=None, dk=None, dv=No
     if impl is None:
         impl = "tc" if head_dim == 128 else "mma"
     name = "lemo_flash_bwd_tc" if impl == "tc" else "lemo_flash_bwd"
+    INSTRUMENT.note(name, n)
     call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(delta), ptr(dq),
          ptr(dk), ptr(dv), n, h, head_dim, float(scale), _s())
     return dq, dk, dv
