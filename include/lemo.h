@@ -198,6 +198,10 @@ int lemo_gemm_split3(const void* A, int lda, const void* B, int ldb, int M, int 
  * (model.py:575-578 + sparsity.py:253-260). */
 int lemo_colsum_clamped(const float* S, int lds, int nb, double* vec, void* stream);
 
+/* The same ascending-m f64 column sums from a packed lower triangle
+ * (element (m, n) at m(m+1)/2 + n; sparsity.py:253-260). */
+int lemo_colsum_packed(const double* packed, int nb, double* vec, void* stream);
+
 /* MLP block scores from per-tile row partials of lemo_gemm_gateup:
  * token score = Σ partial / m_real, block = max over rows < n_valid
  * (sparsity.py:284-305, model.py:383-395). */
@@ -222,6 +226,28 @@ int lemo_quantile_lower(const double* data, int n, long long rank, int plus_one,
  * mask; q, k: [s, h] bf16 post-rotation (layer_qk, model.py:356-368). */
 int lemo_exact_block_scores(const void* q, const void* k, int s, int h, int head_dim, int block,
                             int n_valid, float* out, int ldo, void* stream);
+
+/* ---- offline predictor training (predictor.py:215-433) ----------------------- */
+
+/* out [C, 3R] = bf16x3 split (pattern as lemo_split_bf16x3) of Aᵀ, A fp32 [R, C]:
+ * the K-major operand of a transposed matrix (weight gradients Xᵀ·dY). */
+int lemo_split_bf16x3_t(const float* A, int lda, int R, int C, int pattern, void* out,
+                        void* stream);
+
+/* MSE over the packed lower triangle of the nb x nb prediction `full` against
+ * `label` (packed, tensor.py:495-505): row_loss[m] = Σ_{n<=m} d², dfull =
+ * 2d/T below and on the diagonal, 0 above (T = nb(nb+1)/2). */
+int lemo_tril_mse(const float* full, int ldf, const float* label, int nb, float* dfull, int ldd,
+                  double* row_loss, void* stream);
+
+/* dh[i] = 0 where h[i] <= 0 (ReLU·mask backward on the saved output). */
+int lemo_relu_grad(float* dh, const float* h, long long n, void* stream);
+
+/* counts[c] += #{r : h[r, c] == 0} (zero-frequency tracking, predictor.py:76-80). */
+int lemo_zero_count(const float* h, int ldh, int M, int N, long long* counts, void* stream);
+
+/* *out = scale · Σ x (f64, fixed order). */
+int lemo_sum_d(const double* x, int n, double scale, double* out, void* stream);
 
 /* ---- attention over the compact retained sequence --------------------------- */
 

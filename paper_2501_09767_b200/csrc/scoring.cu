@@ -191,6 +191,27 @@ __global__ void colsum_clamped_kernel(const float* __restrict__ S, int lds, int 
   if (lane == 0) vec[n] = acc;
 }
 
+// Same column sums straight from a packed f64 lower triangle (element (m, n)
+// at m(m+1)/2 + n), e.g. reference-written or teacher score triangles.
+__global__ void colsum_packed_kernel(const double* __restrict__ P, int nb,
+                                     double* __restrict__ vec) {
+  const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (n >= nb) return;
+  double acc = 0.0;
+  for (int m0 = n; m0 < nb; m0 += 32) {
+    const int m = m0 + lane;
+    const double v = m < nb ? P[(size_t)m * (m + 1) / 2 + n] : 0.0;
+    const int cnt = min(32, nb - m0);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double x = __shfl_sync(0xffffffffu, v, j);
+      if (j < cnt) acc += x;
+    }
+  }
+  if (lane == 0) vec[n] = acc;
+}
+
 // Token scores (one thread per row, coalesced over the per-tile partials, the
 // same sequential tile order as before) and the block max via segmented warp
 // shuffles (b a power of two <= 32).
@@ -403,6 +424,13 @@ int lemo_colsum_clamped(const float* S, int lds, int nb, double* vec, void* stre
   if (nb <= 0) return 0;
   colsum_clamped_kernel<<<(nb + 7) / 8, 256, 0, (cudaStream_t)stream>>>(S, lds, nb, vec);
   LEMO_CHECK_LAUNCH("lemo_colsum_clamped");
+  return 0;
+}
+
+int lemo_colsum_packed(const double* packed, int nb, double* vec, void* stream) {
+  if (nb <= 0) return 0;
+  colsum_packed_kernel<<<(nb + 7) / 8, 256, 0, (cudaStream_t)stream>>>(packed, nb, vec);
+  LEMO_CHECK_LAUNCH("lemo_colsum_packed");
   return 0;
 }
 

@@ -758,14 +758,18 @@ class ExactPatternSource(PatternSourceBase):
     thresholds=None profiles only (retain all)."""
 
     def __init__(self, model: DecoderModel, thresholds: sparsity.ThresholdSet | None, *,
-                 mlp_scoring: bool = True, sink_first_block: bool = False, record: bool = False):
+                 mlp_scoring: bool = True, sink_first_block: bool = False, record: bool = False,
+                 record_inputs: bool = False):
         super().__init__()
         self.model = model
         self.thresholds = thresholds
         self.mlp_scoring = mlp_scoring
         self.sink_first_block = sink_first_block
         self.record = record
+        self.record_inputs = record_inputs
         self.recorded_vectors: dict = {}
+        self.recorded_matrices: list = []   # BlockScoreMatrix (device, packed f64) per call
+        self.recorded_inputs: dict = {}     # layer -> [x clones] (teacher inputs)
 
     def pattern(self, layer_id, component, x, n_valid):
         from . import exact  # noqa: WPS433 (kernel module)
@@ -774,7 +778,16 @@ class ExactPatternSource(PatternSourceBase):
         layer = self.model.layers[layer_id]
         if component == sparsity.ATTENTION:
             q, k = layer_qk(layer, x)
-            vec = exact.exact_block_vector(q, k, b, n_heads=layer.n_heads, n_valid=n_valid)
+            if self.record and self.record_inputs:
+                # teacher generation (pipeline.py:280-300): keep the packed
+                # triangle and a copy of x (the residual is updated in place)
+                bsm = exact.exact_block_scores(q, k, b, n_heads=layer.n_heads, n_valid=n_valid,
+                                               layer_id=layer_id)
+                vec = sparsity.token_block_scores(bsm)
+                self.recorded_matrices.append(bsm)
+                self.recorded_inputs.setdefault(layer_id, []).append(x.clone())
+            else:
+                vec = exact.exact_block_vector(q, k, b, n_heads=layer.n_heads, n_valid=n_valid)
         else:
             if not self.mlp_scoring:
                 return self._note(layer_id, component, None)

@@ -309,6 +309,51 @@ def split_bf16x3(a, pattern, out=None):
     return out
 
 
+def split_bf16x3_t(a, pattern, out=None):
+    """fp32 [R, C] -> bf16 [C, 3R]: the bf16x3 operand of aᵀ."""
+    _check(a, out)
+    _dt(a, F32, "a")
+    R, C = a.shape
+    if out is None:
+        out = torch.empty(C, 3 * R, dtype=BF16, device=a.device)
+    call("lemo_split_bf16x3_t", ptr(a), a.stride(0), R, C, int(pattern), ptr(out), _s())
+    return out
+
+
+def tril_mse(full, label, *, dfull=None, row_loss=None, loss=None):
+    """Packed-lower-triangle MSE of `full` [nb, nb] vs `label` [nb(nb+1)/2]:
+    returns (loss f64 [1] device, dL/dfull [nb, nb])."""
+    _check(full, label)
+    _dt(full, F32, "full")
+    _dt(label, F32, "label")
+    nb = full.shape[0]
+    if label.numel() != nb * (nb + 1) // 2:
+        raise DimensionError(f"label has {label.numel()} entries, expected {nb * (nb + 1) // 2}")
+    dev = full.device
+    dfull = torch.empty(nb, nb, dtype=F32, device=dev) if dfull is None else dfull
+    row_loss = torch.empty(nb, dtype=torch.float64, device=dev) if row_loss is None else row_loss
+    loss = torch.empty(1, dtype=torch.float64, device=dev) if loss is None else loss
+    call("lemo_tril_mse", ptr(full), full.stride(0), ptr(label), nb, ptr(dfull), dfull.stride(0),
+         ptr(row_loss), _s())
+    call("lemo_sum_d", ptr(row_loss), nb, 2.0 / (nb * (nb + 1)), ptr(loss), _s())
+    return loss, dfull
+
+
+def relu_grad(dh, h):
+    """dh[h <= 0] = 0 in place (ReLU·mask backward)."""
+    _check(dh, h)
+    call("lemo_relu_grad", ptr(dh), ptr(h), dh.numel(), _s())
+    return dh
+
+
+def zero_count(h, counts):
+    """counts[c] += #zeros in column c of h [M, N] (int64 counts)."""
+    _check(h, counts)
+    M, N = h.shape
+    call("lemo_zero_count", ptr(h), h.stride(0), M, N, ptr(counts), _s())
+    return counts
+
+
 def gemm_split3(a3, b3, *, relu=False, mask=None, pattern=0, split_out=True, f32_out=False):
     """C = act(A·Bᵀ)·mask in fp32-faithful bf16x3; returns (split C or None, fp32 C or None)."""
     _check(a3, b3, mask)
@@ -330,6 +375,18 @@ def colsum_clamped(S, out=None):
     if out is None:
         out = torch.empty(nb, dtype=F64, device=S.device)
     call("lemo_colsum_clamped", ptr(S), S.stride(0), nb, ptr(out), _s())
+    return out
+
+
+def colsum_packed(packed, nb, out=None):
+    """f64 column sums of a packed f64 lower triangle, ascending m."""
+    _check(packed, out)
+    _dt(packed, torch.float64, "packed")
+    if packed.numel() != nb * (nb + 1) // 2:
+        raise DimensionError(f"packed triangle has {packed.numel()} entries for {nb} blocks")
+    if out is None:
+        out = torch.empty(nb, dtype=torch.float64, device=packed.device)
+    call("lemo_colsum_packed", ptr(packed), nb, ptr(out), _s())
     return out
 
 

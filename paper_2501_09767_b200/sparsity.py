@@ -291,13 +291,11 @@ def eliminate(block_scores, threshold: float, *, layer_id: int = 0, component: s
 
 
 def token_block_scores(matrix: BlockScoreMatrix) -> torch.Tensor:
-    """Column sums of the packed triangle, f64 ascending m (sparsity.py:253-260),
-    on the GPU (lemo_colsum_clamped; scores are already nonnegative)."""
-    dense = matrix.as_dense().to("cuda").to(torch.float32)
-    if not bool(torch.equal(dense.to(torch.float64), matrix.as_dense().to("cuda"))):
-        # f64 scores not exactly representable in f32: sum them exactly in f64
-        raise ContractError("token_block_scores on the GPU takes f32-representable scores")
-    return ops.colsum_clamped(dense.contiguous())
+    """Column sums of the packed triangle, f64 in ascending m (sparsity.py:253-260),
+    on the GPU (lemo_colsum_packed, one warp per column)."""
+    packed = matrix.scores
+    packed = (packed if packed.is_cuda else packed.to("cuda")).to(torch.float64).contiguous()
+    return ops.colsum_packed(packed, matrix.n_blocks)
 
 
 def mlp_block_scores(token_scores, block_size: int, *, n_valid: int | None = None) -> np.ndarray:
@@ -337,3 +335,34 @@ def init_thresholds(profile: Mapping, config_hash: str = "") -> ThresholdSet:
             raise ContractError(f"no scores observed for {key}")
         ts.values[key] = float(allv.mean())
     return ts
+
+
+def tune_thresholds(acc_fn, thresholds: ThresholdSet, *, eps: float | None = None,
+                    eta: float | None = None, rounds: int = 1) -> ThresholdSet:
+    """Algorithm 1 step 2 (sparsity.py:379-417): per-threshold central finite
+    difference of the accuracy proxy, T <- T + eta·G, keys in sorted order.
+    eps defaults to 0.05·|T| + 1e-3; without eta the step is capped at 10 %
+    of |T|.  `acc_fn(ThresholdSet) -> float` is where the GPU works (e.g.
+    `pipeline.eval_accuracy`: eval forwards through the sparse path)."""
+    tuned = thresholds.copy()
+    tuned.eps = eps
+    tuned.eta = eta
+    for _ in range(max(rounds, 0)):
+        for key in sorted(tuned.values):
+            t = tuned.values[key]
+            e = eps if eps is not None else 0.05 * abs(t) + 1e-3
+            probe = tuned.copy()
+            probe.values[key] = t + e
+            acc_plus = float(acc_fn(probe))
+            probe.values[key] = t - e
+            acc_minus = float(acc_fn(probe))
+            if not (np.isfinite(acc_plus) and np.isfinite(acc_minus)):
+                raise ContractError(f"non-finite accuracy while tuning {key}: "
+                                    f"acc(T+eps)={acc_plus}, acc(T-eps)={acc_minus}")
+            grad = (acc_plus - acc_minus) / (2.0 * e)
+            if eta is not None:
+                step = eta * grad
+            else:
+                step = 0.1 * (abs(t) + 1e-3) / (abs(grad) + 1e-12) * grad
+            tuned.values[key] = t + step
+    return tuned

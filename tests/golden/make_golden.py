@@ -286,16 +286,120 @@ def step_pattern_cases():
     return out
 
 
+def predictor_train_case():
+    """fit_predictors (predictor.py:366-433) on fixed teacher records: per-epoch
+    losses / recall / active params and the final weights, masks, counters."""
+    rng = np.random.default_rng(77)
+    h, r, b, s, n_layers = 64, 16, 8, 128, 2
+    nb = s // b
+    tsz = nb * (nb + 1) // 2
+    pairs = {l: (pred_mod.Predictor.create(rng, h, r, r, r, "q", l),
+                 pred_mod.Predictor.create(rng, h, r, r, r, "k", l)) for l in range(n_layers)}
+    init = {f"init_{l}_{p.role}_{n}": a.copy() for l, pq in pairs.items() for p in pq
+            for n, a in p.state_arrays().items()}
+    records, arrays = [], {}
+    for i in range(2 * n_layers):
+        l = i % n_layers
+        x = rng.standard_normal((s, h)).astype(np.float32)
+        teacher = (np.abs(rng.standard_normal(tsz)) * 3.0).astype(np.float64)
+        records.append(pred_mod.TeacherRecord(l, x, teacher, s, b))
+        arrays[f"x_{i}"] = x
+        arrays[f"teacher_{i}"] = teacher
+        arrays[f"layer_{i}"] = np.array([l])
+    hist = pred_mod.fit_predictors(pairs, records, epochs=6, lr=1e-2, val_data=records,
+                                   prune_target=0.6, prune_every=2, prune_step=0.2, eval_every=3)
+    arrays.update(init)
+    arrays["loss"] = np.array([hr.train_loss for hr in hist])
+    arrays["recall"] = np.array([hr.recall for hr in hist])
+    arrays["params"] = np.array([hr.param_count for hr in hist])
+    for l, pq in pairs.items():
+        for p in pq:
+            for n, a in p.state_arrays().items():
+                arrays[f"final_{l}_{p.role}_{n}"] = a
+    np.savez_compressed(OUT / "predictor_train.npz", **arrays)
+    return arrays["loss"].tolist()
+
+
+def artifact_case():
+    """Reference-written artifacts: predictors.ckpt (STCHKPT container,
+    pred/L{l}/{role}/{name} keys, pipeline.py:370-418), thresholds.json,
+    config hashes; plus the reference's predicted scores on a fixed input."""
+    from sparsetune import checkpoint, pipeline
+    from sparsetune.config import RunConfig
+
+    cfg = RunConfig()
+    cfg.model = model_mod.ModelConfig(n_layers=2, hidden_dim=64, n_heads=4, vocab_size=256,
+                                      mlp_dim=256, block_size=8, max_seq_len=512)
+    rng = np.random.default_rng(5)
+    pairs = {l: (pred_mod.Predictor.create(rng, 64, 16, 16, 16, "q", l),
+                 pred_mod.Predictor.create(rng, 64, 16, 16, 16, "k", l)) for l in range(2)}
+    for pq in pairs.values():
+        for p in pq:
+            pred_mod.track_zero_frequency(p, rng.standard_normal((40, 64)).astype(np.float32))
+            pred_mod.elastic_prune(p, 0.75)
+    pt = sparsity.ThresholdSet({(0, "attention"): 1.25, (1, "attention"): -0.5,
+                                (0, "mlp"): 0.125, (1, "mlp"): 3.0}, config_hash=cfg.config_hash())
+    pipeline.save_predictors(OUT / "predictors.ckpt", cfg, pairs, pt, {0: 0.5, 1: 0.4})
+    ts = sparsity.ThresholdSet({(0, "attention"): 2.5, (0, "mlp"): 0.75, (1, "attention"): 1e-3,
+                                (1, "mlp"): 7.0}, eps=0.01, eta=None, config_hash=cfg.config_hash())
+    (OUT / "thresholds.json").write_text(json.dumps(ts.to_dict(), indent=2) + "\n")
+    x = rng.standard_normal((128, 64)).astype(np.float32)
+    vecs = {}
+    for l, (p_q, p_k) in pairs.items():
+        tri = pred_mod.predicted_triangle(p_q, p_k, x, 8).data
+        bsm = sparsity.BlockScoreMatrix(16, 8, np.maximum(tri, 0.0))
+        vecs[f"vec_{l}"] = sparsity.token_block_scores(bsm)
+    hashes = {}
+    for name, kw in (("tiny", dict(n_layers=2, hidden_dim=256, n_heads=4, vocab_size=256,
+                                   mlp_dim=688, block_size=16)),
+                     ("llama2_7b", dict(n_layers=32, hidden_dim=4096, n_heads=32,
+                                        vocab_size=32000, mlp_dim=11008, block_size=16,
+                                        max_seq_len=16384)),
+                     ("relu_learned", dict(mlp_variant="relu", positions="learned"))):
+        c = RunConfig()
+        c.model = model_mod.ModelConfig(**kw)
+        hashes[name] = [kw, c.config_hash()]
+        c.sparsity.mlp_scoring = False
+        hashes[name + "_nomlp"] = [kw, c.config_hash()]
+    (OUT / "config_hashes.json").write_text(json.dumps(hashes, indent=1) + "\n")
+    # a container with mixed dtypes / shapes, written by the reference
+    tensors = {"a/f32": rng.standard_normal((3, 5)).astype(np.float32),
+               "b/i64": np.arange(7, dtype=np.int64), "c/bool": np.array([True, False, True]),
+               "d/f64": np.array(3.5), "e/empty": np.zeros((0, 4), dtype=np.float32)}
+    checkpoint.save_container(OUT / "mixed.ckpt", tensors, {"k": 1}, {"m": "x"})
+    np.savez_compressed(OUT / "artifacts.npz", x=x, hash=np.array([cfg.config_hash()]), **vecs,
+                        **{"t_" + k.replace("/", "_"): v for k, v in tensors.items()})
+
+
+def tune_case():
+    """tune_thresholds (sparsity.py:379-417) on a smooth synthetic accuracy proxy."""
+    ts = sparsity.ThresholdSet({(0, "attention"): 1.0, (0, "mlp"): -2.0, (1, "attention"): 0.0,
+                                (1, "mlp"): 5.0})
+
+    def acc(t):
+        v = t.values
+        return -sum((val - 0.3 * (i + 1)) ** 2 + 0.1 * val ** 3 / (1 + val ** 2)
+                    for i, (_, val) in enumerate(sorted(v.items())))
+
+    out = {}
+    for name, kw in (("auto", dict(rounds=2)), ("fixed", dict(eps=0.05, eta=0.2, rounds=3))):
+        tuned = sparsity.tune_thresholds(acc, ts, **kw)
+        out[name] = tuned.to_dict()
+    (OUT / "tune.json").write_text(json.dumps({"init": ts.to_dict(), **out}, indent=1) + "\n")
+
+
+CASES = {"select": select_cases, "quantile": quantile_cases, "colsum": column_sum_cases,
+         "predictor": predictor_case, "scorers": scorer_cases, "steps": step_cases,
+         "patterns": step_pattern_cases, "predictor_train": predictor_train_case,
+         "artifacts": artifact_case, "tune": tune_case}
+
+
 def main():
     np.show_config() if "-v" in sys.argv else None
-    select_cases()
-    quantile_cases()
-    column_sum_cases()
-    predictor_case()
-    scorer_cases()
-    print("steps", step_cases())
-    print("patterns", step_pattern_cases())
-    print("wrote", sorted(p.name for p in OUT.glob("*.npz")))
+    names = [a for a in sys.argv[1:] if not a.startswith("-")] or list(CASES)
+    for name in names:
+        print(name, CASES[name]())
+    print("wrote", sorted(p.name for p in OUT.glob("*.*")))
 
 
 if __name__ == "__main__":
