@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--config", default="llama2_7b_16k", choices=list(CONFIGS))
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-law", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=4096)
     ap.add_argument("--profile-tag", default="")
     return ap.parse_args()
@@ -323,6 +324,30 @@ def main():
             "peak_step_gb": (torch.cuda.max_memory_allocated(dev) - base_d) / 1e9,
         }
 
+    # memory law (acceptance criterion 9) at this workload: logical saved-for-
+    # backward bytes of the attention/MLP blocks (ledger) at evenly spaced
+    # retained fractions, next to the allocator's post-forward mark
+    law = None
+    if not args.no_law:
+        from paper_2501_09767_b200 import ledger as L
+        pts = []
+        for f in (1.0, 0.5, 0.25):
+            led = L.Ledger(keep_series=False)
+            with L.use(led):
+                loss, _ = model.forward_step(staged, pattern_source=M.FractionSource(
+                    f, cfg.block_size), segments=segments)
+                loss.backward()
+            opt.zero_grad()
+            rep = led.report()
+            pts.append((f, rep.activation_bytes("layer") / 1e9,
+                        model.last_stats["activation_bytes_post_forward"] / 1e9))
+        a, c, r2 = L.affine_fit([p[0] for p in pts], [p[1] for p in pts])
+        law = {"retained_fraction": [p[0] for p in pts],
+               "block_activation_gb": [round(p[1], 4) for p in pts],
+               "allocator_gb_post_forward": [round(p[2], 4) for p in pts],
+               "fit_gb": {"slope": a, "intercept": c, "r2": r2},
+               "ratio_f0.5": (pts[1][1] - c) / (pts[0][1] - c)}
+
     # roofline of the dominant kernel (MLP-scoring gate/up GEMM, all s rows)
     pk, pk_src = peaks()
     flops_gemm = 4.0 * seq * cfg.hidden_dim * cfg.mlp_dim  # algorithmic (SwiGLU gate+up)
@@ -392,6 +417,7 @@ def main():
         "speedup_vs_dense": (value / dense["value"]) if dense else None,
         "activation_reduction_vs_dense": (dense["activation_gb_post_forward"] / act_gb)
         if dense else None,
+        "memory_law": law,
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": 2 * seq * 4,
                 "d2h_bytes_per_step": 4},
         "gpu_launches": int(round(launches_per_step * args.steps)),

@@ -20,7 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import kernels, ops, predictor as predictor_mod, sparsity
+from . import kernels, ledger, ops, predictor as predictor_mod, sparsity
 from .errors import ContractError, DimensionError
 
 PAD_TOKEN = 0
@@ -528,16 +528,19 @@ class _Step:
                       m.pos_embed[: self.n_pad].contiguous() if m.pos_embed is not None else None)
         saved = []
         src = self.source
+        led = ledger.get()
         for layer in m.layers:
             pat = src.pattern(layer.layer_id, sparsity.ATTENTION, x, self.n_valid) \
                 if src is not None else None
             plan = DecoderModel._plan_from(pat, self.n_pad, dev)
             sa = kernels.attention_forward(x, plan, layer, save=need_grad)
+            ledger.retain_saved(led, f"layer{layer.layer_id}.attn", sa)
             pat = src.pattern(layer.layer_id, sparsity.MLP, x, self.n_valid) \
                 if src is not None else None
             plan = DecoderModel._plan_from(pat, self.n_pad, dev)
             scored = m._mlp_scored.pop(layer.layer_id, None)
             sm = kernels.mlp_forward(x, plan, layer, scored=scored, save=need_grad)
+            ledger.retain_saved(led, f"layer{layer.layer_id}.mlp", sm)
             del scored
             saved.append((sa, sm))
         inv_f = torch.empty(self.n_pad, dtype=F32, device=dev)
@@ -547,6 +550,9 @@ class _Step:
             hidden, m.lm_head_t, m.lm_head, self.tgts, self.count, plan, IGNORE_INDEX,
             need_grad=need_grad)
         self.hidden = hidden
+        if need_grad:
+            ledger.retain_saved(led, "head", {"x": x, "inv_f": inv_f, "grad_hidden": grad_hidden})
+        led.mark("post_forward")
         # post_forward mark (model.py:296): activation bytes = everything still
         # allocated by this step that backward needs
         mark = torch.cuda.memory_allocated(dev)
@@ -563,12 +569,17 @@ class _Step:
         dx = torch.empty_like(self.x)
         ops.rmsnorm_bwd(self.grad_hidden, self.x, self.inv_f, m.final_norm_w, dx, None,
                         gscale=gval, accumulate=False)
+        led = ledger.get()
+        ledger.release_saved(led, {"x": self.x, "inv_f": self.inv_f,
+                                   "grad_hidden": self.grad_hidden})
         self.grad_hidden = self.x = self.inv_f = None
         for layer, (sa, sm) in zip(reversed(m.layers), reversed(self.saved)):
             if sm is not None:
                 kernels.mlp_backward(dx, sm, layer)
+                ledger.release_saved(led, sm)
             if sa is not None:
                 kernels.attention_backward(dx, sa, layer, layer.grad_views(grad))
+                ledger.release_saved(led, sa)
             self.saved.pop()
         self.saved = None
         return grad
