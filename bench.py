@@ -41,9 +41,12 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
-    "llama2_7b_16k": dict(seq=16384, model="llama2_7b"),
-    "llama2_7b_4k": dict(seq=4096, model="llama2_7b"),
-    "tiny": dict(seq=2048, model="tiny_t"),
+    "llama2_7b_16k": dict(seq=16384, model="llama2_7b", name="Llama2-7B"),
+    "llama2_7b_4k": dict(seq=4096, model="llama2_7b", name="Llama2-7B"),
+    "llama2_7b_32k": dict(seq=32768, model="llama2_7b", name="Llama2-7B"),
+    "opt_6.7b_64k": dict(seq=65536, model="opt_6_7b", name="OPT-6.7B (reference family: "
+                                                          "RMSNorm, no bias; ReLU, learned pos.)"),
+    "tiny": dict(seq=2048, model="tiny_t", name="tiny T"),
 }
 METRIC = "fine-tune tokens/sec + peak activation GB at 16K ctx (1/2/4/8 B200) vs CPU ref"
 
@@ -148,7 +151,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config}: Llama2-7B LoRA+LeMo predicted mode",
+        "config": {"workload": f"{args.config}: {wl['name']} LoRA+LeMo predicted mode",
                    "seq_len": wl["seq"], "parallelism": "cpu"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
                          "sample": f"oracle restatement, 1 decoder layer at h=4096 on {sample.s} "
@@ -310,19 +313,27 @@ def main():
 
     dense = None
     if not args.no_dense:
-        for _ in range(2):
-            step(None, staged)
-        torch.cuda.synchronize()
-        torch.cuda.reset_peak_memory_stats(dev)
-        base_d = torch.cuda.memory_allocated(dev)
-        ms_d = timed(None, lambda: staged, args.steps)
-        dense_stats = dict(model.last_stats)
-        dense = {
-            "value": world * seq * args.steps / (ms_d / 1e3), "unit": "tokens/s",
-            "ms_per_step": ms_d / args.steps,
-            "activation_gb_post_forward": dense_stats["activation_bytes_post_forward"] / 1e9,
-            "peak_step_gb": (torch.cuda.max_memory_allocated(dev) - base_d) / 1e9,
-        }
+        try:
+            for _ in range(2):
+                step(None, staged)
+            torch.cuda.synchronize()
+            torch.cuda.reset_peak_memory_stats(dev)
+            base_d = torch.cuda.memory_allocated(dev)
+            ms_d = timed(None, lambda: staged, args.steps)
+            dense_stats = dict(model.last_stats)
+            dense = {
+                "value": world * seq * args.steps / (ms_d / 1e3), "unit": "tokens/s",
+                "ms_per_step": ms_d / args.steps,
+                "activation_gb_post_forward": dense_stats["activation_bytes_post_forward"] / 1e9,
+                "peak_step_gb": (torch.cuda.max_memory_allocated(dev) - base_d) / 1e9,
+            }
+        except torch.cuda.OutOfMemoryError:
+            _lib.INSTRUMENT.enabled = False
+            opt.zero_grad()
+            torch.cuda.empty_cache()
+            dense = {"value": None, "oom": True, "note": "dense LoRA (full retention) does not "
+                     f"fit in {torch.cuda.get_device_properties(dev).total_memory / 1e9:.0f} GB "
+                     f"at {seq} tokens on one GPU"}
 
     # memory law (acceptance criterion 9) at this workload: logical saved-for-
     # backward bytes of the attention/MLP blocks (ledger) at evenly spaced
@@ -350,14 +361,16 @@ def main():
 
     # roofline of the dominant kernel (MLP-scoring gate/up GEMM, all s rows)
     pk, pk_src = peaks()
-    flops_gemm = 4.0 * seq * cfg.hidden_dim * cfg.mlp_dim  # algorithmic (SwiGLU gate+up)
+    flops_gemm = (2.0 if cfg.mlp_variant == "relu" else 4.0) * seq * cfg.hidden_dim * cfg.mlp_dim
     avg_gemm_s = (sum(gemm_ms) / max(len(gemm_ms), 1)) / 1e3
     ach = flops_gemm / avg_gemm_s / 1e12 if gemm_ms else None
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
     if tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get("gemm_gateup_bytes_per_launch")
+            tj = json.loads(tfile.read_text())
+            if tj.get("seq_len") == seq and tj.get("model") == wl["model"]:
+                traffic = tj.get("gemm_gateup_bytes_per_launch")
         except Exception:  # noqa: BLE001
             traffic = None
     roofline = {"kernel": "gemm_tn_kernel<256,EpiGateUp> (lemo_gemm_gateup, MLP scoring)",
@@ -404,7 +417,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic tokens, random-init weights",
-        "config": {"workload": f"{args.config}: Llama2-7B LoRA(r=8,q/v)+LeMo predicted patterns",
+        "config": {"workload": f"{args.config}: {wl['name']} LoRA(r=8,q/v)+LeMo predicted patterns",
                    "model": wl["model"], "global_batch": world, "seq_len": seq,
                    "parallelism": f"dp{world}", "l2": "inputs/weights larger than L2 (no flush)",
                    "segments": segments, "block_size": cfg.block_size,
@@ -414,9 +427,9 @@ def main():
         "retained_mean": {"attention": float(np.mean(attn_f)) if attn_f else None,
                           "mlp": float(np.mean(mlp_f)) if mlp_f else None},
         "dense_lora": dense,
-        "speedup_vs_dense": (value / dense["value"]) if dense else None,
+        "speedup_vs_dense": (value / dense["value"]) if dense and dense["value"] else None,
         "activation_reduction_vs_dense": (dense["activation_gb_post_forward"] / act_gb)
-        if dense else None,
+        if dense and dense["value"] else None,
         "memory_law": law,
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": 2 * seq * 4,
                 "d2h_bytes_per_step": 4},

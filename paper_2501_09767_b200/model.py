@@ -89,6 +89,18 @@ def llama2_7b(**kw) -> ModelConfig:
     return ModelConfig(**base)
 
 
+def opt_6_7b(**kw) -> ModelConfig:
+    """OPT-6.7B geometry inside the reference's model family (BASELINE
+    configs[4]): h=4096, 32 heads, ReLU MLP m=16384, learned positions,
+    V=50272.  The reference has RMSNorm and no biases, so neither has this
+    model (OPT's LayerNorm/bias are outside the reference)."""
+    base = dict(n_layers=32, hidden_dim=4096, n_heads=32, vocab_size=50272, max_seq_len=65536,
+                mlp_dim=16384, mlp_variant="relu", positions="learned", lora_rank=8,
+                lora_alpha=16.0, block_size=16)
+    base.update(kw)
+    return ModelConfig(**base)
+
+
 def tiny_t(**kw) -> ModelConfig:
     """Config T of SURVEY §8 (BASELINE configs[0])."""
     base = dict(n_layers=2, hidden_dim=256, n_heads=4, vocab_size=256, max_seq_len=2048,
