@@ -44,6 +44,8 @@ CONFIGS = {
     "llama2_7b_16k": dict(seq=16384, model="llama2_7b", name="Llama2-7B"),
     "llama2_7b_4k": dict(seq=4096, model="llama2_7b", name="Llama2-7B"),
     "llama2_7b_32k": dict(seq=32768, model="llama2_7b", name="Llama2-7B"),
+    "llama3_8b_16k": dict(seq=16384, model="llama3_8b", name="Llama3-8B (GQA 32/8)"),
+    "mistral_7b_32k": dict(seq=32768, model="mistral_7b", name="Mistral-7B (GQA 32/8, no SWA)"),
     "opt_6.7b_64k": dict(seq=65536, model="opt_6_7b", name="OPT-6.7B (reference family: "
                                                           "RMSNorm, no bias; ReLU, learned pos.)"),
     "tiny": dict(seq=2048, model="tiny_t", name="tiny T"),

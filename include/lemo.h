@@ -63,20 +63,23 @@ int lemo_gemm_scatter_add(const void* A, int lda, const void* B, int ldb, float*
  * (lemo_lora_qkv_prep) and w_qkv_t = [W_qkvᵀ | B_qᵀ, B_vᵀ | 0]
  * (lemo_lora_pack_b), so q = xn·Wq + s·(xn·A_q)·B_q (kernels.py:95-100) is
  * accumulated by the tensor core itself.  Without LoRA, K = h.
- * w_qkv_t: [nmat·h, ldw] bf16 (nmat = 2: q, k only, as layer_qk does,
- * model.py:356-368); inv_freq: [head_dim/2] float64 = base^(-j/half). */
-int lemo_gemm_qkv(const void* xn, int ldx, const void* w_qkv_t, int ldw, int M, int h, int K,
-                  int nmat, void* q, void* k, void* v, int head_dim, int rope,
+ * w_qkv_t: [h + (nmat-1)·kv, ldw] bf16 (nmat = 2: q, k only, as layer_qk does,
+ * model.py:356-368); q is [M, h], k and v are [M, kv] (kv = h for multi-head,
+ * kv = n_kv_heads·head_dim < h for grouped-query attention, an extension
+ * beyond the reference); inv_freq: [head_dim/2] float64 = base^(-j/half). */
+int lemo_gemm_qkv(const void* xn, int ldx, const void* w_qkv_t, int ldw, int M, int h, int kv,
+                  int K, int nmat, void* q, void* k, void* v, int head_dim, int rope,
                   const double* inv_freq, const int* pos, void* stream);
 
 /* A-side LoRA K-extension: xn_ext[i, h+j] = bf16(scale·t[i, j]) (j < r2), 0 up to 64. */
 int lemo_lora_qkv_prep(const float* t, int ldt, int M, int r2, float scale, void* xn_ext, int ldx,
                        int h, void* stream);
 
-/* B-side LoRA K-extension of w_qkv_t [3h, ldw]: columns h..h+63 ← B_qᵀ (q rows),
- * B_vᵀ (v rows, offset r), zeros elsewhere.  Re-run after every optimizer step. */
-int lemo_lora_pack_b(const float* Bq, const float* Bv, int h, int r, void* w_ext, int ldw,
-                     void* stream);
+/* B-side LoRA K-extension of w_qkv_t [h+2kv, ldw]: columns h..h+63 ← B_qᵀ (q rows),
+ * B_vᵀ (v rows, offset r; B_v is [r, kv]), zeros elsewhere.  Re-run after every
+ * optimizer step. */
+int lemo_lora_pack_b(const float* Bq, const float* Bv, int h, int kv, int r, void* w_ext,
+                     int ldw, void* stream);
 
 /* Gate/up half of mlp_core (kernels.py:119-124) with the MLP token
  * informativeness (model.py:371-396, sparsity.py:284-290) in the epilogue.
@@ -130,15 +133,16 @@ int lemo_mlp_compact(const void* gu_all, const float* x, int ldx, const float* i
 
 /* After attention backward: RoPE backward of dq/dk (tensor.py:627-632; dq is
  * rewritten in place pre-rotation) and packed bf16 [dq|dk|dv] rows (row stride
- * ldo >= 3h) for the dX GEMM. */
-int lemo_qkv_grad_prep(float* dq, const float* dk, const float* dv, int M, int h, int head_dim,
-                       int rope, const void* rope_tab, const int* pos, void* dqkv, int ldo,
-                       void* stream);
+ * ldo >= h + 2kv; dq [M, h], dk/dv [M, kv]) for the dX GEMM. */
+int lemo_qkv_grad_prep(float* dq, const float* dk, const float* dv, int M, int h, int kv,
+                       int head_dim, int rope, const void* rope_tab, const int* pos, void* dqkv,
+                       int ldo, void* stream);
 
-/* out [32, 3h] bf16: row j < r = [Bq[j] | 0 | 0], r <= j < 2r = [0 | 0 | Bv[j-r]];
+/* out [32, h+2kv] bf16: row j < r = [Bq[j] | 0 | 0], r <= j < 2r = [0 | 0 | Bv[j-r]];
  * u = dqkv·outᵀ gives [dq·Bqᵀ | dv·Bvᵀ] (the LoRA backward factors of
  * kernels.py:95-100) as one tcgen05 GEMM. */
-int lemo_lora_pack_bt(const float* Bq, const float* Bv, int h, int r, void* out, void* stream);
+int lemo_lora_pack_bt(const float* Bq, const float* Bv, int h, int kv, int r, void* out,
+                      void* stream);
 
 /* w[c, col0 + j] = bf16(A[c*lda + j]) for j < r2, 0 up to 64 — the LoRA
  * K-extension of the dX weight, so dxn += s·u·Aᵀ runs inside the GEMM. */
@@ -151,9 +155,9 @@ int lemo_lora_pack_a_ext(const float* A, int lda, int h, int r2, void* w, int ld
  * and are reduced in a fixed order: deterministic, no atomics. */
 int lemo_lora_grads_workspace(int M, int h, int r); /* floats; not a status */
 int lemo_lora_grads(const void* xg, const float* inv, const float* w, const float* t,
-                    const float* u, int ld, const float* g0, const float* g1, int M, int h, int r,
-                    float scale, int lda, float* dA0, float* dB0, float* dA1, float* dB1,
-                    float* workspace, void* stream);
+                    const float* u, int ld, const float* g0, const float* g1, int M, int h,
+                    int kv, int r, float scale, int lda, float* dA0, float* dB0, float* dA1,
+                    float* dB1, float* workspace, void* stream);
 
 /* Cross-entropy rows of segmented_loss_and_grad (kernels.py:256-273): per-row
  * loss terms and dlogits = (softmax - onehot)·inv_count (bf16); ignore rows
@@ -224,8 +228,8 @@ int lemo_quantile_lower(const double* data, int n, long long rank, int plus_one,
 /* Exact block informativeness (sparsity.py:173-219): out[m*ldo + n] (n <= m)
  * = max over the 16x16 tile of Σ_h max(q·k, 0)/H with the causal / n_valid
  * mask; q, k: [s, h] bf16 post-rotation (layer_qk, model.py:356-368). */
-int lemo_exact_block_scores(const void* q, const void* k, int s, int h, int head_dim, int block,
-                            int n_valid, float* out, int ldo, void* stream);
+int lemo_exact_block_scores(const void* q, const void* k, int s, int h, int kv, int head_dim,
+                            int block, int n_valid, float* out, int ldo, void* stream);
 
 /* ---- offline predictor training (predictor.py:215-433) ----------------------- */
 
@@ -258,9 +262,10 @@ int lemo_flash_fwd(const void* q, const void* k, const void* v, void* o, float* 
 
 /* Same contract as lemo_flash_fwd on the tcgen05 path: two query tiles per
  * CTA ping-ponging two softmax warpgroups, S/O in TMEM, P as a bf16 TMEM A
- * operand, single-thread MMA issue; head_dim must be 128. */
+ * operand, single-thread MMA issue; head_dim must be 128.  k, v are [n, kv]:
+ * query head hd reads key/value head hd / (h/kv) (grouped-query attention). */
 int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float* lse, int n,
-                      int h, int head_dim, float scale, void* stream);
+                      int h, int kv, int head_dim, float scale, void* stream);
 
 /* delta[hd, i] = Σ_d dO[i, hd·D + d] · O[i, hd·D + d]  (tensor.py:696). */
 int lemo_attn_delta(const void* o, const void* dout, float* delta, int n, int h, int head_dim,
@@ -269,10 +274,12 @@ int lemo_attn_delta(const void* o, const void* dout, float* delta, int n, int h,
 /* Attention backward on the tcgen05 path (head_dim 128): an atomic-free dK/dV
  * kernel (transposed formulation, dK/dV resident in TMEM, Pᵀ/dSᵀ as bf16 TMEM
  * A operands) and a dQ kernel, both recomputing P from lse and pipelined so
- * the element-wise phases overlap the MMAs.  Same contract as lemo_flash_bwd. */
+ * the element-wise phases overlap the MMAs.  Same contract as lemo_flash_bwd,
+ * with k, v, dk, dv [n, kv]: each dK/dV CTA accumulates over the h/kv query
+ * heads of its group (grouped-query attention). */
 int lemo_flash_bwd_tc(const void* q, const void* k, const void* v, const void* o,
                       const void* dout, const float* lse, float* delta, float* dq, float* dk,
-                      float* dv, int n, int h, int head_dim, float scale, void* stream);
+                      float* dv, int n, int h, int kv, int head_dim, float scale, void* stream);
 
 /* Attention backward (tensor.py:693-722): dq/dk/dv fp32 [n, h]; delta is a
  * caller workspace [h/head_dim, n] fp32. */

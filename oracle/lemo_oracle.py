@@ -197,9 +197,13 @@ def rope_bwd(g: np.ndarray, positions, n_heads: int, base: float) -> np.ndarray:
 
 def causal_attention_fwd(q, k, v, n_heads: int):
     """Multi-head causal softmax attention (tensor.py:646-691), computed per
-    head with a dense masked score matrix.  Returns (out [n,h], lse [H,n])."""
+    head with a dense masked score matrix.  Returns (out [n,h], lse [H,n]).
+    GQA extension (not in the reference): k, v narrower than q carry
+    h/kv-fold fewer heads, query head hd reads key head hd // group — the
+    same math as the reference on K/V heads repeated `group` times."""
     n, h = q.shape
     d = h // n_heads
+    group = h // k.shape[1]
     dt = q.dtype
     scale = dt.type(1.0 / np.sqrt(d))
     out = np.empty_like(q)
@@ -207,13 +211,14 @@ def causal_attention_fwd(q, k, v, n_heads: int):
     mask = np.tril(np.ones((n, n), dtype=bool))
     for hd in range(n_heads):
         sl = slice(hd * d, (hd + 1) * d)
-        s = (q[:, sl] * scale) @ k[:, sl].T
+        kl = slice((hd // group) * d, (hd // group + 1) * d)
+        s = (q[:, sl] * scale) @ k[:, kl].T
         s = np.where(mask, s, dt.type(NEG_INF))
         mx = s.max(axis=-1, keepdims=True)
         with np.errstate(under="ignore"):
             e = np.exp(s - mx)
         l = e.sum(axis=-1, keepdims=True)
-        out[:, sl] = (e / l) @ v[:, sl]
+        out[:, sl] = (e / l) @ v[:, kl]
         lse[hd] = (mx + np.log(l))[:, 0]
     return out, lse
 
@@ -222,23 +227,25 @@ def causal_attention_bwd(g, q, k, v, out, lse, n_heads: int):
     """tensor.py:693-722 (P recomputed from lse, Δ = rowsum(dO·O))."""
     n, h = q.shape
     d = h // n_heads
+    group = h // k.shape[1]
     dt = q.dtype
     scale = dt.type(1.0 / np.sqrt(d))
     dq, dk, dv = np.zeros_like(q), np.zeros_like(k), np.zeros_like(v)
     mask = np.tril(np.ones((n, n), dtype=bool))
     for hd in range(n_heads):
         sl = slice(hd * d, (hd + 1) * d)
+        kl = slice((hd // group) * d, (hd // group + 1) * d)
         qs = q[:, sl] * scale
-        s = np.where(mask, qs @ k[:, sl].T, dt.type(NEG_INF))
+        s = np.where(mask, qs @ k[:, kl].T, dt.type(NEG_INF))
         with np.errstate(under="ignore"):
             p = np.exp(s - lse[hd][:, None])
         gi = g[:, sl]
         delta = (gi * out[:, sl]).sum(axis=-1, keepdims=True)
-        dp = gi @ v[:, sl].T
+        dp = gi @ v[:, kl].T
         ds = p * (dp - delta)
-        dq[:, sl] = ds @ k[:, sl] * scale
-        dk[:, sl] = ds.T @ qs
-        dv[:, sl] = p.T @ gi
+        dq[:, sl] = ds @ k[:, kl] * scale
+        dk[:, kl] += ds.T @ qs   # GQA: the group's query heads accumulate
+        dv[:, kl] += p.T @ gi
     return dq, dk, dv
 
 
@@ -261,10 +268,15 @@ class Config:
     block_size: int = 16
     positions: str = "rope"
     rope_base: float = 10000.0
+    n_kv_heads: int = 0  # GQA extension (0 = n_heads, the reference's MHA)
 
     @property
     def head_dim(self) -> int:
         return self.hidden_dim // self.n_heads
+
+    @property
+    def kv_dim(self) -> int:
+        return (self.n_kv_heads or self.n_heads) * self.head_dim
 
 
 @dataclass
@@ -285,6 +297,7 @@ class Layer:
     rope: bool
     rope_base: float
     mlp_variant: str
+    n_kv_heads: int = 0
     predictor_q: "Predictor | None" = None
     predictor_k: "Predictor | None" = None
 
@@ -336,7 +349,8 @@ def init_model(cfg: Config, seed: int = 0, dtype=np.float32, fast: bool = False)
     for _ in range(cfg.n_layers):
         def w(rows, cols):
             return (rng.standard_normal((rows, cols)) * std).astype(dtype)
-        wq, wk, wv, wo = w(h, h), w(h, h), w(h, h), w(h, h)
+        kv = cfg.kv_dim
+        wq, wk, wv, wo = w(h, h), w(h, kv), w(h, kv), w(h, h)
         w_up = w(h, m)
         w_down = w(m, h)
         w_gate = w(h, m) if cfg.mlp_variant == "silu" else None
@@ -345,10 +359,11 @@ def init_model(cfg: Config, seed: int = 0, dtype=np.float32, fast: bool = False)
             lq = [(rng.standard_normal((h, cfg.lora_rank)) / np.sqrt(h)).astype(dtype),
                   np.zeros((cfg.lora_rank, h), dtype=dtype)]
             lv = [(rng.standard_normal((h, cfg.lora_rank)) / np.sqrt(h)).astype(dtype),
-                  np.zeros((cfg.lora_rank, h), dtype=dtype)]
+                  np.zeros((cfg.lora_rank, kv), dtype=dtype)]
         layers.append(Layer(wq, wk, wv, wo, np.ones(h, dtype), np.ones(h, dtype), w_up, w_down,
                             w_gate, lq, lv, cfg.lora_alpha / max(cfg.lora_rank, 1), cfg.n_heads,
-                            cfg.positions == "rope", cfg.rope_base, cfg.mlp_variant))
+                            cfg.positions == "rope", cfg.rope_base, cfg.mlp_variant,
+                            cfg.n_kv_heads or cfg.n_heads))
     final = np.ones(h, dtype)
     lm = (rng.standard_normal((h, cfg.vocab_size)) * std).astype(dtype)
     return Model(cfg, embed, pos, layers, final, lm)
@@ -445,13 +460,15 @@ def layer_qk(L: Layer, x: np.ndarray):
     if L.lora_q is not None:
         q = q + (xn @ L.lora_q[0]) @ L.lora_q[1] * L.scaling
     k = xn @ L.wk
+    nkv = L.n_kv_heads or L.n_heads
     if L.rope:
         pos = np.arange(n)
         q = rope_fwd(q, pos, L.n_heads, L.rope_base)
-        k = rope_fwd(k, pos, L.n_heads, L.rope_base)
+        k = rope_fwd(k, pos, nkv, L.rope_base)
     d = h // L.n_heads
-    th = lambda a: np.ascontiguousarray(a.reshape(n, L.n_heads, d).transpose(1, 0, 2))
-    return th(q), th(k)
+    th = lambda a, H: np.ascontiguousarray(a.reshape(n, H, d).transpose(1, 0, 2))
+    # GQA extension: key heads repeated to the query heads for Eq. 2
+    return th(q, L.n_heads), np.repeat(th(k, nkv), L.n_heads // nkv, axis=0)
 
 
 def exact_block_dense(q, k, block_size, n_valid=None) -> np.ndarray:
@@ -675,7 +692,7 @@ def _attention_fwd(L: Layer, x, idx):
         v = v + (tv @ L.lora_v[1]) * np.float32(s)
     if L.rope:
         q = rope_fwd(q, idx, L.n_heads, L.rope_base)
-        k = rope_fwd(k, idx, L.n_heads, L.rope_base)
+        k = rope_fwd(k, idx, L.n_kv_heads or L.n_heads, L.rope_base)
     att, lse = causal_attention_fwd(q, k, v, L.n_heads)
     out = att @ L.wo
     saved = dict(idx=idx, xg=xg, xn=xn, inv=inv, tq=tq, tv=tv, q=q, k=k, v=v, att=att, lse=lse)
@@ -689,7 +706,7 @@ def _attention_bwd(L: Layer, dx, S, grads, li):
     dq, dk, dv = causal_attention_bwd(datt, S["q"], S["k"], S["v"], S["att"], S["lse"], L.n_heads)
     if L.rope:
         dq = rope_bwd(dq, idx, L.n_heads, L.rope_base)
-        dk = rope_bwd(dk, idx, L.n_heads, L.rope_base)
+        dk = rope_bwd(dk, idx, L.n_kv_heads or L.n_heads, L.rope_base)
     xn = S["xn"]
     dxn = dq @ L.wq.T + dk @ L.wk.T + dv @ L.wv.T
     s = np.float32(L.scaling)

@@ -110,8 +110,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                           const __grid_constant__ CUtensorMap tmV,
                           const __grid_constant__ CUtensorMap tmO,
                           const float* __restrict__ lse, const float* __restrict__ delta,
-                          float* __restrict__ dk, float* __restrict__ dv, int n, int h, float sl2,
-                          float scale) {
+                          float* __restrict__ dk, float* __restrict__ dv, int n, int h, int kv,
+                          float sl2, float scale) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = aligned_smem(smem_raw);
   uint8_t* sK = smem;
@@ -133,9 +133,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mm_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = blockIdx.x, hd = blockIdx.y;
-  const int k0 = kb * kT, c0 = hd * kD;
+  // CTA = (key tile, key/value head); with grouped-query attention the loop
+  // runs over the `group` query heads sharing this key head (u = g·T + t)
+  const int kb = blockIdx.x, kvh = blockIdx.y;
+  const int group = h / kv;
+  const int k0 = kb * kT, c0 = kvh * kD;
   const int T = (n - k0 + kT - 1) / kT;  // query tiles from the diagonal on
+  const int U = group * T;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -172,17 +176,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_load_2d(&tmK, kv_full, sK + kBox, c0 + 64, k0);
       tma_load_2d(&tmV, kv_full, sV, c0, k0);
       tma_load_2d(&tmV, kv_full, sV + kBox, c0 + 64, k0);
-      for (int t = 0; t < T; ++t) {
-        const int q0 = k0 + t * kT;
+      for (int t = 0; t < U; ++t) {
+        const int q0 = k0 + (t % T) * kT, cq = (kvh * group + t / T) * kD;
         const int sq = t % kQStages, so = t % kOStages;
         mbar_wait(&q_empty[sq], ((t / kQStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&q_full[sq], kTile);
-        tma_load_2d(&tmQ, &q_full[sq], sQ + sq * kTile, c0, q0);
-        tma_load_2d(&tmQ, &q_full[sq], sQ + sq * kTile + kBox, c0 + 64, q0);
+        tma_load_2d(&tmQ, &q_full[sq], sQ + sq * kTile, cq, q0);
+        tma_load_2d(&tmQ, &q_full[sq], sQ + sq * kTile + kBox, cq + 64, q0);
         mbar_wait(&o_empty[so], ((t / kOStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&o_full[so], kTile);
-        tma_load_2d(&tmO, &o_full[so], sO + so * kTile, c0, q0);
-        tma_load_2d(&tmO, &o_full[so], sO + so * kTile + kBox, c0 + 64, q0);
+        tma_load_2d(&tmO, &o_full[so], sO + so * kTile, cq, q0);
+        tma_load_2d(&tmO, &o_full[so], sO + so * kTile + kBox, cq + 64, q0);
       }
     }
   } else if (warp == 1) {
@@ -213,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     issue_s(0);
     issue_dp(0);
-    for (int t = 0; t < T; ++t) {
+    for (int t = 0; t < U; ++t) {
       mbar_wait(p_full, t & 1);
       tc_fence_after();
       if (lane == 0) {
@@ -221,16 +225,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&o_empty[t % kOStages]);
       }
       __syncwarp();
-      if (t + 1 < T) issue_s(t + 1);
+      if (t + 1 < U) issue_s(t + 1);
       mbar_wait(ds_full, t & 1);
       tc_fence_after();
       if (lane == 0) {
         mma_tk<idesc_g>(tdK, tP, aQ + (t % kQStages) * kTile, t > 0);
         umma_commit(&q_empty[t % kQStages]);
-        if (t == T - 1) umma_commit(mm_done);
+        if (t == U - 1) umma_commit(mm_done);
       }
       __syncwarp();
-      if (t + 1 < T) issue_dp(t + 1);
+      if (t + 1 < U) issue_dp(t + 1);
     }
   } else if (warp >= 4) {
     const int wg = (warp - 4) >> 2;  // columns 64·wg … 64·wg + 63 of every query tile
@@ -239,19 +243,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int key = k0 + r;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     const uint32_t tSw = tS + lane_off + 64 * wg, tPw = tP + lane_off + 64 * wg;
-    for (int t = 0; t < T; ++t) {
+    for (int u = 0; u < U; ++u) {
+      const int t = u % T, hq = kvh * group + u / T;  // query tile, query head
       const int qw = k0 + t * kT + 64 * wg;  // first query of this WG's columns
-      float* L = sLD + (wg * 2 + (t & 1)) * kT;
+      float* L = sLD + (wg * 2 + (u & 1)) * kT;
       {
         const int c = r & 63, q = qw + c;
-        L[r] = q < n ? (r < 64 ? lse[(size_t)hd * n + q] * kLog2e : delta[(size_t)hd * n + q])
+        L[r] = q < n ? (r < 64 ? lse[(size_t)hq * n + q] * kLog2e : delta[(size_t)hq * n + q])
                      : 0.f;
       }
       named_bar_sync(1 + wg, 128);
       const bool edge = (t == 0) || (qw + 64 > n) || (key >= n);
       float p[64];
       // phase A: Pᵀ
-      mbar_wait(s_full, t & 1);
+      mbar_wait(s_full, u & 1);
       tc_fence_after();
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
       // phase B: dSᵀ
-      mbar_wait(dp_full, t & 1);
+      mbar_wait(dp_full, u & 1);
       tc_fence_after();
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
@@ -297,9 +302,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const bool ok = key < n;
     if (wg == 0)
-      store_row_f32<kD>(tdV + lane_off, dv + (size_t)key * h + c0, 1.f, ok);
+      store_row_f32<kD>(tdV + lane_off, dv + (size_t)key * kv + c0, 1.f, ok);
     else
-      store_row_f32<kD>(tdK + lane_off, dk + (size_t)key * h + c0, scale, ok);
+      store_row_f32<kD>(tdK + lane_off, dk + (size_t)key * kv + c0, scale, ok);
   }
   tc_fence_before();
   __syncthreads();
@@ -321,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tmV,
                         const __grid_constant__ CUtensorMap tmO,
                         const float* __restrict__ lse, const float* __restrict__ delta,
-                        float* __restrict__ dq, int n, int h, float sl2, float scale) {
+                        float* __restrict__ dq, int n, int h, int kv, float sl2, float scale) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = aligned_smem(smem_raw);
   uint8_t* sQ = smem;
@@ -345,6 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int qb = (int)(gridDim.x - 1 - blockIdx.x);  // heavy tiles first
   const int hd = blockIdx.y;
   const int q0 = qb * kT, c0 = hd * kD;
+  const int ck = (hd / (h / kv)) * kD;  // key/value head of this query head
   const int T = qb + 1;  // key tiles 0 … diagonal
 
   if (warp == 0 && lane == 0) {
@@ -388,12 +394,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int sk = j % kKStages, sv = j % kVStages;
         mbar_wait(&k_empty[sk], ((j / kKStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&k_full[sk], kTile);
-        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile, c0, j * kT);
-        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile + kBox, c0 + 64, j * kT);
+        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile, ck, j * kT);
+        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile + kBox, ck + 64, j * kT);
         mbar_wait(&v_empty[sv], ((j / kVStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&v_full[sv], kTile);
-        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile, c0, j * kT);
-        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile + kBox, c0 + 64, j * kT);
+        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile, ck, j * kT);
+        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile + kBox, ck + 64, j * kT);
       }
     }
   } else if (warp == 1) {
@@ -518,16 +524,17 @@ int lemo_attn_delta(const void* o, const void* dout, float* delta, int n, int h,
 
 int lemo_flash_bwd_tc(const void* q, const void* k, const void* v, const void* o,
                       const void* dout, const float* lse, float* delta, float* dq, float* dk,
-                      float* dv, int n, int h, int head_dim, float scale, void* stream) {
+                      float* dv, int n, int h, int kv, int head_dim, float scale, void* stream) {
   if (n <= 0) return 0;
   LEMO_ARG_CHECK(head_dim == fab::kD, "lemo_flash_bwd_tc: head_dim must be 128");
-  LEMO_ARG_CHECK(h % head_dim == 0, "lemo_flash_bwd_tc: h % head_dim");
+  LEMO_ARG_CHECK(h % head_dim == 0 && kv % head_dim == 0 && kv > 0 && h % kv == 0,
+                 "lemo_flash_bwd_tc: h, kv must be multiples of head_dim with kv | h");
   int rc = lemo_attn_delta(o, dout, delta, n, h, head_dim, stream);
   if (rc) return rc;
   CUtensorMap tq, tk, tv, to;
   rc = make_tma_bf16_2d(&tq, q, (uint64_t)n, (uint64_t)h, (uint64_t)h, fab::kT);
-  if (!rc) rc = make_tma_bf16_2d(&tk, k, (uint64_t)n, (uint64_t)h, (uint64_t)h, fab::kT);
-  if (!rc) rc = make_tma_bf16_2d(&tv, v, (uint64_t)n, (uint64_t)h, (uint64_t)h, fab::kT);
+  if (!rc) rc = make_tma_bf16_2d(&tk, k, (uint64_t)n, (uint64_t)kv, (uint64_t)kv, fab::kT);
+  if (!rc) rc = make_tma_bf16_2d(&tv, v, (uint64_t)n, (uint64_t)kv, (uint64_t)kv, fab::kT);
   if (!rc) rc = make_tma_bf16_2d(&to, dout, (uint64_t)n, (uint64_t)h, (uint64_t)h, fab::kT);
   if (rc) LEMO_RETURN_RC("lemo_flash_bwd_tc", rc);
   static bool attr = false;
@@ -542,12 +549,12 @@ int lemo_flash_bwd_tc(const void* q, const void* k, const void* v, const void* o
     attr = true;
   }
   const float sl2 = scale * fab::kLog2e;
-  dim3 grid((n + fab::kT - 1) / fab::kT, h / head_dim);
+  const int nt = (n + fab::kT - 1) / fab::kT;
   cudaStream_t st = (cudaStream_t)stream;
-  fab::flash_bwd_dkdv_kernel<<<grid, fab::kThreads, fab::kSmemKV, st>>>(
-      tq, tk, tv, to, lse, delta, dk, dv, n, h, sl2, scale);
-  fab::flash_bwd_dq_kernel<<<grid, fab::kThreads, fab::kSmemQ, st>>>(tq, tk, tv, to, lse, delta,
-                                                                     dq, n, h, sl2, scale);
+  fab::flash_bwd_dkdv_kernel<<<dim3(nt, kv / head_dim), fab::kThreads, fab::kSmemKV, st>>>(
+      tq, tk, tv, to, lse, delta, dk, dv, n, h, kv, sl2, scale);
+  fab::flash_bwd_dq_kernel<<<dim3(nt, h / head_dim), fab::kThreads, fab::kSmemQ, st>>>(
+      tq, tk, tv, to, lse, delta, dq, n, h, kv, sl2, scale);
   LEMO_CHECK_LAUNCH("lemo_flash_bwd_tc");
   return 0;
 }

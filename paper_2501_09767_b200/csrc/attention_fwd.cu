@@ -62,7 +62,7 @@ __device__ __forceinline__ void mma_pv(uint32_t d, uint32_t p, uint32_t b, bool 
 __global__ void __launch_bounds__(kThreads, 1)
     flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ o,
-                     float* __restrict__ lse, int n, int h, float sl2) {
+                     float* __restrict__ lse, int n, int h, int group, float sl2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = aligned_smem(smem_raw);
   uint8_t* sQ = smem;                          // Q0 | Q1
@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nt = (n + kT - 1) / kT;
   const int pair = (int)(gridDim.x - 1 - blockIdx.x);  // heavy pairs first
   const int hd = blockIdx.y, c0 = hd * kD;
+  const int ck = (hd / group) * kD;  // key/value head of this query head
   const int qt0 = 2 * pair;
   const bool two = qt0 + 1 < nt;
   const int T = two ? qt0 + 2 : qt0 + 1;  // KV tiles; Q0 uses [0, qt0], Q1 uses [0, qt0+1]
@@ -124,12 +125,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int sk = j % kKStages, sv = j % kVStages;
         mbar_wait(&k_empty[sk], ((j / kKStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&k_full[sk], kTile);
-        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile, c0, j * kT);
-        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile + kBox, c0 + 64, j * kT);
+        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile, ck, j * kT);
+        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile + kBox, ck + 64, j * kT);
         mbar_wait(&v_empty[sv], ((j / kVStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&v_full[sv], kTile);
-        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile, c0, j * kT);
-        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile + kBox, c0 + 64, j * kT);
+        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile, ck, j * kT);
+        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile + kBox, ck + 64, j * kT);
       }
     }
   } else if (warp == 9) {
@@ -300,14 +301,15 @@ using namespace lemo;
 extern "C" {
 
 int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float* lse, int n,
-                      int h, int head_dim, float scale, void* stream) {
+                      int h, int kv, int head_dim, float scale, void* stream) {
   if (n <= 0) return 0;
   LEMO_ARG_CHECK(head_dim == faf::kD, "lemo_flash_fwd_tc: head_dim must be 128");
-  LEMO_ARG_CHECK(h % head_dim == 0, "lemo_flash_fwd_tc: h % head_dim");
+  LEMO_ARG_CHECK(h % head_dim == 0 && kv % head_dim == 0 && kv > 0 && h % kv == 0,
+                 "lemo_flash_fwd_tc: h, kv must be multiples of head_dim with kv | h");
   CUtensorMap tq, tk, tv;
   int rc = make_tma_bf16_2d(&tq, q, (uint64_t)n, (uint64_t)h, (uint64_t)h, faf::kT);
-  if (!rc) rc = make_tma_bf16_2d(&tk, k, (uint64_t)n, (uint64_t)h, (uint64_t)h, faf::kT);
-  if (!rc) rc = make_tma_bf16_2d(&tv, v, (uint64_t)n, (uint64_t)h, (uint64_t)h, faf::kT);
+  if (!rc) rc = make_tma_bf16_2d(&tk, k, (uint64_t)n, (uint64_t)kv, (uint64_t)kv, faf::kT);
+  if (!rc) rc = make_tma_bf16_2d(&tv, v, (uint64_t)n, (uint64_t)kv, (uint64_t)kv, faf::kT);
   if (rc) LEMO_RETURN_RC("lemo_flash_fwd_tc", rc);
   static bool attr = false;
   if (!attr) {
@@ -319,7 +321,7 @@ int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, floa
   const int nt = (n + faf::kT - 1) / faf::kT;
   dim3 grid((nt + 1) / 2, h / head_dim);
   faf::flash_fwd_kernel<<<grid, faf::kThreads, faf::kSmem, (cudaStream_t)stream>>>(
-      tq, tk, tv, reinterpret_cast<__nv_bfloat16*>(o), lse, n, h, scale * faf::kLog2e);
+      tq, tk, tv, reinterpret_cast<__nv_bfloat16*>(o), lse, n, h, h / kv, scale * faf::kLog2e);
   LEMO_CHECK_LAUNCH("lemo_flash_fwd_tc");
   return 0;
 }

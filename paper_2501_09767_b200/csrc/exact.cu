@@ -15,7 +15,7 @@ namespace fa {
 template <int D>
 __global__ void __launch_bounds__(128) exact_block_scores_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k, int s, int h,
-    int n_valid, float* __restrict__ out, int ldo) {
+    int kv, int n_valid, float* __restrict__ out, int ldo) {
   using T = Tile<D>;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t sQ[2] = {smem_u32(smem), smem_u32(smem) + T::kBytes};
@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(128) exact_block_scores_kernel(
   const int kt = t - qt * (qt + 1) / 2;
   const int q0 = qt * 64, k0 = kt * 64;
   const int H = h / D;
+  const int group = h / kv;  // query heads per key head (grouped-query attention)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
 
@@ -36,13 +37,13 @@ __global__ void __launch_bounds__(128) exact_block_scores_kernel(
   for (int i = 0; i < 8; ++i) agg[i][0] = agg[i][1] = agg[i][2] = agg[i][3] = 0.f;
 
   T::load(sQ[0], q, h, q0, 0, s, tid, 128);
-  T::load(sK[0], k, h, k0, 0, s, tid, 128);
+  T::load(sK[0], k, kv, k0, 0, s, tid, 128);
   cp_async_commit();
   for (int hd = 0; hd < H; ++hd) {
     const int buf = hd & 1;
     if (hd + 1 < H) {
       T::load(sQ[buf ^ 1], q, h, q0, (hd + 1) * D, s, tid, 128);
-      T::load(sK[buf ^ 1], k, h, k0, (hd + 1) * D, s, tid, 128);
+      T::load(sK[buf ^ 1], k, kv, k0, ((hd + 1) / group) * D, s, tid, 128);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -106,9 +107,11 @@ using namespace lemo::fa;
 
 extern "C" {
 
-int lemo_exact_block_scores(const void* q, const void* k, int s, int h, int head_dim, int block,
-                            int n_valid, float* out, int ldo, void* stream) {
+int lemo_exact_block_scores(const void* q, const void* k, int s, int h, int kv, int head_dim,
+                            int block, int n_valid, float* out, int ldo, void* stream) {
   if (s <= 0) return 0;
+  LEMO_ARG_CHECK(kv > 0 && kv <= h && h % kv == 0 && kv % head_dim == 0,
+                 "lemo_exact_block_scores: bad k width");
   LEMO_ARG_CHECK(block == 16, "lemo_exact_block_scores: block size must be 16");
   LEMO_ARG_CHECK(head_dim == 64 || head_dim == 128, "lemo_exact_block_scores: head_dim 64/128");
   const int T = (s + 63) / 64;
@@ -121,10 +124,11 @@ int lemo_exact_block_scores(const void* q, const void* k, int s, int h, int head
     static int once = (int)cudaFuncSetAttribute(exact_block_scores_kernel<128>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     (void)once;
-    exact_block_scores_kernel<128><<<tiles, 128, smem, st>>>(qp, kp, s, h, n_valid, out, ldo);
+    exact_block_scores_kernel<128><<<tiles, 128, smem, st>>>(qp, kp, s, h, kv, n_valid, out,
+                                                              ldo);
   } else {
     const int smem = 4 * Tile<64>::kBytes;
-    exact_block_scores_kernel<64><<<tiles, 128, smem, st>>>(qp, kp, s, h, n_valid, out, ldo);
+    exact_block_scores_kernel<64><<<tiles, 128, smem, st>>>(qp, kp, s, h, kv, n_valid, out, ldo);
   }
   LEMO_CHECK_LAUNCH("lemo_exact_block_scores");
   return 0;

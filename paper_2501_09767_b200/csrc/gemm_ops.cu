@@ -141,13 +141,14 @@ struct EpiScatterAdd {
 // mod 2π in float64, then fp32 sincos of the reduced angle — no table gathers.
 struct EpiQKV {
   __nv_bfloat16 *q, *k, *v;
-  int h, head_dim, rope;
+  int h, kv, head_dim, rope;  // q width h, k / v width kv (grouped-query attention: kv < h)
   const double* inv_freq;  // [head_dim/2]
   const int* pos;
   template <int BN>
   __device__ void run(int row, bool valid, int col0, uint32_t taddr, int part) const {
-    const int which = col0 / h;
-    const int cbase = col0 - which * h;
+    const int which = col0 < h ? 0 : (col0 < h + kv ? 1 : 2);
+    const int cbase = col0 - (which == 0 ? 0 : (which == 1 ? h : h + kv));
+    const int ld = which == 0 ? h : kv;
     __nv_bfloat16* out = which == 0 ? q : (which == 1 ? k : v);
     const double dp = (valid && rope) ? (double)__ldg(pos + row) : 0.0;
     const int half = head_dim >> 1;
@@ -174,8 +175,8 @@ struct EpiQKV {
           b[i] = xa * sn + xb * cs;
         }
       }
-      store_bf16x32(out + (size_t)row * h + ca, a);
-      store_bf16x32(out + (size_t)row * h + cb, b);
+      store_bf16x32(out + (size_t)row * ld + ca, a);
+      store_bf16x32(out + (size_t)row * ld + cb, b);
     }
   }
 };
@@ -399,18 +400,20 @@ int lemo_gemm_scatter_add(const void* A, int lda, const void* B, int ldb, float*
                  gemm_auto(A, lda, B, ldb, M, N, K, e, (cudaStream_t)stream));
 }
 
-int lemo_gemm_qkv(const void* xn, int ldx, const void* w_qkv_t, int ldw, int M, int h, int K,
-                  int nmat, void* q, void* k, void* v, int head_dim, int rope,
+int lemo_gemm_qkv(const void* xn, int ldx, const void* w_qkv_t, int ldw, int M, int h, int kv,
+                  int K, int nmat, void* q, void* k, void* v, int head_dim, int rope,
                   const double* inv_freq, const int* pos, void* stream) {
   LEMO_ARG_CHECK(head_dim % 64 == 0, "lemo_gemm_qkv: head_dim must be a multiple of 64");
   LEMO_ARG_CHECK(nmat == 2 || nmat == 3, "lemo_gemm_qkv: nmat must be 2 (q,k) or 3 (q,k,v)");
+  LEMO_ARG_CHECK(kv > 0 && kv <= h && kv % head_dim == 0, "lemo_gemm_qkv: bad k/v width");
   EpiQKV e{reinterpret_cast<__nv_bfloat16*>(q), reinterpret_cast<__nv_bfloat16*>(k),
-           reinterpret_cast<__nv_bfloat16*>(v), h, head_dim, rope, inv_freq, pos};
+           reinterpret_cast<__nv_bfloat16*>(v), h, kv, head_dim, rope, inv_freq, pos};
+  const int N = h + (nmat - 1) * kv;
   int rc;
-  if (h % 256 == 0 && 256 % head_dim == 0)
-    rc = gemm<256>(xn, ldx, w_qkv_t, ldw, M, nmat * h, K, e, (cudaStream_t)stream);
-  else if (h % 128 == 0 && 128 % head_dim == 0)
-    rc = gemm<128>(xn, ldx, w_qkv_t, ldw, M, nmat * h, K, e, (cudaStream_t)stream);
+  if (h % 256 == 0 && kv % 256 == 0 && 256 % head_dim == 0)
+    rc = gemm<256>(xn, ldx, w_qkv_t, ldw, M, N, K, e, (cudaStream_t)stream);
+  else if (h % 128 == 0 && kv % 128 == 0 && 128 % head_dim == 0)
+    rc = gemm<128>(xn, ldx, w_qkv_t, ldw, M, N, K, e, (cudaStream_t)stream);
   else {
     set_error_msg("lemo_gemm_qkv: hidden dim must be a multiple of 128 and of head_dim");
     return LEMO_ERR_REPORTED;

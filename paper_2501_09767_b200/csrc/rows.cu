@@ -94,13 +94,12 @@ __global__ void lora_qkv_prep_kernel(const float* __restrict__ t, int ldt, int M
 }
 
 __global__ void lora_pack_b_kernel(const float* __restrict__ Bq, const float* __restrict__ Bv,
-                                   int h, int r, __nv_bfloat16* __restrict__ w, int ldw) {
-  const int row = blockIdx.x;  // 0 .. 3h-1
+                                   int h, int kv, int r, __nv_bfloat16* __restrict__ w, int ldw) {
+  const int row = blockIdx.x;  // 0 .. h+2kv-1: q rows, k rows, v rows
   const int j = threadIdx.x;   // 0 .. 63
-  const int which = row / h, c = row - which * h;
   float val = 0.f;
-  if (which == 0 && j < r) val = Bq[(size_t)j * h + c];
-  if (which == 2 && j >= r && j < 2 * r) val = Bv[(size_t)(j - r) * h + c];
+  if (row < h && j < r) val = Bq[(size_t)j * h + row];
+  if (row >= h + kv && j >= r && j < 2 * r) val = Bv[(size_t)(j - r) * kv + (row - h - kv)];
   w[(size_t)row * ldw + h + j] = __float2bfloat16_rn(val);
 }
 
@@ -278,46 +277,46 @@ __global__ void mlp_compact_kernel(const __nv_bfloat16* __restrict__ gu_all, int
 // pre-rotation dq (in place) for the LoRA gradients.  Pure streaming.
 __global__ void __launch_bounds__(256) qkv_grad_prep_kernel(
     float* __restrict__ dq, const float* __restrict__ dk, const float* __restrict__ dv, int h,
-    int head_dim, int rope, const float2* __restrict__ rope_tab, const int* __restrict__ pos,
-    __nv_bfloat16* __restrict__ dqkv, int ldo) {
+    int kv, int head_dim, int rope, const float2* __restrict__ rope_tab,
+    const int* __restrict__ pos, __nv_bfloat16* __restrict__ dqkv, int ldo) {
   const int row = blockIdx.x;
   const int half = head_dim >> 1;
   const int p = rope ? __ldg(pos + row) : 0;
   float* dqr = dq + (size_t)row * h;
-  const float* dkr = dk + (size_t)row * h;
-  const float* dvr = dv + (size_t)row * h;
+  const float* dkr = dk + (size_t)row * kv;
+  const float* dvr = dv + (size_t)row * kv;
   __nv_bfloat16* o = dqkv + (size_t)row * ldo;
-  // each thread: two consecutive rotation pairs (ca, ca+1) / (cb, cb+1) of one head
-  for (int e2 = threadIdx.x; e2 < (h >> 2); e2 += blockDim.x) {
-    const int e = e2 * 2;
+  // each thread: two consecutive rotation pairs (ca, ca+1) / (cb, cb+1) of one
+  // head; items [0, h/4) are dq, [h/4, (h+kv)/4) are dk and dv (kv <= h)
+  for (int e2 = threadIdx.x; e2 < ((h + kv) >> 2); e2 += blockDim.x) {
+    const bool isq = e2 < (h >> 2);
+    const int e = (isq ? e2 : e2 - (h >> 2)) * 2;
     const int hd = e / half, j = e - hd * half;
     const int ca = hd * head_dim + j, cb = ca + half;
-    float2 qa = *reinterpret_cast<const float2*>(dqr + ca);
-    float2 qb = *reinterpret_cast<const float2*>(dqr + cb);
-    float2 ka = *reinterpret_cast<const float2*>(dkr + ca);
-    float2 kb = *reinterpret_cast<const float2*>(dkr + cb);
-    const float2 va = *reinterpret_cast<const float2*>(dvr + ca);
-    const float2 vb = *reinterpret_cast<const float2*>(dvr + cb);
+    const float* src = isq ? dqr : dkr;
+    float2 xa = *reinterpret_cast<const float2*>(src + ca);
+    float2 xb = *reinterpret_cast<const float2*>(src + cb);
     if (rope) {
       const float4 cs = *reinterpret_cast<const float4*>(rope_tab + (size_t)p * half + j);
       // (cs.x, cs.y) = (cos, sin) of pair j, (cs.z, cs.w) of pair j+1
-      float t0 = qa.x * cs.x + qb.x * cs.y, t1 = -qa.x * cs.y + qb.x * cs.x;
-      float u0 = qa.y * cs.z + qb.y * cs.w, u1 = -qa.y * cs.w + qb.y * cs.z;
-      qa = make_float2(t0, u0);
-      qb = make_float2(t1, u1);
-      t0 = ka.x * cs.x + kb.x * cs.y; t1 = -ka.x * cs.y + kb.x * cs.x;
-      u0 = ka.y * cs.z + kb.y * cs.w; u1 = -ka.y * cs.w + kb.y * cs.z;
-      ka = make_float2(t0, u0);
-      kb = make_float2(t1, u1);
+      const float t0 = xa.x * cs.x + xb.x * cs.y, t1 = -xa.x * cs.y + xb.x * cs.x;
+      const float u0 = xa.y * cs.z + xb.y * cs.w, u1 = -xa.y * cs.w + xb.y * cs.z;
+      xa = make_float2(t0, u0);
+      xb = make_float2(t1, u1);
     }
-    *reinterpret_cast<float2*>(dqr + ca) = qa;
-    *reinterpret_cast<float2*>(dqr + cb) = qb;
-    *reinterpret_cast<uint32_t*>(o + ca) = pack_bf16x2(qa.x, qa.y);
-    *reinterpret_cast<uint32_t*>(o + cb) = pack_bf16x2(qb.x, qb.y);
-    *reinterpret_cast<uint32_t*>(o + h + ca) = pack_bf16x2(ka.x, ka.y);
-    *reinterpret_cast<uint32_t*>(o + h + cb) = pack_bf16x2(kb.x, kb.y);
-    *reinterpret_cast<uint32_t*>(o + 2 * h + ca) = pack_bf16x2(va.x, va.y);
-    *reinterpret_cast<uint32_t*>(o + 2 * h + cb) = pack_bf16x2(vb.x, vb.y);
+    if (isq) {
+      *reinterpret_cast<float2*>(dqr + ca) = xa;
+      *reinterpret_cast<float2*>(dqr + cb) = xb;
+      *reinterpret_cast<uint32_t*>(o + ca) = pack_bf16x2(xa.x, xa.y);
+      *reinterpret_cast<uint32_t*>(o + cb) = pack_bf16x2(xb.x, xb.y);
+    } else {
+      const float2 va = *reinterpret_cast<const float2*>(dvr + ca);
+      const float2 vb = *reinterpret_cast<const float2*>(dvr + cb);
+      *reinterpret_cast<uint32_t*>(o + h + ca) = pack_bf16x2(xa.x, xa.y);
+      *reinterpret_cast<uint32_t*>(o + h + cb) = pack_bf16x2(xb.x, xb.y);
+      *reinterpret_cast<uint32_t*>(o + h + kv + ca) = pack_bf16x2(va.x, va.y);
+      *reinterpret_cast<uint32_t*>(o + h + kv + cb) = pack_bf16x2(vb.x, vb.y);
+    }
   }
 }
 
@@ -325,15 +324,15 @@ __global__ void __launch_bounds__(256) qkv_grad_prep_kernel(
 //  Bt [32, 3h]:  row j < r: [Bq[j] | 0 | 0];  r <= j < 2r: [0 | 0 | Bv[j-r]]  (u = dqkv·Btᵀ)
 //  A-extension of the dX weight: w[c, col0 + j] = A[c, j] (j < 2r), 0 up to 64.
 __global__ void lora_pack_bt_kernel(const float* __restrict__ Bq, const float* __restrict__ Bv,
-                                    int h, int r, __nv_bfloat16* __restrict__ out) {
+                                    int h, int kv, int r, __nv_bfloat16* __restrict__ out) {
   const int j = blockIdx.y;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= 3 * h) return;
-  const int which = c / h, cc = c - which * h;
+  const int n = h + 2 * kv;
+  if (c >= n) return;
   float val = 0.f;
-  if (which == 0 && j < r) val = Bq[(size_t)j * h + cc];
-  if (which == 2 && j >= r && j < 2 * r) val = Bv[(size_t)(j - r) * h + cc];
-  out[(size_t)j * 3 * h + c] = __float2bfloat16_rn(val);
+  if (c < h && j < r) val = Bq[(size_t)j * h + c];
+  if (c >= h + kv && j >= r && j < 2 * r) val = Bv[(size_t)(j - r) * kv + (c - h - kv)];
+  out[(size_t)j * n + c] = __float2bfloat16_rn(val);
 }
 
 __global__ void lora_pack_a_ext_kernel(const float* __restrict__ A, int lda, int h, int r2,
@@ -352,7 +351,7 @@ template <int R>
 __global__ void __launch_bounds__(128) lora_grads_kernel(
     const __nv_bfloat16* __restrict__ xg, const float* __restrict__ inv, const float* __restrict__ w,
     const float* __restrict__ t, const float* __restrict__ u, int ld, const float* __restrict__ g0,
-    const float* __restrict__ g1, int M, int h, float* __restrict__ part) {
+    const float* __restrict__ g1, int M, int h, int kv, float* __restrict__ part) {
   // per row: [t_q (R) | t_v (R)] and [u_q (R) | u_v (R)], read as float4 broadcasts
   __shared__ __align__(16) float st[kLoraRows][2 * R];
   __shared__ __align__(16) float su[kLoraRows][2 * R];
@@ -378,7 +377,7 @@ __global__ void __launch_bounds__(128) lora_grads_kernel(
   for (int i = 0; i < nrow; ++i) {
     const size_t off = (size_t)(r0 + i) * h + c;
     const float xn = __bfloat162float(xg[off]) * sinv[i] * wc;
-    const float q = g0[off], v = g1[off];
+    const float q = g0[off], v = c < kv ? g1[(size_t)(r0 + i) * kv + c] : 0.f;
     float tv[2 * R], uv[2 * R];
 #pragma unroll
     for (int j = 0; j < 2 * R; j += 4) {
@@ -413,7 +412,7 @@ __global__ void __launch_bounds__(128) lora_grads_kernel(
 // into the gradients: no atomics, so all-retain ≡ dense bitwise
 // (tests/test_model.py:186-191) and repeated steps are reproducible.
 __global__ void __launch_bounds__(256) lora_grads_reduce_kernel(
-    const float* __restrict__ part, int G, int R, int h, float scale, int lda,
+    const float* __restrict__ part, int G, int R, int h, int kv, float scale, int lda,
     float* __restrict__ dA0, float* __restrict__ dB0, float* __restrict__ dA1,
     float* __restrict__ dB1) {
   const int n = 4 * R * h;
@@ -422,10 +421,11 @@ __global__ void __launch_bounds__(256) lora_grads_reduce_kernel(
   float acc = 0.f;
   for (int g = 0; g < G; ++g) acc += part[(size_t)g * n + e];
   const int q = e / (R * h), rem = e - q * R * h, j = rem / h, c = rem - j * h;
+  if (q == 3 && c >= kv) return;  // dB1 is [R, kv]
   float* dst = q == 0 ? dA0 + (size_t)c * lda + j
              : q == 1 ? dA1 + (size_t)c * lda + j
              : q == 2 ? dB0 + (size_t)j * h + c
-                      : dB1 + (size_t)j * h + c;
+                      : dB1 + (size_t)j * kv + c;
   *dst += scale * acc;
 }
 
@@ -544,11 +544,11 @@ int lemo_lora_qkv_prep(const float* t, int ldt, int M, int r2, float scale, void
   return 0;
 }
 
-int lemo_lora_pack_b(const float* Bq, const float* Bv, int h, int r, void* w_ext, int ldw,
-                     void* stream) {
+int lemo_lora_pack_b(const float* Bq, const float* Bv, int h, int kv, int r, void* w_ext,
+                     int ldw, void* stream) {
   LEMO_ARG_CHECK(2 * r <= 64 && ldw >= h + 64, "lemo_lora_pack_b: need 64 extension columns");
-  lora_pack_b_kernel<<<3 * h, 64, 0, (cudaStream_t)stream>>>(
-      Bq, Bv, h, r, reinterpret_cast<__nv_bfloat16*>(w_ext), ldw);
+  lora_pack_b_kernel<<<h + 2 * kv, 64, 0, (cudaStream_t)stream>>>(
+      Bq, Bv, h, kv, r, reinterpret_cast<__nv_bfloat16*>(w_ext), ldw);
   LEMO_CHECK_LAUNCH("lemo_lora_pack_b");
   return 0;
 }
@@ -625,24 +625,26 @@ int lemo_mlp_compact(const void* gu_all, const float* x, int ldx, const float* i
   return 0;
 }
 
-int lemo_qkv_grad_prep(float* dq, const float* dk, const float* dv, int M, int h, int head_dim,
-                       int rope, const void* rope_tab, const int* pos, void* dqkv, int ldo,
-                       void* stream) {
+int lemo_qkv_grad_prep(float* dq, const float* dk, const float* dv, int M, int h, int kv,
+                       int head_dim, int rope, const void* rope_tab, const int* pos, void* dqkv,
+                       int ldo, void* stream) {
   if (M <= 0) return 0;
-  LEMO_ARG_CHECK(head_dim % 4 == 0 && ldo >= 3 * h && ldo % 2 == 0,
+  LEMO_ARG_CHECK(head_dim % 4 == 0 && kv <= h && kv % head_dim == 0 && ldo >= h + 2 * kv &&
+                     ldo % 2 == 0,
                  "lemo_qkv_grad_prep: bad geometry");
   qkv_grad_prep_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(
-      dq, dk, dv, h, head_dim, rope, reinterpret_cast<const float2*>(rope_tab), pos,
+      dq, dk, dv, h, kv, head_dim, rope, reinterpret_cast<const float2*>(rope_tab), pos,
       reinterpret_cast<__nv_bfloat16*>(dqkv), ldo);
   LEMO_CHECK_LAUNCH("lemo_qkv_grad_prep");
   return 0;
 }
 
-int lemo_lora_pack_bt(const float* Bq, const float* Bv, int h, int r, void* out, void* stream) {
+int lemo_lora_pack_bt(const float* Bq, const float* Bv, int h, int kv, int r, void* out,
+                      void* stream) {
   LEMO_ARG_CHECK(2 * r <= 32, "lemo_lora_pack_bt: 2r <= 32");
-  dim3 grid((3 * h + 255) / 256, 32);
+  dim3 grid((h + 2 * kv + 255) / 256, 32);
   lora_pack_bt_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
-      Bq, Bv, h, r, reinterpret_cast<__nv_bfloat16*>(out));
+      Bq, Bv, h, kv, r, reinterpret_cast<__nv_bfloat16*>(out));
   LEMO_CHECK_LAUNCH("lemo_lora_pack_bt");
   return 0;
 }
@@ -667,9 +669,9 @@ int lemo_lora_grads_workspace(int M, int h, int r) {
 }
 
 int lemo_lora_grads(const void* xg, const float* inv, const float* w, const float* t,
-                    const float* u, int ld, const float* g0, const float* g1, int M, int h, int r,
-                    float scale, int lda, float* dA0, float* dB0, float* dA1, float* dB1,
-                    float* workspace, void* stream) {
+                    const float* u, int ld, const float* g0, const float* g1, int M, int h,
+                    int kv, int r, float scale, int lda, float* dA0, float* dB0, float* dA1,
+                    float* dB1, float* workspace, void* stream) {
   if (M <= 0) return 0;
   LEMO_ARG_CHECK(r <= 16, "lemo_lora_grads: LoRA rank <= 16");
   LEMO_ARG_CHECK(workspace != nullptr, "lemo_lora_grads: workspace required");
@@ -678,7 +680,7 @@ int lemo_lora_grads(const void* xg, const float* inv, const float* w, const floa
   cudaStream_t st = (cudaStream_t)stream;
   auto* xgp = reinterpret_cast<const __nv_bfloat16*>(xg);
 #define LG(RR) \
-  lora_grads_kernel<RR><<<grid, 128, 0, st>>>(xgp, inv, w, t, u, ld, g0, g1, M, h, workspace)
+  lora_grads_kernel<RR><<<grid, 128, 0, st>>>(xgp, inv, w, t, u, ld, g0, g1, M, h, kv, workspace)
   switch (r) {
     case 2: LG(2); break;
     case 4: LG(4); break;
@@ -688,8 +690,8 @@ int lemo_lora_grads(const void* xg, const float* inv, const float* w, const floa
   }
 #undef LG
   const int n = 4 * r * h;
-  lora_grads_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(workspace, G, r, h, scale, lda, dA0,
-                                                            dB0, dA1, dB1);
+  lora_grads_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(workspace, G, r, h, kv, scale, lda,
+                                                            dA0, dB0, dA1, dB1);
   LEMO_CHECK_LAUNCH("lemo_lora_grads");
   return 0;
 }

@@ -19,16 +19,16 @@ from .sparsity import BlockScoreMatrix, n_blocks_for
 def exact_block_dense(q: torch.Tensor, k: torch.Tensor, block_size: int, *, n_heads: int,
                       n_valid: int | None = None) -> torch.Tensor:
     """Dense [nb, nb] fp32 tile maxima (upper triangle zero).  q, k: [s, h] bf16."""
-    if q.shape != k.shape:
-        raise ContractError(f"q/k shapes differ: {tuple(q.shape)} vs {tuple(k.shape)}")
+    if q.shape[0] != k.shape[0] or q.shape[1] % k.shape[1]:
+        raise ContractError(f"q/k shapes incompatible: {tuple(q.shape)} vs {tuple(k.shape)}")
     s, h = q.shape
     if block_size > s:
         raise ContractError(f"block size {block_size} exceeds sequence length {s}")
     n_valid = s if n_valid is None else n_valid
     nb = n_blocks_for(s, block_size)
     out = torch.zeros(nb, nb, dtype=torch.float32, device=q.device)
-    call("lemo_exact_block_scores", ptr(q.contiguous()), ptr(k.contiguous()), s, h, h // n_heads,
-         block_size, n_valid, ptr(out), out.stride(0), stream_ptr())
+    call("lemo_exact_block_scores", ptr(q.contiguous()), ptr(k.contiguous()), s, h, k.shape[1],
+         h // n_heads, block_size, n_valid, ptr(out), out.stride(0), stream_ptr())
     return out
 
 

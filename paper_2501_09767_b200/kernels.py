@@ -134,7 +134,7 @@ def attention_forward(x: torch.Tensor, plan: GatherPlan, layer, *, save: bool = 
     ops.rmsnorm_gather(x, layer.attn_norm_w, idx, xn=xn, xg=xg, inv=inv)
     t = layer.qkv_input(xn) if r else None
     q, kk, v = ops.gemm_qkv(xn, layer.w_qkv_t, h=h, head_dim=layer.head_dim, rope=layer.rope,
-                            inv_freq=layer.inv_freq, pos=idx)
+                            inv_freq=layer.inv_freq, pos=idx, kv=layer.kv)
     del xn
     o, lse = ops.flash_fwd(q, kk, v, head_dim=layer.head_dim, scale=1.0 / math.sqrt(layer.head_dim))
     ops.gemm_scatter_add(o, layer.w_o_t, x, idx)

@@ -45,8 +45,14 @@ class ModelConfig:
     positions: str = "rope"  # "rope" | "learned"
     rope_base: float = 10000.0
     dtype: str = "float32"
+    # grouped-query attention (an extension beyond the reference; 0 = n_heads):
+    # k / v carry n_kv_heads heads, query head i reads key head i // (H / n_kv)
+    n_kv_heads: int = 0
 
     def __post_init__(self):
+        if self.n_kv_heads and (self.n_kv_heads < 0 or self.n_heads % self.n_kv_heads):
+            raise DimensionError(f"n_heads {self.n_heads} not a multiple of n_kv_heads "
+                                 f"{self.n_kv_heads}")
         if self.hidden_dim % self.n_heads != 0:
             raise DimensionError(f"hidden_dim {self.hidden_dim} not divisible by {self.n_heads} heads")
         if self.positions == "rope" and self.head_dim % 2 != 0:
@@ -60,6 +66,14 @@ class ModelConfig:
             raise ContractError(f"unknown position mode {self.positions!r}")
         if self.dtype not in ("float32", "float64", "bfloat16"):
             raise ContractError(f"unsupported dtype {self.dtype!r}")
+
+    @property
+    def kv_heads(self) -> int:
+        return self.n_kv_heads or self.n_heads
+
+    @property
+    def kv_dim(self) -> int:
+        return self.kv_heads * self.head_dim
 
     @property
     def head_dim(self) -> int:
@@ -79,12 +93,35 @@ class ModelConfig:
             raise ContractError("GPU kernels need vocab_size % 32 == 0")
         if self.lora_rank > 16:
             raise ContractError("GPU kernels support LoRA rank <= 16")
+        if self.kv_heads != self.n_heads and (self.head_dim != 128 or self.kv_dim % 128):
+            raise ContractError("grouped-query attention runs on the tcgen05 path: head_dim 128")
 
 
 def llama2_7b(**kw) -> ModelConfig:
     """Llama2-7B geometry (BASELINE configs[1], north star at 16K)."""
     base = dict(n_layers=32, hidden_dim=4096, n_heads=32, vocab_size=32000, max_seq_len=16384,
                 mlp_dim=11008, lora_rank=8, lora_alpha=16.0, block_size=16)
+    base.update(kw)
+    return ModelConfig(**base)
+
+
+def llama3_8b(**kw) -> ModelConfig:
+    """Llama3-8B geometry (BASELINE configs[2]): 32 query / 8 key-value heads
+    (grouped-query attention, pinned through the repeated-head reference
+    model), m=14336, V=128256, RoPE base 500000."""
+    base = dict(n_layers=32, hidden_dim=4096, n_heads=32, n_kv_heads=8, vocab_size=128256,
+                max_seq_len=16384, mlp_dim=14336, rope_base=500000.0, lora_rank=8,
+                lora_alpha=16.0, block_size=16)
+    base.update(kw)
+    return ModelConfig(**base)
+
+
+def mistral_7b(**kw) -> ModelConfig:
+    """Mistral-7B geometry (BASELINE configs[3]): 32 / 8 heads, m=14336,
+    V=32000.  Full causal attention: sliding-window attention is not part of
+    the reference and is not modelled."""
+    base = dict(n_layers=32, hidden_dim=4096, n_heads=32, n_kv_heads=8, vocab_size=32000,
+                max_seq_len=32768, mlp_dim=14336, lora_rank=8, lora_alpha=16.0, block_size=16)
     base.update(kw)
     return ModelConfig(**base)
 
@@ -170,6 +207,7 @@ class LayerState:
         self.layer_id = layer_id
         self.n_heads = cfg.n_heads
         self.head_dim = cfg.head_dim
+        self.kv = kv = cfg.kv_dim  # k / v width (= h unless grouped-query)
         self.rope = cfg.positions == "rope"
         self.rope_base = cfg.rope_base
         self.mlp_variant = cfg.mlp_variant
@@ -184,13 +222,14 @@ class LayerState:
             return t.to(device=dev, dtype=F32)
 
         wq, wk, wv, wo = g("wq"), g("wk"), g("wv"), g("wo")
-        w_qkv = torch.cat([wq, wk, wv], dim=1)  # [h, 3h]   (x·W layout)
+        w_qkv = torch.cat([wq, wk, wv], dim=1)  # [h, h+2kv]   (x·W layout)
+        nq = h + 2 * kv
         kext = ops.LORA_K_EXT if cfg.lora_rank else 0
-        # backward dX operand [h, 3h (+64: A_q|A_v, the LoRA term of dxn)]
-        self.w_qkv = torch.zeros(h, 3 * h + kext, dtype=BF16, device=dev)
-        self.w_qkv[:, :3 * h] = w_qkv.to(BF16)
-        # forward operand [3h, h (+64 LoRA K-extension columns, see lemo_gemm_qkv)]
-        self.w_qkv_t = torch.zeros(3 * h, h + kext, dtype=BF16, device=dev)
+        # backward dX operand [h, h+2kv (+64: A_q|A_v, the LoRA term of dxn)]
+        self.w_qkv = torch.zeros(h, nq + kext, dtype=BF16, device=dev)
+        self.w_qkv[:, :nq] = w_qkv.to(BF16)
+        # forward operand [h+2kv, h (+64 LoRA K-extension columns, see lemo_gemm_qkv)]
+        self.w_qkv_t = torch.zeros(nq, h + kext, dtype=BF16, device=dev)
         self.w_qkv_t[:, :h] = w_qkv.t().to(BF16)
         self.inv_freq = model.inv_freq
         self.w_o = wo.to(BF16).contiguous()
@@ -229,11 +268,11 @@ class LayerState:
             self.lora_q = self.lora_v = None
 
     def _views(self, flat):
-        h, r = self.head_dim * self.n_heads, self.lora_rank
+        h, r, kv = self.head_dim * self.n_heads, self.lora_rank, self.kv
         o = self._off
         A = flat[o:o + 2 * h * r].view(h, 2 * r)
         Bq = flat[o + 2 * h * r:o + 3 * h * r].view(r, h)
-        Bv = flat[o + 3 * h * r:o + 4 * h * r].view(r, h)
+        Bv = flat[o + 3 * h * r:o + 3 * h * r + kv * r].view(r, kv)
         return A, Bq, Bv
 
     def lora_A_packed(self) -> torch.Tensor:
@@ -256,9 +295,10 @@ class LayerState:
         s·u into dqkv_ext's extension columns and A_q|A_v into the dX weight's,
         so dxn = dqkv·W_qkvᵀ + s·u·Aᵀ (kernels.py:95-100 backward) is one GEMM."""
         h, r = self.w_qkv.shape[0], self.lora_rank
-        u = ops.gemm_f32(dqkv_ext[:, :3 * h], ops.lora_pack_bt(self.lora_Bq, self.lora_Bv, r, h))
-        ops.lora_qkv_prep(u, r, self.lora_scaling, dqkv_ext, 3 * h)
-        ops.lora_pack_a_ext(self.lora_A, r, self.w_qkv, 3 * h)
+        nq = h + 2 * self.kv
+        u = ops.gemm_f32(dqkv_ext[:, :nq], ops.lora_pack_bt(self.lora_Bq, self.lora_Bv, r, h))
+        ops.lora_qkv_prep(u, r, self.lora_scaling, dqkv_ext, nq)
+        ops.lora_pack_a_ext(self.lora_A, r, self.w_qkv, nq)
         return u
 
     def grad_views(self, flat_grad):
@@ -286,7 +326,9 @@ def reference_init_arrays(cfg: ModelConfig, seed: int) -> dict:
 
         def w(rows, cols):
             return (rng.standard_normal((rows, cols)) * std).astype(np.float32)
-        out[f"{p}.wq"], out[f"{p}.wk"], out[f"{p}.wv"], out[f"{p}.wo"] = (w(h, h) for _ in range(4))
+        kv = cfg.kv_dim
+        out[f"{p}.wq"], out[f"{p}.wk"], out[f"{p}.wv"], out[f"{p}.wo"] = (
+            w(h, h), w(h, kv), w(h, kv), w(h, h))
         out[f"{p}.attn_norm"] = np.ones(h, np.float32)
         out[f"{p}.mlp_norm"] = np.ones(h, np.float32)
         out[f"{p}.w_up"] = w(h, m)
@@ -294,10 +336,10 @@ def reference_init_arrays(cfg: ModelConfig, seed: int) -> dict:
         if cfg.mlp_variant == "silu":
             out[f"{p}.w_gate"] = w(h, m)
         if cfg.lora_rank > 0:
-            for tag in ("lora_q", "lora_v"):
+            for tag, width in (("lora_q", h), ("lora_v", cfg.kv_dim)):
                 out[f"{p}.{tag}.a"] = (rng.standard_normal((h, cfg.lora_rank)) /
                                        np.sqrt(h)).astype(np.float32)
-                out[f"{p}.{tag}.b"] = np.zeros((cfg.lora_rank, h), np.float32)
+                out[f"{p}.{tag}.b"] = np.zeros((cfg.lora_rank, width), np.float32)
     out["final_norm"] = np.ones(h, np.float32)
     out["lm_head"] = (rng.standard_normal((h, cfg.vocab_size)) * std).astype(np.float32)
     return out
@@ -319,7 +361,9 @@ class _TorchInit:
         cfg = self.cfg
         h, m = cfg.hidden_dim, cfg.mlp_dim
         std = 1.0 / math.sqrt(h)
-        d = {n: self.normal(h, h, std) for n in ("wq", "wk", "wv", "wo")}
+        kv = cfg.kv_dim
+        d = {n: self.normal(h, h if n in ("wq", "wo") else kv, std)
+             for n in ("wq", "wk", "wv", "wo")}
         d["w_up"] = self.normal(h, m, std)
         d["w_down"] = self.normal(m, h, std)
         if cfg.mlp_variant == "silu":
@@ -327,9 +371,9 @@ class _TorchInit:
         d["attn_norm"] = torch.ones(h, device=self.dev)
         d["mlp_norm"] = torch.ones(h, device=self.dev)
         if cfg.lora_rank:
-            for tag in ("lora_q", "lora_v"):
+            for tag, width in (("lora_q", h), ("lora_v", kv)):
                 d[f"{tag}.a"] = self.normal(h, cfg.lora_rank, std)
-                d[f"{tag}.b"] = torch.zeros(cfg.lora_rank, h, device=self.dev)
+                d[f"{tag}.b"] = torch.zeros(cfg.lora_rank, width, device=self.dev)
         return d
 
 
@@ -354,7 +398,8 @@ class DecoderModel:
         half = cfg.head_dim // 2
         self.inv_freq = torch.as_tensor(
             cfg.rope_base ** (-np.arange(half, dtype=np.float64) / half)).to(dev)
-        self.lora_param = torch.zeros(max(4 * h * r * L, 1), dtype=F32, device=dev)
+        self.lora_param = torch.zeros(max((3 * h + cfg.kv_dim) * r * L, 1), dtype=F32,
+                                      device=dev)
         if arrays is None and init == "reference":
             arrays = reference_init_arrays(cfg, seed)
         if arrays is not None:
@@ -400,7 +445,8 @@ class DecoderModel:
     # -- parameters -------------------------------------------------------------
 
     def _lora_offset(self, layer_id: int) -> int:
-        return 4 * self.config.hidden_dim * self.config.lora_rank * layer_id
+        c = self.config
+        return (3 * c.hidden_dim + c.kv_dim) * c.lora_rank * layer_id
 
     def adapter_parameters(self):
         out = []
@@ -645,7 +691,7 @@ def layer_qk(layer: LayerState, x: torch.Tensor):
         layer.qkv_input(xn)
     pos = torch.arange(s, dtype=torch.int32, device=x.device)
     q, k = ops.gemm_qkv(xn, layer.w_qkv_t, h=h, head_dim=layer.head_dim, rope=layer.rope,
-                        inv_freq=layer.inv_freq, pos=pos, nmat=2)
+                        inv_freq=layer.inv_freq, pos=pos, nmat=2, kv=layer.kv)
     return q, k
 
 

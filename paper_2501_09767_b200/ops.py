@@ -92,19 +92,22 @@ def gemm_scatter_add(a, b, resid, idx=None):
     return resid
 
 
-def gemm_qkv(xn, w_qkv_t, *, h, head_dim, rope, inv_freq, pos, nmat=3, out=None):
-    """q, k(, v) = rope(xn·Wᵀ) at positions pos over K = xn.shape[1] columns
-    (h, or h + 64 with the LoRA K-extension) — see lemo_gemm_qkv."""
+def gemm_qkv(xn, w_qkv_t, *, h, head_dim, rope, inv_freq, pos, nmat=3, kv=None, out=None):
+    """q [M, h], k(, v) [M, kv] = rope(xn·Wᵀ) at positions pos over K =
+    xn.shape[1] columns (h, or h + 64 with the LoRA K-extension) — see
+    lemo_gemm_qkv.  kv < h: grouped-query attention (kv = n_kv_heads·head_dim)."""
     M, K = xn.shape
+    kv = h if kv is None else kv
     _check(xn, w_qkv_t, pos, inv_freq)
-    if w_qkv_t.shape[1] < K or w_qkv_t.shape[0] < nmat * h:
+    if w_qkv_t.shape[1] < K or w_qkv_t.shape[0] < h + (nmat - 1) * kv:
         raise DimensionError("q/k/v weight does not cover the requested output")
     if out is None:
-        out = [torch.empty(M, h, dtype=BF16, device=xn.device) for _ in range(nmat)]
+        out = [torch.empty(M, h if i == 0 else kv, dtype=BF16, device=xn.device)
+               for i in range(nmat)]
     q, k = out[0], out[1]
     v = out[2] if nmat == 3 else None
-    call("lemo_gemm_qkv", ptr(xn), xn.stride(0), ptr(w_qkv_t), w_qkv_t.stride(0), M, h, K, nmat,
-         ptr(q), ptr(k), ptr(v), head_dim, int(bool(rope)), ptr(inv_freq), ptr(pos), _s())
+    call("lemo_gemm_qkv", ptr(xn), xn.stride(0), ptr(w_qkv_t), w_qkv_t.stride(0), M, h, kv, K,
+         nmat, ptr(q), ptr(k), ptr(v), head_dim, int(bool(rope)), ptr(inv_freq), ptr(pos), _s())
     return out
 
 
@@ -151,9 +154,10 @@ def lora_qkv_prep(t, r, scale, xn_ext, h):
 
 
 def lora_pack_b(Bq, Bv, r, w_ext, h):
-    """w_ext[:, h:h+64] = [B_qᵀ | B_vᵀ | 0] on the q / v rows (bf16)."""
+    """w_ext[:, h:h+64] = [B_qᵀ | B_vᵀ | 0] on the q / v rows (bf16); B_v is [r, kv]."""
     _check(Bq, Bv, w_ext)
-    call("lemo_lora_pack_b", ptr(Bq), ptr(Bv), h, r, ptr(w_ext), w_ext.stride(0), _s())
+    call("lemo_lora_pack_b", ptr(Bq), ptr(Bv), h, Bv.shape[1], r, ptr(w_ext), w_ext.stride(0),
+         _s())
 
 
 LORA_T_COLS = 32  # t / u buffers are [k, 32] (2r <= 32, zero-padded)
@@ -212,19 +216,21 @@ def mlp_compact(gu_all, x, inv_all, idx, *, m_pad, relu, gu_out, inner_out, xg_o
 
 
 def qkv_grad_prep(dq, dk, dv, *, head_dim, rope, rope_tab, pos, dqkv):
-    """RoPE backward of dq/dk (dq rewritten in place) + bf16 [dq|dk|dv] rows."""
-    _check(dq, dk, dv, rope_tab, pos, dqkv)
+    """RoPE backward of dq (in place, fp32) / dk and the bf16 [dq|dk|dv] rows."""
+    _check(dq, dk, dv, pos, dqkv)
     M, h = dq.shape
-    call("lemo_qkv_grad_prep", ptr(dq), ptr(dk), ptr(dv), M, h, head_dim, int(bool(rope)),
-         ptr(rope_tab), ptr(pos), ptr(dqkv), dqkv.stride(0), _s())
+    call("lemo_qkv_grad_prep", ptr(dq), ptr(dk), ptr(dv), M, h, dk.shape[1], head_dim,
+         int(bool(rope)), ptr(rope_tab), ptr(pos), ptr(dqkv), dqkv.stride(0), _s())
+    return dqkv
 
 
 def lora_pack_bt(Bq, Bv, r, h, out=None):
-    """[32, 3h] bf16 with B_q (q block) / B_v (v block) rows for u = dqkv·outᵀ."""
+    """[32, h+2kv] bf16 LoRA B operand of u = dqkv·Btᵀ (lemo_lora_pack_bt)."""
     _check(Bq, Bv, out)
+    kv = Bv.shape[1]
     if out is None:
-        out = torch.empty(LORA_T_COLS, 3 * h, dtype=BF16, device=Bq.device)
-    call("lemo_lora_pack_bt", ptr(Bq), ptr(Bv), h, r, ptr(out), _s())
+        out = torch.empty(LORA_T_COLS, h + 2 * kv, dtype=BF16, device=Bq.device)
+    call("lemo_lora_pack_bt", ptr(Bq), ptr(Bv), h, kv, r, ptr(out), _s())
     return out
 
 
@@ -242,8 +248,8 @@ def lora_grads(xg, inv, w, t, u, g0, g1, *, r, scale, dA, dB0, dB1):
     ws = torch.empty(max(1, lib().lemo_lora_grads_workspace(M, h, r)), dtype=torch.float32,
                      device=xg.device)
     call("lemo_lora_grads", ptr(xg), ptr(inv), ptr(w), ptr(t), ptr(u), t.stride(0), ptr(g0),
-         ptr(g1), M, h, r, float(scale), dA.stride(0), ptr(dA), ptr(dB0), ptr(dA[:, r:]),
-         ptr(dB1), ptr(ws), _s())
+         ptr(g1), M, h, g1.shape[1], r, float(scale), dA.stride(0), ptr(dA), ptr(dB0),
+         ptr(dA[:, r:]), ptr(dB1), ptr(ws), _s())
 
 
 def ce_rows(logits, targets, *, V, ignore, inv_count, dlogits, row_loss, bad):
@@ -434,7 +440,14 @@ def flash_fwd(q, k, v, *, head_dim, scale, o=None, lse=None, impl=None):
         impl = "tc" if head_dim == 128 else "mma"
     name = "lemo_flash_fwd_tc" if impl == "tc" else "lemo_flash_fwd"
     INSTRUMENT.note(name, n)
-    call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(lse), n, h, head_dim, float(scale), _s())
+    kv = k.shape[1]
+    if impl == "tc":
+        call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(lse), n, h, kv, head_dim, float(scale),
+             _s())
+    else:
+        if kv != h:
+            raise ContractError("grouped-query attention needs the tcgen05 path (head_dim 128)")
+        call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(lse), n, h, head_dim, float(scale), _s())
     return o, lse
 
 
@@ -443,14 +456,21 @@ def flash_bwd(q, k, v, o, dout, lse, *, head_dim, scale, dq=None, dk=None, dv=No
     _check(q, k, v, o, dout, lse)
     n, h = q.shape
     dev = q.device
+    kv = k.shape[1]
     delta = torch.empty(h // head_dim, n, dtype=F32, device=dev)
     dq = torch.empty(n, h, dtype=F32, device=dev) if dq is None else dq
-    dk = torch.empty(n, h, dtype=F32, device=dev) if dk is None else dk
-    dv = torch.empty(n, h, dtype=F32, device=dev) if dv is None else dv
+    dk = torch.empty(n, kv, dtype=F32, device=dev) if dk is None else dk
+    dv = torch.empty(n, kv, dtype=F32, device=dev) if dv is None else dv
     if impl is None:
         impl = "tc" if head_dim == 128 else "mma"
     name = "lemo_flash_bwd_tc" if impl == "tc" else "lemo_flash_bwd"
     INSTRUMENT.note(name, n)
-    call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(delta), ptr(dq),
-         ptr(dk), ptr(dv), n, h, head_dim, float(scale), _s())
+    if impl == "tc":
+        call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(delta), ptr(dq),
+             ptr(dk), ptr(dv), n, h, kv, head_dim, float(scale), _s())
+    else:
+        if kv != h:
+            raise ContractError("grouped-query attention needs the tcgen05 path (head_dim 128)")
+        call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(delta), ptr(dq),
+             ptr(dk), ptr(dv), n, h, head_dim, float(scale), _s())
     return dq, dk, dv

@@ -388,10 +388,58 @@ def tune_case():
     (OUT / "tune.json").write_text(json.dumps({"init": ts.to_dict(), **out}, indent=1) + "\n")
 
 
+GQA_CFG = dict(n_layers=2, hidden_dim=512, n_heads=4, vocab_size=256, max_seq_len=512,
+               mlp_dim=344, block_size=16, lora_rank=8, lora_alpha=16.0)
+GQA_KV_HEADS = 2
+
+
+def gqa_case():
+    """Grouped-query attention is not in the reference; pin it through the
+    equivalent multi-head model: K/V (and LoRA B_v) head blocks repeated
+    `group` times.  The oracle's GQA model (seed 5) supplies the weights; the
+    reference runs the repeated MHA model; gradients of the repeated blocks
+    are folded back (summed) to the GQA shapes."""
+    sys.path.insert(0, str(OUT.parent.parent))
+    from oracle import lemo_oracle as O
+
+    om = O.init_model(O.Config(**GQA_CFG, n_kv_heads=GQA_KV_HEADS), seed=5)
+    O.perturb_lora_b(om, 6)
+    h, H = GQA_CFG["hidden_dim"], GQA_CFG["n_heads"]
+    d, g = h // H, H // GQA_KV_HEADS
+    rep = lambda w: np.concatenate([w[..., (hd // g) * d:(hd // g + 1) * d]  # noqa: E731
+                                    for hd in range(H)], axis=-1)
+    state = {"embed": om.embed, "final_norm": om.final_norm, "lm_head": om.lm_head}
+    for i, L in enumerate(om.layers):
+        p = f"layer{i}"
+        state.update({f"{p}.wq": L.wq, f"{p}.wk": rep(L.wk), f"{p}.wv": rep(L.wv),
+                      f"{p}.wo": L.wo, f"{p}.attn_norm": L.attn_norm, f"{p}.mlp_norm": L.mlp_norm,
+                      f"{p}.w_up": L.w_up, f"{p}.w_down": L.w_down, f"{p}.w_gate": L.w_gate,
+                      f"{p}.lora_q.a": L.lora_q[0], f"{p}.lora_q.b": L.lora_q[1],
+                      f"{p}.lora_v.a": L.lora_v[0], f"{p}.lora_v.b": rep(L.lora_v[1])})
+    rng = np.random.default_rng(8)
+    tokens = rng.integers(0, GQA_CFG["vocab_size"], size=300)
+    out = {"tokens": tokens}
+    for mode in ("dense", "fraction"):
+        m = model_mod.DecoderModel(model_mod.ModelConfig(**GQA_CFG), seed=0)
+        m.load_state_arrays({k: np.asarray(v, np.float32) for k, v in state.items()})
+        src = model_mod.FractionSource(0.5, 16) if mode == "fraction" else None
+        loss, _ = m.forward_step(tokens, segments=2, pattern_source=src)
+        T.backward(loss)
+        out[f"{mode}_loss"] = np.array(float(loss.data))
+        for name, gr in _grads(m).items():
+            if name.endswith("lora_v.b"):  # fold the repeated head blocks
+                gr = np.concatenate([sum(gr[:, hd * d:(hd + 1) * d]
+                                         for hd in range(kvh * g, (kvh + 1) * g))
+                                     for kvh in range(GQA_KV_HEADS)], axis=-1)
+            out[f"{mode}_grad__{name}"] = gr
+    np.savez_compressed(OUT / "step_gqa.npz", **out)
+    return {k: float(v) for k, v in out.items() if k.endswith("_loss")}
+
+
 CASES = {"select": select_cases, "quantile": quantile_cases, "colsum": column_sum_cases,
          "predictor": predictor_case, "scorers": scorer_cases, "steps": step_cases,
          "patterns": step_pattern_cases, "predictor_train": predictor_train_case,
-         "artifacts": artifact_case, "tune": tune_case}
+         "artifacts": artifact_case, "tune": tune_case, "gqa": gqa_case}
 
 
 def main():

@@ -338,3 +338,31 @@ def test_flash_bwd_tc_vs_torch(cuda, n, H):
         err = (got - ref).norm() / torch.maximum(ref.norm(), floor)
         assert err < 2e-2, (name, float(err))
 
+
+
+@pytest.mark.parametrize("n,H,Hkv", [(100, 4, 2), (257, 4, 1), (1000, 8, 2), (2049, 4, 4)])
+def test_flash_gqa_vs_torch(cuda, n, H, Hkv):
+    """Grouped-query attention on the tcgen05 kernels: fwd + bwd vs fp32 torch
+    on K/V heads repeated to the query heads (dK/dV summed over the group)."""
+    d = 128
+    g = torch.Generator(device=cuda).manual_seed(n + H)
+    h, kv = H * d, Hkv * d
+    q = torch.randn(n, h, device=cuda, generator=g).bfloat16()
+    k = torch.randn(n, kv, device=cuda, generator=g).bfloat16()
+    v = torch.randn(n, kv, device=cuda, generator=g).bfloat16()
+    o, lse = ops.flash_fwd(q, k, v, head_dim=d, scale=1 / math.sqrt(d))
+    rep = lambda t: t.view(n, Hkv, d).repeat_interleave(H // Hkv, dim=1).reshape(n, h)  # noqa
+    qr = q.float().requires_grad_(True)
+    kr = k.float().requires_grad_(True)
+    vr = v.float().requires_grad_(True)
+    oref, lref = _torch_attn(qr, rep(kr), rep(vr), H)
+    torch.testing.assert_close(o.float(), oref, rtol=2e-2, atol=2e-2)
+    torch.testing.assert_close(lse, lref, rtol=1e-3, atol=1e-3)
+    dout = torch.randn(n, h, device=cuda, generator=g).bfloat16()
+    oref.backward(dout.float())
+    dq, dk, dv = ops.flash_bwd(q, k, v, o, dout, lse, head_dim=d, scale=1 / math.sqrt(d))
+    assert dk.shape == (n, kv) and dv.shape == (n, kv)
+    floor = 1e-2 * dout.float().norm()
+    for name, got, ref in (("dq", dq, qr.grad), ("dk", dk, kr.grad), ("dv", dv, vr.grad)):
+        err = (got - ref).norm() / torch.maximum(ref.norm(), floor)
+        assert err < 2e-2, (name, float(err))

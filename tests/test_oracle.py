@@ -290,3 +290,26 @@ def test_quantile_lower_rule():
         a = rng.standard_normal(n)
         for q in (0.0, 0.1, 0.5, 0.999, 1.0):
             assert O.quantile_lower(a, q) == np.quantile(a, q, method="lower")
+
+
+def test_oracle_gqa_matches_reference_on_repeated_heads():
+    """GQA is an extension; the reference pins it through the equivalent MHA
+    model with repeated K/V (and LoRA B_v) head blocks (make_golden.gqa_case)."""
+    z = np.load(G / "step_gqa.npz")
+    cfg = dict(n_layers=2, hidden_dim=512, n_heads=4, vocab_size=256, max_seq_len=512,
+               mlp_dim=344, block_size=16, lora_rank=8, lora_alpha=16.0, n_kv_heads=2)
+    for mode in ("dense", "fraction"):
+        om = O.init_model(O.Config(**cfg), seed=5)
+        O.perturb_lora_b(om, 6)
+        src = None
+        if mode == "fraction":  # FractionSource(0.5, 16) on the padded 304 tokens
+            nb = O.n_blocks_for(304, 16)
+            keep = max(1, int(round(nb * 0.5)))
+            blocks = tuple(np.unique(np.linspace(0, nb - 1, keep).round().astype(int)).tolist())
+            src = O.FixedSource({(l, c): blocks for l in range(2) for c in (O.ATTENTION, O.MLP)})
+        ref = O.train_step(om, z["tokens"], source=src, segments=2)
+        assert abs(ref["loss"] - float(z[f"{mode}_loss"])) <= 1e-5 * abs(float(z[f"{mode}_loss"]))
+        for name, g in ref["grads"].items():
+            r = z[f"{mode}_grad__{name}"]
+            assert g.shape == r.shape, name
+            assert np.linalg.norm(g - r) <= 1e-4 * max(np.linalg.norm(r), 1e-30), name

@@ -165,3 +165,36 @@ def test_full_width_layer_vs_oracle(cuda, frac):
     assert abs(float(loss) - oref["loss"]) <= LOSS_RTOL * abs(oref["loss"])
     for name, g in model.adapter_grads().items():
         assert _rl2(g, oref["grads"][name]) <= GRAD_RL2, (name, _rl2(g, oref["grads"][name]))
+
+
+def _oracle_arrays(om):
+    arrays = {"embed": om.embed, "final_norm": om.final_norm, "lm_head": om.lm_head}
+    for i, L in enumerate(om.layers):
+        p = f"layer{i}"
+        arrays.update({f"{p}.wq": L.wq, f"{p}.wk": L.wk, f"{p}.wv": L.wv, f"{p}.wo": L.wo,
+                       f"{p}.attn_norm": L.attn_norm, f"{p}.mlp_norm": L.mlp_norm,
+                       f"{p}.w_up": L.w_up, f"{p}.w_down": L.w_down, f"{p}.w_gate": L.w_gate,
+                       f"{p}.lora_q.a": L.lora_q[0], f"{p}.lora_q.b": L.lora_q[1],
+                       f"{p}.lora_v.a": L.lora_v[0], f"{p}.lora_v.b": L.lora_v[1]})
+    return arrays
+
+
+@pytest.mark.parametrize("mode", ["dense", "fraction"])
+def test_gqa_step_matches_reference_repeated_heads(cuda, mode):
+    """Grouped-query attention (4 query heads over 2 key/value heads) vs the
+    reference run on the equivalent repeated-head MHA model (step_gqa.npz)."""
+    z = np.load(G / "step_gqa.npz")
+    cfg = dict(n_layers=2, hidden_dim=512, n_heads=4, vocab_size=256, max_seq_len=512,
+               mlp_dim=344, block_size=16, lora_rank=8, lora_alpha=16.0, n_kv_heads=2)
+    om = O.init_model(O.Config(**cfg), seed=5)
+    O.perturb_lora_b(om, 6)
+    model = M.DecoderModel(M.ModelConfig(**cfg), 0, arrays=_oracle_arrays(om))
+    src = M.FractionSource(0.5, 16) if mode == "fraction" else None
+    loss, _ = model.forward_step(z["tokens"], pattern_source=src, segments=2)
+    loss.backward()
+    ref_loss = float(z[f"{mode}_loss"])
+    assert abs(float(loss.detach()) - ref_loss) <= LOSS_RTOL * abs(ref_loss)
+    for name, g in model.adapter_grads().items():
+        ref = z[f"{mode}_grad__{name}"]
+        assert g.shape == ref.shape, name
+        assert _rl2(g, ref) <= GRAD_RL2, (name, _rl2(g, ref))
