@@ -243,56 +243,61 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int key = k0 + r;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     const uint32_t tSw = tS + lane_off + 64 * wg, tPw = tP + lane_off + 64 * wg;
+    // thread r stages one of this WG's 64 lse₂ (r < 64) or Δ values of tile u;
+    // the global load for u+1 is issued one phase ahead (latency hidden)
+    auto stage_val = [&](int u) {
+      const int q = k0 + (u % T) * kT + 64 * wg + (r & 63), hq = kvh * group + u / T;
+      return q < n ? (r < 64 ? lse[(size_t)hq * n + q] * kLog2e : delta[(size_t)hq * n + q])
+                   : 0.f;
+    };
+    float lv = stage_val(0);
     for (int u = 0; u < U; ++u) {
-      const int t = u % T, hq = kvh * group + u / T;  // query tile, query head
+      const int t = u % T;                   // query tile
       const int qw = k0 + t * kT + 64 * wg;  // first query of this WG's columns
       float* L = sLD + (wg * 2 + (u & 1)) * kT;
-      {
-        const int c = r & 63, q = qw + c;
-        L[r] = q < n ? (r < 64 ? lse[(size_t)hq * n + q] * kLog2e : delta[(size_t)hq * n + q])
-                     : 0.f;
-      }
+      L[r] = lv;
       named_bar_sync(1 + wg, 128);
       const bool edge = (t == 0) || (qw + 64 > n) || (key >= n);
       float p[64];
-      // phase A: Pᵀ
+      // phase A: Pᵀ (both 32-column halves in flight before one wait)
       mbar_wait(s_full, u & 1);
       tc_fence_after();
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        uint32_t raw[32];
-        tmem_ld_32x32b_x32(tSw + 32 * hf, raw);
+      {
+        uint32_t raw[64];
+        tmem_ld_32x32b_x32(tSw, *reinterpret_cast<uint32_t(*)[32]>(raw));
+        tmem_ld_32x32b_x32(tSw + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
         tmem_ld_wait();
-        float* ph = p + 32 * hf;
 #pragma unroll
-        for (int c = 0; c < 32; ++c)
-          ph[c] = ex2_approx(fmaf(__uint_as_float(raw[c]), sl2, -L[32 * hf + c]));
-        if (edge) {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int q = qw + 32 * hf + c;
-            if (key > q || q >= n || key >= n) ph[c] = 0.f;
-          }
-        }
-        st_bf16x32(tSw + 16 * hf, ph);  // packed half lands below the fp32 half still unread
+        for (int c = 0; c < 64; ++c)
+          p[c] = ex2_approx(fmaf(__uint_as_float(raw[c]), sl2, -L[c]));
       }
+      if (edge) {
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const int q = qw + c;
+          if (key > q || q >= n || key >= n) p[c] = 0.f;
+        }
+      }
+      st_bf16x32(tSw, p);        // packed halves over the (already read) fp32 columns
+      st_bf16x32(tSw + 16, p + 32);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+      if (u + 1 < U) lv = stage_val(u + 1);
       // phase B: dSᵀ
       mbar_wait(dp_full, u & 1);
       tc_fence_after();
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        uint32_t raw[32];
-        tmem_ld_32x32b_x32(tPw + 32 * hf, raw);
+      {
+        uint32_t raw[64];
+        tmem_ld_32x32b_x32(tPw, *reinterpret_cast<uint32_t(*)[32]>(raw));
+        tmem_ld_32x32b_x32(tPw + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
         tmem_ld_wait();
-        float* ph = p + 32 * hf;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) ph[c] *= (__uint_as_float(raw[c]) - L[64 + 32 * hf + c]);
-        st_bf16x32(tPw + 16 * hf, ph);
+        for (int c = 0; c < 64; ++c) p[c] *= (__uint_as_float(raw[c]) - L[64 + c]);
       }
+      st_bf16x32(tPw, p);
+      st_bf16x32(tPw + 16, p + 32);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -459,23 +464,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kw = j * kT + 64 * wg;  // first key of this WG's columns
       const bool edge = (j == qb) || (kw + 64 > n) || (qr >= n);
       float p[64];
-      // phase A: P (registers only)
+      // phase A: P (registers only; both halves in flight before one wait)
       mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        uint32_t raw[32];
-        tmem_ld_32x32b_x32(tmem + 128 * b + lane_off + 64 * wg + 32 * hf, raw);
+      {
+        uint32_t raw[64];
+        const uint32_t ts = tmem + 128 * b + lane_off + 64 * wg;
+        tmem_ld_32x32b_x32(ts, *reinterpret_cast<uint32_t(*)[32]>(raw));
+        tmem_ld_32x32b_x32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
         tmem_ld_wait();
-        float* ph = p + 32 * hf;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) ph[c] = ex2_approx(fmaf(__uint_as_float(raw[c]), sl2, -lse2));
-        if (edge) {
+        for (int c = 0; c < 64; ++c) p[c] = ex2_approx(fmaf(__uint_as_float(raw[c]), sl2, -lse2));
+      }
+      if (edge) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int key = kw + 32 * hf + c;
-            if (key > qr || key >= n || qr >= n) ph[c] = 0.f;
-          }
+        for (int c = 0; c < 64; ++c) {
+          const int key = kw + c;
+          if (key > qr || key >= n || qr >= n) p[c] = 0.f;
         }
       }
       tc_fence_before();
@@ -484,16 +489,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       // phase B: dS
       mbar_wait(dp_full, j & 1);
       tc_fence_after();
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        uint32_t raw[32];
-        tmem_ld_32x32b_x32(tPw + 32 * hf, raw);
+      {
+        uint32_t raw[64];
+        tmem_ld_32x32b_x32(tPw, *reinterpret_cast<uint32_t(*)[32]>(raw));
+        tmem_ld_32x32b_x32(tPw + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
         tmem_ld_wait();
-        float* ph = p + 32 * hf;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) ph[c] *= (__uint_as_float(raw[c]) - dl);
-        st_bf16x32(tPw + 16 * hf, ph);
+        for (int c = 0; c < 64; ++c) p[c] *= (__uint_as_float(raw[c]) - dl);
       }
+      st_bf16x32(tPw, p);
+      st_bf16x32(tPw + 16, p + 32);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();

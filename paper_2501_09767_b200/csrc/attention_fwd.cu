@@ -16,8 +16,9 @@
 // lazy (only when the running max grows by > 8 in log2 units) and need no
 // extra wait: when S_g(j) is complete, PV_g(j-1) is complete too.
 // Row max with 3-input FMNMX3, scaling and row sums with packed FFMA2/FADD2.
-// (Moving a share of the exponentials to an FMA-pipe polynomial, as
-// common.cuh:exp2_poly2 allows, measured slower here: 1/4 of them → −11 %.)
+// (Moving a share of the exponentials to an FMA-pipe degree-3 polynomial, the
+// FA4 trick, measured slower on this kernel and on the backward: 1/4 of them
+// → −11 % forward, −2 % backward — the SFU is not the binding limit here.)
 #include "gemm.cuh"
 #include "lemo_internal.h"
 

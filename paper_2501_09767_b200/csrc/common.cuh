@@ -98,28 +98,6 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return d;
 }
 
-// 2^x for a pair on the FMA pipe instead of the SFU (relieves MUFU, which
-// is the softmax bottleneck: 16 ex2/clk/SM against 8192 MMA flop/clk/SM):
-// x = j + f with j = rint(x) (magic-number rounding), f in [-1/2, 1/2],
-// 2^f by a degree-3 minimax polynomial (max rel. error 2.1e-4, well below
-// the bf16 rounding P gets before its MMA), 2^j added to the exponent field.
-// x is clamped at -125 (result >= 2^-125.5, i.e. ~0, never a denormal).
-__device__ __forceinline__ float2 exp2_poly2(float2 x) {
-  constexpr float kMagic = 12582912.f;  // 1.5 * 2^23
-  x.x = fmaxf(x.x, -125.f);
-  x.y = fmaxf(x.y, -125.f);
-  const float2 t = fadd2(x, make_float2(kMagic, kMagic));
-  const float2 r = fadd2(t, make_float2(-kMagic, -kMagic));
-  const float2 f = fsub2(x, r);
-  float2 p = ffma2(make_float2(0.05484800228f, 0.05484800228f), f,
-                   make_float2(0.24180660515f, 0.24180660515f));
-  p = ffma2(p, f, make_float2(0.69324819546f, 0.69324819546f));
-  p = ffma2(p, f, make_float2(0.99998865568f, 0.99998865568f));
-  // (bits(t) - bits(magic)) << 23 == bits(t) << 23 mod 2^32 (magic's low 9 bits are 0)
-  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
-                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
-}
-
 // Stable logistic, same branch structure as the reference sigmoid_np
 // (tensor.py:368-374); expf on the negative magnitude never overflows.
 __device__ __forceinline__ float sigmoid_stable(float x) {
