@@ -82,8 +82,11 @@ def lib():
 
 
 def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    """Raw cudaStream_t of `stream` (default: torch's current stream on the
+    current device) — the cheap C query, this runs once per launch."""
+    if stream is not None:
+        return int(stream.cuda_stream)
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def ptr(t) -> int | None:

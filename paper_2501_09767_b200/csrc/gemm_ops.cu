@@ -358,11 +358,26 @@ static int gemm(const void* A, int lda, const void* B, int ldb, int M, int N, in
   return launch_gemm_tn<BN>(A, lda, B, ldb, M, N, K, b, st);
 }
 
+// Tile width: the widest BN whose tile count still fills the 148 SMs (wide
+// tiles re-read A less and run the MMA at full rate; BN = 64 costs 48 instead
+// of 32 cycles per MMA but doubles the CTAs of small GEMMs such as the
+// predictor layers, Eq. 3 and the rank-r LoRA products).
+static int pick_bn(int M, int N) {
+  const int tm = (M + kBlockM - 1) / kBlockM;
+  if (N <= 64) return 64;
+  if (tm * ((N + 255) / 256) >= kNumSMs) return 256;
+  if (tm * ((N + 127) / 128) >= kNumSMs) return 128;
+  return 64;
+}
+
 template <class Epi>
 static int gemm_auto(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
                      const Epi& e, cudaStream_t st) {
-  if (N % 256 == 0 || N > 256) return gemm<256>(A, lda, B, ldb, M, N, K, e, st);
-  return gemm<128>(A, lda, B, ldb, M, N, K, e, st);
+  switch (pick_bn(M, N)) {
+    case 256: return gemm<256>(A, lda, B, ldb, M, N, K, e, st);
+    case 128: return gemm<128>(A, lda, B, ldb, M, N, K, e, st);
+    default: return gemm<64>(A, lda, B, ldb, M, N, K, e, st);
+  }
 }
 
 }  // namespace lemo
@@ -435,9 +450,10 @@ int lemo_gemm_split3(const void* A, int lda, const void* B, int ldb, int M, int 
                      float* f32, int ldf, void* stream) {
   LEMO_ARG_CHECK(K3 % 3 == 0, "lemo_gemm_split3: K' must be 3K");
   EpiSplit3 e{reinterpret_cast<__nv_bfloat16*>(out), ldo, f32, ldf, N, pattern, relu, mask};
-  // BN = 128: these GEMMs are small in M (n_blocks) — twice the CTAs of BN = 256
-  LEMO_RETURN_RC("lemo_gemm_split3",
-                 gemm<128>(A, lda, B, ldb, M, N, K3, e, (cudaStream_t)stream));
+  // small in M (n_blocks): BN = 128 or 64 so the grid fills the SMs
+  const int rc = pick_bn(M, N) == 64 ? gemm<64>(A, lda, B, ldb, M, N, K3, e, (cudaStream_t)stream)
+                                     : gemm<128>(A, lda, B, ldb, M, N, K3, e, (cudaStream_t)stream);
+  LEMO_RETURN_RC("lemo_gemm_split3", rc);
 }
 
 int lemo_gemm_dgateup(const void* dy, const void* w_down, int M, int m_pad, int h, const void* gu,
