@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-law", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N>1 (gloo only to smoke-test several "
+                         "ranks sharing one GPU)")
     ap.add_argument("--cpu-tokens", type=int, default=4096)
     ap.add_argument("--profile-tag", default="")
     return ap.parse_args()
@@ -193,11 +196,14 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     from paper_2501_09767_b200 import _lib, model as M, parallel, predictor as P, sparsity as S
     from paper_2501_09767_b200.optim import Adam
