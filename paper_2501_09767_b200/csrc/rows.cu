@@ -431,19 +431,41 @@ __global__ void __launch_bounds__(256) lora_grads_reduce_kernel(
 
 // Cross-entropy rows of segmented_loss_and_grad (kernels.py:256-273,
 // tensor.py:446-468): per row lse, loss term, and dlogits = (p - onehot)/count.
-__global__ void __launch_bounds__(256) ce_rows_kernel(const float* __restrict__ logits, int ldl,
+template <int kThreads>
+__device__ __forceinline__ float block_max(float v, float* red) {
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float m = red[0];
+#pragma unroll
+  for (int i = 1; i < kThreads / 32; ++i) m = fmaxf(m, red[i]);
+  __syncthreads();
+  return m;
+}
+
+// One CTA per row, float4 loads / 4-wide bf16 stores.  kSmem: the row is
+// read from HBM once into shared memory (V·4 bytes, e.g. 128 KB at V=32000)
+// and the max / exp-sum / dlogits passes run from there; otherwise (very
+// large vocabularies) the three passes re-read global memory.
+template <bool kSmem>
+__global__ void __launch_bounds__(512) ce_rows_kernel(const float* __restrict__ logits, int ldl,
                                                       const int* __restrict__ targets, int V,
                                                       int ignore, float inv_count,
                                                       __nv_bfloat16* __restrict__ dlogits, int ldd,
                                                       float* __restrict__ row_loss,
                                                       int* __restrict__ bad) {
-  __shared__ float red[8];
+  constexpr int kT = 512;
+  extern __shared__ __align__(16) float srow[];
+  __shared__ float red[kT / 32];
   const int row = blockIdx.x;
   const float* l = logits + (size_t)row * ldl;
   __nv_bfloat16* d = dlogits + (size_t)row * ldd;
+  const int V4 = V >> 2;  // host guarantees V, ldl, ldd multiples of 4
+  const float4* l4 = reinterpret_cast<const float4*>(l);
+  uint2* d4 = reinterpret_cast<uint2*>(d);
   const int t = targets[row];
   if (t == ignore) {
-    for (int c = threadIdx.x; c < V; c += blockDim.x) d[c] = __float2bfloat16_rn(0.f);
+    for (int c = threadIdx.x; c < V4; c += kT) d4[c] = make_uint2(0u, 0u);
     if (threadIdx.x == 0) row_loss[row] = 0.f;
     return;
   }
@@ -451,23 +473,32 @@ __global__ void __launch_bounds__(256) ce_rows_kernel(const float* __restrict__ 
     if (threadIdx.x == 0) atomicOr(bad, 1);
     return;
   }
+  const float4* src = kSmem ? reinterpret_cast<const float4*>(srow) : l4;
   float mx = -INFINITY;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) mx = fmaxf(mx, l[c]);
-  mx = warp_max(mx);
-  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-  if (ln == 0) red[w] = mx;
-  __syncthreads();
-  mx = red[0];
-#pragma unroll
-  for (int i = 1; i < 8; ++i) mx = fmaxf(mx, red[i]);
+  for (int c = threadIdx.x; c < V4; c += kT) {
+    const float4 v = l4[c];
+    if (kSmem) reinterpret_cast<float4*>(srow)[c] = v;
+    mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+  }
+  mx = block_max<kT>(mx, red);  // (its __syncthreads also publishes srow)
   float se = 0.f;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) se += expf(l[c] - mx);
-  se = block_sum<256>(se, red);
+  for (int c = threadIdx.x; c < V4; c += kT) {
+    const float4 v = src[c];
+    se += (expf(v.x - mx) + expf(v.y - mx)) + (expf(v.z - mx) + expf(v.w - mx));
+  }
+  se = block_sum<kT>(se, red);
   const float inv_se = 1.f / se;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) {
-    float p = expf(l[c] - mx) * inv_se;
-    if (c == t) p -= 1.f;
-    d[c] = __float2bfloat16_rn(p * inv_count);
+  for (int c = threadIdx.x; c < V4; c += kT) {
+    const float4 v = src[c];
+    float p0 = expf(v.x - mx) * inv_se, p1 = expf(v.y - mx) * inv_se;
+    float p2 = expf(v.z - mx) * inv_se, p3 = expf(v.w - mx) * inv_se;
+    const int c0 = 4 * c;
+    if (t == c0) p0 -= 1.f;
+    if (t == c0 + 1) p1 -= 1.f;
+    if (t == c0 + 2) p2 -= 1.f;
+    if (t == c0 + 3) p3 -= 1.f;
+    d4[c] = make_uint2(pack_bf16x2(p0 * inv_count, p1 * inv_count),
+                       pack_bf16x2(p2 * inv_count, p3 * inv_count));
   }
   if (threadIdx.x == 0) row_loss[row] = logf(se) + mx - l[t];
 }
@@ -700,9 +731,21 @@ int lemo_ce_rows(const float* logits, int ldl, const int* targets, int n, int V,
                  float inv_count, void* dlogits, int ldd, float* row_loss, int* bad,
                  void* stream) {
   if (n <= 0) return 0;
-  ce_rows_kernel<<<n, 256, 0, (cudaStream_t)stream>>>(logits, ldl, targets, V, ignore, inv_count,
-                                                      reinterpret_cast<__nv_bfloat16*>(dlogits),
-                                                      ldd, row_loss, bad);
+  LEMO_ARG_CHECK(V % 4 == 0 && ldl % 4 == 0 && ldd % 4 == 0,
+                 "lemo_ce_rows: V and the row strides must be multiples of 4");
+  cudaStream_t st = (cudaStream_t)stream;
+  auto* dl = reinterpret_cast<__nv_bfloat16*>(dlogits);
+  const size_t smem = (size_t)V * sizeof(float);
+  if (smem <= 200 * 1024) {
+    static int attr = cudaFuncSetAttribute(ce_rows_kernel<true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    (void)attr;
+    ce_rows_kernel<true><<<n, 512, smem, st>>>(logits, ldl, targets, V, ignore, inv_count, dl, ldd,
+                                               row_loss, bad);
+  } else {
+    ce_rows_kernel<false><<<n, 512, 0, st>>>(logits, ldl, targets, V, ignore, inv_count, dl, ldd,
+                                             row_loss, bad);
+  }
   LEMO_CHECK_LAUNCH("lemo_ce_rows");
   return 0;
 }
