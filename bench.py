@@ -253,11 +253,12 @@ def main():
     del prof, cal
     opt = Adam(model.lora_param, lr=1e-4)
 
+    if world > 1:  # the path's only exchange: per-layer LoRA-gradient buckets
+        model.grad_reducer = parallel.BucketedGradReducer()  # overlapped with backward (§8e)
+
     def step(src, batch, read_loss=False):
         loss, _ = model.forward_step(batch, pattern_source=src, segments=segments)
         loss.backward()
-        if world > 1:  # the path's only exchange: mean of the LoRA gradients (§8e)
-            parallel.allreduce_mean_(model.lora_param.grad)
         opt.step()
         opt.zero_grad()
         return float(loss.detach()) if read_loss else loss

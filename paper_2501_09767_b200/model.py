@@ -441,6 +441,9 @@ class DecoderModel:
         self.lora_param.requires_grad_(cfg.lora_rank > 0)
         self._mlp_scored = {}
         self.last_stats: dict = {}
+        # data parallelism: called with each layer's LoRA-gradient slice as soon
+        # as the backward sweep has finished it (parallel.BucketedGradReducer)
+        self.grad_reducer = None
 
     # -- parameters -------------------------------------------------------------
 
@@ -638,8 +641,14 @@ class _Step:
             if sa is not None:
                 kernels.attention_backward(dx, sa, layer, layer.grad_views(grad))
                 ledger.release_saved(led, sa)
+            if m.grad_reducer is not None and layer.lora_rank:
+                off = m._lora_offset(layer.layer_id)
+                m.grad_reducer.layer_ready(layer.layer_id,
+                                           grad[off:off + m._lora_offset(1)])
             self.saved.pop()
         self.saved = None
+        if m.grad_reducer is not None:
+            m.grad_reducer.finish()
         return grad
 
 
