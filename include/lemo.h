@@ -250,6 +250,10 @@ int lemo_relu_grad(float* dh, const float* h, long long n, void* stream);
 /* counts[c] += #{r : h[r, c] == 0} (zero-frequency tracking, predictor.py:76-80). */
 int lemo_zero_count(const float* h, int ldh, int M, int N, long long* counts, void* stream);
 
+/* Backward of the per-block row mean of token pooling (predictor.py:126-135):
+ * out [nb·b, w] rows i = g[i / b] / b. */
+int lemo_block_expand(const float* g, int nb, int w, int b, float* out, void* stream);
+
 /* *out = scale · Σ x (f64, fixed order). */
 int lemo_sum_d(const double* x, int n, double scale, double* out, void* stream);
 

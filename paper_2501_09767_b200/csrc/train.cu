@@ -84,6 +84,16 @@ __global__ void zero_count_kernel(const float* __restrict__ h, int ldh, int M, i
   counts[c] += z;
 }
 
+// Backward of the per-block row mean (token pooling, predictor.py:126-135):
+// out[i, :] = g[i / b, :] / b.
+__global__ void block_expand_kernel(const float* __restrict__ g, int w, int b,
+                                    float* __restrict__ out, long long total) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const long long row = e / w, c = e - row * w;
+  out[e] = g[(row / b) * w + c] / (float)b;
+}
+
 // out[slot] = Σ x (f64, one CTA, fixed order) — the per-record loss.
 __global__ void sum_d_kernel(const double* __restrict__ x, int n, double scale,
                              double* __restrict__ out) {
@@ -137,6 +147,15 @@ int lemo_zero_count(const float* h, int ldh, int M, int N, long long* counts, vo
   if (M <= 0 || N <= 0) return 0;
   zero_count_kernel<<<(N + 127) / 128, 128, 0, (cudaStream_t)stream>>>(h, ldh, M, N, counts);
   LEMO_CHECK_LAUNCH("lemo_zero_count");
+  return 0;
+}
+
+int lemo_block_expand(const float* g, int nb, int w, int b, float* out, void* stream) {
+  const long long total = (long long)nb * b * w;
+  if (total <= 0) return 0;
+  block_expand_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      g, w, b, out, total);
+  LEMO_CHECK_LAUNCH("lemo_block_expand");
   return 0;
 }
 

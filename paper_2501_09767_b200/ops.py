@@ -352,6 +352,16 @@ def relu_grad(dh, h):
     return dh
 
 
+def block_expand(g, b, out=None):
+    """[nb, w] -> [nb·b, w], rows repeated b times and divided by b."""
+    _check(g, out)
+    nb, w = g.shape
+    if out is None:
+        out = torch.empty(nb * b, w, dtype=F32, device=g.device)
+    call("lemo_block_expand", ptr(g), nb, w, b, ptr(out), _s())
+    return out
+
+
 def zero_count(h, counts):
     """counts[c] += #zeros in column c of h [M, N] (int64 counts)."""
     _check(h, counts)

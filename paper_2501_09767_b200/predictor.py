@@ -439,8 +439,8 @@ def fit_predictors(pairs: dict, train_data: list, *, epochs: int, lr: float, val
     reduced on device and read back once per epoch."""
     if not train_data:
         raise ContractError("no teacher records to train on")
-    if pooling != "mean":
-        raise ContractError("GPU predictor training implements pooling='mean' (the default)")
+    if pooling not in ("mean", "token"):
+        raise ContractError(f"unknown pooling mode {pooling!r}")
     opt = _PairAdam(pairs, lr)
     labels = [_teacher_label(rec, log_scale) for rec in train_data]
     grads = {}
@@ -456,9 +456,19 @@ def fit_predictors(pairs: dict, train_data: list, *, epochs: int, lr: float, val
             opt.lr = lr * (0.02 + 0.98 * 0.5 * (1.0 + math.cos(math.pi * (epoch - 1) / epochs)))
         for i, rec in enumerate(train_data):
             p_q, p_k = pairs[rec.layer_id]
-            xb = block_embed(rec.x, rec.block_size)
-            eq, saved_q = p_q.forward_train(xb, track=True)
-            ek, saved_k = p_k.forward_train(xb, track=True)
+            b = rec.block_size
+            if pooling == "mean":  # pool tokens, then predict (predictor.py:165-167)
+                xb = block_embed(rec.x, b)
+                eq, saved_q = p_q.forward_train(xb, track=True)
+                ek, saved_k = p_k.forward_train(xb, track=True)
+            else:  # predict per token, then block means (predictor.py:168-172)
+                xt = _dev_f32(rec.x, p_q.w1.device)
+                if xt.shape[0] % b:
+                    raise ContractError(f"sequence length {xt.shape[0]} not a multiple of "
+                                        "block size")
+                oq, saved_q = p_q.forward_train(xt, track=True)
+                ok, saved_k = p_k.forward_train(xt, track=True)
+                eq, ek = ops.block_embed(oq, b), ops.block_embed(ok, b)
             full = ops.gemm_split3(ops.split_bf16x3(eq, 0), ops.split_bf16x3(ek, 1),
                                    split_out=False, f32_out=True)[1]
             _, dfull = ops.tril_mse(full, labels[i], loss=losses[i:i + 1])
@@ -467,6 +477,8 @@ def fit_predictors(pairs: dict, train_data: list, *, epochs: int, lr: float, val
                                    split_out=False, f32_out=True)[1]
             d_ek = ops.gemm_split3(ops.split_bf16x3_t(dfull, 0), ops.split_bf16x3_t(eq, 1),
                                    split_out=False, f32_out=True)[1]
+            if pooling == "token":
+                d_eq, d_ek = ops.block_expand(d_eq, b), ops.block_expand(d_ek, b)
             p_q.backward_train(d_eq, saved_q, grads[id(p_q)])
             p_k.backward_train(d_ek, saved_k, grads[id(p_k)])
             opt.step([(p_q, grads[id(p_q)]), (p_k, grads[id(p_k)])])

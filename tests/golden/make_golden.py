@@ -286,7 +286,7 @@ def step_pattern_cases():
     return out
 
 
-def predictor_train_case():
+def predictor_train_case(pooling="mean"):
     """fit_predictors (predictor.py:366-433) on fixed teacher records: per-epoch
     losses / recall / active params and the final weights, masks, counters."""
     rng = np.random.default_rng(77)
@@ -307,7 +307,8 @@ def predictor_train_case():
         arrays[f"teacher_{i}"] = teacher
         arrays[f"layer_{i}"] = np.array([l])
     hist = pred_mod.fit_predictors(pairs, records, epochs=6, lr=1e-2, val_data=records,
-                                   prune_target=0.6, prune_every=2, prune_step=0.2, eval_every=3)
+                                   prune_target=0.6, prune_every=2, prune_step=0.2, eval_every=3,
+                                   pooling=pooling)
     arrays.update(init)
     arrays["loss"] = np.array([hr.train_loss for hr in hist])
     arrays["recall"] = np.array([hr.recall for hr in hist])
@@ -316,7 +317,8 @@ def predictor_train_case():
         for p in pq:
             for n, a in p.state_arrays().items():
                 arrays[f"final_{l}_{p.role}_{n}"] = a
-    np.savez_compressed(OUT / "predictor_train.npz", **arrays)
+    suffix = "" if pooling == "mean" else "_" + pooling
+    np.savez_compressed(OUT / f"predictor_train{suffix}.npz", **arrays)
     return arrays["loss"].tolist()
 
 
@@ -439,6 +441,7 @@ def gqa_case():
 CASES = {"select": select_cases, "quantile": quantile_cases, "colsum": column_sum_cases,
          "predictor": predictor_case, "scorers": scorer_cases, "steps": step_cases,
          "patterns": step_pattern_cases, "predictor_train": predictor_train_case,
+         "predictor_train_token": lambda: predictor_train_case("token"),
          "artifacts": artifact_case, "tune": tune_case, "gqa": gqa_case}
 
 

@@ -26,8 +26,9 @@ def _rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-def test_fit_predictors_matches_reference(cuda):
-    z = np.load(G / "predictor_train.npz")
+@pytest.mark.parametrize("pooling", ["mean", "token"])
+def test_fit_predictors_matches_reference(cuda, pooling):
+    z = np.load(G / ("predictor_train.npz" if pooling == "mean" else f"predictor_train_{pooling}.npz"))
     pairs = {}
     for l in range(2):
         pair = []
@@ -42,7 +43,8 @@ def test_fit_predictors_matches_reference(cuda):
                                        torch.as_tensor(z[f"x_{i}"]).to(cuda),
                                        torch.as_tensor(z[f"teacher_{i}"]).to(cuda), 128, 8))
     hist = P.fit_predictors(pairs, records, epochs=6, lr=1e-2, val_data=records,
-                            prune_target=0.6, prune_every=2, prune_step=0.2, eval_every=3)
+                            prune_target=0.6, prune_every=2, prune_step=0.2, eval_every=3,
+                            pooling=pooling)
     loss = np.array([h.train_loss for h in hist])
     assert np.allclose(loss, z["loss"], rtol=1e-3, atol=0), (loss, z["loss"])
     assert [h.param_count for h in hist] == z["params"].tolist()
