@@ -134,22 +134,32 @@ class Clocks:
 # reference arm: the reference algorithm (oracle restatement) on host cores
 
 
+def cpu_geometry(cfg) -> dict:
+    """Oracle CpuSample geometry of a ModelConfig (same widths as the GPU run)."""
+    return dict(hidden=cfg.hidden_dim, heads=cfg.n_heads, kv_heads=cfg.kv_heads,
+                mlp=cfg.mlp_dim, vocab=cfg.vocab_size, n_layers_model=cfg.n_layers,
+                block=cfg.block_size, lora_rank=cfg.lora_rank, mlp_variant=cfg.mlp_variant,
+                positions=cfg.positions)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from oracle.cpu_sample import CpuSample, host_cores
+    from paper_2501_09767_b200 import model as M
 
     wl = CONFIGS[args.config]
     cores = host_cores()
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    sample = CpuSample(sample_tokens=min(args.cpu_tokens, wl["seq"]))
+    mcfg = getattr(M, wl["model"])(max_seq_len=wl["seq"])
+    sample = CpuSample(sample_tokens=min(args.cpu_tokens, wl["seq"]), **cpu_geometry(mcfg))
     for _ in range(args.warmup):
         sample.time_step()
     t_head = sample.time_head()
     times = [sample.time_step()[0] for _ in range(args.steps)]
     t_layer = max(float(np.median(times)) - t_head, 1e-9)
-    per_step = 32 * t_layer + t_head
+    per_step = mcfg.n_layers * t_layer + t_head
     value = sample.s / per_step
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
@@ -159,9 +169,9 @@ def run_reference(args):
         "config": {"workload": f"{args.config}: {wl['name']} LoRA+LeMo predicted mode",
                    "seq_len": wl["seq"], "parallelism": "cpu"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle restatement, 1 decoder layer at h=4096 on {sample.s} "
-                                   "tokens fwd+bwd (+LM head timed separately), extrapolated to "
-                                   "32 layers"},
+                         "sample": f"oracle restatement, 1 decoder layer at h={mcfg.hidden_dim} "
+                                   f"on {sample.s} tokens fwd+bwd (+LM head timed separately), "
+                                   f"extrapolated to {mcfg.n_layers} layers"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -286,6 +296,8 @@ def main():
             dist.barrier()
         return ms
 
+    wbytes = sum(t.numel() * t.element_size() for L in model.layers
+                 for t in (L.w_qkv_t, L.w_gu_t, L.w_down_t, L.w_o_t))
     staged = model.stage_tokens(tokens)
     for _ in range(args.warmup):
         step(source, staged)
@@ -405,13 +417,13 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             from oracle.cpu_sample import CpuSample, host_cores
-            cs = CpuSample(sample_tokens=min(args.cpu_tokens, seq))
+            cs = CpuSample(sample_tokens=min(args.cpu_tokens, seq), **cpu_geometry(cfg))
             meas = cs.measure()
             cpu = {"value": meas["tokens_per_s"], "unit": "tokens/s", "cores": host_cores(),
                    "kind": "port",
-                   "sample": f"oracle restatement of the reference, 1 Llama2-7B-width decoder "
-                             f"layer on {cs.s} tokens fwd+bwd in LeMo predicted mode (+LM head "
-                             f"timed separately), extrapolated to 32 layers "
+                   "sample": f"oracle restatement of the reference, 1 {wl['name']}-width "
+                             f"decoder layer on {cs.s} tokens fwd+bwd in LeMo predicted mode (+LM "
+                             f"head timed separately), extrapolated to {cfg.n_layers} layers "
                              f"(t_layer={meas['t_layer_s']:.2f}s, t_head={meas['t_head_s']:.2f}s)"}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "tokens/s", "cores": None, "kind": "port",
@@ -428,7 +440,9 @@ def main():
         "data": "synthetic tokens, random-init weights",
         "config": {"workload": f"{args.config}: {wl['name']} LoRA(r=8,q/v)+LeMo predicted patterns",
                    "model": wl["model"], "global_batch": world, "seq_len": seq,
-                   "parallelism": f"dp{world}", "l2": "inputs/weights larger than L2 (no flush)",
+                   "parallelism": f"dp{world}",
+                   "l2": "weights + activations far larger than the 126 MB L2 (no flush)"
+                   if wbytes > 126e6 else "fits in L2 (tiny model: launch-bound, no flush)",
                    "segments": segments, "block_size": cfg.block_size,
                    "target_retention": 0.5},
         "activation_gb_post_forward": act_gb,

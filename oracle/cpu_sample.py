@@ -5,8 +5,9 @@ TEST/BENCH INFRASTRUCTURE ONLY (the cpu_baseline leg of bench.py and its
 the GPU box, so its algorithm runs here through the oracle restatement
 (oracle/lemo_oracle.py, pinned to reference outputs by tests/test_oracle.py).
 
-Sample: one decoder layer at the workload's full width (Llama2-7B: h=4096,
-32 heads, m=11008, V=32000, LoRA r=8) on `sample_tokens` tokens, trained one
+Sample: one decoder layer at the workload's full width (default Llama2-7B:
+h=4096, 32 heads, m=11008, V=32000, LoRA r=8; bench.py passes the geometry of
+the configuration it runs) on `sample_tokens` tokens, trained one
 step in LeMo predicted mode (random predictors r1=r2=d_p=h/4, attention
 retention 0.5 by the quantile rule, MLP threshold = pooled mean of the
 exact MLP scores), forward + backward.  The LM-head/loss cost is timed
@@ -25,12 +26,17 @@ from . import lemo_oracle as O
 
 class CpuSample:
     def __init__(self, *, hidden=4096, heads=32, mlp=11008, vocab=32000, n_layers_model=32,
-                 sample_tokens=4096, block=16, lora_rank=8, seed=0):
+                 sample_tokens=4096, block=16, lora_rank=8, seed=0, kv_heads=0,
+                 mlp_variant="silu", positions="rope"):
         self.n_layers_model = n_layers_model
         self.s = sample_tokens
+        self.geometry = dict(hidden=hidden, heads=heads, kv_heads=kv_heads or heads, mlp=mlp,
+                             vocab=vocab, layers=n_layers_model, mlp_variant=mlp_variant,
+                             positions=positions)
         cfg = O.Config(n_layers=1, hidden_dim=hidden, n_heads=heads, vocab_size=vocab,
                        max_seq_len=sample_tokens, mlp_dim=mlp, block_size=block,
-                       lora_rank=lora_rank, lora_alpha=2.0 * lora_rank)
+                       lora_rank=lora_rank, lora_alpha=2.0 * lora_rank, n_kv_heads=kv_heads,
+                       mlp_variant=mlp_variant, positions=positions)
         self.model = O.init_model(cfg, seed=seed, fast=True)
         rng = np.random.default_rng(seed + 1)
         L = self.model.layers[0]
