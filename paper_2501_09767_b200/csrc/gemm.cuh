@@ -194,6 +194,152 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 // --------------------------------------------------------------------------
+// CTA-pair variant (cluster of 2, tcgen05 cta_group::2): one 256 x 256 output
+// tile per pair; each CTA stages its 128-row half of the A tile and its
+// 128-row half of the B tile (so per-SM operand traffic per FLOP drops by a
+// third versus the 128 x 256 single-CTA tile), the leader CTA issues
+// M256·N256·K16 MMAs that read both CTAs' smem and write each CTA's 128
+// accumulator lanes; both CTAs' epilogues drain their own TMEM.
+//   full[s]  (leader) : leader's expect_tx + the peer's remote arrive, TMA
+//                       bytes of both CTAs
+//   empty[s] (both)   : multicast commit
+//   tfull[a] (both)   : multicast commit;  tempty[a] (leader): 16 epilogue warps
+
+constexpr int kStagesPair = 6;
+constexpr int kSmemPair = kStagesPair * 2 * kBlockM * kBlockK * 2 + 1024 + 256;
+
+template <class Epi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm_tn_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, int M, int N, int K, Epi epi) {
+  constexpr int BN = 256;
+  constexpr int kHalf = kBlockM * kBlockK * 2;  // one 128 x 64 bf16 box = 16 KB
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + kStagesPair * kHalf;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kStagesPair * kHalf);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + kStagesPair;
+  uint64_t* tfull_bar = bars + 2 * kStagesPair;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int num_m = (M + 2 * kBlockM - 1) / (2 * kBlockM);  // 256-row tiles
+  const int num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (K + kBlockK - 1) / kBlockK;
+  const int cid = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kStagesPair; ++s) {
+      mbar_init(&full_bar[s], 2);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 16);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);  // the leader's barriers
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < num_tiles; t += nclusters) {
+        const TileCoord tc = tile_coord(t, num_m, num_n);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          const uint32_t fb = full0 + stage * 8;
+          if (leader)
+            mbar_arrive_expect_tx(&full_bar[stage], 4 * kHalf);
+          else
+            mbar_arrive_cluster(fb);
+          tma_load_2d_pair(&tmA, fb, smem_a + stage * kHalf, kb * kBlockK,
+                           tc.m * 2 * kBlockM + (int)rank * kBlockM);
+          tma_load_2d_pair(&tmB, fb, smem_b + stage * kHalf, kb * kBlockK,
+                           tc.n * BN + (int)rank * kBlockM);
+          if (++stage == kStagesPair) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * kBlockM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = cid; t < num_tiles; t += nclusters, ++local) {
+        const int acc = local & 1;
+        mbar_wait(&tempty_bar[acc], ((local >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(smem_a + stage * kHalf);
+            const uint32_t b_addr = smem_u32(smem_b + stage * kHalf);
+#pragma unroll
+            for (int k = 0; k < kBlockK / kUmmaK; ++k)
+              umma_bf16_ss_pair(d_tmem, umma_desc_k_sw128(a_addr + k * kUmmaK * 2),
+                                umma_desc_k_sw128(b_addr + k * kUmmaK * 2), idesc,
+                                (kb | k) != 0 ? 1u : 0u);
+            umma_commit_pair(&empty_bar[stage]);
+            if (kb == num_kb - 1) umma_commit_pair(&tfull_bar[acc]);
+          }
+          __syncwarp();
+          if (++stage == kStagesPair) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int wq = warp & 3;
+    const int part = (warp - 4) >> 2;
+    const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
+    int local = 0;
+    for (int t = cid; t < num_tiles; t += nclusters, ++local) {
+      const TileCoord tc = tile_coord(t, num_m, num_n);
+      const int acc = local & 1;
+      mbar_wait(&tfull_bar[acc], (local >> 1) & 1);
+      tc_fence_after();
+      const int row = tc.m * 2 * kBlockM + (int)rank * kBlockM + wq * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
+      epi(row, row < M, tc.n * BN, taddr, part);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem_base);
+  }
+}
+
+// --------------------------------------------------------------------------
 // host side
 
 struct GemmShape {
@@ -232,6 +378,30 @@ int launch_gemm_tn(const void* A, int lda, const void* B, int ldb, int M, int N,
   const int grid = tiles < gemm_num_sms() ? tiles : gemm_num_sms();
   gemm_tn_kernel<BN, Epi, kBMN><<<grid, kGemmThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K,
                                                                                epi);
+  return (int)cudaGetLastError();
+}
+
+// Pair-tile launch (BN = 256, non-transposed B): grid = 2 x (tiles capped at
+// half the SMs), cluster dims fixed by __cluster_dims__.
+template <class Epi>
+int launch_gemm_tn_pair(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
+                        const Epi& epi, cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return 0;
+  CUtensorMap ta, tb;
+  int rc = make_tma_bf16_2d(&ta, A, (uint64_t)M, (uint64_t)K, (uint64_t)lda, kBlockM);
+  if (!rc) rc = make_tma_bf16_2d(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, kBlockM);
+  if (rc) return rc;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tn_pair_kernel<Epi>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemPair);
+    if (e != cudaSuccess) return (int)e;
+    attr_set = true;
+  }
+  const int tiles = ((M + 2 * kBlockM - 1) / (2 * kBlockM)) * ((N + 255) / 256);
+  const int pairs = gemm_num_sms() / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  gemm_tn_pair_kernel<Epi><<<grid, kGemmThreads, kSmemPair, stream>>>(ta, tb, M, N, K, epi);
   return (int)cudaGetLastError();
 }
 

@@ -16,6 +16,7 @@
 // 32q..32q+31 (= output rows) and the `part`-th half of the tile's columns.
 #include "gemm.cuh"
 #include "lemo_internal.h"
+#include <cstdlib>
 
 namespace lemo {
 
@@ -351,10 +352,20 @@ struct Bound {
   }
 };
 
+// BN = 256 GEMMs run as CTA pairs (256 x 256 tiles) when M spans at least two
+// row tiles; LEMO_GEMM_PAIR=0 forces the single-CTA kernel (A/B comparisons).
+static bool use_pair(int M) {
+  static const int env = getenv("LEMO_GEMM_PAIR") ? atoi(getenv("LEMO_GEMM_PAIR")) : 1;
+  return env != 0 && M > kBlockM;
+}
+
 template <int BN, class Epi>
 static int gemm(const void* A, int lda, const void* B, int ldb, int M, int N, int K, const Epi& e,
                 cudaStream_t st) {
   Bound<BN, Epi> b{e};
+  if constexpr (BN == 256) {
+    if (use_pair(M)) return launch_gemm_tn_pair(A, lda, B, ldb, M, N, K, b, st);
+  }
   return launch_gemm_tn<BN>(A, lda, B, ldb, M, N, K, b, st);
 }
 
@@ -363,6 +374,8 @@ static int gemm(const void* A, int lda, const void* B, int ldb, int M, int N, in
 // of 32 cycles per MMA but doubles the CTAs of small GEMMs such as the
 // predictor layers, Eq. 3 and the rank-r LoRA products).
 static int pick_bn(int M, int N) {
+  static const int forced = getenv("LEMO_GEMM_BN") ? atoi(getenv("LEMO_GEMM_BN")) : 0;
+  if (forced) return forced;
   const int tm = (M + kBlockM - 1) / kBlockM;
   if (N <= 64) return 64;
   if (tm * ((N + 255) / 256) >= kNumSMs) return 256;

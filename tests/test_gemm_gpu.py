@@ -28,7 +28,8 @@ def test_gemm_bf16(cuda, M, N, K):
 
 
 @pytest.mark.parametrize("M,N,K,acc", [(256, 512, 256, True), (333, 250, 512, False),
-                                       (128, 4096, 4096, True), (1024, 10, 3072, False)])
+                                       (128, 4096, 4096, True), (1024, 10, 3072, False),
+                                       (2085, 2560, 320, True), (4099, 4096, 1088, False)])
 def test_gemm_f32(cuda, M, N, K, acc):
     g = torch.Generator(device=cuda).manual_seed(3)
     a = torch.randn(M, K, device=cuda, generator=g).bfloat16()
@@ -42,11 +43,12 @@ def test_gemm_f32(cuda, M, N, K, acc):
     assert err <= 1e-3 * ref.abs().max().item() + 1e-3
 
 
-def test_gemm_scatter_add(cuda):
+@pytest.mark.parametrize("s,h,K,k", [(1024, 512, 256, 400), (8192, 4096, 512, 4111)])
+def test_gemm_scatter_add(cuda, s, h, K, k):
+    """(the second case runs as 256 x 256 CTA-pair tiles)"""
     g = torch.Generator(device=cuda).manual_seed(5)
-    s, h, K = 1024, 512, 256
-    idx = torch.randperm(s, device=cuda, generator=g)[:400].sort().values.int()
-    a = torch.randn(400, K, device=cuda, generator=g).bfloat16()
+    idx = torch.randperm(s, device=cuda, generator=g)[:k].sort().values.int()
+    a = torch.randn(k, K, device=cuda, generator=g).bfloat16()
     b = torch.randn(h, K, device=cuda, generator=g).bfloat16()
     resid = torch.randn(s, h, device=cuda, generator=g)
     ref = resid.clone()
