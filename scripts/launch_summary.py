@@ -6,6 +6,9 @@ def short(name):
     m = re.search(r"gemm_tn_kernel<(\d+), lemo::Bound<\d+, lemo::(\w+)>", name)
     if m:
         return f"gemm_tn_kernel<{m.group(1)},{m.group(2)}>"
+    m = re.search(r"gemm_tn_pair_kernel<(?:lemo::)?Bound<256, (?:lemo::)?(\w+)>", name)
+    if m:
+        return f"gemm_tn_pair_kernel<{m.group(1)}> (256x256 CTA pair)"
     name = re.sub(r"\(.*", "", name)
     name = re.sub(r"^void ", "", name)
     return name.replace("lemo::fa::", "").replace("lemo::", "")
