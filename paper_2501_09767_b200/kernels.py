@@ -28,6 +28,7 @@ reference's value semantics (they return a new tensor).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -143,9 +144,25 @@ def attention_forward(x: torch.Tensor, plan: GatherPlan, layer, *, save: bool = 
     return dict(idx=idx, xg=xg, inv=inv, t=t, q=q, k=kk, v=v, o=o, lse=lse)
 
 
-def attention_backward(dx: torch.Tensor, saved: dict, layer, grads) -> None:
+_SIDE: dict = {}
+_SERIAL = os.environ.get("LEMO_SERIAL_LORA_GRADS", "0") == "1"  # A/B switch
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    """Per-device side stream for the memory-bound LoRA weight-gradient kernel,
+    which then runs under the compute-bound dX GEMM of the same layer."""
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=dev)
+    return _SIDE[key]
+
+
+def attention_backward(dx: torch.Tensor, saved: dict, layer, grads):
     """dx[idx] += d(attention block)/dx (in place); LoRA grads accumulated
-    into grads = (dA_qv, dBq, dBv) views of the flat gradient buffer."""
+    into grads = (dA_qv, dBq, dBv) views of the flat gradient buffer.  The
+    LoRA-gradient kernel runs on a side stream, overlapping the dX GEMM;
+    returns the event the caller must wait on before reading `grads`
+    (None when there is nothing pending)."""
     idx = saved["idx"]
     k, h = idx.shape[0], dx.shape[1]
     dev = dx.device
@@ -159,15 +176,28 @@ def attention_backward(dx: torch.Tensor, saved: dict, layer, grads) -> None:
     dqkv = torch.empty(k, layer.w_qkv.shape[1], dtype=BF16, device=dev)  # [dq|dk|dv|LoRA ext]
     ops.qkv_grad_prep(dq, dk, dv, head_dim=layer.head_dim, rope=layer.rope,
                       rope_tab=layer.rope_tab, pos=idx, dqkv=dqkv)
+    done = None
     if r:
         u = layer.qkv_grad_input(dqkv)
-        if grads is not None:
+        if grads is not None and not _SERIAL:
+            dA, dBq, dBv = grads
+            side = _side_stream(dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                ops.lora_grads(saved["xg"], saved["inv"], layer.attn_norm_w, saved["t"], u, dq,
+                               dv, r=r, scale=layer.lora_scaling, dA=dA, dB0=dBq, dB1=dBv)
+                done = torch.cuda.Event()
+                done.record(side)
+            for t in (saved["xg"], saved["inv"], saved["t"], u, dq, dv):
+                t.record_stream(side)  # allocator: in use on the side stream
+        elif grads is not None:
             dA, dBq, dBv = grads
             ops.lora_grads(saved["xg"], saved["inv"], layer.attn_norm_w, saved["t"], u, dq, dv,
                            r=r, scale=layer.lora_scaling, dA=dA, dB0=dBq, dB1=dBv)
     del dq, dk, dv
     dxn = ops.gemm_f32(dqkv, layer.w_qkv)  # LoRA term inside the K-extension
     ops.rmsnorm_bwd(dxn, saved["xg"], saved["inv"], layer.attn_norm_w, dx, idx, accumulate=True)
+    return done
 
 
 # ---------------------------------------------------------------------------

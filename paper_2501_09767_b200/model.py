@@ -634,18 +634,27 @@ class _Step:
         ledger.release_saved(led, {"x": self.x, "inv_f": self.inv_f,
                                    "grad_hidden": self.grad_hidden})
         self.grad_hidden = self.x = self.inv_f = None
+        main = torch.cuda.current_stream(m.device)
+        pending = []  # LoRA-gradient kernels still running on the side stream
         for layer, (sa, sm) in zip(reversed(m.layers), reversed(self.saved)):
             if sm is not None:
                 kernels.mlp_backward(dx, sm, layer)
                 ledger.release_saved(led, sm)
             if sa is not None:
-                kernels.attention_backward(dx, sa, layer, layer.grad_views(grad))
+                ev = kernels.attention_backward(dx, sa, layer, layer.grad_views(grad))
+                if ev is not None:
+                    pending.append(ev)
                 ledger.release_saved(led, sa)
             if m.grad_reducer is not None and layer.lora_rank:
+                for ev in pending:  # this layer's bucket must be final before it is reduced
+                    main.wait_event(ev)
+                pending = []
                 off = m._lora_offset(layer.layer_id)
                 m.grad_reducer.layer_ready(layer.layer_id,
                                            grad[off:off + m._lora_offset(1)])
             self.saved.pop()
+        for ev in pending:
+            main.wait_event(ev)
         self.saved = None
         if m.grad_reducer is not None:
             m.grad_reducer.finish()
