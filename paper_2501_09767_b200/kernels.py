@@ -310,8 +310,10 @@ class _SparseBlock(torch.autograd.Function):
         dlora = torch.zeros(ctx.lora_shape, dtype=F32, device=dx.device)
         if ctx.saved_state is not None:
             if ctx.kind == "attention":
-                attention_backward(dx, ctx.saved_state, ctx.layer,
-                                   ctx.layer.grad_views(dlora))
+                ev = attention_backward(dx, ctx.saved_state, ctx.layer,
+                                        ctx.layer.grad_views(dlora))
+                if ev is not None:  # side-stream LoRA gradients must land first
+                    torch.cuda.current_stream(dx.device).wait_event(ev)
             else:
                 mlp_backward(dx, ctx.saved_state, ctx.layer)
         ctx.saved_state = None
