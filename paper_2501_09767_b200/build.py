@@ -20,7 +20,7 @@ OBJ = PKG / "_build"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
-         "-Xptxas", "-warn-spills"]
+         "-Xptxas", "-warn-spills"] + os.environ.get("LEMO_EXTRA_NVCC_FLAGS", "").split()
 
 
 def _nvcc() -> str:

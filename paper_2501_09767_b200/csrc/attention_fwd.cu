@@ -15,12 +15,23 @@
 // reads them because tcgen05.mma executes in issue order.  O rescales are
 // lazy (only when the running max grows by > 8 in log2 units) and need no
 // extra wait: when S_g(j) is complete, PV_g(j-1) is complete too.
+// Measured timeline (scripts/fa_trace.py, 8K rows): softmax of a 128-key tile
+// ≈ 1850 clk per warpgroup, then ≈ 1630 clk until the next S is ready (PV + S
+// on the tensor core ≈ 1024 + issue/commit latency ≈ 600): the loop is bound
+// by E + L + 1024 per warpgroup; the softmax is MUFU/issue-bound, and both a
+// speculative-max pass and FMA-pipe exponentials measured slower.
 // Row max with 3-input FMNMX3, scaling and row sums with packed FFMA2/FADD2.
 // (Moving a share of the exponentials to an FMA-pipe degree-3 polynomial, the
 // FA4 trick, measured slower on this kernel and on the backward: 1/4 of them
 // → −11 % forward, −2 % backward — the SFU is not the binding limit here.)
 #include "gemm.cuh"
 #include "lemo_internal.h"
+
+#ifdef LEMO_FA_TRACE
+// debug builds only (LEMO_EXTRA_NVCC_FLAGS=-DLEMO_FA_TRACE, scripts/fa_trace.py):
+// per-iteration timestamps of the heaviest CTA's softmax warpgroups
+__device__ unsigned long long g_fa_trace[2][4][64];  // [wg][event][iteration]
+#endif
 
 namespace lemo {
 namespace faf {
@@ -193,8 +204,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tS = tmem + 128 * g + lane_off, tO = tmem + 256 + 128 * g + lane_off;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j <= qt; ++j) {
+#ifdef LEMO_FA_TRACE
+        const bool trace = blockIdx.x == 0 && blockIdx.y == 0 && r == 0 && j < 64;
+        if (trace) g_fa_trace[g][0][j] = clock64();
+#endif
         mbar_wait(&s_full[g], j & 1);
         tc_fence_after();
+#ifdef LEMO_FA_TRACE
+        if (trace) g_fa_trace[g][1][j] = clock64();
+#endif
         float s[kT];
         {
           uint32_t raw[kT];
@@ -263,6 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[g]);
+#ifdef LEMO_FA_TRACE
+        if (trace) g_fa_trace[g][2][j] = clock64();
+#endif
       }
       mbar_wait(&o_done[g], 0);
       tc_fence_after();
@@ -296,6 +317,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace faf
 }  // namespace lemo
+
+#ifdef LEMO_FA_TRACE
+extern "C" int lemo_fa_trace_get(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_fa_trace, sizeof(g_fa_trace));
+}
+#endif
 
 using namespace lemo;
 
