@@ -394,7 +394,8 @@ def main():
                 traffic = tj.get("gemm_gateup_bytes_per_launch")
         except Exception:  # noqa: BLE001
             traffic = None
-    roofline = {"kernel": "gemm_tn_kernel<256,EpiGateUp> (lemo_gemm_gateup, MLP scoring)",
+    roofline = {"kernel": "gemm_tn_pair_kernel<EpiGateUp> (lemo_gemm_gateup, MLP scoring, "
+                          "256x256 CTA-pair tiles)",
                 "bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops_sustained"],
                 "unit": "TFLOP/s", "frac": (ach / pk["bf16_tflops_sustained"]) if ach else None,
                 "frac_burst": (ach / pk["bf16_tflops"]) if ach else None,
