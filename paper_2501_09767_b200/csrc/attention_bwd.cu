@@ -28,6 +28,12 @@
 #include "gemm.cuh"
 #include "lemo_internal.h"
 
+#ifdef LEMO_FA_TRACE
+// debug builds only: timestamps of the heaviest dK/dV CTA (key tile 0, head 0)
+// [0] before S wait, [1] S ready, [2] P arrive, [3] dP ready, [4] dS arrive
+__device__ unsigned long long g_fab_trace[2][5][128];
+#endif
+
 namespace lemo {
 namespace fab {
 
@@ -259,9 +265,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       named_bar_sync(1 + wg, 128);
       const bool edge = (t == 0) || (qw + 64 > n) || (key >= n);
       float p[64];
+#ifdef LEMO_FA_TRACE
+      const bool trace = blockIdx.x == 0 && blockIdx.y == 0 && r == 0 && u < 128;
+      if (trace) g_fab_trace[wg][0][u] = clock64();
+#endif
       // phase A: Pᵀ (both 32-column halves in flight before one wait)
       mbar_wait(s_full, u & 1);
       tc_fence_after();
+#ifdef LEMO_FA_TRACE
+      if (trace) g_fab_trace[wg][1][u] = clock64();
+#endif
       {
         uint32_t raw[64];
         tmem_ld_32x32b_x32(tSw, *reinterpret_cast<uint32_t(*)[32]>(raw));
@@ -284,10 +297,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+#ifdef LEMO_FA_TRACE
+      if (trace) g_fab_trace[wg][2][u] = clock64();
+#endif
       if (u + 1 < U) lv = stage_val(u + 1);
       // phase B: dSᵀ
       mbar_wait(dp_full, u & 1);
       tc_fence_after();
+#ifdef LEMO_FA_TRACE
+      if (trace) g_fab_trace[wg][3][u] = clock64();
+#endif
       {
         uint32_t raw[64];
         tmem_ld_32x32b_x32(tPw, *reinterpret_cast<uint32_t(*)[32]>(raw));
@@ -302,6 +321,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
+#ifdef LEMO_FA_TRACE
+      if (trace) g_fab_trace[wg][4][u] = clock64();
+#endif
     }
     mbar_wait(mm_done, 0);
     tc_fence_after();
@@ -519,6 +541,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace fab
 }  // namespace lemo
+
+#ifdef LEMO_FA_TRACE
+extern "C" int lemo_fab_trace_get(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_fab_trace, sizeof(g_fab_trace));
+}
+#endif
 
 using namespace lemo;
 
