@@ -394,13 +394,20 @@ def main():
                 traffic = tj.get("gemm_gateup_bytes_per_launch")
         except Exception:  # noqa: BLE001
             traffic = None
+    # The sustained figure (torch.matmul back to back for 4 s) is the ceiling for a
+    # kernel inside a long step unless the kernel beats it -- the step interleaves
+    # HBM-bound kernels, so the power cap bites less -- then the burst figure is.
+    use_burst = bool(ach) and ach > pk["bf16_tflops_sustained"]
+    peak_g = pk["bf16_tflops"] if use_burst else pk["bf16_tflops_sustained"]
     roofline = {"kernel": "gemm_tn_pair_kernel<EpiGateUp> (lemo_gemm_gateup, MLP scoring, "
                           "256x256 CTA-pair tiles)",
-                "bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops_sustained"],
-                "unit": "TFLOP/s", "frac": (ach / pk["bf16_tflops_sustained"]) if ach else None,
-                "frac_burst": (ach / pk["bf16_tflops"]) if ach else None,
+                "bound": "tensor", "achieved": ach, "peak": peak_g,
+                "unit": "TFLOP/s", "frac": (ach / peak_g) if ach else None,
+                "frac_sustained": (ach / pk["bf16_tflops_sustained"]) if ach else None,
                 "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
-                "peak_source": f"{pk_src} bf16_tflops_sustained (kernel timed inside the step)",
+                "peak_source": (f"{pk_src} bf16_tflops (burst; the kernel exceeds the measured "
+                                "sustained figure inside the step)" if use_burst else
+                                f"{pk_src} bf16_tflops_sustained (kernel timed inside the step)"),
                 "algorithmic_per_launch": flops_gemm, "launches_timed": len(gemm_ms),
                 "avg_launch_ms": avg_gemm_s * 1e3}
     nb = seq // cfg.block_size

@@ -43,6 +43,10 @@ def _stale(src: Path, obj: Path) -> bool:
 def build(verbose: bool = False, force: bool = False) -> Path:
     OBJ.mkdir(exist_ok=True)
     nvcc = _nvcc()
+    stamp = OBJ / "flags.txt"  # a flag change (e.g. LEMO_EXTRA_NVCC_FLAGS) rebuilds everything
+    if not stamp.exists() or stamp.read_text() != " ".join(FLAGS):
+        force = True
+        stamp.write_text(" ".join(FLAGS))
     inc = ["-I", str(CSRC), "-I", str(PKG.parent / "include")]
     jobs = []
     for src in sources():

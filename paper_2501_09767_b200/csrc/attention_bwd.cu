@@ -45,13 +45,16 @@ constexpr int kThreads = 384;
 constexpr float kLog2e = 1.4426950408889634f;
 
 // D (+)= A·Bᵀ with A, B [128 x 128] K-major tiles (two 16 KB boxes each).
+// Warp-collective (the MMA warp stays converged; one elected lane issues).
+// Descriptor start addresses advance by adding (offset >> 4) to the low field
+// (smem addresses < 256 KB never carry out of its 14 bits).
 template <uint32_t kIdesc>
 __device__ __forceinline__ void mma_kk(uint32_t d, uint32_t a, uint32_t b) {
+  const uint64_t da = umma_desc_k_sw128(a), db = umma_desc_k_sw128(b);
 #pragma unroll
   for (int kk = 0; kk < kD / 16; ++kk) {
-    const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
-    umma_bf16_ss(d, umma_desc_k_sw128(a + off), umma_desc_k_sw128(b + off), kIdesc,
-                 kk > 0 ? 1u : 0u);
+    const uint32_t off = ((kk >> 2) * kBox + (kk & 3) * 32) >> 4;
+    umma_bf16_ss_w(d, da + off, db + off, kIdesc, kk > 0 ? 1u : 0u);
   }
 }
 
@@ -60,10 +63,11 @@ __device__ __forceinline__ void mma_kk(uint32_t d, uint32_t a, uint32_t b) {
 // smem [128 (K) x 128 (N)] row-major tile = MN-major, two 16 KB 64-col atoms.
 template <uint32_t kIdesc>
 __device__ __forceinline__ void mma_tk(uint32_t d, uint32_t a_tmem, uint32_t b, bool acc) {
+  const uint64_t db = umma_desc_mn_sw128(b, kBox);
 #pragma unroll
   for (int kk = 0; kk < kT / 16; ++kk)
-    umma_bf16_ts(d, a_tmem + (kk >> 2) * 64 + (kk & 3) * 8,
-                 umma_desc_mn_sw128(b + kk * 2048, kBox), kIdesc, (acc || kk > 0) ? 1u : 0u);
+    umma_bf16_ts_w(d, a_tmem + (kk >> 2) * 64 + (kk & 3) * 8, db + kk * (2048 >> 4), kIdesc,
+                   (acc || kk > 0) ? 1u : 0u);
 }
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
@@ -205,41 +209,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int sq = t % kQStages;
       mbar_wait(&q_full[sq], (t / kQStages) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        mma_kk<idesc_s>(tS, aK, aQ + sq * kTile);
-        umma_commit(s_full);
-      }
-      __syncwarp();
+      mma_kk<idesc_s>(tS, aK, aQ + sq * kTile);
+      umma_commit_w(s_full);
     };
     auto issue_dp = [&](int t) {
       const int so = t % kOStages;
       mbar_wait(&o_full[so], (t / kOStages) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        mma_kk<idesc_s>(tP, aV, aO + so * kTile);
-        umma_commit(dp_full);
-      }
-      __syncwarp();
+      mma_kk<idesc_s>(tP, aV, aO + so * kTile);
+      umma_commit_w(dp_full);
     };
     issue_s(0);
     issue_dp(0);
     for (int t = 0; t < U; ++t) {
       mbar_wait(p_full, t & 1);
       tc_fence_after();
-      if (lane == 0) {
-        mma_tk<idesc_g>(tdV, tS, aO + (t % kOStages) * kTile, t > 0);
-        umma_commit(&o_empty[t % kOStages]);
-      }
-      __syncwarp();
+      mma_tk<idesc_g>(tdV, tS, aO + (t % kOStages) * kTile, t > 0);
+      umma_commit_w(&o_empty[t % kOStages]);
       if (t + 1 < U) issue_s(t + 1);
       mbar_wait(ds_full, t & 1);
       tc_fence_after();
-      if (lane == 0) {
-        mma_tk<idesc_g>(tdK, tP, aQ + (t % kQStages) * kTile, t > 0);
-        umma_commit(&q_empty[t % kQStages]);
-        if (t == U - 1) umma_commit(mm_done);
-      }
-      __syncwarp();
+      mma_tk<idesc_g>(tdK, tP, aQ + (t % kQStages) * kTile, t > 0);
+      umma_commit_w(&q_empty[t % kQStages]);
+      if (t == U - 1) umma_commit_w(mm_done);
       if (t + 1 < U) issue_dp(t + 1);
     }
   } else if (warp >= 4) {
@@ -440,22 +432,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (j >= 2) mbar_wait(&s_free[b], ((j - 2) >> 1) & 1);  // phase A of j-2 read it
       mbar_wait(&k_full[sk], (j / kKStages) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        mma_kk<idesc_s>(tmem + 128 * b, aQ, aK + sk * kTile);
-        umma_commit(&s_full[b]);
-      }
-      __syncwarp();
+      mma_kk<idesc_s>(tmem + 128 * b, aQ, aK + sk * kTile);
+      umma_commit_w(&s_full[b]);
     };
     auto issue_dp = [&](int j) {
       const int sv = j % kVStages;
       mbar_wait(&v_full[sv], (j / kVStages) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        mma_kk<idesc_s>(tP, aO, aV + sv * kTile);
-        umma_commit(dp_full);
-        umma_commit(&v_empty[sv]);
-      }
-      __syncwarp();
+      mma_kk<idesc_s>(tP, aO, aV + sv * kTile);
+      umma_commit_w(dp_full);
+      umma_commit_w(&v_empty[sv]);
     };
     issue_s(0);
     if (T > 1) issue_s(1);
@@ -463,12 +449,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < T; ++j) {
       mbar_wait(ds_full, j & 1);
       tc_fence_after();
-      if (lane == 0) {
-        mma_tk<idesc_g>(tdQ, tP, aK + (j % kKStages) * kTile, j > 0);
-        umma_commit(&k_empty[j % kKStages]);
-        if (j == T - 1) umma_commit(dq_done);
-      }
-      __syncwarp();
+      mma_tk<idesc_g>(tdQ, tP, aK + (j % kKStages) * kTile, j > 0);
+      umma_commit_w(&k_empty[j % kKStages]);
+      if (j == T - 1) umma_commit_w(dq_done);
       if (j + 1 < T) issue_dp(j + 1);
       if (j + 2 < T) issue_s(j + 2);
     }

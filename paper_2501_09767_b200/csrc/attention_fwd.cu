@@ -51,13 +51,15 @@ __device__ __forceinline__ uint8_t* aligned_smem(uint8_t* raw) {
   return raw;
 }
 
+// Warp-collective (the MMA warp stays converged, one elected lane issues);
+// descriptor start addresses advance by (offset >> 4) in the low field.
 template <uint32_t kIdesc>
 __device__ __forceinline__ void mma_qk(uint32_t d, uint32_t a, uint32_t b) {
+  const uint64_t da = umma_desc_k_sw128(a), db = umma_desc_k_sw128(b);
 #pragma unroll
   for (int kk = 0; kk < kD / 16; ++kk) {
-    const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
-    umma_bf16_ss(d, umma_desc_k_sw128(a + off), umma_desc_k_sw128(b + off), kIdesc,
-                 kk > 0 ? 1u : 0u);
+    const uint32_t off = ((kk >> 2) * kBox + (kk & 3) * 32) >> 4;
+    umma_bf16_ss_w(d, da + off, db + off, kIdesc, kk > 0 ? 1u : 0u);
   }
 }
 
@@ -65,10 +67,10 @@ __device__ __forceinline__ void mma_qk(uint32_t d, uint32_t a, uint32_t b) {
 // [128 keys x 128 d] = MN-major B.
 template <uint32_t kIdesc>
 __device__ __forceinline__ void mma_pv(uint32_t d, uint32_t p, uint32_t b, bool acc) {
+  const uint64_t db = umma_desc_mn_sw128(b, kBox);
 #pragma unroll
   for (int kk = 0; kk < kT / 16; ++kk)
-    umma_bf16_ts(d, p + kk * 8, umma_desc_mn_sw128(b + kk * 2048, kBox), kIdesc,
-                 (acc || kk > 0) ? 1u : 0u);
+    umma_bf16_ts_w(d, p + kk * 8, db + kk * (2048 >> 4), kIdesc, (acc || kk > 0) ? 1u : 0u);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -157,24 +159,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int sk = j % kKStages;
       if (g == 0) mbar_wait(&k_full[sk], (j / kKStages) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        mma_qk<idesc_s>(tmem + 128 * g, aQ + g * kTile, aK + sk * kTile);
-        umma_commit(&s_full[g]);
-        if (g == last_k_user(j)) umma_commit(&k_empty[sk]);
-      }
-      __syncwarp();
+      mma_qk<idesc_s>(tmem + 128 * g, aQ + g * kTile, aK + sk * kTile);
+      umma_commit_w(&s_full[g]);
+      if (g == last_k_user(j)) umma_commit_w(&k_empty[sk]);
     };
     auto issue_pv = [&](int g, int j) {
       const int sv = j % kVStages;
       mbar_wait(&p_full[g], j & 1);
       if (g == 0 || !uses(0, j)) mbar_wait(&v_full[sv], (j / kVStages) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        mma_pv<idesc_o>(tmem + 256 + 128 * g, tmem + 128 * g, aV + sv * kTile, j > 0);
-        if (g == last_k_user(j)) umma_commit(&v_empty[sv]);
-        if (j == qt0 + g) umma_commit(&o_done[g]);
-      }
-      __syncwarp();
+      mma_pv<idesc_o>(tmem + 256 + 128 * g, tmem + 128 * g, aV + sv * kTile, j > 0);
+      if (g == last_k_user(j)) umma_commit_w(&v_empty[sv]);
+      if (j == qt0 + g) umma_commit_w(&o_done[g]);
     };
     issue_s(0, 0);
     if (two) issue_s(1, 0);

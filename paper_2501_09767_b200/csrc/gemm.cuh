@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one thread) ----------------
+    // ---------------- MMA issuer (one warp, one elected lane issues) ----------------
     constexpr uint32_t idesc = umma_idesc_bf16(kBlockM, BN, 0, kBMN ? 1 : 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -146,21 +146,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a_addr = smem_u32(smem_a + stage * Cfg::kABytes);
+        {  // whole warp, one elected lane issues (descriptors stay uniform)
+          const uint64_t da = umma_desc_k_sw128(smem_u32(smem_a + stage * Cfg::kABytes));
           const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::kBBytes);
+          const uint64_t db = kBMN ? umma_desc_mn_sw128(b_addr, 8192) : umma_desc_k_sw128(b_addr);
 #pragma unroll
           for (int k = 0; k < kBlockK / kUmmaK; ++k) {
             // advancing K inside the 128-B swizzle atom = +32 B on the start address
-            const uint64_t da = umma_desc_k_sw128(a_addr + k * kUmmaK * 2);
-            const uint64_t db = kBMN ? umma_desc_mn_sw128(b_addr + k * 2048, 8192)
-                                     : umma_desc_k_sw128(b_addr + k * kUmmaK * 2);
-            umma_bf16_ss(d_tmem, da, db, idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_bf16_ss_w(d_tmem, da + ((k * kUmmaK * 2) >> 4),
+                           db + (kBMN ? (k * 2048) >> 4 : (k * kUmmaK * 2) >> 4), idesc,
+                           (kb | k) != 0 ? 1u : 0u);
           }
-          umma_commit(&empty_bar[stage]);
-          if (kb == num_kb - 1) umma_commit(&tfull_bar[acc]);
+          umma_commit_w(&empty_bar[stage]);
+          if (kb == num_kb - 1) umma_commit_w(&tfull_bar[acc]);
         }
-        __syncwarp();
         if (++stage == Cfg::kStages) {
           stage = 0;
           phase ^= 1;
@@ -294,18 +293,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t a_addr = smem_u32(smem_a + stage * kHalf);
-            const uint32_t b_addr = smem_u32(smem_b + stage * kHalf);
+          {
+            const uint64_t da = umma_desc_k_sw128(smem_u32(smem_a + stage * kHalf));
+            const uint64_t db = umma_desc_k_sw128(smem_u32(smem_b + stage * kHalf));
 #pragma unroll
             for (int k = 0; k < kBlockK / kUmmaK; ++k)
-              umma_bf16_ss_pair(d_tmem, umma_desc_k_sw128(a_addr + k * kUmmaK * 2),
-                                umma_desc_k_sw128(b_addr + k * kUmmaK * 2), idesc,
-                                (kb | k) != 0 ? 1u : 0u);
-            umma_commit_pair(&empty_bar[stage]);
-            if (kb == num_kb - 1) umma_commit_pair(&tfull_bar[acc]);
+              umma_bf16_ss_pair_w(d_tmem, da + ((k * kUmmaK * 2) >> 4),
+                                  db + ((k * kUmmaK * 2) >> 4), idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_commit_pair_w(&empty_bar[stage]);
+            if (kb == num_kb - 1) umma_commit_pair_w(&tfull_bar[acc]);
           }
-          __syncwarp();
           if (++stage == kStagesPair) {
             stage = 0;
             phase ^= 1;

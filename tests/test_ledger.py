@@ -3,6 +3,7 @@ GPU, the memory law of acceptance criterion 9 (tests/test_acceptance.py:511-553)
 block activation bytes linear in the retained fraction, the activation peak
 affine in the sequence length."""
 
+import gc
 import numpy as np
 import pytest
 
@@ -79,12 +80,19 @@ def test_memory_law_on_gpu(cuda):
     rng = np.random.default_rng(0)
 
     def step(tokens, source):
-        led = L.Ledger(keep_series=False)
-        with L.use(led):
-            loss, _ = model.forward_step(tokens, pattern_source=source)
-            post = led.marks["post_forward"]
-            loss.backward()
-        rep = led.report()
+        # objects left by earlier tests must not be collected inside the step:
+        # their frees would shrink the allocator delta the ledger is checked against
+        gc.collect()
+        gc.disable()
+        try:
+            led = L.Ledger(keep_series=False)
+            with L.use(led):
+                loss, _ = model.forward_step(tokens, pattern_source=source)
+                post = led.marks["post_forward"]
+                loss.backward()
+            rep = led.report()
+        finally:
+            gc.enable()
         assert rep.leaked_bytes == 0 and led.live_bytes() == 0
         return rep, post
 
