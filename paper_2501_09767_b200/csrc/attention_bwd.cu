@@ -31,7 +31,7 @@
 #ifdef LEMO_FA_TRACE
 // debug builds only: timestamps of the heaviest dK/dV CTA (key tile 0, head 0)
 // [0] before S wait, [1] S ready, [2] P arrive, [3] dP ready, [4] dS arrive
-__device__ unsigned long long g_fab_trace[2][5][128];
+__device__ unsigned long long g_fab_trace[3][8][128];  // [EW wg0, wg1, MMA warp][event][tile]
 #endif
 
 namespace lemo {
@@ -43,6 +43,10 @@ constexpr int kBox = kT * 64 * 2;      // [128 x 64] bf16 SW128 box = 16 KB
 constexpr int kTile = 2 * kBox;        // [128 x 128] = 32 KB
 constexpr int kThreads = 384;
 constexpr float kLog2e = 1.4426950408889634f;
+#ifndef LEMO_FAB_POLY
+#define LEMO_FAB_POLY 0
+#endif
+constexpr int kPolyEvery = LEMO_FAB_POLY;  // every k-th exponential on the FMA pipe (0 = none)
 
 // D (+)= A·Bᵀ with A, B [128 x 128] K-major tiles (two 16 KB boxes each).
 // Warp-collective (the MMA warp stays converged; one elected lane issues).
@@ -204,10 +208,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc_g = umma_idesc_bf16(kT, kD, 0, 1);
     const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
     const uint32_t aQ = smem_u32(sQ), aO = smem_u32(sO);
+#ifdef LEMO_FA_TRACE
+    const bool mtrace = blockIdx.x == 0 && blockIdx.y == 0 && lane == 0;
+#define MT(i) if (mtrace && t < 128) g_fab_trace[2][i][t] = clock64();
+#else
+#define MT(i)
+#endif
     mbar_wait(kv_full, 0);
     auto issue_s = [&](int t) {
       const int sq = t % kQStages;
       mbar_wait(&q_full[sq], (t / kQStages) & 1);
+      MT(6)
       tc_fence_after();
       mma_kk<idesc_s>(tS, aK, aQ + sq * kTile);
       umma_commit_w(s_full);
@@ -215,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_dp = [&](int t) {
       const int so = t % kOStages;
       mbar_wait(&o_full[so], (t / kOStages) & 1);
+      MT(7)
       tc_fence_after();
       mma_kk<idesc_s>(tP, aV, aO + so * kTile);
       umma_commit_w(dp_full);
@@ -223,17 +235,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     issue_dp(0);
     for (int t = 0; t < U; ++t) {
       mbar_wait(p_full, t & 1);
+      MT(0)
       tc_fence_after();
       mma_tk<idesc_g>(tdV, tS, aO + (t % kOStages) * kTile, t > 0);
       umma_commit_w(&o_empty[t % kOStages]);
       if (t + 1 < U) issue_s(t + 1);
+      MT(1)
       mbar_wait(ds_full, t & 1);
+      MT(2)
       tc_fence_after();
       mma_tk<idesc_g>(tdK, tP, aQ + (t % kQStages) * kTile, t > 0);
       umma_commit_w(&q_empty[t % kQStages]);
       if (t == U - 1) umma_commit_w(mm_done);
       if (t + 1 < U) issue_dp(t + 1);
+      MT(3)
     }
+#undef MT
   } else if (warp >= 4) {
     const int wg = (warp - 4) >> 2;  // columns 64·wg … 64·wg + 63 of every query tile
     const int wq = warp & 3;
@@ -243,17 +260,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tSw = tS + lane_off + 64 * wg, tPw = tP + lane_off + 64 * wg;
     // thread r stages one of this WG's 64 lse₂ (r < 64) or Δ values of tile u;
     // the global load for u+1 is issued one phase ahead (latency hidden)
+    // (raw load only: the log2e scaling is applied at the smem store, so no
+    // arithmetic waits on the load before the next phase)
+    const float* src = r < 64 ? lse : delta;
+    const float stage_mul = r < 64 ? kLog2e : 1.f;
     auto stage_val = [&](int u) {
       const int q = k0 + (u % T) * kT + 64 * wg + (r & 63), hq = kvh * group + u / T;
-      return q < n ? (r < 64 ? lse[(size_t)hq * n + q] * kLog2e : delta[(size_t)hq * n + q])
-                   : 0.f;
+      return __ldg(src + (size_t)hq * n + min(q, n - 1));  // q ≥ n: masked (P = 0) anyway
     };
     float lv = stage_val(0);
     for (int u = 0; u < U; ++u) {
       const int t = u % T;                   // query tile
       const int qw = k0 + t * kT + 64 * wg;  // first query of this WG's columns
       float* L = sLD + (wg * 2 + (u & 1)) * kT;
-      L[r] = lv;
+      L[r] = lv * stage_mul;
       named_bar_sync(1 + wg, 128);
       const bool edge = (t == 0) || (qw + 64 > n) || (key >= n);
       float p[64];
@@ -274,7 +294,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
 #pragma unroll
         for (int c = 0; c < 64; ++c)
-          p[c] = ex2_approx(fmaf(__uint_as_float(raw[c]), sl2, -L[c]));
+          p[c] = (kPolyEvery && c % kPolyEvery == kPolyEvery - 1)  // share of 2^x off the SFU
+                     ? ex2_poly3(fmaf(__uint_as_float(raw[c]), sl2, -L[c]))
+                     : ex2_approx(fmaf(__uint_as_float(raw[c]), sl2, -L[c]));
       }
       if (edge) {
 #pragma unroll

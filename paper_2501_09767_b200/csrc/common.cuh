@@ -62,6 +62,21 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// 2^x on the FMA/ALU pipes (offloads the SFU): round-to-nearest split with the
+// 1.5·2^23 magic constant, f ∈ [-0.5, 0.5], degree-3 minimax polynomial
+// (max rel. error 2.2e-4, far below the bf16 rounding of P), exponent add.
+// Valid for x ∈ [-126, 127]; callers clamp below (x ≤ 0 for softmax-style use).
+__device__ __forceinline__ float ex2_poly3(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;            // round(x) in the low mantissa bits
+  const float j = t - 12582912.f;
+  const float f = x - j;
+  float p = fmaf(f, 0.05286732f, 0.24215215f);
+  p = fmaf(p, f, 0.69358683f);
+  p = fmaf(p, f, 0.99996275f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 // Three-input max (FMNMX3, sm_100).
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;

@@ -10,11 +10,22 @@ do = torch.randn_like(o)
 for _ in range(3):
     ops.flash_bwd(q, k, v, o, do, lse, head_dim=d, scale=1 / math.sqrt(d))
 torch.cuda.synchronize()
-buf = np.zeros((2, 5, 128), dtype=np.uint64)
+buf = np.zeros((3, 8, 128), dtype=np.uint64)
 _lib.lib().lemo_fab_trace_get(ctypes.c_void_p(buf.ctypes.data))
 t = buf.astype(np.int64)[:, :, 4:60]
 for g in range(2):
-    a0, s_rdy, p_arr, dp_rdy, ds_arr = t[g]
+    a0, s_rdy, p_arr, dp_rdy, ds_arr = t[g][:5]
     print(f"WG{g}: wait S {np.mean(s_rdy - a0):.0f} | phase A {np.mean(p_arr - s_rdy):.0f} | "
           f"wait dP {np.mean(dp_rdy - p_arr):.0f} | phase B {np.mean(ds_arr - dp_rdy):.0f} | "
           f"period {np.mean(np.diff(ds_arr)):.0f} clk")
+# MMA warp: [0] p_full seen, [1] dV+S(t+1) issued, [2] ds_full seen, [3] dK+dP(t+1) issued,
+# [6] q_full(t) seen, [7] o_full(t) seen; one row per event, three consecutive tiles
+m = t[2]
+ev = {"MMA p_full seen": m[0], "MMA dV,S(t+1) issued": m[1], "MMA ds_full seen": m[2],
+      "MMA dK,dP(t+1) issued": m[3], "MMA q_full(t+1) seen": np.roll(m[6], -1),
+      "MMA o_full(t+1) seen": np.roll(m[7], -1),
+      "EW0 S(t) seen": t[0][1], "EW0 p arrive": t[0][2], "EW0 dP(t) seen": t[0][3],
+      "EW0 ds arrive": t[0][4]}
+base = m[0][10]
+for k, v in sorted(ev.items(), key=lambda kv: kv[1][10]):
+    print(f"  {k:24s} " + " ".join(f"{int(x - base):6d}" for x in v[10:13]))

@@ -54,6 +54,26 @@ __global__ void __launch_bounds__(512, 1) probe(int iters, unsigned long long* c
     if (SPIN == 2) {  // polling with a nanosleep back-off
       while (!mbar_try_wait(&spin, 0)) __nanosleep(64);
     }
+    if (SPIN == 3 || SPIN == 4) {  // element-wise warps streaming TMEM (ld, or ld + st) meanwhile
+      const uint32_t row = slot + (((warp & 3) * 32) << 16) + ((warp >> 2) - 1) * 64;
+      uint32_t v[32], acc = 0;
+      while (!mbar_try_wait(&spin, 0)) {
+        tmem_ld_32x32b_x32(row, v);
+        uint32_t w[32];
+        tmem_ld_32x32b_x32(row + 32, w);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc += v[j] ^ w[j];
+        if (SPIN == 4) {
+          uint32_t p16[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) p16[j] = v[j] + w[j];
+          tmem_st_32x32b_x16(row, p16);
+          tmem_st_wait();
+        }
+      }
+      if (acc == 0x12345u) *cyc = acc;
+    }
   }
   if (threadIdx.x == 0) {
     constexpr uint32_t id_k = umma_idesc_bf16(128, 128, 0, 0);
@@ -151,6 +171,9 @@ void run(const char* name, int fill, int iters = 1000, int warps = 4) {
 }
 
 int main() {
+  run<6, 3>("bwd pattern + 8 warps streaming tcgen05.ld", 1, 1000, 12);
+  run<6, 4>("bwd pattern + 8 warps tcgen05.ld + st", 1, 1000, 12);
+  run<0, 3>("SS x4 + 8 warps streaming tcgen05.ld", 1, 1000, 12);
   run<9>("kernel smem map, dK SS (A=dS smem)", 1);
   run<10>("kernel smem map, dK TS (A=dS TMEM)", 1);
   for (int fill = 0; fill < 2; ++fill) {
