@@ -95,8 +95,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = (n + kT - 1) / kT;
-  const int pair = (int)(gridDim.x - 1 - blockIdx.x);  // heavy pairs first
-  const int hd = blockIdx.y, c0 = hd * kD;
+  // grid (heads, pairs): blocks are dispatched x-fastest, so every head's heavy
+  // (late, long) pairs go first and the light ones fill the tail
+  const int pair = (int)(gridDim.y - 1 - blockIdx.y);
+  const int hd = blockIdx.x, c0 = hd * kD;
   const int ck = (hd / group) * kD;  // key/value head of this query head
   const int qt0 = 2 * pair;
   const bool two = qt0 + 1 < nt;
@@ -343,7 +345,7 @@ int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, floa
     attr = true;
   }
   const int nt = (n + faf::kT - 1) / faf::kT;
-  dim3 grid((nt + 1) / 2, h / head_dim);
+  dim3 grid(h / head_dim, (nt + 1) / 2);
   faf::flash_fwd_kernel<<<grid, faf::kThreads, faf::kSmem, (cudaStream_t)stream>>>(
       tq, tk, tv, reinterpret_cast<__nv_bfloat16*>(o), lse, n, h, h / kv, scale * faf::kLog2e);
   LEMO_CHECK_LAUNCH("lemo_flash_fwd_tc");
