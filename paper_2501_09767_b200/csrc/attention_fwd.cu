@@ -38,6 +38,10 @@ namespace faf {
 
 constexpr int kT = 128;
 constexpr int kD = 128;
+#ifndef LEMO_FA_POLY
+#define LEMO_FA_POLY 0
+#endif
+constexpr int kPolyEvery = LEMO_FA_POLY;  // every k-th exponential pair on the FMA pipe (0 = none)
 constexpr int kBox = kT * 64 * 2;   // [128 x 64] bf16 SW128 box = 16 KB
 constexpr int kTile = 2 * kBox;     // [128 x 128] = 32 KB
 constexpr int kKStages = 3, kVStages = 2;
@@ -264,8 +268,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float2 x = ffma2(make_float2(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]), sl2x2, negm);
-            x.x = ex2_approx(x.x);
-            x.y = ex2_approx(x.y);
+            if (kPolyEvery && i % kPolyEvery == kPolyEvery - 1) {  // share off the SFU
+              x.x = ex2_poly3(x.x);
+              x.y = ex2_poly3(x.y);
+            } else {
+              x.x = ex2_approx(x.x);
+              x.y = ex2_approx(x.y);
+            }
             sm[i & 3] = fadd2(sm[i & 3], x);
             pk[i] = pack_bf16x2(x.x, x.y);
           }
