@@ -207,10 +207,55 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 constexpr int kStagesPair = 6;
 constexpr int kSmemPair = kStagesPair * 2 * kBlockM * kBlockK * 2 + 1024 + 256;
 
+// Split-K tail.  Tiles are all the same cost, so T tiles on C clusters take
+// ceil(T / C) tile-times even when the last wave holds a handful of tiles
+// (M = 8208 rows at N = 4096 is 528 tiles = 7.14 waves -> 8).  When the last
+// wave is at most half full, its R tiles are each cut into `split` K-ranges
+// (R·split ≤ C units, one per cluster): the first split-1 units of a tile
+// store their fp32 partial accumulators to `ws` and bump a per-(tile, CTA)
+// counter; the last unit (highest cluster index of the tile's units, so the
+// others are dispatched no later) waits for them, adds the partials to its
+// TMEM accumulator in a fixed order (deterministic) and runs the epilogue.
+constexpr int kPairTailMaxSplit = 4;  // the last unit reads split-1 partials: keep it short
+
+struct PairTail {
+  int full_tiles;  // tiles computed whole (the first full waves)
+  int split;       // K-ranges per tail tile (1 = no split-K tail)
+  float* ws;       // [unit][rank][part][c32][j][row] float4 partials
+  int* ctr;        // [tail tile][rank] arrival counters (reset by the last unit)
+};
+
+// Epilogues that may take the split-K tail (specialised next to their
+// definitions).  The heavy epilogues (GateUp, DGateUp, QKV) run at full
+// register pressure already; the tail's partial-sum code would make them spill.
+template <class Epi>
+struct PairTailOK {
+  static constexpr bool value = false;
+};
+
+struct PairUnit {
+  int tile, kb0, kb1, chunk;  // chunk = -1 for a whole tile
+};
+
+__device__ __forceinline__ PairUnit pair_unit(int u, const PairTail& tl, int num_kb) {
+  PairUnit w;
+  if (u < tl.full_tiles) {
+    w.tile = u; w.kb0 = 0; w.kb1 = num_kb; w.chunk = -1;
+  } else {
+    const int v = u - tl.full_tiles;
+    w.tile = tl.full_tiles + v / tl.split;
+    w.chunk = v % tl.split;
+    w.kb0 = w.chunk * num_kb / tl.split;
+    w.kb1 = (w.chunk + 1) * num_kb / tl.split;
+  }
+  return w;
+}
+
 template <class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_tn_pair_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, int M, int N, int K, Epi epi) {
+                        const __grid_constant__ CUtensorMap tmB, int M, int N, int K, Epi epi,
+                        PairTail tl) {
   constexpr int BN = 256;
   constexpr int kHalf = kBlockM * kBlockK * 2;  // one 128 x 64 bf16 box = 16 KB
   extern __shared__ uint8_t smem_raw[];
@@ -234,6 +279,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int num_tiles = num_m * num_n;
   const int num_kb = (K + kBlockK - 1) / kBlockK;
   const int cid = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int num_units = tl.full_tiles + (num_tiles - tl.full_tiles) * tl.split;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -259,9 +305,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);  // the leader's barriers
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cid; t < num_tiles; t += nclusters) {
-        const TileCoord tc = tile_coord(t, num_m, num_n);
-        for (int kb = 0; kb < num_kb; ++kb) {
+      for (int u = cid; u < num_units; u += nclusters) {
+        const PairUnit w = pair_unit(u, tl, num_kb);
+        const TileCoord tc = tile_coord(w.tile, num_m, num_n);
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           const uint32_t fb = full0 + stage * 8;
           if (leader)
@@ -285,12 +332,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = cid; t < num_tiles; t += nclusters, ++local) {
+      for (int u = cid; u < num_units; u += nclusters, ++local) {
+        const PairUnit w = pair_unit(u, tl, num_kb);
         const int acc = local & 1;
         mbar_wait(&tempty_bar[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           {
@@ -299,9 +347,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int k = 0; k < kBlockK / kUmmaK; ++k)
               umma_bf16_ss_pair_w(d_tmem, da + ((k * kUmmaK * 2) >> 4),
-                                  db + ((k * kUmmaK * 2) >> 4), idesc, (kb | k) != 0 ? 1u : 0u);
+                                  db + ((k * kUmmaK * 2) >> 4), idesc,
+                                  (kb > w.kb0 || k > 0) ? 1u : 0u);
             umma_commit_pair_w(&empty_bar[stage]);
-            if (kb == num_kb - 1) umma_commit_pair_w(&tfull_bar[acc]);
+            if (kb == w.kb1 - 1) umma_commit_pair_w(&tfull_bar[acc]);
           }
           if (++stage == kStagesPair) {
             stage = 0;
@@ -315,14 +364,81 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const int part = (warp - 4) >> 2;
     const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
     int local = 0;
-    for (int t = cid; t < num_tiles; t += nclusters, ++local) {
-      const TileCoord tc = tile_coord(t, num_m, num_n);
+    for (int u = cid; u < num_units; u += nclusters, ++local) {
+      const PairUnit w = pair_unit(u, tl, num_kb);
+      const TileCoord tc = tile_coord(w.tile, num_m, num_n);
       const int acc = local & 1;
       mbar_wait(&tfull_bar[acc], (local >> 1) & 1);
       tc_fence_after();
       const int row = tc.m * 2 * kBlockM + (int)rank * kBlockM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
-      epi(row, row < M, tc.n * BN, taddr, part);
+      bool run_epi = true;
+      if constexpr (PairTailOK<Epi>::value) {
+      if (w.chunk >= 0) {
+        // partial-sum slot of (unit, rank, part): [c32 4][j 8][row 128] float4
+        const int tail = w.tile - tl.full_tiles, v0 = tail * tl.split;
+        const int r128 = wq * 32 + lane;
+        auto slot = [&](int c) {
+          return reinterpret_cast<float4*>(tl.ws) + (((size_t)(v0 + c) * 2 + rank) * 2 + part) * 4096;
+        };
+        int* ctr = tl.ctr + tail * 2 + rank;
+        if (w.chunk < tl.split - 1) {
+          float4* dst = slot(w.chunk);
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(taddr + part * 128 + c * 32, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              __stcg(dst + (c * 8 + j) * 128 + r128,
+                     make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                 __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
+          }
+          __threadfence();
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          if (threadIdx.x == 128) atomicAdd(ctr, 1);
+          run_epi = false;
+        } else {
+          if (threadIdx.x == 128) {
+            while (atomicAdd(ctr, 0) < tl.split - 1) __nanosleep(256);
+            atomicExch(ctr, 0);  // ready for the next launch
+            __threadfence();
+          }
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(taddr + part * 128 + c * 32, v);
+            tmem_ld_wait();
+            // all partial loads of this 32-column chunk in flight at once, then
+            // the adds in a fixed order (deterministic)
+            float4 x[kPairTailMaxSplit - 1][8];
+#pragma unroll
+            for (int k = 0; k < kPairTailMaxSplit - 1; ++k)
+              if (k < tl.split - 1) {
+                const float4* src = slot(k);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) x[k][j] = __ldcg(src + (c * 8 + j) * 128 + r128);
+              }
+#pragma unroll
+            for (int k = 0; k < kPairTailMaxSplit - 1; ++k)
+              if (k < tl.split - 1) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  v[4 * j] = __float_as_uint(__uint_as_float(v[4 * j]) + x[k][j].x);
+                  v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + x[k][j].y);
+                  v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + x[k][j].z);
+                  v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + x[k][j].w);
+                }
+              }
+            tmem_st_32x32b_x32(taddr + part * 128 + c * 32, v);
+          }
+          tmem_st_wait();
+        }
+      }
+      }
+      if (run_epi) epi(row, row < M, tc.n * BN, taddr, part);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
@@ -349,6 +465,12 @@ int make_tma_bf16_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t
                      uint64_t ld_elems, uint32_t box_rows);
 
 int gemm_num_sms();
+
+// Split-K tail scratch of the pair GEMM, one per stream (kernels on one stream
+// are ordered, so they may share it): `units` partial slots of 2 x 128 x 256
+// fp32 and `tiles` x 2 zeroed counters.  LEMO_GEMM_TAIL=0 disables the tail.
+int pair_tail_workspace(cudaStream_t stream, int units, int tiles, float** ws, int** ctr);
+bool pair_tail_enabled();
 
 template <int BN, class Epi, bool kBMN = false>
 int launch_gemm_tn(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
@@ -397,8 +519,23 @@ int launch_gemm_tn_pair(const void* A, int lda, const void* B, int ldb, int M, i
   }
   const int tiles = ((M + 2 * kBlockM - 1) / (2 * kBlockM)) * ((N + 255) / 256);
   const int pairs = gemm_num_sms() / 2;
-  const int grid = 2 * (tiles < pairs ? tiles : pairs);
-  gemm_tn_pair_kernel<Epi><<<grid, kGemmThreads, kSmemPair, stream>>>(ta, tb, M, N, K, epi);
+  const int clusters = tiles < pairs ? tiles : pairs;
+  PairTail tl{tiles, 1, nullptr, nullptr};
+  const int rem = tiles % clusters, num_kb = (K + kBlockK - 1) / kBlockK;
+  if (PairTailOK<Epi>::value && tiles > clusters && rem > 0 && 2 * rem <= clusters &&
+      pair_tail_enabled()) {
+    int split = clusters / rem;
+    if (split > kPairTailMaxSplit) split = kPairTailMaxSplit;
+    if (split > num_kb / 4) split = num_kb / 4;  // keep ≥ 4 k-blocks per unit
+    if (split >= 2) {
+      rc = pair_tail_workspace(stream, rem * split, rem, &tl.ws, &tl.ctr);
+      if (rc) return rc;
+      tl.full_tiles = tiles - rem;
+      tl.split = split;
+    }
+  }
+  gemm_tn_pair_kernel<Epi><<<2 * clusters, kGemmThreads, kSmemPair, stream>>>(ta, tb, M, N, K,
+                                                                             epi, tl);
   return (int)cudaGetLastError();
 }
 

@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -102,6 +103,43 @@ int make_tma_bf16_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t
   std::lock_guard<std::mutex> lk(g_tma_mu);
   if (g_tma_cache.size() > 8192) g_tma_cache.clear();
   g_tma_cache.emplace(key, *out);
+  return 0;
+}
+
+bool pair_tail_enabled() {
+  static const int env = getenv("LEMO_GEMM_TAIL") ? atoi(getenv("LEMO_GEMM_TAIL")) : 1;
+  return env != 0;
+}
+
+namespace {
+struct TailWs {
+  float* ws = nullptr;
+  int* ctr = nullptr;
+};
+std::mutex g_tail_mu;
+std::unordered_map<std::string, TailWs> g_tail_ws;
+}  // namespace
+
+int pair_tail_workspace(cudaStream_t stream, int units, int tiles, float** ws, int** ctr) {
+  // sized once for the largest possible tail (one unit per cluster)
+  const int max_units = gemm_num_sms() / 2;
+  if (units > max_units || tiles > max_units) return (int)cudaErrorInvalidValue;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::string key = std::to_string(dev) + ":" + std::to_string((uintptr_t)stream);
+  std::lock_guard<std::mutex> lk(g_tail_mu);
+  auto it = g_tail_ws.find(key);
+  if (it == g_tail_ws.end()) {
+    TailWs t;
+    const size_t bytes = (size_t)max_units * 2 * 128 * 256 * sizeof(float);
+    cudaError_t e = cudaMalloc(&t.ws, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&t.ctr, (size_t)max_units * 2 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(t.ctr, 0, (size_t)max_units * 2 * sizeof(int), stream);
+    if (e != cudaSuccess) return (int)e;
+    it = g_tail_ws.emplace(key, t).first;
+  }
+  *ws = it->second.ws;
+  *ctr = it->second.ctr;
   return 0;
 }
 

@@ -71,3 +71,40 @@ def test_gemm_nn_mn_major_b(cuda, M, N, K):
     ref = a.float() @ b.float()
     err = (c.float() - ref).abs().max().item()
     assert err <= 1e-2 * ref.abs().max().item() + 1e-3, err
+
+
+@pytest.mark.parametrize("M,N,K,acc", [(8208, 4096, 1024, False), (7045, 4096, 2048, True),
+                                       (4096, 4096, 4096, False)])
+def test_gemm_pair_split_k_tail(cuda, M, N, K, acc):
+    """Shapes whose last wave of 256 x 256 pair tiles is at most half full run
+    that wave as split-K units (partials summed in a fixed order): same result
+    as the fp32 reference, and bit-identical run to run."""
+    tiles = -(-M // 256) * (N // 256)
+    assert tiles % 74 and 2 * (tiles % 74) <= 74  # the tail path is taken on 148 SMs
+    g = torch.Generator(device=cuda).manual_seed(11)
+    a = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    b = torch.randn(N, K, device=cuda, generator=g).bfloat16()
+    base = torch.randn(M, N, device=cuda, generator=g)
+    outs = []
+    for _ in range(2):
+        out = base.clone()
+        ops.gemm_f32(a, b, out, accumulate=acc)
+        outs.append(out)
+    torch.cuda.synchronize()
+    ref = (base if acc else 0) + _ref(a, b)
+    assert (outs[0] - ref).abs().max().item() <= 1e-3 * ref.abs().max().item() + 1e-3
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_gemm_scatter_add_split_k_tail(cuda):
+    s, h, K, k = 16384, 4096, 1024, 7045
+    g = torch.Generator(device=cuda).manual_seed(12)
+    idx = torch.randperm(s, device=cuda, generator=g)[:k].sort().values.int()
+    a = torch.randn(k, K, device=cuda, generator=g).bfloat16()
+    b = torch.randn(h, K, device=cuda, generator=g).bfloat16()
+    resid = torch.randn(s, h, device=cuda, generator=g)
+    ref = resid.clone()
+    ref[idx.long()] += _ref(a, b)
+    ops.gemm_scatter_add(a, b, resid, idx)
+    torch.cuda.synchronize()
+    assert torch.allclose(resid, ref, atol=1e-3, rtol=1e-3)
