@@ -147,8 +147,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* o_empty = o_full + kOStages;    // [kOStages]
   uint64_t* s_full = o_empty + kOStages;
   uint64_t* dp_full = s_full + 1;
-  uint64_t* p_full = dp_full + 1;
-  uint64_t* ds_full = p_full + 1;
+  uint64_t* p_full = dp_full + 1;   // [2]: Pᵀ columns of query halves 0-31 / 32-63 of each WG
+  uint64_t* ds_full = p_full + 2;
   uint64_t* mm_done = ds_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mm_done + 1);
 
@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
-    mbar_init(p_full, 8);
+    mbar_init(&p_full[0], 8);
+    mbar_init(&p_full[1], 8);
     mbar_init(ds_full, 8);
     mbar_init(mm_done, 1);
     fence_barrier_init();
@@ -247,11 +248,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     issue_s(0);
     issue_dp(0);
+    const uint64_t dO0 = umma_desc_mn_sw128(aO, kBox);
     for (int t = 0; t < U; ++t) {
-      mbar_wait(p_full, t & 1);
-      MT(0)
-      tc_fence_after();
-      mma_tk<idesc_g>(tdV, tS, aO + (t % kOStages) * kTile, t > 0);
+      // dV(t) in two K halves, each issued as soon as the element-wise warps
+      // have stored that half of every warpgroup's Pᵀ columns
+      const uint64_t dO = dO0 + (((t % kOStages) * kTile) >> 4);
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        mbar_wait(&p_full[hf], t & 1);
+        if (hf == 0) MT(0)
+        tc_fence_after();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int kk = (i >> 1) * 4 + hf * 2 + (i & 1);  // WG (i>>1), K-slice 2·hf + (i&1)
+          umma_bf16_ts_w(tdV, tS + (kk >> 2) * 64 + (kk & 3) * 8, dO + kk * (2048 >> 4),
+                         idesc_g, (t > 0 || kk > 0) ? 1u : 0u);
+        }
+      }
       umma_commit_w(&o_empty[t % kOStages]);
       if (t + 1 < U) issue_s(t + 1);
       MT(1)
@@ -306,25 +319,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_32x32b_x32(tSw, *reinterpret_cast<uint32_t(*)[32]>(raw));
         tmem_ld_32x32b_x32(tSw + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
         tmem_ld_wait();
+        // two halves of 32 columns, each stored (bf16, packed over the already
+        // read fp32 columns) and signalled before the next is exponentiated
 #pragma unroll
-        for (int c = 0; c < 64; ++c)
-          p[c] = (kPolyEvery && c % kPolyEvery == kPolyEvery - 1)  // share of 2^x off the SFU
-                     ? ex2_poly3(fmaf(__uint_as_float(raw[c]), sl2, -L[c]))
-                     : ex2_approx(fmaf(__uint_as_float(raw[c]), sl2, -L[c]));
-      }
-      if (edge) {
+        for (int hf = 0; hf < 2; ++hf) {
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const int q = qw + c;
-          if (key > q || q >= n || key >= n) p[c] = 0.f;
+          for (int c = 32 * hf; c < 32 * hf + 32; ++c)
+            p[c] = (kPolyEvery && c % kPolyEvery == kPolyEvery - 1)  // share of 2^x off the SFU
+                       ? ex2_poly3(fmaf(__uint_as_float(raw[c]), sl2, -L[c]))
+                       : ex2_approx(fmaf(__uint_as_float(raw[c]), sl2, -L[c]));
+          if (edge) {
+#pragma unroll
+            for (int c = 32 * hf; c < 32 * hf + 32; ++c) {
+              const int q = qw + c;
+              if (key > q || q >= n || key >= n) p[c] = 0.f;
+            }
+          }
+          st_bf16x32(tSw + 16 * hf, p + 32 * hf);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[hf]);
         }
       }
-      st_bf16x32(tSw, p);        // packed halves over the (already read) fp32 columns
-      st_bf16x32(tSw + 16, p + 32);
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
 #ifdef LEMO_FA_TRACE
       if (trace) g_fab_trace[wg][2][u] = clock64();
 #endif
