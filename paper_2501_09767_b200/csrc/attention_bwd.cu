@@ -31,7 +31,13 @@
 #ifdef LEMO_FA_TRACE
 // debug builds only: timestamps of the heaviest dK/dV CTA (key tile 0, head 0)
 // [0] before S wait, [1] S ready, [2] P arrive, [3] dP ready, [4] dS arrive
-__device__ unsigned long long g_fab_trace[3][8][128];  // [EW wg0, wg1, MMA warp][event][tile]
+__device__ unsigned long long g_fab_trace[3][8][128];
+__device__ unsigned long long g_fab_cta[2][8192][6];  // [kernel][cta]: start, end, smid, units, first S seen, all MMAs done
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}  // [EW wg0, wg1, MMA warp][event][tile]
 #endif
 
 namespace lemo {
@@ -43,11 +49,8 @@ constexpr int kBox = kT * 64 * 2;      // [128 x 64] bf16 SW128 box = 16 KB
 constexpr int kTile = 2 * kBox;        // [128 x 128] = 32 KB
 constexpr int kThreads = 384;
 constexpr float kLog2e = 1.4426950408889634f;
-#ifndef LEMO_FAB_GRID_DKDV
-#define LEMO_FAB_GRID_DKDV 0
-#endif
-#ifndef LEMO_FAB_GRID_DQ
-#define LEMO_FAB_GRID_DQ 0
+#ifndef LEMO_FAB_HEAD_GROUP
+#define LEMO_FAB_HEAD_GROUP 4
 #endif
 #ifndef LEMO_FAB_POLY
 #define LEMO_FAB_POLY 0
@@ -111,11 +114,67 @@ __device__ __forceinline__ void store_row_f32(uint32_t taddr, float* dst, float 
   }
 }
 
+// A warpgroup's 128 rows x kCols fp32 accumulator (TMEM columns [0, kCols)
+// at taddr, times scale) -> global via smem staging and TMA tile stores
+// (boxes of 128 rows x 32 columns, SW128; rows past the tensor are clipped).
+// Thread r of the warpgroup owns TMEM lane / tile row r.  Row-per-thread
+// st.global of the same data measured ≈ 22 GB/s per SM (5.8 us per dK/dV
+// CTA); the bulk store runs at the SM's full write rate.
+template <int kCols>
+__device__ __forceinline__ void store_tile_f32_tma(uint32_t taddr, uint8_t* stage,
+                                                   const CUtensorMap* map, int x0, int y0,
+                                                   float scale, int r, int bar_id) {
+#pragma unroll 1
+  for (int c = 0; c < kCols / 32; ++c) {
+    uint32_t raw[32];
+    tmem_ld_32x32b_x32(taddr + c * 32, raw);
+    tmem_ld_wait();
+    uint8_t* row = stage + c * 16384 + r * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<float4*>(row + ((j ^ (r & 7)) << 4)) =
+          make_float4(__uint_as_float(raw[4 * j]) * scale, __uint_as_float(raw[4 * j + 1]) * scale,
+                      __uint_as_float(raw[4 * j + 2]) * scale,
+                      __uint_as_float(raw[4 * j + 3]) * scale);
+  }
+  fence_proxy_async_smem();
+  named_bar_sync(bar_id, 128);
+  if (r == 0) {
+#pragma unroll
+    for (int c = 0; c < kCols / 32; ++c) tma_store_2d(map, stage + c * 16384, x0 + 32 * c, y0);
+    tma_store_commit_and_wait_read();
+  }
+}
+
 // The 227 KB budget leaves no room for a 1 KB alignment pad: the dynamic
 // window must already be 1024-B aligned (it is when no static smem precedes it).
 __device__ __forceinline__ uint8_t* aligned_smem(uint8_t* raw) {
   if (smem_u32(raw) & 1023u) __trap();
   return raw;
+}
+
+// CTA dispatch order of both backward kernels (1-D grid of tiles x heads).
+// Blocks are dispatched in index order.  Heads are taken in groups of
+// LEMO_FAB_HEAD_GROUP; within a group, tile rank k (heavy first) is the slow
+// index and the head the fast one.  So (a) co-resident CTAs span only a few
+// heads and share their Q/dO (dK/dV) or K/V (dQ) tiles in L2, and (b) every
+// group's heavy CTAs start early -- with one group per head the last head's
+// heaviest CTA started at the very end and left a ~80 us tail (measured
+// with scripts/fab_cta.py); with all heads in one group the L2 reuse is lost
+// (2-7 % slower).
+struct CtaOrder {
+  int tile, head;  // tile rank (0 = heaviest), head
+};
+__device__ __forceinline__ CtaOrder cta_order(int idx, int nblocks, int heads) {
+  const int nt = nblocks / heads;
+  const int G = heads < LEMO_FAB_HEAD_GROUP ? heads : LEMO_FAB_HEAD_GROUP;
+  const int g = idx / (nt * G);
+  const int base = g * G, gs = min(G, heads - base);
+  const int rem = idx - g * nt * G;
+  CtaOrder o;
+  o.tile = rem / gs;
+  o.head = base + rem % gs;
+  return o;
 }
 
 // ---------------------------------------------------------------------------
@@ -130,7 +189,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                           const __grid_constant__ CUtensorMap tmV,
                           const __grid_constant__ CUtensorMap tmO,
                           const float* __restrict__ lse, const float* __restrict__ delta,
-                          float* __restrict__ dk, float* __restrict__ dv, int n, int h, int kv,
+                          const __grid_constant__ CUtensorMap tmdK,
+                          const __grid_constant__ CUtensorMap tmdV, int n, int h, int kv,
                           float sl2, float scale) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = aligned_smem(smem_raw);
@@ -155,15 +215,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // CTA = (key tile, key/value head); with grouped-query attention the loop
   // runs over the `group` query heads sharing this key head (u = g·T + t)
-  // grid (key tiles, kv heads): concurrently resident CTAs belong to the same
-  // head and stream the same Q/dO tiles (L2 reuse).  The alternative order
-  // (heads fastest: every head's heavy CTAs first, as the forward does)
-  // measured 2-7 % slower here (LEMO_FAB_GRID_DKDV / _DQ = 1 select it).
-#if LEMO_FAB_GRID_DKDV
-  const int kb = blockIdx.y, kvh = blockIdx.x;
-#else
-  const int kb = blockIdx.x, kvh = blockIdx.y;
-#endif
+  const CtaOrder co = cta_order(blockIdx.x, gridDim.x, kv / kD);
+  const int kb = co.tile, kvh = co.head;  // key tile 0 has the most query tiles
   const int group = h / kv;
   const int k0 = kb * kT, c0 = kvh * kD;
   const int T = (n - k0 + kT - 1) / kT;  // query tiles from the diagonal on
@@ -191,6 +244,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(mm_done, 1);
     fence_barrier_init();
   }
+#ifdef LEMO_FA_TRACE
+  const int cta_id = blockIdx.x;
+  if (threadIdx.x == 0 && cta_id < 8192) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_fab_cta[0][cta_id][0] = gtimer();
+    g_fab_cta[0][cta_id][2] = smid;
+    g_fab_cta[0][cta_id][3] = U;
+  }
+#endif
   if (warp == 2) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -312,6 +375,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(s_full, u & 1);
       tc_fence_after();
 #ifdef LEMO_FA_TRACE
+      if (u == 0 && warp == 4 && lane == 0 && blockIdx.x < 8192)
+        g_fab_cta[0][blockIdx.x][4] = gtimer();
+#endif
+#ifdef LEMO_FA_TRACE
       if (trace) g_fab_trace[wg][1][u] = clock64();
 #endif
       {
@@ -372,11 +439,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_wait(mm_done, 0);
     tc_fence_after();
-    const bool ok = key < n;
+#ifdef LEMO_FA_TRACE
+    if (warp == 4 && lane == 0 && cta_id < 8192) g_fab_cta[0][cta_id][5] = gtimer();
+#endif
+    // operand buffers are all consumed: stage dV (WG0) / dK (WG1) in smem
     if (wg == 0)
-      store_row_f32<kD>(tdV + lane_off, dv + (size_t)key * kv + c0, 1.f, ok);
+      store_tile_f32_tma<kD>(tdV + lane_off, smem, &tmdV, c0, k0, 1.f, r, 1);
     else
-      store_row_f32<kD>(tdK + lane_off, dk + (size_t)key * kv + c0, scale, ok);
+      store_tile_f32_tma<kD>(tdK + lane_off, smem + kD * kT * 4, &tmdK, c0, k0, scale, r, 2);
   }
   tc_fence_before();
   __syncthreads();
@@ -384,6 +454,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+#ifdef LEMO_FA_TRACE
+  if (threadIdx.x == 0 && cta_id < 8192) g_fab_cta[0][cta_id][1] = gtimer();
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -398,7 +471,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tmV,
                         const __grid_constant__ CUtensorMap tmO,
                         const float* __restrict__ lse, const float* __restrict__ delta,
-                        float* __restrict__ dq, int n, int h, int kv, float sl2, float scale) {
+                        const __grid_constant__ CUtensorMap tmdQ, int n, int h, int kv,
+                        float sl2, float scale) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = aligned_smem(smem_raw);
   uint8_t* sQ = smem;
@@ -419,13 +493,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#if LEMO_FAB_GRID_DQ
-  const int qb = (int)(gridDim.y - 1 - blockIdx.y);  // heavy tiles first (grid: heads, tiles)
-  const int hd = blockIdx.x;
-#else
-  const int qb = (int)(gridDim.x - 1 - blockIdx.x);
-  const int hd = blockIdx.y;
-#endif
+  const CtaOrder co = cta_order(blockIdx.x, gridDim.x, h / kD);
+  const int ntq = (int)gridDim.x / (h / kD);
+  const int qb = ntq - 1 - co.tile, hd = co.head;  // the last query tile has the most key tiles
   const int q0 = qb * kT, c0 = hd * kD;
   const int ck = (hd / (h / kv)) * kD;  // key/value head of this query head
   const int T = qb + 1;  // key tiles 0 … diagonal
@@ -453,6 +523,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(dq_done, 1);
     fence_barrier_init();
   }
+#ifdef LEMO_FA_TRACE
+  const int cta_id = blockIdx.x;
+  if (threadIdx.x == 0 && cta_id < 8192) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_fab_cta[1][cta_id][0] = gtimer();
+    g_fab_cta[1][cta_id][2] = smid;
+    g_fab_cta[1][cta_id][3] = T;
+  }
+#endif
   if (warp == 2) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -569,8 +649,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_wait(dq_done, 0);
     tc_fence_after();
-    store_row_f32<64>(tdQ + lane_off + 64 * wg, dq + (size_t)qr * h + c0 + 64 * wg, scale,
-                      qr < n);
+    store_tile_f32_tma<64>(tdQ + lane_off + 64 * wg, smem + wg * 64 * kT * 4, &tmdQ,
+                           c0 + 64 * wg, q0, scale, r, 1 + wg);
   }
   tc_fence_before();
   __syncthreads();
@@ -578,6 +658,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+#ifdef LEMO_FA_TRACE
+  if (threadIdx.x == 0 && cta_id < 8192) g_fab_cta[1][cta_id][1] = gtimer();
+#endif
 }
 
 }  // namespace fab
@@ -586,6 +669,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef LEMO_FA_TRACE
 extern "C" int lemo_fab_trace_get(void* host) {
   return (int)cudaMemcpyFromSymbol(host, g_fab_trace, sizeof(g_fab_trace));
+}
+extern "C" int lemo_fab_cta_get(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_fab_cta, sizeof(g_fab_cta));
 }
 #endif
 
@@ -610,6 +696,10 @@ int lemo_flash_bwd_tc(const void* q, const void* k, const void* v, const void* o
   if (!rc) rc = make_tma_bf16_2d(&tk, k, (uint64_t)n, (uint64_t)kv, (uint64_t)kv, fab::kT);
   if (!rc) rc = make_tma_bf16_2d(&tv, v, (uint64_t)n, (uint64_t)kv, (uint64_t)kv, fab::kT);
   if (!rc) rc = make_tma_bf16_2d(&to, dout, (uint64_t)n, (uint64_t)h, (uint64_t)h, fab::kT);
+  CUtensorMap tdq, tdk, tdv;  // fp32 gradient outputs (TMA stores)
+  if (!rc) rc = make_tma_f32_2d(&tdq, dq, (uint64_t)n, (uint64_t)h, (uint64_t)h, fab::kT);
+  if (!rc) rc = make_tma_f32_2d(&tdk, dk, (uint64_t)n, (uint64_t)kv, (uint64_t)kv, fab::kT);
+  if (!rc) rc = make_tma_f32_2d(&tdv, dv, (uint64_t)n, (uint64_t)kv, (uint64_t)kv, fab::kT);
   if (rc) LEMO_RETURN_RC("lemo_flash_bwd_tc", rc);
   static bool attr = false;
   if (!attr) {
@@ -625,10 +715,10 @@ int lemo_flash_bwd_tc(const void* q, const void* k, const void* v, const void* o
   const float sl2 = scale * fab::kLog2e;
   const int nt = (n + fab::kT - 1) / fab::kT;
   cudaStream_t st = (cudaStream_t)stream;
-  fab::flash_bwd_dkdv_kernel<<<LEMO_FAB_GRID_DKDV ? dim3(kv / head_dim, nt) : dim3(nt, kv / head_dim), fab::kThreads, fab::kSmemKV, st>>>(
-      tq, tk, tv, to, lse, delta, dk, dv, n, h, kv, sl2, scale);
-  fab::flash_bwd_dq_kernel<<<LEMO_FAB_GRID_DQ ? dim3(h / head_dim, nt) : dim3(nt, h / head_dim), fab::kThreads, fab::kSmemQ, st>>>(
-      tq, tk, tv, to, lse, delta, dq, n, h, kv, sl2, scale);
+  fab::flash_bwd_dkdv_kernel<<<nt * (kv / head_dim), fab::kThreads, fab::kSmemKV, st>>>(
+      tq, tk, tv, to, lse, delta, tdk, tdv, n, h, kv, sl2, scale);
+  fab::flash_bwd_dq_kernel<<<nt * (h / head_dim), fab::kThreads, fab::kSmemQ, st>>>(
+      tq, tk, tv, to, lse, delta, tdq, n, h, kv, sl2, scale);
   LEMO_CHECK_LAUNCH("lemo_flash_bwd_tc");
   return 0;
 }

@@ -463,6 +463,9 @@ struct GemmShape {
 // over a row-major [rows, cols] matrix with a (box_rows x 64) SW128 box.
 int make_tma_bf16_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols,
                      uint64_t ld_elems, uint32_t box_rows);
+// fp32 row-major [rows, cols] with a (box_rows x 32) SW128 box (TMA stores)
+int make_tma_f32_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols,
+                    uint64_t ld_elems, uint32_t box_rows);
 
 int gemm_num_sms();
 

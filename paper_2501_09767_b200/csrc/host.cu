@@ -64,9 +64,24 @@ struct TmaKeyHash {
 static std::mutex g_tma_mu;
 static std::unordered_map<TmaKey, CUtensorMap, TmaKeyHash> g_tma_cache;
 
+static int make_tma_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols,
+                       uint64_t ld_elems, uint32_t box_rows, bool f32);
+
 int make_tma_bf16_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols,
                      uint64_t ld_elems, uint32_t box_rows) {
-  TmaKey key{(uint64_t)base, rows, cols, ld_elems, box_rows};
+  return make_tma_2d(out, base, rows, cols, ld_elems, box_rows, false);
+}
+
+int make_tma_f32_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols,
+                    uint64_t ld_elems, uint32_t box_rows) {
+  return make_tma_2d(out, base, rows, cols, ld_elems, box_rows, true);
+}
+
+// box = (128 B of columns) x box_rows, SWIZZLE_128B; f32 keys are tagged in `box`
+static int make_tma_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols,
+                       uint64_t ld_elems, uint32_t box_rows, bool f32) {
+  const uint64_t esz = f32 ? 4 : 2;
+  TmaKey key{(uint64_t)base, rows, cols, ld_elems, box_rows | (f32 ? (1ull << 40) : 0ull)};
   {
     std::lock_guard<std::mutex> lk(g_tma_mu);
     auto it = g_tma_cache.find(key);
@@ -80,15 +95,16 @@ int make_tma_bf16_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t
     set_error_msg("cuTensorMapEncodeTiled unavailable");
     return LEMO_ERR_REPORTED;
   }
-  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld_elems * 2) & 15)) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld_elems * esz) & 15)) {
     set_error_msg("TMA operand must be 16-byte aligned with a 16-byte multiple row pitch");
     return LEMO_ERR_REPORTED;
   }
   cuuint64_t gdim[2] = {cols, rows};
-  cuuint64_t gstride[1] = {ld_elems * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint64_t gstride[1] = {ld_elems * esz};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / esz), box_rows};
   cuuint32_t estride[2] = {1, 1};
-  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim,
+  CUresult r = fn(out, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                  2, const_cast<void*>(base), gdim,
                   gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
