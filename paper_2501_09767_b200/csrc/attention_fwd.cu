@@ -79,7 +79,7 @@ __device__ __forceinline__ void mma_pv(uint32_t d, uint32_t p, uint32_t b, bool 
 
 __global__ void __launch_bounds__(kThreads, 1)
     flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                     const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ o,
+                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                      float* __restrict__ lse, int n, int h, int group, float sl2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = aligned_smem(smem_raw);
@@ -295,21 +295,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&o_done[g], 0);
       tc_fence_after();
       const float inv_l = 1.f / l;
+      // O_g = acc / l as bf16, staged over Q_g (every MMA reading it is done)
+      // in two 64-column SW128 boxes, then written by TMA (rows ≥ n clipped)
+      uint8_t* stage = sQ + g * kTile;
 #pragma unroll 1
       for (int c = 0; c < kD / 32; ++c) {
         uint32_t raw[32];
         tmem_ld_32x32b_x32(tO + c * 32, raw);
         tmem_ld_wait();
-        if (qr < n) {
-          uint4* dst = reinterpret_cast<uint4*>(o + (size_t)qr * h + c0 + c * 32);
+        uint8_t* row = stage + (c >> 1) * kBox + r * 128;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            dst[q] = make_uint4(
-                pack_bf16x2(__uint_as_float(raw[8 * q + 0]) * inv_l, __uint_as_float(raw[8 * q + 1]) * inv_l),
-                pack_bf16x2(__uint_as_float(raw[8 * q + 2]) * inv_l, __uint_as_float(raw[8 * q + 3]) * inv_l),
-                pack_bf16x2(__uint_as_float(raw[8 * q + 4]) * inv_l, __uint_as_float(raw[8 * q + 5]) * inv_l),
-                pack_bf16x2(__uint_as_float(raw[8 * q + 6]) * inv_l, __uint_as_float(raw[8 * q + 7]) * inv_l));
-        }
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<uint4*>(row + ((((c & 1) * 4 + q) ^ (r & 7)) << 4)) = make_uint4(
+              pack_bf16x2(__uint_as_float(raw[8 * q + 0]) * inv_l, __uint_as_float(raw[8 * q + 1]) * inv_l),
+              pack_bf16x2(__uint_as_float(raw[8 * q + 2]) * inv_l, __uint_as_float(raw[8 * q + 3]) * inv_l),
+              pack_bf16x2(__uint_as_float(raw[8 * q + 4]) * inv_l, __uint_as_float(raw[8 * q + 5]) * inv_l),
+              pack_bf16x2(__uint_as_float(raw[8 * q + 6]) * inv_l, __uint_as_float(raw[8 * q + 7]) * inv_l));
+      }
+      fence_proxy_async_smem();
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+      if (r == 0) {
+        tma_store_2d(&tmO, stage, c0, qt * kT);
+        tma_store_2d(&tmO, stage + kBox, c0 + 64, qt * kT);
+        tma_store_commit_and_wait_read();
       }
       if (qr < n) lse[(size_t)hd * n + qr] = (m + log2f(l)) * kLn2;
     }
@@ -345,6 +353,8 @@ int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, floa
   int rc = make_tma_bf16_2d(&tq, q, (uint64_t)n, (uint64_t)h, (uint64_t)h, faf::kT);
   if (!rc) rc = make_tma_bf16_2d(&tk, k, (uint64_t)n, (uint64_t)kv, (uint64_t)kv, faf::kT);
   if (!rc) rc = make_tma_bf16_2d(&tv, v, (uint64_t)n, (uint64_t)kv, (uint64_t)kv, faf::kT);
+  CUtensorMap to;  // output (TMA stores)
+  if (!rc) rc = make_tma_bf16_2d(&to, o, (uint64_t)n, (uint64_t)h, (uint64_t)h, faf::kT);
   if (rc) LEMO_RETURN_RC("lemo_flash_fwd_tc", rc);
   static bool attr = false;
   if (!attr) {
@@ -356,7 +366,7 @@ int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, floa
   const int nt = (n + faf::kT - 1) / faf::kT;
   dim3 grid(h / head_dim, (nt + 1) / 2);
   faf::flash_fwd_kernel<<<grid, faf::kThreads, faf::kSmem, (cudaStream_t)stream>>>(
-      tq, tk, tv, reinterpret_cast<__nv_bfloat16*>(o), lse, n, h, h / kv, scale * faf::kLog2e);
+      tq, tk, tv, to, lse, n, h, h / kv, scale * faf::kLog2e);
   LEMO_CHECK_LAUNCH("lemo_flash_fwd_tc");
   return 0;
 }
