@@ -353,7 +353,6 @@ struct Bound {
 };
 
 template <> struct PairTailOK<Bound<256, EpiStoreF32>> { static constexpr bool value = true; };
-template <> struct PairTailOK<Bound<256, EpiScatterAdd>> { static constexpr bool value = true; };
 template <> struct PairTailOK<Bound<256, EpiStoreBF16>> { static constexpr bool value = true; };
 
 // BN = 256 GEMMs run as CTA pairs (256 x 256 tiles) when M spans at least two
