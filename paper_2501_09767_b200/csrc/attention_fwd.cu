@@ -38,6 +38,9 @@ namespace faf {
 
 constexpr int kT = 128;
 constexpr int kD = 128;
+#ifndef LEMO_FA_HEAD_GROUP
+#define LEMO_FA_HEAD_GROUP 8
+#endif
 #ifndef LEMO_FA_POLY
 #define LEMO_FA_POLY 0
 #endif
@@ -99,10 +102,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = (n + kT - 1) / kT;
-  // grid (heads, pairs): blocks are dispatched x-fastest, so every head's heavy
-  // (late, long) pairs go first and the light ones fill the tail
-  const int pair = (int)(gridDim.y - 1 - blockIdx.y);
-  const int hd = blockIdx.x, c0 = hd * kD;
+  // 1-D grid over (pairs x heads), dispatched in index order: heads in groups
+  // of LEMO_FA_HEAD_GROUP, heavy (late) pairs first within a group, so the
+  // co-resident CTAs share a few heads' K/V in L2 and no heavy pair starts late
+  const int heads = h / kD, npairs = (int)gridDim.x / heads;
+  const int G = heads < LEMO_FA_HEAD_GROUP ? heads : LEMO_FA_HEAD_GROUP;
+  const int grp = (int)blockIdx.x / (npairs * G), gbase = grp * G;
+  const int gsz = min(G, heads - gbase), rem = (int)blockIdx.x - grp * npairs * G;
+  const int pair = npairs - 1 - rem / gsz;
+  const int hd = gbase + rem % gsz, c0 = hd * kD;
   const int ck = (hd / group) * kD;  // key/value head of this query head
   const int qt0 = 2 * pair;
   const bool two = qt0 + 1 < nt;
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j <= qt; ++j) {
 #ifdef LEMO_FA_TRACE
-        const bool trace = blockIdx.x == 0 && blockIdx.y == 0 && r == 0 && j < 64;
+        const bool trace = blockIdx.x == 0 && r == 0 && j < 64;
         if (trace) g_fa_trace[g][0][j] = clock64();
 #endif
         mbar_wait(&s_full[g], j & 1);
@@ -364,7 +372,7 @@ int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, floa
     attr = true;
   }
   const int nt = (n + faf::kT - 1) / faf::kT;
-  dim3 grid(h / head_dim, (nt + 1) / 2);
+  dim3 grid((h / head_dim) * ((nt + 1) / 2));
   faf::flash_fwd_kernel<<<grid, faf::kThreads, faf::kSmem, (cudaStream_t)stream>>>(
       tq, tk, tv, to, lse, n, h, h / kv, scale * faf::kLog2e);
   LEMO_CHECK_LAUNCH("lemo_flash_fwd_tc");
