@@ -95,31 +95,12 @@ __device__ __forceinline__ void st_bf16x32(uint32_t taddr, const float* v) {
   tmem_st_32x32b_x16(taddr, p);
 }
 
-// This thread's TMEM row segment [0, kCols) × scale → fp32 dst.
-template <int kCols>
-__device__ __forceinline__ void store_row_f32(uint32_t taddr, float* dst, float scale, bool ok) {
-#pragma unroll 1
-  for (int c = 0; c < kCols / 32; ++c) {
-    uint32_t raw[32];
-    tmem_ld_32x32b_x32(taddr + c * 32, raw);
-    tmem_ld_wait();
-    if (ok) {
-      float4* p = reinterpret_cast<float4*>(dst + c * 32);
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        p[q] = make_float4(__uint_as_float(raw[4 * q]) * scale, __uint_as_float(raw[4 * q + 1]) * scale,
-                           __uint_as_float(raw[4 * q + 2]) * scale,
-                           __uint_as_float(raw[4 * q + 3]) * scale);
-    }
-  }
-}
-
 // A warpgroup's 128 rows x kCols fp32 accumulator (TMEM columns [0, kCols)
 // at taddr, times scale) -> global via smem staging and TMA tile stores
 // (boxes of 128 rows x 32 columns, SW128; rows past the tensor are clipped).
 // Thread r of the warpgroup owns TMEM lane / tile row r.  Row-per-thread
-// st.global of the same data measured ≈ 22 GB/s per SM (5.8 us per dK/dV
-// CTA); the bulk store runs at the SM's full write rate.
+// st.global of the same data (the previous epilogue) measured ≈ 22 GB/s per
+// SM, 5.8 us per dK/dV CTA; this one takes 3.3 us (scripts/fab_cta.py).
 template <int kCols>
 __device__ __forceinline__ void store_tile_f32_tma(uint32_t taddr, uint8_t* stage,
                                                    const CUtensorMap* map, int x0, int y0,
