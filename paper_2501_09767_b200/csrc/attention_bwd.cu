@@ -105,26 +105,27 @@ template <int kCols>
 __device__ __forceinline__ void store_tile_f32_tma(uint32_t taddr, uint8_t* stage,
                                                    const CUtensorMap* map, int x0, int y0,
                                                    float scale, int r, int bar_id) {
-#pragma unroll 1
+  // all TMEM loads in flight before one wait; each 32-column box is handed to
+  // the TMA engine as soon as the warpgroup has staged it
+  uint32_t raw[kCols / 32][32];
+#pragma unroll
+  for (int c = 0; c < kCols / 32; ++c) tmem_ld_32x32b_x32(taddr + c * 32, raw[c]);
+  tmem_ld_wait();
+#pragma unroll
   for (int c = 0; c < kCols / 32; ++c) {
-    uint32_t raw[32];
-    tmem_ld_32x32b_x32(taddr + c * 32, raw);
-    tmem_ld_wait();
     uint8_t* row = stage + c * 16384 + r * 128;
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       *reinterpret_cast<float4*>(row + ((j ^ (r & 7)) << 4)) =
-          make_float4(__uint_as_float(raw[4 * j]) * scale, __uint_as_float(raw[4 * j + 1]) * scale,
-                      __uint_as_float(raw[4 * j + 2]) * scale,
-                      __uint_as_float(raw[4 * j + 3]) * scale);
+          make_float4(__uint_as_float(raw[c][4 * j]) * scale,
+                      __uint_as_float(raw[c][4 * j + 1]) * scale,
+                      __uint_as_float(raw[c][4 * j + 2]) * scale,
+                      __uint_as_float(raw[c][4 * j + 3]) * scale);
+    fence_proxy_async_smem();
+    named_bar_sync(bar_id, 128);
+    if (r == 0) tma_store_2d(map, stage + c * 16384, x0 + 32 * c, y0);
   }
-  fence_proxy_async_smem();
-  named_bar_sync(bar_id, 128);
-  if (r == 0) {
-#pragma unroll
-    for (int c = 0; c < kCols / 32; ++c) tma_store_2d(map, stage + c * 16384, x0 + 32 * c, y0);
-    tma_store_commit_and_wait_read();
-  }
+  if (r == 0) tma_store_commit_and_wait_read();
 }
 
 // The 227 KB budget leaves no room for a 1 KB alignment pad: the dynamic
