@@ -163,6 +163,7 @@ __device__ __forceinline__ CtaOrder cta_order(int idx, int nblocks, int heads) {
 // dK / dV
 
 constexpr int kQStages = 3, kOStages = 2;
+static_assert(kOStages <= kQStages, "the pre-barrier loads fill both rings' first kOStages slots");
 constexpr int kSmemKV = (2 + kQStages + kOStages) * kTile + 2 * 2 * kT * 4 + 256;
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -225,6 +226,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(ds_full, 8);
     mbar_init(mm_done, 1);
     fence_barrier_init();
+    // the first loads go out before the TMEM allocation / CTA barrier (their
+    // ring slots are free on the first pass, so no waits are needed)
+    mbar_arrive_expect_tx(kv_full, 2 * kTile);
+    tma_load_2d(&tmK, kv_full, sK, c0, k0);
+    tma_load_2d(&tmK, kv_full, sK + kBox, c0 + 64, k0);
+    tma_load_2d(&tmV, kv_full, sV, c0, k0);
+    tma_load_2d(&tmV, kv_full, sV + kBox, c0 + 64, k0);
+    for (int t = 0; t < min(U, kOStages); ++t) {
+      const int q0 = k0 + (t % T) * kT, cq = (kvh * group + t / T) * kD;
+      mbar_arrive_expect_tx(&q_full[t], kTile);
+      tma_load_2d(&tmQ, &q_full[t], sQ + t * kTile, cq, q0);
+      tma_load_2d(&tmQ, &q_full[t], sQ + t * kTile + kBox, cq + 64, q0);
+      mbar_arrive_expect_tx(&o_full[t], kTile);
+      tma_load_2d(&tmO, &o_full[t], sO + t * kTile, cq, q0);
+      tma_load_2d(&tmO, &o_full[t], sO + t * kTile + kBox, cq + 64, q0);
+    }
   }
 #ifdef LEMO_FA_TRACE
   const int cta_id = blockIdx.x;
@@ -245,12 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(kv_full, 2 * kTile);
-      tma_load_2d(&tmK, kv_full, sK, c0, k0);
-      tma_load_2d(&tmK, kv_full, sK + kBox, c0 + 64, k0);
-      tma_load_2d(&tmV, kv_full, sV, c0, k0);
-      tma_load_2d(&tmV, kv_full, sV + kBox, c0 + 64, k0);
-      for (int t = 0; t < U; ++t) {
+      for (int t = min(U, kOStages); t < U; ++t) {
         const int q0 = k0 + (t % T) * kT, cq = (kvh * group + t / T) * kD;
         const int sq = t % kQStages, so = t % kOStages;
         mbar_wait(&q_empty[sq], ((t / kQStages) & 1) ^ 1);
@@ -445,6 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // dQ
 
 constexpr int kKStages = 3, kVStages = 2;
+static_assert(kVStages <= kKStages, "the pre-barrier loads fill both rings' first kVStages slots");
 constexpr int kSmemQ = (2 + kKStages + kVStages) * kTile + 256;
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -504,6 +517,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(ds_full, 8);
     mbar_init(dq_done, 1);
     fence_barrier_init();
+    // the first loads go out before the TMEM allocation / CTA barrier
+    mbar_arrive_expect_tx(q_full, 2 * kTile);
+    tma_load_2d(&tmQ, q_full, sQ, c0, q0);
+    tma_load_2d(&tmQ, q_full, sQ + kBox, c0 + 64, q0);
+    tma_load_2d(&tmO, q_full, sO, c0, q0);
+    tma_load_2d(&tmO, q_full, sO + kBox, c0 + 64, q0);
+    for (int j = 0; j < min(T, kVStages); ++j) {
+      mbar_arrive_expect_tx(&k_full[j], kTile);
+      tma_load_2d(&tmK, &k_full[j], sK + j * kTile, ck, j * kT);
+      tma_load_2d(&tmK, &k_full[j], sK + j * kTile + kBox, ck + 64, j * kT);
+      mbar_arrive_expect_tx(&v_full[j], kTile);
+      tma_load_2d(&tmV, &v_full[j], sV + j * kTile, ck, j * kT);
+      tma_load_2d(&tmV, &v_full[j], sV + j * kTile + kBox, ck + 64, j * kT);
+    }
   }
 #ifdef LEMO_FA_TRACE
   const int cta_id = blockIdx.x;
@@ -524,12 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, 2 * kTile);
-      tma_load_2d(&tmQ, q_full, sQ, c0, q0);
-      tma_load_2d(&tmQ, q_full, sQ + kBox, c0 + 64, q0);
-      tma_load_2d(&tmO, q_full, sO, c0, q0);
-      tma_load_2d(&tmO, q_full, sO + kBox, c0 + 64, q0);
-      for (int j = 0; j < T; ++j) {
+      for (int j = min(T, kVStages); j < T; ++j) {
         const int sk = j % kKStages, sv = j % kVStages;
         mbar_wait(&k_empty[sk], ((j / kKStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&k_full[sk], kTile);
