@@ -135,6 +135,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&o_done[g], 1);
     }
     fence_barrier_init();
+    // the first loads go out before the TMEM allocation / CTA barrier (first
+    // pass over the rings: no empty-slot waits needed)
+    mbar_arrive_expect_tx(q_full, (two ? 2 : 1) * kTile);
+    for (int g = 0; g < (two ? 2 : 1); ++g) {
+      tma_load_2d(&tmQ, q_full, sQ + g * kTile, c0, (qt0 + g) * kT);
+      tma_load_2d(&tmQ, q_full, sQ + g * kTile + kBox, c0 + 64, (qt0 + g) * kT);
+    }
+    for (int j = 0; j < min(T, kVStages); ++j) {
+      mbar_arrive_expect_tx(&k_full[j], kTile);
+      tma_load_2d(&tmK, &k_full[j], sK + j * kTile, ck, j * kT);
+      tma_load_2d(&tmK, &k_full[j], sK + j * kTile + kBox, ck + 64, j * kT);
+      mbar_arrive_expect_tx(&v_full[j], kTile);
+      tma_load_2d(&tmV, &v_full[j], sV + j * kTile, ck, j * kT);
+      tma_load_2d(&tmV, &v_full[j], sV + j * kTile + kBox, ck + 64, j * kT);
+    }
   }
   if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
@@ -144,12 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 8) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, (two ? 2 : 1) * kTile);
-      for (int g = 0; g < (two ? 2 : 1); ++g) {
-        tma_load_2d(&tmQ, q_full, sQ + g * kTile, c0, (qt0 + g) * kT);
-        tma_load_2d(&tmQ, q_full, sQ + g * kTile + kBox, c0 + 64, (qt0 + g) * kT);
-      }
-      for (int j = 0; j < T; ++j) {
+      for (int j = min(T, kVStages); j < T; ++j) {
         const int sk = j % kKStages, sv = j % kVStages;
         mbar_wait(&k_empty[sk], ((j / kKStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&k_full[sk], kTile);
