@@ -222,16 +222,29 @@ class ThresholdSet:
 
 
 class SelectWorkspace:
-    """Reusable device/pinned buffers for one select call (sized by nb)."""
+    """Buffers of one select call.  The retained block / token lists are fresh
+    per call (the returned pattern keeps views of them); the scratch mask,
+    counters and the pinned read-back slot are cached per (device, nb) -- they
+    are consumed before select_device returns (it synchronises)."""
+
+    _scratch: dict = {}
 
     def __init__(self, nb: int, n_tokens: int, block_size: int, device):
         self.nb = nb
-        self.mask = torch.empty(max(nb, 1), dtype=torch.uint8, device=device)
         self.blocks = torch.empty(max(nb, 1), dtype=torch.int32, device=device)
         self.tokens = torch.empty(max(nb * block_size, 1), dtype=torch.int32, device=device)
-        self.counts = torch.empty(4, dtype=torch.int32, device=device)
-        self.thr = torch.empty(1, dtype=torch.float64, device=device)
-        self.host = torch.empty(6, dtype=torch.float64, pin_memory=True)
+        key = (str(device), nb)
+        sc = SelectWorkspace._scratch.get(key)
+        if sc is None:
+            host_i = torch.empty(4, dtype=torch.int32, pin_memory=True)
+            host_f = torch.empty(1, dtype=torch.float64, pin_memory=True)
+            sc = (torch.empty(max(nb, 1), dtype=torch.uint8, device=device),
+                  torch.empty(4, dtype=torch.int32, device=device),
+                  torch.empty(1, dtype=torch.float64, device=device), host_i, host_f,
+                  host_i.numpy(), host_f.numpy())
+            SelectWorkspace._scratch[key] = sc
+        (self.mask, self.counts, self.thr, self.host_i, self.host_f, self.host_i_np,
+         self.host_f_np) = sc
 
 
 def _force_mask(force_blocks, nb, device):
@@ -262,15 +275,16 @@ def select_device(vec: torch.Tensor, threshold: float | None = None, *, thr_dev=
     thr = 0.0 if threshold is None else float(threshold)
     ops.select(vec, b=block_size, n_tokens=n_tokens, thr=thr, thr_dev=thr_dev, force=force,
                mask=ws.mask, blocks=ws.blocks, tokens=ws.tokens, counts=ws.counts, thr_out=ws.thr)
-    ws.host[:3].copy_(ws.counts[:3].to(torch.float64), non_blocking=True)
-    ws.host[3:4].copy_(ws.thr, non_blocking=True)
+    ws.host_i.copy_(ws.counts, non_blocking=True)
+    ws.host_f.copy_(ws.thr, non_blocking=True)
     torch.cuda.current_stream().synchronize()
-    k, nkept, bad = int(ws.host[0]), int(ws.host[1]), int(ws.host[2])
+    hi = ws.host_i_np  # numpy views of the pinned slots: no per-element tensor dispatch
+    k, nkept, bad, used = int(hi[0]), int(hi[1]), int(hi[2]), float(ws.host_f_np[0])
     if bad:
         raise ContractError("block scores must be finite")
     pat = SparsityPattern._from_device(layer_id, component, block_size, n_tokens, ws.blocks,
                                        ws.tokens, nkept, k)
-    return pat, float(ws.host[3])
+    return pat, used
 
 
 def _as_device_vec(block_scores, device=None) -> torch.Tensor:
