@@ -32,6 +32,7 @@
 // debug builds only: timestamps of the heaviest dK/dV CTA (key tile 0, head 0)
 // [0] before S wait, [1] S ready, [2] P arrive, [3] dP ready, [4] dS arrive
 __device__ unsigned long long g_fab_trace[3][8][128];
+__device__ unsigned long long g_fabq_trace[2][5][128];  // dQ kernel [wg][event][key tile]
 __device__ unsigned long long g_fab_cta[2][8192][6];  // [kernel][cta]: start, end, smid, units, first S seen, all MMAs done
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -611,9 +612,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kw = j * kT + 64 * wg;  // first key of this WG's columns
       const bool edge = (j == qb) || (kw + 64 > n) || (qr >= n);
       float p[64];
+#ifdef LEMO_FA_TRACE
+      const bool qtrace = blockIdx.x == 0 && r == 0 && j < 128;
+      if (qtrace) g_fabq_trace[wg][0][j] = clock64();
+#endif
       // phase A: P (registers only; both halves in flight before one wait)
       mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
+#ifdef LEMO_FA_TRACE
+      if (qtrace) g_fabq_trace[wg][1][j] = clock64();
+#endif
       {
         uint32_t raw[64];
         const uint32_t ts = tmem + 128 * b + lane_off + 64 * wg;
@@ -633,9 +641,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_free[b]);
+#ifdef LEMO_FA_TRACE
+      if (qtrace) g_fabq_trace[wg][2][j] = clock64();
+#endif
       // phase B: dS
       mbar_wait(dp_full, j & 1);
       tc_fence_after();
+#ifdef LEMO_FA_TRACE
+      if (qtrace) g_fabq_trace[wg][3][j] = clock64();
+#endif
       {
         uint32_t raw[64];
         tmem_ld_32x32b_x32(tPw, *reinterpret_cast<uint32_t(*)[32]>(raw));
@@ -650,6 +664,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
+#ifdef LEMO_FA_TRACE
+      if (qtrace) g_fabq_trace[wg][4][j] = clock64();
+#endif
     }
     mbar_wait(dq_done, 0);
     tc_fence_after();
@@ -673,6 +690,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef LEMO_FA_TRACE
 extern "C" int lemo_fab_trace_get(void* host) {
   return (int)cudaMemcpyFromSymbol(host, g_fab_trace, sizeof(g_fab_trace));
+}
+extern "C" int lemo_fabq_trace_get(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_fabq_trace, sizeof(g_fabq_trace));
 }
 extern "C" int lemo_fab_cta_get(void* host) {
   return (int)cudaMemcpyFromSymbol(host, g_fab_cta, sizeof(g_fab_cta));
