@@ -16,7 +16,8 @@
 //            dV += Pᵀ·dO_t, dK += dSᵀ·Q_t  (A operand read from TMEM)
 //          issue order  S(0) dP(0) | dV(t) S(t+1) dK(t) dP(t+1) | …  so the
 //          tensor core computes S(t+1) while phase B(t) runs and dP(t+1) while
-//          phase A(t+1) runs.  dV, dK stay in TMEM (4 × 128 columns in all).
+//          phase A(t+1) runs; dV(t) goes out in two K halves as each half of
+//          Pᵀ is stored.  dV, dK stay in TMEM (4 × 128 columns in all).
 //   dQ     CTA = one 128-query tile, thread = query row.  Per key tile j:
 //            S_j = Q·K_jᵀ (double-buffered), dP_j = dO·V_jᵀ,
 //            phase A: P = exp2(S·c − lse₂) (registers), phase B: dS = P∘(dP − Δ)
@@ -25,20 +26,28 @@
 //
 // A later MMA that overwrites TMEM columns still read (as bf16 A operand) by
 // an earlier one is safe without a wait: tcgen05.mma executes in issue order.
+// The MMA warp issues warp-collectively (umma_*_w: elect.sync inside the asm).
+// CTAs are dispatched in head groups, heavy tiles first (cta_order); the first
+// tiles are loaded before the TMEM allocation; gradients leave through smem
+// staging + TMA tile stores (store_tile_f32_tma).  Timelines: scripts/
+// fab_trace.py, fabq_trace.py, fab_cta.py (debug build, -DLEMO_FA_TRACE).
 #include "gemm.cuh"
 #include "lemo_internal.h"
 
 #ifdef LEMO_FA_TRACE
-// debug builds only: timestamps of the heaviest dK/dV CTA (key tile 0, head 0)
-// [0] before S wait, [1] S ready, [2] P arrive, [3] dP ready, [4] dS arrive
+// debug builds only.  Heaviest dK/dV CTA (key tile 0, head 0), [EW wg0, wg1,
+// MMA warp][event][tile]: EW [0] before S wait, [1] S ready, [2] P arrive,
+// [3] dP ready, [4] dS arrive; MMA [0] p_full seen, [1] dV,S issued, [2]
+// ds_full seen, [3] dK,dP issued, [6]/[7] q_full/o_full seen.
 __device__ unsigned long long g_fab_trace[3][8][128];
 __device__ unsigned long long g_fabq_trace[2][5][128];  // dQ kernel [wg][event][key tile]
-__device__ unsigned long long g_fab_cta[2][8192][6];  // [kernel][cta]: start, end, smid, units, first S seen, all MMAs done
+// per CTA [kernel][cta]: start, end, smid, units, first S seen, all MMAs done
+__device__ unsigned long long g_fab_cta[2][8192][6];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
-}  // [EW wg0, wg1, MMA warp][event][tile]
+}
 #endif
 
 namespace lemo {
