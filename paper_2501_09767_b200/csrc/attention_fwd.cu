@@ -16,14 +16,16 @@
 // lazy (only when the running max grows by > 8 in log2 units) and need no
 // extra wait: when S_g(j) is complete, PV_g(j-1) is complete too.
 // Measured timeline (scripts/fa_trace.py, 8K rows): softmax of a 128-key tile
-// ≈ 1850 clk per warpgroup, then ≈ 1630 clk until the next S is ready (PV + S
-// on the tensor core ≈ 1024 + issue/commit latency ≈ 600): the loop is bound
-// by E + L + 1024 per warpgroup; the softmax is MUFU/issue-bound, and both a
-// speculative-max pass and FMA-pipe exponentials measured slower.
-// Row max with 3-input FMNMX3, scaling and row sums with packed FFMA2/FADD2.
-// (Moving a share of the exponentials to an FMA-pipe degree-3 polynomial, the
-// FA4 trick, measured slower on this kernel and on the backward: 1/4 of them
-// → −11 % forward, −2 % backward — the SFU is not the binding limit here.)
+// ≈ 1.85 k cycles per warpgroup (two warpgroups exponentiating at once), then
+// ≈ 1.45 k until the next S is ready (PV + S on the tensor core + issue /
+// commit latency): the loop is bound by E + L + 1024 per warpgroup.  An
+// ablation without exponentials cuts E to 1.07 k; FMA-pipe polynomial or
+// f16x2 exponentials and SFU turn-taking between the warpgroups all measured
+// neutral or slower.  Row max with 3-input FMNMX3, scaling and
+// row sums with packed FFMA2/FADD2.  The MMA warp issues warp-collectively;
+// CTAs are dispatched in head groups of LEMO_FA_HEAD_GROUP, heavy pairs
+// first; the first Q/K/V loads precede the TMEM allocation; O leaves through
+// smem staging (over the finished Q tile) and TMA tile stores.
 #include "gemm.cuh"
 #include "lemo_internal.h"
 
