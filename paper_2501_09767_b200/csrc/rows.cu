@@ -233,6 +233,29 @@ __global__ void mlp_compact_kernel(const __nv_bfloat16* __restrict__ gu_all, int
   const int s = __ldg(idx + row);
   const uint4* src = reinterpret_cast<const uint4*>(gu_all + (size_t)s * ldgu);
   uint4* dst = reinterpret_cast<uint4*>(gu_out + (size_t)row * ldgu);
+  if (!relu && ldgu == 2 * m_pad) {
+    // one pass: every 8-column gate chunk and its up chunk are read once,
+    // copied to the compact row and turned into 8 SwiGLU outputs
+    for (int c8 = threadIdx.x; c8 < (m_pad >> 3); c8 += blockDim.x) {
+      const int mc = c8 * 8;
+      const int gcol = (mc >> 7) * 256 + (mc & 127);
+      const uint4 g = src[gcol >> 3];
+      const uint4 u = src[(gcol + 128) >> 3];
+      dst[gcol >> 3] = g;
+      dst[(gcol + 128) >> 3] = u;
+      const uint32_t gv[4] = {g.x, g.y, g.z, g.w}, uv[4] = {u.x, u.y, u.z, u.w};
+      float in[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float g0 = bf16_lo(gv[e]), g1 = bf16_hi(gv[e]);
+        in[2 * e] = g0 * sigmoid_stable(g0) * bf16_lo(uv[e]);
+        in[2 * e + 1] = g1 * sigmoid_stable(g1) * bf16_hi(uv[e]);
+      }
+      reinterpret_cast<uint4*>(inner_out + (size_t)row * m_pad)[c8] =
+          make_uint4(pack_bf16x2(in[0], in[1]), pack_bf16x2(in[2], in[3]),
+                     pack_bf16x2(in[4], in[5]), pack_bf16x2(in[6], in[7]));
+    }
+  } else {
   for (int c = threadIdx.x; c < (ldgu >> 3); c += blockDim.x) dst[c] = src[c];
   // inner: silu -> 8 columns at a time from one 8-col group of gate and up
   for (int c8 = threadIdx.x; c8 < (m_pad >> 3); c8 += blockDim.x) {
@@ -261,6 +284,7 @@ __global__ void mlp_compact_kernel(const __nv_bfloat16* __restrict__ gu_all, int
     reinterpret_cast<uint4*>(inner_out + (size_t)row * m_pad)[c8] =
         make_uint4(pack_bf16x2(in[0], in[1]), pack_bf16x2(in[2], in[3]),
                    pack_bf16x2(in[4], in[5]), pack_bf16x2(in[6], in[7]));
+  }
   }
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)s * ldx);
   uint2* xo = reinterpret_cast<uint2*>(xg_out + (size_t)row * h);
