@@ -172,6 +172,26 @@ __global__ void flash_bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
                                        float* __restrict__ delta, int n, int h, int D) {
   const int row = blockIdx.x;
   const int H = h / D;
+  if (D == 128) {
+    // 16-byte loads: a half-warp covers one head (16 lanes x 8 elements)
+    const int lane16 = threadIdx.x & 15;
+    for (int base = 0; base < H; base += blockDim.x >> 4) {  // warp-uniform trip count
+      const int hd = base + (threadIdx.x >> 4);
+      const bool ok = hd < H;
+      const size_t off = (size_t)row * h + (ok ? hd : 0) * 128 + lane16 * 8;
+      const uint4 a = ok ? *reinterpret_cast<const uint4*>(o + off) : make_uint4(0, 0, 0, 0);
+      const uint4 b = ok ? *reinterpret_cast<const uint4*>(dout + off) : make_uint4(0, 0, 0, 0);
+      const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        acc += bf16_lo(av[e]) * bf16_lo(bv[e]) + bf16_hi(av[e]) * bf16_hi(bv[e]);
+#pragma unroll
+      for (int m = 8; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+      if (ok && lane16 == 0) delta[(size_t)hd * n + row] = acc;
+    }
+    return;
+  }
   for (int hd = threadIdx.x >> 5; hd < H; hd += blockDim.x >> 5) {
     float acc = 0.f;
     for (int d = (threadIdx.x & 31) * 2; d < D; d += 64) {
