@@ -508,14 +508,22 @@ __global__ void __launch_bounds__(512) ce_rows_kernel(const float* __restrict__ 
   float se = 0.f;
   for (int c = threadIdx.x; c < V4; c += kT) {
     const float4 v = src[c];
-    se += (expf(v.x - mx) + expf(v.y - mx)) + (expf(v.z - mx) + expf(v.w - mx));
+    const float4 e = make_float4(expf(v.x - mx), expf(v.y - mx), expf(v.z - mx), expf(v.w - mx));
+    if (kSmem) reinterpret_cast<float4*>(srow)[c] = e;  // the dlogits pass reuses them
+    se += (e.x + e.y) + (e.z + e.w);
   }
   se = block_sum<kT>(se, red);
   const float inv_se = 1.f / se;
   for (int c = threadIdx.x; c < V4; c += kT) {
     const float4 v = src[c];
-    float p0 = expf(v.x - mx) * inv_se, p1 = expf(v.y - mx) * inv_se;
-    float p2 = expf(v.z - mx) * inv_se, p3 = expf(v.w - mx) * inv_se;
+    float4 e;
+    if (kSmem) {
+      e = v;  // exp(v - max) stored by the previous pass
+    } else {
+      e = make_float4(expf(v.x - mx), expf(v.y - mx), expf(v.z - mx), expf(v.w - mx));
+    }
+    float p0 = e.x * inv_se, p1 = e.y * inv_se;
+    float p2 = e.z * inv_se, p3 = e.w * inv_se;
     const int c0 = 4 * c;
     if (t == c0) p0 -= 1.f;
     if (t == c0 + 1) p1 -= 1.f;
