@@ -21,9 +21,8 @@
 //   dQ     CTA = one 128-query tile, thread = query row.  Per key tile j:
 //            S_j = Q·K_jᵀ (double-buffered), dP_j = dO·V_jᵀ,
 //            phase A: P = exp2(S·c − lse₂) (registers), phase B: dS = P∘(dP − Δ)
-//            → bf16 over the S_j columns phase A consumed, dQ += dS·K_j (A from TMEM)
-//          issue order  S(0) S(1) dP(0) | dP(j+1) dQ(j) S(j+2) | …  (dP(j+1) as soon
-//          as phase B has loaded dP(j))
+//            → bf16 over the dP columns, dQ += dS·K_j (A from TMEM)
+//          issue order  S(0) S(1) dP(0) | dQ(j) dP(j+1) S(j+2) | …
 //
 // A later MMA that overwrites TMEM columns still read (as bf16 A operand) by
 // an earlier one is safe without a wait: tcgen05.mma executes in issue order.
@@ -494,8 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* s_full = v_empty + kVStages;     // [2]
   uint64_t* s_free = s_full + 2;             // [2]
   uint64_t* dp_full = s_free + 2;
-  uint64_t* dp_free = dp_full + 1;  // phase B has loaded dP(j): dP(j+1) may overwrite it
-  uint64_t* ds_full = dp_free + 1;
+  uint64_t* ds_full = dp_full + 1;
   uint64_t* dq_done = ds_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
 
@@ -526,7 +524,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&s_free[b], 8);
     }
     mbar_init(dp_full, 1);
-    mbar_init(dp_free, 8);
     mbar_init(ds_full, 8);
     mbar_init(dq_done, 1);
     fence_barrier_init();
@@ -601,19 +598,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     issue_s(0);
     if (T > 1) issue_s(1);
     issue_dp(0);
-    // dS(j) is written (bf16) into S buffer j&1, whose S(j) phase A already
-    // consumed, so dP(j+1) only waits for phase B to have *loaded* dP(j):
-    // order dP(j+1) | dQ(j) S(j+2), S(j+2) after dQ(j) has read dS(j).
     for (int j = 0; j < T; ++j) {
-      if (j + 1 < T) {
-        mbar_wait(dp_free, j & 1);
-        issue_dp(j + 1);
-      }
       mbar_wait(ds_full, j & 1);
       tc_fence_after();
-      mma_tk<idesc_g>(tdQ, tmem + 128 * (j & 1), aK + (j % kKStages) * kTile, j > 0);
+      mma_tk<idesc_g>(tdQ, tP, aK + (j % kKStages) * kTile, j > 0);
       umma_commit_w(&k_empty[j % kKStages]);
       if (j == T - 1) umma_commit_w(dq_done);
+      if (j + 1 < T) issue_dp(j + 1);
       if (j + 2 < T) issue_s(j + 2);
     }
   } else if (warp >= 4) {
@@ -673,15 +664,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_32x32b_x32(tPw, *reinterpret_cast<uint32_t(*)[32]>(raw));
         tmem_ld_32x32b_x32(tPw + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
         tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(dp_free);
 #pragma unroll
         for (int c = 0; c < 64; ++c) p[c] *= (__uint_as_float(raw[c]) - dl);
       }
-      const uint32_t tdS = tmem + 128 * b + lane_off + 64 * wg;  // over this WG's S(j) columns
-      st_bf16x32(tdS, p);
-      st_bf16x32(tdS + 16, p + 32);
+      st_bf16x32(tPw, p);
+      st_bf16x32(tPw + 16, p + 32);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
