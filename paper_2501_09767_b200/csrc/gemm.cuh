@@ -216,7 +216,7 @@ constexpr int kSmemPair = kStagesPair * 2 * kBlockM * kBlockK * 2 + 1024 + 256;
 // counter; the last unit (highest cluster index of the tile's units, so the
 // others are dispatched no later) waits for them, adds the partials to its
 // TMEM accumulator in a fixed order (deterministic) and runs the epilogue.
-constexpr int kPairTailMaxSplit = 4;  // the last unit reads split-1 partials: keep it short
+constexpr int kPairTailMaxSplit = 4;  // the completing unit reads all partials: keep it short
 
 struct PairTail {
   int full_tiles;  // tiles computed whole (the first full waves)
@@ -360,6 +360,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp >= 4) {
+    __shared__ int tail_last;  // split-K tail: this unit completed its tile
     const int wq = warp & 3;
     const int part = (warp - 4) >> 2;
     const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
@@ -382,56 +383,66 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           return reinterpret_cast<float4*>(tl.ws) + (((size_t)(v0 + c) * 2 + rank) * 2 + part) * 4096;
         };
         int* ctr = tl.ctr + tail * 2 + rank;
-        if (w.chunk < tl.split - 1) {
-          float4* dst = slot(w.chunk);
+        // every unit stores its partial; the unit whose arrival completes the
+        // tile's count (whichever finishes last -- no unit ever waits for
+        // another) sums all partials in chunk order and runs the epilogue
+        float4* dst = slot(w.chunk);
 #pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(taddr + part * 128 + c * 32, v);
-            tmem_ld_wait();
+        for (int c = 0; c < 4; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(taddr + part * 128 + c * 32, v);
+          tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              __stcg(dst + (c * 8 + j) * 128 + r128,
-                     make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                 __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
-          }
-          __threadfence();
-          asm volatile("bar.sync 1, 256;" ::: "memory");
-          if (threadIdx.x == 128) atomicAdd(ctr, 1);
-          run_epi = false;
-        } else {
-          if (threadIdx.x == 128) {
-            while (atomicAdd(ctr, 0) < tl.split - 1) __nanosleep(256);
+          for (int j = 0; j < 8; ++j)
+            __stcg(dst + (c * 8 + j) * 128 + r128,
+                   make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                               __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (threadIdx.x == 128) {
+          const int old = atomicAdd(ctr, 1);
+          tail_last = old == tl.split - 1;
+          if (tail_last) {
             atomicExch(ctr, 0);  // ready for the next launch
             __threadfence();
           }
-          asm volatile("bar.sync 1, 256;" ::: "memory");
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (!tail_last) {
+          run_epi = false;
+        } else {
 #pragma unroll 1
           for (int c = 0; c < 4; ++c) {
+            // per 8 columns, all partial loads in flight at once, then
+            // ((p0 + p1) + p2) + p3: the same order whoever is last
             uint32_t v[32];
-            tmem_ld_32x32b_x32(taddr + part * 128 + c * 32, v);
-            tmem_ld_wait();
-            // all partial loads of this 32-column chunk in flight at once, then
-            // the adds in a fixed order (deterministic)
-            float4 x[kPairTailMaxSplit - 1][8];
 #pragma unroll
-            for (int k = 0; k < kPairTailMaxSplit - 1; ++k)
-              if (k < tl.split - 1) {
-                const float4* src = slot(k);
+            for (int h = 0; h < 4; ++h) {
+              float4 x[kPairTailMaxSplit][2];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) x[k][j] = __ldcg(src + (c * 8 + j) * 128 + r128);
-              }
+              for (int k = 0; k < kPairTailMaxSplit; ++k)
+                if (k < tl.split) {
+                  const float4* src = slot(k);
 #pragma unroll
-            for (int k = 0; k < kPairTailMaxSplit - 1; ++k)
-              if (k < tl.split - 1) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  v[4 * j] = __float_as_uint(__uint_as_float(v[4 * j]) + x[k][j].x);
-                  v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + x[k][j].y);
-                  v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + x[k][j].z);
-                  v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + x[k][j].w);
+                  for (int j = 0; j < 2; ++j)
+                    x[k][j] = __ldcg(src + (c * 8 + 2 * h + j) * 128 + r128);
                 }
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                float4 a = x[0][j];
+#pragma unroll
+                for (int k = 1; k < kPairTailMaxSplit; ++k)
+                  if (k < tl.split) {
+                    a.x += x[k][j].x; a.y += x[k][j].y; a.z += x[k][j].z; a.w += x[k][j].w;
+                  }
+                const int e = 4 * (2 * h + j);
+                v[e] = __float_as_uint(a.x);
+                v[e + 1] = __float_as_uint(a.y);
+                v[e + 2] = __float_as_uint(a.z);
+                v[e + 3] = __float_as_uint(a.w);
               }
+            }
             tmem_st_32x32b_x32(taddr + part * 128 + c * 32, v);
           }
           tmem_st_wait();
