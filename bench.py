@@ -151,7 +151,14 @@ def run_reference(args):
 
     wl = CONFIGS[args.config]
     cores = host_cores()
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    # all host threads: torchrun exports OMP_NUM_THREADS=1 to every worker and
+    # numpy's BLAS pool is sized at import, so resize it explicitly
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    try:
+        from threadpoolctl import threadpool_limits
+        _pool = threadpool_limits(limits=cores)  # noqa: F841 (kept for the run)
+    except Exception:  # noqa: BLE001
+        pass
     mcfg = getattr(M, wl["model"])(max_seq_len=wl["seq"])
     sample = CpuSample(sample_tokens=min(args.cpu_tokens, wl["seq"]), **cpu_geometry(mcfg))
     for _ in range(args.warmup):
