@@ -49,6 +49,13 @@ int lemo_gemm_nn_bf16(const void* A, int lda, const void* B, int ldb, void* C, i
 int lemo_gemm_f32(const void* A, int lda, const void* B, int ldb, float* C, int ldc, int M, int N,
                   int K, int accumulate, void* stream);
 
+/* lemo_gemm_f32 with fp32-faithful accumulation: the TMEM partial sum is
+ * restarted every 128 K-columns and promoted into round-to-nearest fp32
+ * registers (the tcgen05 accumulator truncates; see gemm.cuh kPromote).  For
+ * bf16x3 operand pairs (Eq. 3 of the predictor, parity-mode scorers). */
+int lemo_gemm_f32_exact(const void* A, int lda, const void* B, int ldb, float* C, int ldc, int M,
+                        int N, int K, int accumulate, void* stream);
+
 /* R[idx[i], :] += (A·Bᵀ)[i, :]  — index-remapped in-place residual update,
  * replaces T.scatter_add_rows (tensor.py:536-550) after the output projections
  * of sparse_attention_fused / sparse_mlp_fused (kernels.py:153-222). idx may be
@@ -86,9 +93,11 @@ int lemo_lora_pack_b(const float* Bq, const float* Bv, int h, int kv, int r, voi
  * w_gu_t: [N, K] bf16, gate/up columns interleaved in 128-column chunks
  * (silu) or up only (relu).  gu (optional): [M, N] bf16; inner (optional):
  * [M, N/2] (silu) or [M, N] (relu) bf16; partial (optional): [N/256, M] fp32
- * per-tile row sums of |inner|. */
+ * per-tile row sums of |inner|.  exact_score != 0: the scores use the fp32
+ * accumulator (parity mode: xn / w_gu_t given as bf16x3 operands, K = 3h, see
+ * lemo_split_bf16x3) instead of the bf16-rounded gate/up that gu stores. */
 int lemo_gemm_gateup(const void* xn, int ldx, const void* w_gu_t, int M, int N, int K, void* gu,
-                     void* inner, float* partial, int relu, void* stream);
+                     void* inner, float* partial, int relu, int exact_score, void* stream);
 
 /* Backward of the MLP inner product: dinner = dy · W_downᵀ (w_down: [m_pad, h]
  * bf16, reference layout) turned into d(gate), d(up) (tensor.py:289-290,
@@ -227,9 +236,33 @@ int lemo_quantile_lower(const double* data, int n, long long rank, int plus_one,
 
 /* Exact block informativeness (sparsity.py:173-219): out[m*ldo + n] (n <= m)
  * = max over the 16x16 tile of Σ_h max(q·k, 0)/H with the causal / n_valid
- * mask; q, k: [s, h] bf16 post-rotation (layer_qk, model.py:356-368). */
-int lemo_exact_block_scores(const void* q, const void* k, int s, int h, int kv, int head_dim,
-                            int block, int n_valid, float* out, int ldo, void* stream);
+ * mask; q [s, h], k [s, kv] bf16 post-rotation (layer_qk, model.py:356-368;
+ * query head hd reads key head hd / (h/kv)).  tcgen05 kernel: S per head in
+ * TMEM, head sum / clamp / tile max in the epilogue.  q_lo, k_lo (both or
+ * neither): bf16 residuals of fp32 q, k (v ≈ hi + lo) — the fp32-faithful
+ * parity mode issues hi·hi + hi·lo + lo·hi per head.  Entries above the
+ * diagonal are not written (the caller zero-fills out). */
+int lemo_exact_block_scores(const void* q, const void* k, const void* q_lo, const void* k_lo,
+                            int s, int h, int kv, int head_dim, int block, int n_valid,
+                            float* out, int ldo, void* stream);
+
+/* ---- fp32-faithful (parity-mode) scoring helpers ------------------------------ */
+
+/* out[i, :] = x[idx[i]] · inv · w in fp32, inv = 1/sqrt(mean(x²) + 1e-6)
+ * (model.py:333-335 _rmsnorm_np); idx may be NULL; inv (optional) [M]. */
+int lemo_rmsnorm_f32(const float* x, int ldx, const int* idx, int M, int h, const float* w,
+                     float* out, int ldo, float* inv, void* stream);
+
+/* layer_qk tail in fp32 (model.py:338-368): q = qk[:, :h] + ((t[:, :r])·Bq)·scale,
+ * k = qk[:, h:h+kv], RoPE at positions 0..s-1 from rope_tab [s, head_dim/2, 2]
+ * (cos, sin; f64-computed, f32-cast as tensor.py:604-607) when rope != 0; Bq may
+ * be NULL (no adapter).  Writes the bf16 hi/lo split of q [s, h] and k [s, kv]. */
+int lemo_qk_finish(const float* qk, int ldqk, const float* t, int ldt, const float* Bq, int r,
+                   float scale, const float* rope_tab, int s, int h, int kv, int head_dim,
+                   int rope, void* q_hi, void* q_lo, void* k_hi, void* k_lo, void* stream);
+
+/* hi = bf16(a), lo = bf16(a - hi) for a fp32 [M, K] (row stride lda). */
+int lemo_split_hilo(const float* a, int lda, int M, int K, void* hi, void* lo, void* stream);
 
 /* ---- offline predictor training (predictor.py:215-433) ----------------------- */
 

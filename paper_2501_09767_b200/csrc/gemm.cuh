@@ -60,7 +60,17 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int num_m, int num_n) {
 // address of (this warp's lane base, first accumulator column of the tile).
 // The functor must issue the same sequence of tcgen05.ld for every lane of
 // the warp (they are warp-collective) and only store when `valid`.
-template <int BN, class Epi, bool kBMN = false>
+// kPromote > 0: fp32-faithful accumulation.  The tcgen05 fp32 accumulator
+// does not round to nearest when it adds into TMEM: every MMA step loses up
+// to ~2^-23 of the running sum's magnitude toward zero, so a long K loop
+// drifts by ~(K/16)·2^-24 relative (measured: 4e-5 at K = 12288, DESIGN §2,
+// scripts/probes/acc_precision.py).  With kPromote = G the MMA warp restarts
+// the TMEM accumulator every G k-blocks and the epilogue warps add each
+// group's partial into fp32 registers with round-to-nearest adds (the
+// "promotion" of partial sums to CUDA-core accumulators), then write the sum
+// back into TMEM and run the epilogue as usual.  Used by the bf16x3 GEMMs
+// (predictor, parity-mode scorers), where the operands carry fp32 precision.
+template <int BN, class Epi, bool kBMN = false, int kPromote = 0>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int M, int N, int K, Epi epi) {
@@ -134,35 +144,39 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (one warp, one elected lane issues) ----------------
     constexpr uint32_t idesc = umma_idesc_bf16(kBlockM, BN, 0, kBMN ? 1 : 0);
+    const int group = kPromote > 0 ? kPromote : num_kb;  // k-blocks per accumulator group
     int stage = 0;
     uint32_t phase = 0;
-    int local = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&full_bar[stage], phase);
+    int local = 0;  // accumulator groups issued (one per tile unless promoting)
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int kb0 = 0; kb0 < num_kb; kb0 += group, ++local) {
+        const int kb1 = min(kb0 + group, num_kb);
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
-        {  // whole warp, one elected lane issues (descriptors stay uniform)
-          const uint64_t da = umma_desc_k_sw128(smem_u32(smem_a + stage * Cfg::kABytes));
-          const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::kBBytes);
-          const uint64_t db = kBMN ? umma_desc_mn_sw128(b_addr, 8192) : umma_desc_k_sw128(b_addr);
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          {  // whole warp, one elected lane issues (descriptors stay uniform)
+            const uint64_t da = umma_desc_k_sw128(smem_u32(smem_a + stage * Cfg::kABytes));
+            const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::kBBytes);
+            const uint64_t db = kBMN ? umma_desc_mn_sw128(b_addr, 8192) : umma_desc_k_sw128(b_addr);
 #pragma unroll
-          for (int k = 0; k < kBlockK / kUmmaK; ++k) {
-            // advancing K inside the 128-B swizzle atom = +32 B on the start address
-            umma_bf16_ss_w(d_tmem, da + ((k * kUmmaK * 2) >> 4),
-                           db + (kBMN ? (k * 2048) >> 4 : (k * kUmmaK * 2) >> 4), idesc,
-                           (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < kBlockK / kUmmaK; ++k) {
+              // advancing K inside the 128-B swizzle atom = +32 B on the start address
+              umma_bf16_ss_w(d_tmem, da + ((k * kUmmaK * 2) >> 4),
+                             db + (kBMN ? (k * 2048) >> 4 : (k * kUmmaK * 2) >> 4), idesc,
+                             (kb > kb0 || k != 0) ? 1u : 0u);
+            }
+            umma_commit_w(&empty_bar[stage]);
+            if (kb == kb1 - 1) umma_commit_w(&tfull_bar[acc]);
           }
-          umma_commit_w(&empty_bar[stage]);
-          if (kb == num_kb - 1) umma_commit_w(&tfull_bar[acc]);
-        }
-        if (++stage == Cfg::kStages) {
-          stage = 0;
-          phase ^= 1;
+          if (++stage == Cfg::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -171,18 +185,66 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int wq = warp & 3;
     const int part = (warp - 4) >> 2;
     int local = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const TileCoord tc = tile_coord(t, num_m, num_n);
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
       const int row = tc.m * kBlockM + wq * 32 + lane;
-      const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
-      epi(row, row < M, tc.n * BN, taddr, part);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if constexpr (kPromote > 0) {
+        constexpr int kCols = BN / 2;  // this warp's half of the tile
+        float sum[kCols];
+#pragma unroll
+        for (int i = 0; i < kCols; ++i) sum[i] = 0.f;
+        const int ngroups = (num_kb + kPromote - 1) / kPromote;
+        uint32_t taddr = 0;
+        int acc = 0;
+        for (int g = 0; g < ngroups; ++g, ++local) {
+          acc = local & 1;
+          mbar_wait(&tfull_bar[acc], (local >> 1) & 1);
+          tc_fence_after();
+          taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
+#pragma unroll
+          for (int c = 0; c < kCols / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(taddr + part * kCols + c * 32, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sum[c * 32 + i] = __fadd_rn(sum[c * 32 + i], __uint_as_float(v[i]));
+          }
+          if (g + 1 < ngroups) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+          }
+        }
+        // the promoted sum replaces the last group's partial, then the usual epilogue
+#pragma unroll
+        for (int c = 0; c < kCols / 32; ++c) {
+          uint32_t v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(sum[c * 32 + i]);
+          tmem_st_32x32b_x32(taddr + part * kCols + c * 32, v);
+        }
+        tmem_st_wait();
+        // the epilogue functor may read columns the other half's warps wrote
+        // (EpiGateUp pairs gate and up columns): all 8 warps first
+        tc_fence_before();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        tc_fence_after();
+        epi(row, row < M, tc.n * BN, taddr, part);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      } else {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
+        epi(row, row < M, tc.n * BN, taddr, part);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        ++local;
+      }
     }
   }
   __syncthreads();
@@ -486,7 +548,7 @@ int gemm_num_sms();
 int pair_tail_workspace(cudaStream_t stream, int units, int tiles, float** ws, int** ctr);
 bool pair_tail_enabled();
 
-template <int BN, class Epi, bool kBMN = false>
+template <int BN, class Epi, bool kBMN = false, int kPromote = 0>
 int launch_gemm_tn(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
                    const Epi& epi, cudaStream_t stream) {
   if (M <= 0 || N <= 0) return 0;
@@ -501,7 +563,7 @@ int launch_gemm_tn(const void* A, int lda, const void* B, int ldb, int M, int N,
   if (rc) return rc;
   static bool attr_set = false;  // one per template instantiation
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN, Epi, kBMN>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN, Epi, kBMN, kPromote>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::kSmemBytes);
     if (e != cudaSuccess) return (int)e;
@@ -509,8 +571,8 @@ int launch_gemm_tn(const void* A, int lda, const void* B, int ldb, int M, int N,
   }
   const int tiles = ((M + kBlockM - 1) / kBlockM) * ((N + BN - 1) / BN);
   const int grid = tiles < gemm_num_sms() ? tiles : gemm_num_sms();
-  gemm_tn_kernel<BN, Epi, kBMN><<<grid, kGemmThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K,
-                                                                               epi);
+  gemm_tn_kernel<BN, Epi, kBMN, kPromote><<<grid, kGemmThreads, Cfg::kSmemBytes, stream>>>(
+      ta, tb, M, N, K, epi);
   return (int)cudaGetLastError();
 }
 

@@ -189,7 +189,11 @@ struct EpiQKV {
 //   gu      : [M, N] bf16, same interleaved column order (saved for backward)
 //   inner   : [M, N/2] bf16 (silu) or [M, N] (relu), optional
 //   partial : [N/128, M] fp32 row sums of |inner| per half tile, optional
-struct EpiGateUp {
+//   exact   : score from the fp32 accumulator instead of the bf16-rounded
+//             gate/up (the fp32-faithful parity mode: the GEMM then runs on
+//             bf16x3 operands, K = 3h, so the accumulator carries f32 precision)
+template <bool exact>
+struct EpiGateUpT {
   __nv_bfloat16* gu;
   int ldgu;
   __nv_bfloat16* inner;
@@ -210,12 +214,16 @@ struct EpiGateUp {
         // inner from the bf16-rounded gate/up that are saved for backward, so the
         // dense path and the compaction path (mlp_compact) produce identical rows
         float in[32];
+        if constexpr (exact) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) score += fabsf(g[i] * sigmoid_fast(g[i]) * u[i]);
+        }
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           g[i] = round_bf16(g[i]);
           u[i] = round_bf16(u[i]);
           in[i] = g[i] * sigmoid_fast(g[i]) * u[i];
-          score += fabsf(in[i]);
+          if (!exact) score += fabsf(in[i]);
         }
         if (gu) {
           store_bf16x32(gu + (size_t)row * ldgu + col0 + c, g);
@@ -230,11 +238,15 @@ struct EpiGateUp {
         load_chunk(taddr + c, u);
         if (!valid) continue;
         float in[32];
+        if constexpr (exact) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) score += fmaxf(u[i], 0.f);
+        }
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           u[i] = round_bf16(u[i]);
           in[i] = fmaxf(u[i], 0.f);
-          score += in[i];
+          if (!exact) score += in[i];
         }
         if (gu) store_bf16x32(gu + (size_t)row * ldgu + col0 + c, u);
         if (inner) store_bf16x32(inner + (size_t)row * ldi + col0 + c, in);
@@ -243,6 +255,8 @@ struct EpiGateUp {
     if (valid && partial) partial[(size_t)((col0 / 256) * 2 + part) * M + row] = score;
   }
 };
+using EpiGateUp = EpiGateUpT<false>;
+using EpiGateUpExact = EpiGateUpT<true>;
 
 // dinner = dy · W_downᵀ ; epilogue turns it into d(gate), d(up) using the
 // saved gate/up (silu:  dg = dinner·u·σ(g)(1+g(1-σ(g))),  du = dinner·g·σ(g);
@@ -386,6 +400,17 @@ static int pick_bn(int M, int N) {
   return 64;
 }
 
+// fp32-faithful accumulation (see kPromote in gemm.cuh): the TMEM partial is
+// promoted into fp32 registers every kPromoteGroup k-blocks (K = 128).
+constexpr int kPromoteGroup = 2;
+
+template <int BN, class Epi>
+static int gemm_promoted(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
+                         const Epi& e, cudaStream_t st) {
+  Bound<BN, Epi> b{e};
+  return launch_gemm_tn<BN, Bound<BN, Epi>, false, kPromoteGroup>(A, lda, B, ldb, M, N, K, b, st);
+}
+
 template <class Epi>
 static int gemm_auto(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
                      const Epi& e, cudaStream_t st) {
@@ -423,6 +448,19 @@ int lemo_gemm_f32(const void* A, int lda, const void* B, int ldb, float* C, int 
   LEMO_RETURN_RC("lemo_gemm_f32", gemm_auto(A, lda, B, ldb, M, N, K, e, (cudaStream_t)stream));
 }
 
+int lemo_gemm_f32_exact(const void* A, int lda, const void* B, int ldb, float* C, int ldc, int M,
+                        int N, int K, int accumulate, void* stream) {
+  EpiStoreF32 e{C, ldc, N, accumulate};
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  switch (pick_bn(M, N)) {
+    case 256: rc = gemm_promoted<256>(A, lda, B, ldb, M, N, K, e, st); break;
+    case 128: rc = gemm_promoted<128>(A, lda, B, ldb, M, N, K, e, st); break;
+    default: rc = gemm_promoted<64>(A, lda, B, ldb, M, N, K, e, st); break;
+  }
+  LEMO_RETURN_RC("lemo_gemm_f32_exact", rc);
+}
+
 int lemo_gemm_scatter_add(const void* A, int lda, const void* B, int ldb, float* R, int ldr,
                           const int* idx, int M, int N, int K, void* stream) {
   LEMO_ARG_CHECK(N % 32 == 0 && ldr % 4 == 0, "lemo_gemm_scatter_add: N%32, ldr%4");
@@ -453,12 +491,18 @@ int lemo_gemm_qkv(const void* xn, int ldx, const void* w_qkv_t, int ldw, int M, 
 }
 
 int lemo_gemm_gateup(const void* xn, int ldx, const void* w_gu_t, int M, int N, int K, void* gu,
-                     void* inner, float* partial, int relu, void* stream) {
+                     void* inner, float* partial, int relu, int exact_score, void* stream) {
   LEMO_ARG_CHECK(N % 256 == 0, "lemo_gemm_gateup: N must be a multiple of 256 (padded mlp dim)");
-  EpiGateUp e{reinterpret_cast<__nv_bfloat16*>(gu), N, reinterpret_cast<__nv_bfloat16*>(inner),
-              relu ? N : N / 2, partial, M, relu};
-  LEMO_RETURN_RC("lemo_gemm_gateup",
-                 gemm<256>(xn, ldx, w_gu_t, K, M, N, K, e, (cudaStream_t)stream));
+  auto* gup = reinterpret_cast<__nv_bfloat16*>(gu);
+  auto* inp = reinterpret_cast<__nv_bfloat16*>(inner);
+  const int ldi = relu ? N : N / 2;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (exact_score) {  // parity mode: bf16x3 operands, promoted accumulation
+    EpiGateUpExact e{gup, N, inp, ldi, partial, M, relu};
+    LEMO_RETURN_RC("lemo_gemm_gateup", gemm_promoted<256>(xn, ldx, w_gu_t, K, M, N, K, e, st));
+  }
+  EpiGateUp e{gup, N, inp, ldi, partial, M, relu};
+  LEMO_RETURN_RC("lemo_gemm_gateup", gemm<256>(xn, ldx, w_gu_t, K, M, N, K, e, st));
 }
 
 int lemo_gemm_split3(const void* A, int lda, const void* B, int ldb, int M, int N, int K3,
@@ -466,9 +510,11 @@ int lemo_gemm_split3(const void* A, int lda, const void* B, int ldb, int M, int 
                      float* f32, int ldf, void* stream) {
   LEMO_ARG_CHECK(K3 % 3 == 0, "lemo_gemm_split3: K' must be 3K");
   EpiSplit3 e{reinterpret_cast<__nv_bfloat16*>(out), ldo, f32, ldf, N, pattern, relu, mask};
-  // small in M (n_blocks): BN = 128 or 64 so the grid fills the SMs
-  const int rc = pick_bn(M, N) == 64 ? gemm<64>(A, lda, B, ldb, M, N, K3, e, (cudaStream_t)stream)
-                                     : gemm<128>(A, lda, B, ldb, M, N, K3, e, (cudaStream_t)stream);
+  // small in M (n_blocks): BN = 128 or 64 so the grid fills the SMs; fp32-faithful
+  // operands, so the accumulation is promoted (gemm.cuh kPromote)
+  cudaStream_t st = (cudaStream_t)stream;
+  const int rc = pick_bn(M, N) == 64 ? gemm_promoted<64>(A, lda, B, ldb, M, N, K3, e, st)
+                                     : gemm_promoted<128>(A, lda, B, ldb, M, N, K3, e, st);
   LEMO_RETURN_RC("lemo_gemm_split3", rc);
 }
 

@@ -215,6 +215,7 @@ class LayerState:
         self.m = m
         self.m_pad = cfg.mlp_pad
         self.rope_tab = model.rope_tab
+        self.scoring_precision = model.scoring_precision
 
         def g(name):
             a = arrays[name]
@@ -242,6 +243,17 @@ class LayerState:
             gu = _interleave_gate_up(g("w_gate"), w_up, self.m_pad)
         self.w_gu = gu.to(BF16).contiguous()
         self.w_gu_t = gu.t().contiguous().to(BF16)
+        # fp32-faithful scoring (scoring_precision="fp32"): the bf16 residual
+        # lo = bf16(w - hi) of the scoring weights, so hi + lo carries the fp32
+        # weights into the bf16x3 GEMMs (gate/up, q/k)
+        self.w_gu_t_lo = self.w_qk_t_lo = None
+        if model.scoring_precision == "fp32":
+            gut = gu.t().contiguous()
+            self.w_gu_t_lo = (gut - self.w_gu_t.float()).to(BF16)
+            del gut
+            qk_t = w_qkv[:, :h + kv].t().contiguous()
+            self.w_qk_t_lo = (qk_t - self.w_qkv_t[:h + kv, :h].float()).to(BF16)
+            del qk_t
         wd = torch.zeros(self.m_pad, h, device=dev)
         wd[:m] = g("w_down")
         self.w_down = wd.to(BF16).contiguous()
@@ -274,6 +286,20 @@ class LayerState:
         Bq = flat[o + 2 * h * r:o + 3 * h * r].view(r, h)
         Bv = flat[o + 3 * h * r:o + 3 * h * r + kv * r].view(r, kv)
         return A, Bq, Bv
+
+    def gateup_x3(self) -> torch.Tensor:
+        """[N, 3h] bf16x3 B operand [hi | lo | hi] of the gate/up weight."""
+        if self.w_gu_t_lo is None:
+            raise ContractError("fp32 scoring needs a model built with scoring_precision='fp32'")
+        return torch.cat([self.w_gu_t, self.w_gu_t_lo, self.w_gu_t], dim=1)
+
+    def qk_x3(self) -> torch.Tensor:
+        """[h+kv, 3h] bf16x3 B operand of the q/k projections."""
+        if self.w_qk_t_lo is None:
+            raise ContractError("fp32 scoring needs a model built with scoring_precision='fp32'")
+        h = self.w_qkv.shape[0]
+        hi = self.w_qkv_t[:h + self.kv, :h]
+        return torch.cat([hi, self.w_qk_t_lo, hi], dim=1)
 
     def lora_A_packed(self) -> torch.Tensor:
         """[32, h] bf16 copy of [A_q | A_v] for the t = xn·A GEMM (re-packed each
@@ -386,8 +412,14 @@ class DecoderModel:
     """
 
     def __init__(self, cfg: ModelConfig, seed: int = 0, *, device=None, init: str = "torch",
-                 arrays: dict | None = None):
+                 arrays: dict | None = None, scoring_precision: str = "bf16"):
         cfg.check_gpu_geometry()
+        if scoring_precision not in ("bf16", "fp32"):
+            raise ContractError(f"unknown scoring precision {scoring_precision!r}")
+        # "bf16": production scorers on bf16 tensor-core operands;  "fp32": the
+        # fp32-faithful (bf16x3) parity mode that reproduces the reference's
+        # masks (keeps the bf16 residuals of the scoring weights: +~8 % memory)
+        self.scoring_precision = scoring_precision
         self.config = cfg
         self.seed = seed
         self.device = torch.device(device) if device is not None else torch.device("cuda")
@@ -439,7 +471,11 @@ class DecoderModel:
         self.lm_head_t = lm.t().contiguous().to(BF16)      # [V, h]  (logits GEMM)
         del lm
         self.lora_param.requires_grad_(cfg.lora_rank > 0)
+        # layer -> (step epoch, x address, (gu_all, inv_all)): full-sequence
+        # gate/up rows the MLP scorer produced for the CURRENT step's residual;
+        # mlp_forward compacts them instead of recomputing (see take_mlp_rows)
         self._mlp_scored = {}
+        self._epoch = 0
         self.last_stats: dict = {}
         # data parallelism: called with each layer's LoRA-gradient slice as soon
         # as the backward sweep has finished it (parallel.BucketedGradReducer)
@@ -534,6 +570,17 @@ class DecoderModel:
                 loss = step.forward(need_grad=False)
         return loss, step.hidden
 
+    def stash_mlp_rows(self, layer_id: int, x: torch.Tensor, rows) -> None:
+        self._mlp_scored[layer_id] = (self._epoch, x.data_ptr(), rows)
+
+    def take_mlp_rows(self, layer_id: int, x: torch.Tensor):
+        """The scorer's rows for this layer if they were computed from this very
+        residual in this step (else None: the sparse MLP recomputes gate/up)."""
+        ent = self._mlp_scored.pop(layer_id, None)
+        if ent is None or ent[0] != self._epoch or ent[1] != x.data_ptr():
+            return None
+        return ent[2]
+
     @staticmethod
     def _plan_from(pattern, n_pad: int, device) -> kernels.GatherPlan:
         if pattern is None:
@@ -582,7 +629,15 @@ class _Step:
 
     def forward(self, need_grad: bool = True):
         m = self.model
-        cfg = m.config
+        m._epoch += 1
+        m._mlp_scored.clear()
+        try:
+            return self._forward(need_grad)
+        finally:
+            m._mlp_scored.clear()
+
+    def _forward(self, need_grad: bool):
+        m = self.model
         dev = m.device
         mem0 = torch.cuda.memory_allocated(dev)
         x = ops.embed(self.ids, m.embed,
@@ -599,7 +654,7 @@ class _Step:
             pat = src.pattern(layer.layer_id, sparsity.MLP, x, self.n_valid) \
                 if src is not None else None
             plan = DecoderModel._plan_from(pat, self.n_pad, dev)
-            scored = m._mlp_scored.pop(layer.layer_id, None)
+            scored = m.take_mlp_rows(layer.layer_id, x)
             sm = kernels.mlp_forward(x, plan, layer, scored=scored, save=need_grad)
             ledger.retain_saved(led, f"layer{layer.layer_id}.mlp", sm)
             del scored
@@ -678,31 +733,67 @@ class _StepFn(torch.autograd.Function):
 # scoring helpers (model.py:356-396)
 
 
+def _precision(layer: LayerState, precision):
+    p = precision or layer.scoring_precision
+    if p not in ("bf16", "fp32"):
+        raise ContractError(f"unknown scoring precision {p!r}")
+    return p
+
+
 def mlp_block_score_vector(layer: LayerState, x: torch.Tensor, block_size: int, n_valid: int,
-                           *, keep_rows: bool = False):
+                           *, keep_rows: bool = False, precision: str | None = None):
     """Exact MLP block scores (model.py:371-396): RMSNorm of every row, the
     tcgen05 gate/up GEMM with |silu(g)·u| row sums in its epilogue, then
     mean/max per block.  With keep_rows=True also returns (gu_all, inv_all)
-    so the sparse MLP can compact retained rows instead of recomputing."""
+    so the sparse MLP can compact retained rows instead of recomputing.
+
+    precision "fp32" (parity): fp32 RMSNorm, bf16x3 operands over K = 3h and
+    scores from the fp32 accumulator -- the reference's f32 scores to ~1e-6."""
     s, h = x.shape
     dev = x.device
     N = layer.w_gu_t.shape[0]
     inv_all = torch.empty(s, dtype=F32, device=dev)
-    xn_all = ops.rmsnorm_gather(x, layer.mlp_norm_w, None, inv=inv_all)
     gu_all = torch.empty(s, N, dtype=BF16, device=dev) if keep_rows else None
     partial = torch.empty(N // 128, s, dtype=F32, device=dev)
-    ops.gemm_gateup(xn_all, layer.w_gu_t, gu=gu_all, partial=partial, relu=layer.relu)
-    del xn_all
+    if _precision(layer, precision) == "fp32":
+        xnf = ops.rmsnorm_f32(x, layer.mlp_norm_w, inv=inv_all)
+        a3 = ops.split_bf16x3(xnf, 0)
+        del xnf
+        ops.gemm_gateup(a3, layer.gateup_x3(), gu=gu_all, partial=partial, relu=layer.relu,
+                        exact_score=True)
+        del a3
+    else:
+        xn_all = ops.rmsnorm_gather(x, layer.mlp_norm_w, None, inv=inv_all)
+        ops.gemm_gateup(xn_all, layer.w_gu_t, gu=gu_all, partial=partial, relu=layer.relu)
+        del xn_all
     vec = ops.mlp_block_scores(partial, s=s, n_valid=n_valid, b=block_size, m_real=layer.m)
     if keep_rows:
         return vec, (gu_all, inv_all)
     return vec
 
 
-def layer_qk(layer: LayerState, x: torch.Tensor):
-    """model.py:356-368: post-rotation Q (with LoRA) and K (without), [s, h] bf16."""
+def layer_qk(layer: LayerState, x: torch.Tensor, *, precision: str | None = None):
+    """model.py:356-368: post-rotation Q (with LoRA) and K (without).
+
+    "bf16": (q, k) bf16 [s, h] / [s, kv] from the tcgen05 q/k GEMM with RoPE
+    in its epilogue.  "fp32" (parity): ((q_hi, q_lo), (k_hi, k_lo)) -- fp32
+    RMSNorm, bf16x3 projections, LoRA and RoPE in fp32 (lemo_qk_finish)."""
     s, h = x.shape
     r = layer.lora_rank
+    if _precision(layer, precision) == "fp32":
+        xnf = ops.rmsnorm_f32(x, layer.attn_norm_w)
+        a3 = ops.split_bf16x3(xnf, 0)
+        del xnf
+        _, qk = ops.gemm_split3(a3, layer.qk_x3(), split_out=False, f32_out=True)
+        t = None
+        if r:
+            a_t = ops.split_bf16x3_t(layer.lora_A.contiguous(), 1)  # [2r, 3h]
+            _, t = ops.gemm_split3(a3, a_t, split_out=False, f32_out=True)
+        del a3
+        q_hi, q_lo, k_hi, k_lo = ops.qk_finish(
+            qk, t, layer.lora_Bq if r else None, r=r, scale=layer.lora_scaling,
+            rope_tab=layer.rope_tab, h=h, kv=layer.kv, head_dim=layer.head_dim, rope=layer.rope)
+        return (q_hi, q_lo), (k_hi, k_lo)
     xn = torch.empty(s, layer.w_qkv_t.shape[1], dtype=BF16, device=x.device)
     ops.rmsnorm_gather(x, layer.attn_norm_w, None, xn=xn)
     if r:
@@ -826,7 +917,7 @@ class PredictedPatternSource(PatternSourceBase):
             if not self.mlp_scoring:
                 return self._note(layer_id, component, None)
             vec, rows = mlp_block_score_vector(layer, x, b, n_valid, keep_rows=True)
-            self.model._mlp_scored[layer_id] = rows
+            self.model.stash_mlp_rows(layer_id, x, rows)
             thr = self.thresholds.get(layer_id, component)
         if self.record:
             self.recorded_vectors.setdefault((layer_id, component), []).append(vec)
@@ -882,7 +973,7 @@ class ExactPatternSource(PatternSourceBase):
             res = mlp_block_score_vector(layer, x, b, n_valid, keep_rows=keep)
             if keep:
                 vec, rows = res
-                self.model._mlp_scored[layer_id] = rows
+                self.model.stash_mlp_rows(layer_id, x, rows)
             else:
                 vec = res
         if self.record:

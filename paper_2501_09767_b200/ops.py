@@ -80,6 +80,18 @@ def gemm_f32(a, b, out=None, *, accumulate=False):
     return out
 
 
+def gemm_f32_exact(a, b, out=None, *, accumulate=False):
+    """out (+)= a·bᵀ in fp32 with promoted (round-to-nearest) accumulation --
+    for bf16x3 operand pairs whose product must keep fp32 precision."""
+    M, N, K = _mnk(a, b)
+    _check(out)
+    if out is None:
+        out = torch.empty(M, N, dtype=F32, device=a.device)
+    call("lemo_gemm_f32_exact", ptr(a), a.stride(0), ptr(b), b.stride(0), ptr(out), out.stride(0),
+         M, N, K, int(bool(accumulate)), _s())
+    return out
+
+
 def gemm_scatter_add(a, b, resid, idx=None):
     """resid[idx] += a·bᵀ in place (idx None = identity rows)."""
     M, N, K = _mnk(a, b)
@@ -111,12 +123,16 @@ def gemm_qkv(xn, w_qkv_t, *, h, head_dim, rope, inv_freq, pos, nmat=3, kv=None, 
     return out
 
 
-def gemm_gateup(xn, w_gu_t, *, gu=None, inner=None, partial=None, relu=False):
+def gemm_gateup(xn, w_gu_t, *, gu=None, inner=None, partial=None, relu=False, exact_score=False):
+    """exact_score=True: xn / w_gu_t are bf16x3 operands (K = 3h) and the MLP
+    scores come from the fp32 accumulator (parity mode)."""
     M, K = xn.shape
     N = w_gu_t.shape[0]
     _check(xn, w_gu_t, gu, inner, partial)
+    if w_gu_t.shape[1] != K or w_gu_t.stride(0) != K:
+        raise DimensionError(f"gate/up weight {tuple(w_gu_t.shape)} does not match K = {K}")
     call("lemo_gemm_gateup", ptr(xn), xn.stride(0), ptr(w_gu_t), M, N, K, ptr(gu), ptr(inner),
-         ptr(partial), int(bool(relu)), _s())
+         ptr(partial), int(bool(relu)), int(bool(exact_score)), _s())
 
 
 def gemm_dgateup(dy, w_down, gu, dgu, *, m_pad, relu=False):
@@ -144,6 +160,47 @@ def rmsnorm_gather(x, w, idx=None, *, xn=None, xg=None, inv=None):
 
 
 LORA_K_EXT = 64  # extra K columns of the q/k/v GEMM carrying the LoRA terms
+
+
+def rmsnorm_f32(x, w, idx=None, *, out=None, inv=None):
+    """fp32 RMSNorm rows (model.py:333-335), optionally gathered at idx."""
+    _check(x, w, idx, out, inv)
+    _dt(x, F32, "x")
+    M = x.shape[0] if idx is None else idx.shape[0]
+    h = x.shape[1]
+    if out is None:
+        out = torch.empty(M, h, dtype=F32, device=x.device)
+    call("lemo_rmsnorm_f32", ptr(x), x.stride(0), ptr(idx), M, h, ptr(w), ptr(out), out.stride(0),
+         ptr(inv), _s())
+    return out
+
+
+def qk_finish(qk, t, Bq, *, r, scale, rope_tab, h, kv, head_dim, rope):
+    """fp32 layer_qk tail (LoRA add + RoPE) -> (q_hi, q_lo, k_hi, k_lo) bf16."""
+    _check(qk, t, Bq, rope_tab)
+    _dt(qk, F32, "qk")
+    s = qk.shape[0]
+    dev = qk.device
+    q_hi, q_lo = (torch.empty(s, h, dtype=BF16, device=dev) for _ in range(2))
+    k_hi, k_lo = (torch.empty(s, kv, dtype=BF16, device=dev) for _ in range(2))
+    if rope and (rope_tab is None or rope_tab.shape[0] < s):
+        raise ContractError("RoPE table shorter than the sequence")
+    call("lemo_qk_finish", ptr(qk), qk.stride(0), ptr(t), 0 if t is None else t.stride(0),
+         ptr(Bq), int(r), float(scale), ptr(rope_tab), s, h, kv, head_dim, int(bool(rope)),
+         ptr(q_hi), ptr(q_lo), ptr(k_hi), ptr(k_lo), _s())
+    return q_hi, q_lo, k_hi, k_lo
+
+
+def split_hilo(a):
+    """fp32 [M, K] -> (bf16 hi, bf16 lo) with a ≈ hi + lo."""
+    _check(a)
+    _dt(a, F32, "a")
+    _rowmajor(a, "a")
+    M, K = a.shape
+    hi = torch.empty(M, K, dtype=BF16, device=a.device)
+    lo = torch.empty_like(hi)
+    call("lemo_split_hilo", ptr(a), a.stride(0), M, K, ptr(hi), ptr(lo), _s())
+    return hi, lo
 
 
 def lora_qkv_prep(t, r, scale, xn_ext, h):

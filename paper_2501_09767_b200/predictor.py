@@ -211,7 +211,7 @@ def predicted_dense(p_q, p_k, x, block_size: int, pooling: str = "mean") -> torc
     else:
         eq, ek = pair_block_outputs(p_q, p_k, x, block_size, pooling)
         eq3, ek3 = ops.split_bf16x3(eq, 0), ops.split_bf16x3(ek, 1)
-    return ops.gemm_f32(eq3, ek3)
+    return ops.gemm_f32_exact(eq3, ek3)
 
 
 def predicted_triangle(p_q, p_k, x, block_size: int, pooling: str = "mean") -> torch.Tensor:
@@ -234,7 +234,7 @@ def predict_scores(p_q: Predictor, p_k: Predictor, x_blocks, *, layer_id=None) -
         raise ContractError(f"predictor output dims differ: {p_q.d_pred} vs {p_k.d_pred}")
     eq = p_q.predict(x_blocks)
     ek = p_k.predict(x_blocks)
-    full = ops.gemm_f32(ops.split_bf16x3(eq, 0), ops.split_bf16x3(ek, 1))
+    full = ops.gemm_f32_exact(ops.split_bf16x3(eq, 0), ops.split_bf16x3(ek, 1))
     nb = full.shape[0]
     r, c = torch.tril_indices(nb, nb, device=full.device)
     packed = torch.clamp_min(full[r, c], 0.0)

@@ -312,6 +312,48 @@ def token_block_scores(matrix: BlockScoreMatrix) -> torch.Tensor:
     return ops.colsum_packed(packed, matrix.n_blocks)
 
 
+def _as_heads(a) -> torch.Tensor:
+    """sparsity.py:159-166: [s, d] -> [1, s, d]; anything but 2-D/3-D raises."""
+    t = a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a))
+    if t.dim() == 2:
+        t = t[None]
+    if t.dim() != 3:
+        raise ContractError(f"expected [heads, s, d] scores input, got shape {tuple(t.shape)}")
+    return t
+
+
+def exact_block_scores(q, k, block_size: int, *, n_valid: int | None = None, layer_id: int = 0,
+                       component: str = ATTENTION) -> BlockScoreMatrix:
+    """sparsity.py:173-219 with the reference signature: q, k [H, s, d] (or
+    [s, d]).  Runs the tcgen05 exact scorer (csrc/exact.cu); float inputs are
+    scored in the fp32-faithful bf16x3 mode, bf16 CUDA inputs in bf16.  Head
+    dims below 64/128 are zero-padded (q·k is unchanged)."""
+    from . import exact  # kernel module (imports this one)
+
+    qt, kt = _as_heads(q), _as_heads(k)
+    if tuple(qt.shape) != tuple(kt.shape):
+        raise ContractError(f"q/k shapes differ: {tuple(qt.shape)} vs {tuple(kt.shape)}")
+    H, s, d = qt.shape
+    if block_size > s:
+        raise ContractError(f"block size {block_size} exceeds sequence length {s}")
+    if d > 128:
+        raise ContractError(f"head dim {d} > 128 is not supported by the exact scorer")
+    dp = 64 if d <= 64 else 128
+    dev = qt.device if qt.is_cuda else torch.device("cuda")
+    bf16 = qt.dtype == torch.bfloat16 and qt.is_cuda
+
+    def rows(t):  # [H, s, d] -> [s, H*dp], heads side by side
+        out = torch.zeros(s, H, dp, dtype=torch.bfloat16 if bf16 else torch.float32, device=dev)
+        out[:, :, :d] = t.to(device=dev, dtype=out.dtype).permute(1, 0, 2)
+        return out.reshape(s, H * dp)
+
+    qr, kr = rows(qt), rows(kt)
+    if not bf16:
+        qr, kr = ops.split_hilo(qr), ops.split_hilo(kr)
+    return exact.exact_block_scores(qr, kr, block_size, n_heads=H, n_valid=n_valid,
+                                    layer_id=layer_id, component=component)
+
+
 def mlp_block_scores(token_scores, block_size: int, *, n_valid: int | None = None) -> np.ndarray:
     """Block score = max token score in the block (sparsity.py:293-305); host
     helper for already-reduced token scores (the fused GPU path is

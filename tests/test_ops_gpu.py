@@ -176,6 +176,86 @@ def test_layer_qk_matches_oracle(cuda):
     np.testing.assert_allclose(k.float().cpu().numpy(), kref, rtol=3e-2, atol=3e-2)
 
 
+# fp32-faithful (parity) precision: bf16x3 operands, fp32 element-wise steps
+
+
+def _scorer_model_fp32(seed, **kw):
+    cfg = ModelConfig(n_layers=1, hidden_dim=128, n_heads=2, vocab_size=64, max_seq_len=256,
+                      block_size=16, **kw)
+    return DecoderModel(cfg, seed, init="reference", scoring_precision="fp32")
+
+
+def test_mlp_scores_golden_fp32(cuda):
+    z = np.load(G / "scorers.npz")
+    m = _scorer_model_fp32(3, mlp_dim=344, lora_rank=4, lora_alpha=8.0)
+    x = torch.as_tensor(z["x"]).cuda()
+    got = mlp_block_score_vector(m.layers[0], x, 16, int(z["n_valid"])).cpu().numpy()
+    np.testing.assert_allclose(got, z["mlp_vec"], rtol=1e-5)
+    zr = np.load(G / "scorers_relu.npz")
+    mr = _scorer_model_fp32(4, mlp_dim=256, mlp_variant="relu")
+    got = mlp_block_score_vector(mr.layers[0], x, 16, int(zr["n_valid"])).cpu().numpy()
+    np.testing.assert_allclose(got, zr["mlp_vec"], rtol=1e-5)
+
+
+def test_layer_qk_fp32_matches_reference(cuda):
+    z = np.load(G / "scorers.npz")
+    m = _scorer_model_fp32(3, mlp_dim=344, lora_rank=4, lora_alpha=8.0)
+    m.layers[0].lora_q.b.copy_(torch.as_tensor(z["lora_q_b"]))
+    x = torch.as_tensor(z["x"]).cuda()
+    (qh, ql), (kh, kl) = layer_qk(m.layers[0], x)
+    H, s, d = z["q"].shape
+    qref = z["q"].transpose(1, 0, 2).reshape(s, H * d)
+    kref = z["k"].transpose(1, 0, 2).reshape(s, H * d)
+    q = (qh.float() + ql.float()).cpu().numpy()
+    k = (kh.float() + kl.float()).cpu().numpy()
+    np.testing.assert_allclose(q, qref, rtol=0, atol=2e-5 * np.abs(qref).max())
+    np.testing.assert_allclose(k, kref, rtol=0, atol=2e-5 * np.abs(kref).max())
+
+
+def test_exact_scores_reference_signature_fp32(cuda):
+    """sparsity.exact_block_scores(q, k, block_size, *, n_valid, ...) on the
+    reference's own [H, s, d] f32 q/k (sparsity.py:173-181): the tcgen05
+    scorer in bf16x3 mode reproduces the f32 scores to ~1e-6."""
+    z = np.load(G / "scorers.npz")
+    nv = int(z["n_valid"])
+    bsm = S.exact_block_scores(z["q"], z["k"], 16, n_valid=nv, layer_id=3)
+    ref = z["exact_packed"]
+    assert bsm.layer_id == 3 and bsm.n_blocks == 11
+    np.testing.assert_allclose(bsm.scores.cpu().numpy(), ref, rtol=1e-5, atol=1e-6 * ref.max())
+    vec = S.token_block_scores(bsm).cpu().numpy()
+    np.testing.assert_allclose(vec, z["exact_vec"], rtol=1e-5)
+    # [s, d] input = one head; shape mismatch / bad rank raise like the reference
+    one = S.exact_block_scores(z["q"][0], z["k"][0], 16)
+    assert one.n_blocks == 11
+    from paper_2501_09767_b200.errors import ContractError
+    with pytest.raises(ContractError):
+        S.exact_block_scores(z["q"], z["k"][:1], 16)
+    with pytest.raises(ContractError):
+        S.exact_block_scores(z["q"][None], z["k"][None], 16)
+    with pytest.raises(ContractError):
+        S.exact_block_scores(z["q"][:, :8], z["k"][:, :8], 16)
+
+
+@pytest.mark.parametrize("s,H,Hk,d", [(300, 4, 4, 64), (1000, 2, 2, 128), (777, 8, 2, 128),
+                                      (2048, 4, 4, 64)])
+def test_exact_scorer_vs_oracle_shapes(cuda, s, H, Hk, d):
+    """tcgen05 exact scorer (both precisions) on ragged lengths, GQA and both
+    head dims against the oracle's dense tile maxima."""
+    rng = np.random.default_rng(s + H)
+    q = rng.standard_normal((H, s, d)).astype(np.float32) * 0.3
+    kk = rng.standard_normal((Hk, s, d)).astype(np.float32) * 0.3
+    nv = s - 3
+    ref = O.exact_block_dense(q, np.repeat(kk, H // Hk, axis=0), 16, nv)
+    rows = lambda a: torch.as_tensor(a.transpose(1, 0, 2).reshape(s, -1)).cuda()  # noqa: E731
+    qh, ql = ops.split_hilo(rows(q))
+    kh, kl = ops.split_hilo(rows(kk))
+    dense = exact.exact_block_dense((qh, ql), (kh, kl), 16, n_heads=H, n_valid=nv).cpu().numpy()
+    np.testing.assert_allclose(dense, ref, rtol=1e-5, atol=1e-6 * ref.max())
+    dense16 = exact.exact_block_dense(rows(q).bfloat16(), rows(kk).bfloat16(), 16, n_heads=H,
+                                      n_valid=nv).cpu().numpy()
+    np.testing.assert_allclose(dense16, ref, rtol=3e-2, atol=1e-2 * ref.max())
+
+
 # ------------------------------------------------------------------ attention
 
 
