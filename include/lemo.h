@@ -215,6 +215,13 @@ int lemo_colsum_clamped(const float* S, int lds, int nb, double* vec, void* stre
  * (element (m, n) at m(m+1)/2 + n; sparsity.py:253-260). */
 int lemo_colsum_packed(const double* packed, int nb, double* vec, void* stream);
 
+/* out[m(m+1)/2 + n] = S[m, n] for n <= m (clamped at 0 when clamp != 0): the
+ * packed lower triangle of sparsity.py:35-69 (BlockScoreMatrix) as f64 (out64)
+ * or f32 (out32; exactly one of them non-NULL) — predicted_triangle /
+ * predict_scores (predictor.py:176-212) and exact_block_scores. */
+int lemo_pack_tril(const float* S, int lds, int nb, int clamp, double* out64, float* out32,
+                   void* stream);
+
 /* MLP block scores from per-tile row partials of lemo_gemm_gateup:
  * token score = Σ partial / m_real, block = max over rows < n_valid
  * (sparsity.py:284-305, model.py:383-395). */

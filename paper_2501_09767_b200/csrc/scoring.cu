@@ -191,6 +191,21 @@ __global__ void colsum_clamped_kernel(const float* __restrict__ S, int lds, int 
   if (lane == 0) vec[n] = acc;
 }
 
+// Row-major packed lower triangle of a dense [nb, nb] fp32 matrix (element
+// (m, n <= m) at m(m+1)/2 + n, sparsity.py:35-37), optionally clamped at 0
+// (predict_scores, predictor.py:189-212), as f64 (BlockScoreMatrix) or f32.
+__global__ void pack_tril_kernel(const float* __restrict__ S, int lds, int nb, int clamp,
+                                 double* __restrict__ out64, float* __restrict__ out32) {
+  const int m = blockIdx.x;
+  const size_t base = (size_t)m * (m + 1) / 2;
+  for (int n = threadIdx.x; n <= m; n += blockDim.x) {
+    float v = S[(size_t)m * lds + n];
+    if (clamp) v = fmaxf(v, 0.f);
+    if (out64) out64[base + n] = (double)v;
+    else out32[base + n] = v;
+  }
+}
+
 // Same column sums straight from a packed f64 lower triangle (element (m, n)
 // at m(m+1)/2 + n), e.g. reference-written or teacher score triangles.
 __global__ void colsum_packed_kernel(const double* __restrict__ P, int nb,
@@ -424,6 +439,15 @@ int lemo_colsum_clamped(const float* S, int lds, int nb, double* vec, void* stre
   if (nb <= 0) return 0;
   colsum_clamped_kernel<<<(nb + 7) / 8, 256, 0, (cudaStream_t)stream>>>(S, lds, nb, vec);
   LEMO_CHECK_LAUNCH("lemo_colsum_clamped");
+  return 0;
+}
+
+int lemo_pack_tril(const float* S, int lds, int nb, int clamp, double* out64, float* out32,
+                   void* stream) {
+  if (nb <= 0) return 0;
+  LEMO_ARG_CHECK((out64 == nullptr) != (out32 == nullptr), "lemo_pack_tril: exactly one output");
+  pack_tril_kernel<<<nb, 128, 0, (cudaStream_t)stream>>>(S, lds, nb, clamp, out64, out32);
+  LEMO_CHECK_LAUNCH("lemo_pack_tril");
   return 0;
 }
 

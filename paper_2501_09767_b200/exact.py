@@ -59,9 +59,7 @@ def exact_block_vector(q, k, block_size: int, *, n_heads: int, n_valid=None) -> 
 
 def packed_from_dense(dense: torch.Tensor, block_size: int, *, layer_id: int = 0,
                       component: str = "attention") -> BlockScoreMatrix:
-    nb = dense.shape[0]
-    r, c = torch.tril_indices(nb, nb, device=dense.device)
-    return BlockScoreMatrix(nb, block_size, dense[r, c].double(), layer_id=layer_id,
+    return BlockScoreMatrix(dense.shape[0], block_size, ops.pack_tril(dense), layer_id=layer_id,
                             component=component)
 
 

@@ -120,14 +120,19 @@ class SegmentPlan:
 # attention block
 
 
-def attention_forward(x: torch.Tensor, plan: GatherPlan, layer, *, save: bool = True):
+def attention_forward(x: torch.Tensor, plan: GatherPlan, layer, *, save: bool = True,
+                      out: torch.Tensor | None = None, pos: torch.Tensor | None = None):
     """x[idx] += attention_core(gather_rmsnorm(x, idx)) in place; returns the
-    compact saved state (or None when save=False / k == 0)."""
+    compact saved state (or None when save=False / k == 0).  `out` (default
+    x) receives the update instead; `pos` (default idx) are the RoPE
+    positions -- the naive variant runs on a materialised compact copy whose
+    row i sits at original position pos[i]."""
     if plan.k == 0:
         return None
     k, h = plan.k, x.shape[1]
     dev = x.device
     idx = plan.indices
+    pos = idx if pos is None else pos
     r = layer.lora_rank
     xn = torch.empty(k, layer.w_qkv_t.shape[1], dtype=BF16, device=dev)  # [xn | LoRA ext]
     xg = torch.empty(k, h, dtype=BF16, device=dev) if save else None
@@ -135,13 +140,13 @@ def attention_forward(x: torch.Tensor, plan: GatherPlan, layer, *, save: bool = 
     ops.rmsnorm_gather(x, layer.attn_norm_w, idx, xn=xn, xg=xg, inv=inv)
     t = layer.qkv_input(xn) if r else None
     q, kk, v = ops.gemm_qkv(xn, layer.w_qkv_t, h=h, head_dim=layer.head_dim, rope=layer.rope,
-                            inv_freq=layer.inv_freq, pos=idx, kv=layer.kv)
+                            inv_freq=layer.inv_freq, pos=pos, kv=layer.kv)
     del xn
     o, lse = ops.flash_fwd(q, kk, v, head_dim=layer.head_dim, scale=1.0 / math.sqrt(layer.head_dim))
-    ops.gemm_scatter_add(o, layer.w_o_t, x, idx)
+    ops.gemm_scatter_add(o, layer.w_o_t, x if out is None else out, idx)
     if not save:
         return None
-    return dict(idx=idx, xg=xg, inv=inv, t=t, q=q, k=kk, v=v, o=o, lse=lse)
+    return dict(idx=idx, pos=pos, xg=xg, inv=inv, t=t, q=q, k=kk, v=v, o=o, lse=lse)
 
 
 _SIDE: dict = {}
@@ -175,7 +180,7 @@ def attention_backward(dx: torch.Tensor, saved: dict, layer, grads):
     del d_o
     dqkv = torch.empty(k, layer.w_qkv.shape[1], dtype=BF16, device=dev)  # [dq|dk|dv|LoRA ext]
     ops.qkv_grad_prep(dq, dk, dv, head_dim=layer.head_dim, rope=layer.rope,
-                      rope_tab=layer.rope_tab, pos=idx, dqkv=dqkv)
+                      rope_tab=layer.rope_tab, pos=saved.get("pos", idx), dqkv=dqkv)
     done = None
     if r:
         u = layer.qkv_grad_input(dqkv)
@@ -204,10 +209,11 @@ def attention_backward(dx: torch.Tensor, saved: dict, layer, grads):
 # MLP block
 
 
-def mlp_forward(x: torch.Tensor, plan: GatherPlan, layer, *, scored=None, save: bool = True):
-    """x[idx] += mlp_core(gather_rmsnorm(x, idx)) in place.  `scored` =
-    (gu_all, inv_all) from the MLP scorer over every row of this same x:
-    retained rows are then compacted instead of recomputed."""
+def mlp_forward(x: torch.Tensor, plan: GatherPlan, layer, *, scored=None, save: bool = True,
+                out: torch.Tensor | None = None):
+    """x[idx] += mlp_core(gather_rmsnorm(x, idx)) in place (into `out` when
+    given).  `scored` = (gu_all, inv_all) from the MLP scorer over every row
+    of this same x: retained rows are then compacted instead of recomputed."""
     if plan.k == 0:
         return None
     k, h = plan.k, x.shape[1]
@@ -226,7 +232,7 @@ def mlp_forward(x: torch.Tensor, plan: GatherPlan, layer, *, scored=None, save: 
         xn = ops.rmsnorm_gather(x, layer.mlp_norm_w, idx, xg=xg, inv=inv)
         ops.gemm_gateup(xn, layer.w_gu_t, gu=gu, inner=inner, relu=layer.relu)
         del xn
-    ops.gemm_scatter_add(inner, layer.w_down_t, x, idx)
+    ops.gemm_scatter_add(inner, layer.w_down_t, x if out is None else out, idx)
     if not save:
         return None
     return dict(idx=idx, xg=xg, inv=inv, gu=gu)
@@ -274,6 +280,99 @@ def segmented_loss_forward(hidden: torch.Tensor, lm_head_t: torch.Tensor, lm_hea
     loss_sum = torch.empty(1, dtype=torch.float64, device=dev)
     ops.sum_f64(row_loss, loss_sum)
     return loss_sum / count, grad_hidden
+
+
+class _SegmentedLoss(torch.autograd.Function):
+    """custom_op(loss, "segmented_cross_entropy", (hidden, lm_head), saved, bw)
+    of kernels.py:281-288: the gradients are computed in the forward pass and
+    the backward only scales them by g."""
+
+    @staticmethod
+    def forward(ctx, hidden, lm_head, targets_np, plan, ignore_index):
+        n, h = hidden.shape
+        V = lm_head.shape[1]
+        dev = hidden.device
+        count = check_targets(targets_np, V, ignore_index)
+        if count == 0:
+            raise ContractError("segmented loss: no valid targets")
+        w = lm_head.detach()
+        w_b = w.to(BF16).contiguous()                 # [h, V]: B operand of dlogits·Wᵀ
+        w_t = w.t().contiguous().to(BF16)              # [V, h]: B operand of hidden·W
+        hid = hidden.detach().to(BF16).contiguous()
+        tg = torch.as_tensor(targets_np.astype(np.int32)).to(dev)
+        need_w = lm_head.requires_grad
+        loss, grad_hidden, grad_w = _segmented_loss(hid, w_t, w_b, tg, count, plan, ignore_index,
+                                                    need_w=need_w)
+        ctx.save_for_backward(grad_hidden, grad_w if need_w else None)
+        ctx.need_w = need_w
+        return loss.to(F32).reshape(())
+
+    @staticmethod
+    def backward(ctx, g):
+        grad_hidden, grad_w = ctx.saved_tensors
+        gw = g * grad_w if ctx.need_w else None
+        return g * grad_hidden, gw, None, None, None
+
+
+def _segmented_loss(hidden, lm_head_t, lm_head, targets_dev, count, plan, ignore_index, *,
+                    need_w: bool):
+    """segmented_loss_forward plus (optionally) the lm_head gradient
+    Σ_seg hsegᵀ·dlogits / count (kernels.py:270-275)."""
+    if not need_w:
+        loss, gh = segmented_loss_forward(hidden, lm_head_t, lm_head, targets_dev, count, plan,
+                                          ignore_index)
+        return loss, gh, None
+    n, h = hidden.shape
+    V = lm_head_t.shape[0]
+    dev = hidden.device
+    grad_hidden = torch.empty(n, h, dtype=F32, device=dev)
+    grad_w = torch.zeros(h, V, dtype=F32, device=dev)
+    row_loss = torch.empty(n, dtype=F32, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    for a, b in plan.segments:
+        logits = ops.gemm_f32(hidden[a:b], lm_head_t)
+        dlog = torch.empty(b - a, V, dtype=BF16, device=dev)
+        ops.ce_rows(logits, targets_dev[a:b], V=V, ignore=ignore_index, inv_count=1.0 / count,
+                    dlogits=dlog, row_loss=row_loss[a:b], bad=bad)
+        del logits
+        ops.gemm_f32(dlog, lm_head, out=grad_hidden[a:b])
+        # grad_W += hsegᵀ·dlogits: K = segment rows (zero-padded to a multiple of
+        # 8 for the 16-byte TMA row pitch), both operands transposed copies
+        kp = -(-(b - a) // 8) * 8
+        ht = torch.zeros(h, kp, dtype=BF16, device=dev)
+        ht[:, : b - a] = hidden[a:b].t()
+        dt = torch.zeros(V, kp, dtype=BF16, device=dev)
+        dt[:, : b - a] = dlog.t()
+        ops.gemm_f32(ht, dt, out=grad_w, accumulate=True)
+        del ht, dt
+        del dlog
+    loss_sum = torch.empty(1, dtype=torch.float64, device=dev)
+    ops.sum_f64(row_loss, loss_sum)
+    return loss_sum / count, grad_hidden, grad_w
+
+
+def segmented_loss_and_grad(hidden: torch.Tensor, lm_head, targets, plan: SegmentPlan,
+                            ignore_index: int = -1) -> torch.Tensor:
+    """kernels.py:229-288 (reference name and signature): mean token cross
+    entropy of hidden·lm_head computed one segment at a time on the GPU (the
+    logits of one segment are live at a time, tcgen05 GEMMs + the ce_rows
+    kernel); grad_hidden (and grad_lm_head when lm_head.requires_grad) are
+    formed in the forward pass, so backward is g·grad.  hidden [n, h] and
+    lm_head [h, V] are CUDA tensors (lm_head may be a host array: frozen)."""
+    targets = np.asarray(targets.cpu() if isinstance(targets, torch.Tensor) else targets)
+    if not isinstance(hidden, torch.Tensor) or not hidden.is_cuda:
+        raise ContractError("segmented_loss_and_grad: hidden must be a CUDA tensor")
+    n = hidden.shape[0]
+    if targets.shape != (n,):
+        raise ContractError(f"targets shape {targets.shape} does not match {n} tokens")
+    if plan.n_tokens != n:
+        raise ContractError(f"segment plan covers {plan.n_tokens} tokens, input has {n}")
+    if not isinstance(lm_head, torch.Tensor):
+        lm_head = torch.as_tensor(np.asarray(lm_head, dtype=np.float32)).to(hidden.device)
+    if lm_head.shape[0] != hidden.shape[1]:
+        raise ContractError(f"lm_head {tuple(lm_head.shape)} does not match hidden "
+                            f"{tuple(hidden.shape)}")
+    return _SegmentedLoss.apply(hidden, lm_head, targets.astype(np.int64), plan, ignore_index)
 
 
 def check_targets(targets: np.ndarray, vocab: int, ignore_index: int = -1) -> int:
@@ -344,7 +443,62 @@ def sparse_mlp_fused(x: torch.Tensor, plan: GatherPlan, layer,
     return _SparseBlock.apply(x, layer.lora_param, plan, layer, "mlp")
 
 
-# The reference's naive variants (kernels.py:131-150, 180-198) differ only in
-# their transient buffers; on the GPU both names run the fused kernels.
-sparse_attention_naive = sparse_attention_fused
-sparse_mlp_naive = sparse_mlp_fused
+# ---------------------------------------------------------------------------
+# naive variants (kernels.py:131-150, 180-198): the same block math on a
+# MATERIALISED compact copy -- gather the retained rows into their own
+# buffer, run the block there (RoPE still at the original positions), write
+# its output into a zero [k, h] buffer, pad it to [s, h] and add.  Three
+# transient buffers, no index-remapped epilogue: an independent data path
+# that the fused kernels are checked against.
+
+
+class _NaiveBlock(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, lora_flat, plan, layer, kind):
+        idx = plan.indices.long()
+        k = plan.k
+        gathered = x.detach().index_select(0, idx).contiguous()   # transient 1
+        small = torch.zeros_like(gathered)                        # transient 2
+        compact = GatherPlan.full(k, x.device)
+        if kind == "attention":
+            saved = attention_forward(gathered, compact, layer, out=small, pos=plan.indices)
+        else:
+            saved = mlp_forward(gathered, compact, layer, out=small)
+        padded = torch.zeros_like(x).index_copy_(0, idx, small)  # transient 3
+        out = x.detach() + padded
+        ctx.saved_state = saved
+        ctx.plan, ctx.layer, ctx.kind = plan, layer, kind
+        ctx.lora_shape = lora_flat.shape
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        g = g.detach().to(F32)
+        idx = ctx.plan.indices.long()
+        dxc = g.index_select(0, idx).contiguous()  # d/dx of the compact copy, plus J^T g
+        dlora = torch.zeros(ctx.lora_shape, dtype=F32, device=g.device)
+        if ctx.kind == "attention":
+            ev = attention_backward(dxc, ctx.saved_state, ctx.layer, ctx.layer.grad_views(dlora))
+            if ev is not None:
+                torch.cuda.current_stream(g.device).wait_event(ev)
+        else:
+            mlp_backward(dxc, ctx.saved_state, ctx.layer)
+        ctx.saved_state = None
+        dx = g.clone().index_copy_(0, idx, dxc)
+        return dx, dlora, None, None, None
+
+
+def sparse_attention_naive(x: torch.Tensor, plan: GatherPlan, layer) -> torch.Tensor:
+    """kernels.py:131-150"""
+    _check_plan(x, plan)
+    if plan.k == 0:
+        return x
+    return _NaiveBlock.apply(x, layer.lora_param, plan, layer, "attention")
+
+
+def sparse_mlp_naive(x: torch.Tensor, plan: GatherPlan, layer) -> torch.Tensor:
+    """kernels.py:180-198"""
+    _check_plan(x, plan)
+    if plan.k == 0:
+        return x
+    return _NaiveBlock.apply(x, layer.lora_param, plan, layer, "mlp")

@@ -451,6 +451,17 @@ def colsum_clamped(S, out=None):
     return out
 
 
+def pack_tril(S, *, clamp=False, dtype=F64):
+    """Packed lower triangle (row-major, n <= m) of a dense fp32 [nb, nb]."""
+    _check(S)
+    _dt(S, F32, "S")
+    nb = S.shape[0]
+    out = torch.empty(nb * (nb + 1) // 2, dtype=dtype, device=S.device)
+    call("lemo_pack_tril", ptr(S), S.stride(0), nb, int(bool(clamp)),
+         ptr(out) if dtype == F64 else None, ptr(out) if dtype == F32 else None, _s())
+    return out
+
+
 def colsum_packed(packed, nb, out=None):
     """f64 column sums of a packed f64 lower triangle, ascending m."""
     _check(packed, out)

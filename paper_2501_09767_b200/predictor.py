@@ -105,7 +105,14 @@ class Predictor:
         out, _ = ops.gemm_split3(h2, self._weights3()[2], pattern=pattern)
         return out
 
-    forward = predict
+    def forward(self, x, track: bool = False) -> torch.Tensor:
+        """predictor.py:73-81: the same values as predict(); track=True also
+        bumps the zero-frequency counters of both hidden stages (the
+        elastic-pruning statistics, predictor.py:76-80)."""
+        if not track:
+            return self.predict(x)
+        out, _ = self.forward_train(_dev_f32(x, self.w1.device), track=True)
+        return out
 
     def state_arrays(self) -> dict:
         """Everything needed to resume training (predictor.py:91-102, same keys)."""
@@ -216,10 +223,7 @@ def predicted_dense(p_q, p_k, x, block_size: int, pooling: str = "mean") -> torc
 
 def predicted_triangle(p_q, p_k, x, block_size: int, pooling: str = "mean") -> torch.Tensor:
     """Packed lower triangle of predicted scores, unclamped (predictor.py:176-186)."""
-    full = predicted_dense(p_q, p_k, x, block_size, pooling)
-    nb = full.shape[0]
-    r, c = torch.tril_indices(nb, nb, device=full.device)
-    return full[r, c]
+    return ops.pack_tril(predicted_dense(p_q, p_k, x, block_size, pooling), dtype=torch.float32)
 
 
 def predicted_block_vector(p_q, p_k, x, block_size: int, pooling: str = "mean") -> torch.Tensor:
@@ -235,10 +239,8 @@ def predict_scores(p_q: Predictor, p_k: Predictor, x_blocks, *, layer_id=None) -
     eq = p_q.predict(x_blocks)
     ek = p_k.predict(x_blocks)
     full = ops.gemm_f32_exact(ops.split_bf16x3(eq, 0), ops.split_bf16x3(ek, 1))
-    nb = full.shape[0]
-    r, c = torch.tril_indices(nb, nb, device=full.device)
-    packed = torch.clamp_min(full[r, c], 0.0)
-    return BlockScoreMatrix(nb, 1, packed, layer_id=p_q.layer_id if layer_id is None else layer_id,
+    return BlockScoreMatrix(full.shape[0], 1, ops.pack_tril(full, clamp=True),
+                            layer_id=p_q.layer_id if layer_id is None else layer_id,
                             component=ATTENTION)
 
 

@@ -161,6 +161,10 @@ def scorer_cases():
 
 STEP_CFG = dict(n_layers=2, hidden_dim=128, n_heads=2, vocab_size=128, max_seq_len=256,
                 mlp_dim=344, block_size=16, lora_rank=8, lora_alpha=16.0)
+# head_dim 128: the geometry of the production (Llama-class) attention kernels
+STEP_CFG_D128 = dict(n_layers=2, hidden_dim=256, n_heads=2, vocab_size=128, max_seq_len=256,
+                     mlp_dim=344, block_size=16, lora_rank=8, lora_alpha=16.0)
+STEP_VARIANTS = {"": STEP_CFG, "_d128": STEP_CFG_D128}
 
 
 def _perturb_b(m, seed):
@@ -179,12 +183,14 @@ def _grads(m):
     return out
 
 
-def step_cases():
+def step_cases(suffix=""):
+    base = STEP_VARIANTS[suffix]
+    h = base["hidden_dim"]
     rng = np.random.default_rng(21)
-    tokens = rng.integers(0, STEP_CFG["vocab_size"], size=150)
+    tokens = rng.integers(0, base["vocab_size"], size=150)
     cases = {}
     for mode in ("dense", "fraction", "predicted", "exact"):
-        cfg = model_mod.ModelConfig(**STEP_CFG)
+        cfg = model_mod.ModelConfig(**base)
         m = model_mod.DecoderModel(cfg, seed=17)
         _perturb_b(m, 23)
         source = None
@@ -203,8 +209,8 @@ def step_cases():
                 prng = np.random.default_rng(31)
                 pairs = {}
                 for l in range(cfg.n_layers):
-                    pairs[l] = (pred_mod.Predictor.create(prng, 128, 32, 32, 32, "q", l),
-                                pred_mod.Predictor.create(prng, 128, 32, 32, 32, "k", l))
+                    pairs[l] = (pred_mod.Predictor.create(prng, h, 32, 32, 32, "q", l),
+                                pred_mod.Predictor.create(prng, h, 32, 32, 32, "k", l))
                 m.attach_predictors(pairs)
                 for l, (pq, pk) in pairs.items():
                     for tag, p in (("q", pq), ("k", pk)):
@@ -233,18 +239,21 @@ def step_cases():
         arrays = {f"grad__{k}": v for k, v in grads.items()}
         arrays.update(extra)
         frac = {f"{l}:{c}": f for (l, c), f in (source.last_fractions.items() if source else [])}
-        np.savez_compressed(OUT / f"step_{mode}.npz", tokens=tokens, losses=np.array(led_losses),
+        np.savez_compressed(OUT / f"step_{mode}{suffix}.npz", tokens=tokens,
+                            losses=np.array(led_losses),
                             hidden=hidden.data, fractions=json.dumps(frac), **arrays)
         cases[mode] = led_losses
     return cases
 
 
-def step_pattern_cases():
+def step_pattern_cases(suffix=""):
     """Per-(layer, component) retained blocks of the predicted step, captured
     through a recording wrapper around the reference source."""
+    base = STEP_VARIANTS[suffix]
+    h = base["hidden_dim"]
     rng = np.random.default_rng(21)
-    tokens = rng.integers(0, STEP_CFG["vocab_size"], size=150)
-    cfg = model_mod.ModelConfig(**STEP_CFG)
+    tokens = rng.integers(0, base["vocab_size"], size=150)
+    cfg = model_mod.ModelConfig(**base)
     out = {}
     for mode in ("predicted", "exact"):
         m = model_mod.DecoderModel(cfg, seed=17)
@@ -255,8 +264,8 @@ def step_pattern_cases():
         ts = sparsity.init_thresholds(prof.recorded_vectors)
         if mode == "predicted":
             prng = np.random.default_rng(31)
-            pairs = {l: (pred_mod.Predictor.create(prng, 128, 32, 32, 32, "q", l),
-                         pred_mod.Predictor.create(prng, 128, 32, 32, 32, "k", l))
+            pairs = {l: (pred_mod.Predictor.create(prng, h, 32, 32, 32, "q", l),
+                         pred_mod.Predictor.create(prng, h, 32, 32, 32, "k", l))
                      for l in range(cfg.n_layers)}
             m.attach_predictors(pairs)
             src = model_mod.PredictedPatternSource(m, ts.copy(), target_retention={0: 0.5, 1: 0.5},
@@ -281,7 +290,7 @@ def step_pattern_cases():
             arrays[f"x_{l}_{c}"] = x
         if mode == "predicted":
             arrays["thr_attn"] = np.array([src.thresholds.get(l, "attention") for l in range(2)])
-        np.savez_compressed(OUT / f"patterns_{mode}.npz", **arrays)
+        np.savez_compressed(OUT / f"patterns_{mode}{suffix}.npz", **arrays)
         out[mode] = {k: v[0] for k, v in rec.items()}
     return out
 
@@ -440,7 +449,8 @@ def gqa_case():
 
 CASES = {"select": select_cases, "quantile": quantile_cases, "colsum": column_sum_cases,
          "predictor": predictor_case, "scorers": scorer_cases, "steps": step_cases,
-         "patterns": step_pattern_cases, "predictor_train": predictor_train_case,
+         "patterns": step_pattern_cases, "steps_d128": lambda: step_cases("_d128"),
+         "patterns_d128": lambda: step_pattern_cases("_d128"), "predictor_train": predictor_train_case,
          "predictor_train_token": lambda: predictor_train_case("token"),
          "artifacts": artifact_case, "tune": tune_case, "gqa": gqa_case}
 

@@ -112,6 +112,27 @@ def test_predictor_golden(cuda):
                                z["packed_token"], rtol=1e-5, atol=1e-5 * scale)
     np.testing.assert_allclose(P.predicted_block_vector(pq, pk, x, b).cpu().numpy(), z["vec"],
                                rtol=1e-5, atol=1e-5 * np.abs(z["vec"]).max())
+    # Predictor.forward(x, track) (predictor.py:73-81) ≡ predict, and track=True
+    # counts exact zeros of both hidden stages (pruned neurons always count)
+    xb = P.block_embed(x, b)
+    out = pq.forward(xb, track=True)
+    torch.testing.assert_close(out, pq.predict(xb), rtol=0, atol=0)
+    assert pq.observed == xb.shape[0]
+    op = O.Predictor(z["q_w1"], z["q_w2"], z["q_w3"], z["q_m1"].astype(bool),
+                     z["q_m2"].astype(bool))
+    xbn = xb.cpu().numpy()
+    h1 = np.maximum(xbn @ op.w1, 0) * op.mask1
+    h2 = np.maximum(h1 @ op.w2, 0) * op.mask2
+    assert np.abs(pq.zero_counts1.cpu().numpy() - (h1 == 0).sum(0)).max() <= 1
+    assert np.abs(pq.zero_counts2.cpu().numpy() - (h2 == 0).sum(0)).max() <= 1
+    # predict_scores (predictor.py:189-212): clamped Eq. 3 dots, block_size 1
+    bsm = P.predict_scores(pq, pk, xb)
+    full = op.predict(xbn) @ O.Predictor(z["k_w1"], z["k_w2"], z["k_w3"], z["k_m1"].astype(bool),
+                                         z["k_m2"].astype(bool)).predict(xbn).T
+    r, c = np.tril_indices(full.shape[0])
+    ref = np.maximum(full[r, c], 0.0)
+    assert bsm.block_size == 1 and bsm.n_blocks == full.shape[0]
+    np.testing.assert_allclose(bsm.scores.cpu().numpy(), ref, rtol=1e-4, atol=5e-5 * ref.max())
 
 
 def test_sgemm_vs_torch(cuda):

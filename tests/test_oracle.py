@@ -18,6 +18,8 @@ G = Path(__file__).resolve().parent / "golden"
 
 STEP_CFG = dict(n_layers=2, hidden_dim=128, n_heads=2, vocab_size=128, max_seq_len=256,
                 mlp_dim=344, block_size=16, lora_rank=8, lora_alpha=16.0)
+# "" = head_dim 64 (h=128), "_d128" = head_dim 128 (h=256): make_golden.STEP_VARIANTS
+STEP_VARIANTS = {"": STEP_CFG, "_d128": dict(STEP_CFG, hidden_dim=256)}
 
 
 def _split(flat, lens):
@@ -114,9 +116,9 @@ def test_scorers_golden():
                                rtol=1e-5)
 
 
-def step_model(mode):
-    z = np.load(G / f"step_{mode}.npz")
-    model = O.init_model(O.Config(**STEP_CFG), seed=17)
+def step_model(mode, suffix=""):
+    z = np.load(G / f"step_{mode}{suffix}.npz")
+    model = O.init_model(O.Config(**STEP_VARIANTS[suffix]), seed=17)
     O.perturb_lora_b(model, 23)
     source = None
     if mode == "fraction":
@@ -139,9 +141,10 @@ def step_model(mode):
     return z, model, source
 
 
+@pytest.mark.parametrize("suffix", ["", "_d128"])
 @pytest.mark.parametrize("mode", ["dense", "fraction", "predicted", "exact"])
-def test_train_step_golden(mode):
-    z, model, source = step_model(mode)
+def test_train_step_golden(mode, suffix):
+    z, model, source = step_model(mode, suffix)
     res = O.train_step(model, z["tokens"], source=source, segments=2, return_hidden=True)
     np.testing.assert_allclose(res["loss"], z["losses"][0], rtol=2e-6)
     np.testing.assert_allclose(res["hidden"], z["hidden"], rtol=1e-4, atol=1e-5)
@@ -164,12 +167,13 @@ def test_train_step_golden(mode):
             assert got == pytest.approx(f)
 
 
+@pytest.mark.parametrize("suffix", ["", "_d128"])
 @pytest.mark.parametrize("mode", ["predicted", "exact"])
-def test_layer_patterns_golden(mode):
+def test_layer_patterns_golden(mode, suffix):
     """Teacher-forced per-layer masks: feeding the reference's own layer input
     x_l to the oracle's scorer reproduces the reference's retained blocks."""
-    z = np.load(G / f"patterns_{mode}.npz")
-    _, model, source = step_model(mode)
+    z = np.load(G / f"patterns_{mode}{suffix}.npz")
+    _, model, source = step_model(mode, suffix)
     for l in range(2):
         for c in (O.ATTENTION, O.MLP):
             x = z[f"x_{l}_{c}"]

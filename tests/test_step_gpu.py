@@ -4,9 +4,18 @@ The golden fixtures hold the reference's own loss / LoRA gradients / masks
 for a 2-layer model (tests/golden/make_golden.py); the oracle (pinned to the
 same fixtures by test_oracle.py) supplies extra cases at full Llama width.
 
+Two geometries: head_dim 64 (h=128, H=2; suffix "") and head_dim 128
+(h=256, H=2; suffix "_d128", the production attention kernels' head size).
+
 Tolerances (bf16 GEMM operands, fp32 accumulation, fp32 residual stream):
-  loss       relative error <= 1e-2
-  LoRA grads relative L2 error (per tensor) <= 5e-2
+  loss       relative error <= 1e-2   (measured <= 3.6e-4)
+  LoRA grads relative L2 error (per tensor) <= 3e-2
+SURVEY §8c proposes 2e-2 for bf16 runs; the measured worst case is 2.6e-2
+(layer1.lora_q.a of the GQA fixture; 1.6e-2..2.4e-2 on the golden steps): the
+attention backward consumes dO, P and dS as bf16 tensor-core operands and the
+residual gradient enters every dX GEMM rounded to bf16, and layer 1's A_q
+gradient is the deepest product of those roundings.  The errors are printed
+(pytest -s) so the slack stays visible.
 """
 
 import json
@@ -25,17 +34,20 @@ G = Path(__file__).resolve().parent / "golden"
 
 STEP_CFG = dict(n_layers=2, hidden_dim=128, n_heads=2, vocab_size=128, max_seq_len=256,
                 mlp_dim=344, block_size=16, lora_rank=8, lora_alpha=16.0)
+STEP_VARIANTS = {"": STEP_CFG, "_d128": dict(STEP_CFG, hidden_dim=256)}
 LOSS_RTOL = 1e-2
-GRAD_RL2 = 5e-2
+GRAD_RL2 = 3e-2
 
 
-def _model_and_oracle():
-    om = O.init_model(O.Config(**STEP_CFG), seed=17)
+def _model_and_oracle(suffix="", scoring_precision="bf16"):
+    cfg = STEP_VARIANTS[suffix]
+    om = O.init_model(O.Config(**cfg), seed=17)
     O.perturb_lora_b(om, 23)
-    arrays = M.reference_init_arrays(M.ModelConfig(**STEP_CFG), 17)
+    arrays = M.reference_init_arrays(M.ModelConfig(**cfg), 17)
     for name in om.adapter_names():
         arrays[name] = om.adapter(name)
-    return M.DecoderModel(M.ModelConfig(**STEP_CFG), 17, arrays=arrays), om
+    return M.DecoderModel(M.ModelConfig(**cfg), 17, arrays=arrays,
+                          scoring_precision=scoring_precision), om
 
 
 def _rl2(a, b):
@@ -59,19 +71,23 @@ def _source(mode, model, z):
                                     recalibrate_every=1)
 
 
+@pytest.mark.parametrize("suffix", ["", "_d128"])
 @pytest.mark.parametrize("mode", ["dense", "fraction", "predicted", "exact"])
-def test_step_matches_reference(cuda, mode):
-    z = np.load(G / f"step_{mode}.npz")
-    model, _ = _model_and_oracle()
+def test_step_matches_reference(cuda, mode, suffix):
+    z = np.load(G / f"step_{mode}{suffix}.npz")
+    model, _ = _model_and_oracle(suffix)
     src = _source(mode, model, z)
     loss, hidden = model.forward_step(z["tokens"], pattern_source=src, segments=2)
     loss.backward()
     got = float(loss)
-    assert abs(got - z["losses"][0]) <= LOSS_RTOL * abs(z["losses"][0]), (got, z["losses"][0])
+    loss_err = abs(got - z["losses"][0]) / abs(z["losses"][0])
     grads = model.adapter_grads()
-    for name, g in grads.items():
-        ref = z[f"grad__{name}"]
-        assert _rl2(g, ref) <= GRAD_RL2, (name, _rl2(g, ref))
+    errs = {name: _rl2(g, z[f"grad__{name}"]) for name, g in grads.items()}
+    print(f"step {mode}{suffix}: loss rel err {loss_err:.2e}, max grad rel-L2 "
+          f"{max(errs.values()):.2e}")
+    assert loss_err <= LOSS_RTOL, (got, z["losses"][0])
+    for name, e in errs.items():
+        assert e <= GRAD_RL2, (name, e)
     if src is not None and mode in ("fraction",):
         frac = json.loads(str(z["fractions"]))
         for key, f in frac.items():
@@ -86,32 +102,35 @@ def test_step_matches_reference(cuda, mode):
     assert abs(float(loss2) - z["losses"][1]) <= LOSS_RTOL * abs(z["losses"][1])
 
 
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("suffix", ["", "_d128"])
 @pytest.mark.parametrize("mode", ["predicted", "exact"])
-def test_layer_masks_teacher_forced(cuda, mode):
+def test_layer_masks_teacher_forced(cuda, mode, suffix, precision):
     """Feeding the reference's own per-layer input x_l to the GPU hook gives
-    the reference's retained blocks (scores computed on the GPU)."""
-    z = np.load(G / f"patterns_{mode}.npz")
-    zs = np.load(G / f"step_{mode}.npz")
-    model, _ = _model_and_oracle()
+    the reference's retained blocks (scores computed on the GPU), in the
+    production bf16 scorers and the fp32-faithful parity precision."""
+    z = np.load(G / f"patterns_{mode}{suffix}.npz")
+    zs = np.load(G / f"step_{mode}{suffix}.npz")
+    model, _ = _model_and_oracle(suffix, precision)
     src = _source(mode, model, zs)
     flips = 0
     for l in range(2):
         for c in (S.ATTENTION, S.MLP):
             x = torch.as_tensor(z[f"x_{l}_{c}"]).cuda()
             pat = src.pattern(l, c, x, 150)
-            model._mlp_scored.clear()
             want = set(z[f"blocks_{l}_{c}"].tolist())
             flips += len(set(pat.retained_blocks) ^ want)
     assert flips == 0
 
 
-def test_all_retain_equals_dense_bitwise(cuda):
+@pytest.mark.parametrize("suffix", ["", "_d128"])
+def test_all_retain_equals_dense_bitwise(cuda, suffix):
     """tests/test_model.py:186-191: all-retain patterns ≡ dense, bitwise."""
-    z = np.load(G / "step_dense.npz")
-    m1, _ = _model_and_oracle()
+    z = np.load(G / f"step_dense{suffix}.npz")
+    m1, _ = _model_and_oracle(suffix)
     l1, _ = m1.forward_step(z["tokens"], segments=2)
     l1.backward()
-    m2, _ = _model_and_oracle()
+    m2, _ = _model_and_oracle(suffix)
     l2, _ = m2.forward_step(z["tokens"], pattern_source=M.AllRetainSource(), segments=2)
     l2.backward()
     assert float(l1) == float(l2)
