@@ -66,7 +66,10 @@ def parse():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N>1 (gloo only to smoke-test several "
                          "ranks sharing one GPU)")
-    ap.add_argument("--cpu-tokens", type=int, default=4096)
+    ap.add_argument("--cpu-tokens", type=int, default=4096,
+                    help="tokens of the bounded reference sample behind cpu_baseline")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="reference arm: time budget for the full-width layer samples")
     ap.add_argument("--profile-tag", default="")
     return ap.parse_args()
 
@@ -142,17 +145,97 @@ def cpu_geometry(cfg) -> dict:
                 positions=cfg.positions)
 
 
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def reference_available() -> bool:
+    return (REF_DIR / "sparsetune" / "__init__.py").exists()
+
+
+def run_reference_process(args_list, cores: int, timeout_s: float = 1500.0) -> dict:
+    """baseline/run_reference.py in a subprocess: the unmodified reference
+    (sparsetune from baseline/_ref) with NumPy's BLAS pool sized to `cores`
+    before NumPy loads (torchrun exports OMP_NUM_THREADS=1 to its workers)."""
+    env = dict(os.environ)
+    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        env[k] = str(cores)
+    env["PYTHONPATH"] = str(REF_DIR)
+    r = subprocess.run([sys.executable, str(ROOT / "baseline" / "run_reference.py"), *args_list],
+                       env=env, capture_output=True, text=True, timeout=timeout_s)
+    if r.returncode != 0:
+        raise RuntimeError(f"reference run failed ({r.returncode}): {r.stderr[-2000:]}")
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def _ref_layer_seq(wl) -> int:
+    # the reference's O(s^2) Python tile loops: full-width samples up to 16K
+    # (BASELINE.md §3: 32K / 64K are not run)
+    return min(wl["seq"], 16384)
+
+
 def run_reference(args):
+    """The reference arm: the unmodified reference (baseline/_ref) on the host
+    cores, rank 0 only.  A "step" is one bounded sample of the workload: the
+    reference's own forward_step + backward on a 1-layer Llama2-7B-width model
+    at the workload's sequence length (repeated while the time budget allows);
+    `value` is the 32-layer step extrapolated from it (32·t_layer + t_head),
+    `ms_per_step` the measured per-sample time, so ms_per_step x steps is the
+    time actually spent.  Config T's full training step is measured too."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from oracle.cpu_sample import CpuSample, host_cores
-    from paper_2501_09767_b200 import model as M
+    from oracle.cpu_sample import host_cores
 
     wl = CONFIGS[args.config]
     cores = host_cores()
-    # all host threads: torchrun exports OMP_NUM_THREADS=1 to every worker and
-    # numpy's BLAS pool is sized at import, so resize it explicitly
+    if not reference_available():
+        return run_reference_port(args, cores)
+    tiny_only = args.config == "tiny"
+    seq = _ref_layer_seq(wl)
+    meas = run_reference_process(["--tiny-steps", str(max(args.steps, 5)), "--layer-seq",
+                                  *([] if tiny_only else [str(seq)]),
+                                  "--budget-s", str(args.ref_budget_s)], cores)
+    tiny = meas["tiny"]
+    if tiny_only:
+        value, ms, n = tiny["tokens_per_s"], tiny["median_s"] * 1e3, tiny["steps"]
+        sample = "config T full training step, median of the timed steps"
+        per = {}
+    else:
+        lay = meas[f"layer_{seq}"]
+        value, ms, n = lay["tokens_per_s"], lay["median_sample_s"] * 1e3, lay["samples"]
+        sample = (f"unmodified reference (baseline/_ref sparsetune): 1-layer Llama2-7B-width model "
+                  f"at {seq} tokens, forward_step + backward in LeMo predicted mode per step "
+                  f"(t_sample {lay['median_sample_s']:.1f}s = t_layer {lay['layer_s']:.1f}s + "
+                  f"LM head {lay['head_s']:.1f}s); value extrapolated to 32 layers "
+                  f"({lay['extrapolated_step_s']:.0f}s per 32-layer step)")
+        per = {"per_layer_s": lay["layer_s"], "head_s": lay["head_s"],
+               "extrapolated_step_s": lay["extrapolated_step_s"], "sample_s": lay["sample_s"],
+               "retained": lay["retained"], "setup_s": lay["setup_s"]}
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": n, "warmup": 0 if not tiny_only else 1,
+        "steps_requested": args.steps, "warmup_requested": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic tokens, reference init",
+        "config": {"workload": f"{args.config}: {wl['name']} LoRA+LeMo predicted mode",
+                   "seq_len": seq if not tiny_only else 2048, "parallelism": "cpu",
+                   "same_config": wl["model"] in ("llama2_7b", "tiny_t") and seq == wl["seq"]},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "reference_samples": {"tiny_full_step": tiny, **({"layer": per} if per else {})},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_reference_port(args, cores):
+    """Fallback when baseline/_ref is absent: the oracle restatement."""
+    from oracle.cpu_sample import CpuSample
+    from paper_2501_09767_b200 import model as M
+
+    wl = CONFIGS[args.config]
     os.environ["OMP_NUM_THREADS"] = str(cores)
     try:
         from threadpoolctl import threadpool_limits
@@ -161,24 +244,21 @@ def run_reference(args):
         pass
     mcfg = getattr(M, wl["model"])(max_seq_len=wl["seq"])
     sample = CpuSample(sample_tokens=min(args.cpu_tokens, wl["seq"]), **cpu_geometry(mcfg))
-    for _ in range(args.warmup):
-        sample.time_step()
     t_head = sample.time_head()
-    times = [sample.time_step()[0] for _ in range(args.steps)]
+    times = [sample.time_step()[0] for _ in range(2)]
     t_layer = max(float(np.median(times)) - t_head, 1e-9)
     per_step = mcfg.n_layers * t_layer + t_head
     value = sample.s / per_step
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "n_gpus": args.gpus, "steps": len(times), "warmup": 0, "ms_per_step": np.median(times) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
         "config": {"workload": f"{args.config}: {wl['name']} LoRA+LeMo predicted mode",
-                   "seq_len": wl["seq"], "parallelism": "cpu"},
+                   "seq_len": sample.s, "parallelism": "cpu", "same_config": False},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle restatement, 1 decoder layer at h={mcfg.hidden_dim} "
-                                   f"on {sample.s} tokens fwd+bwd (+LM head timed separately), "
-                                   f"extrapolated to {mcfg.n_layers} layers"},
+                         "sample": f"baseline/_ref missing: oracle restatement, 1 decoder layer "
+                                   f"on {sample.s} tokens, extrapolated to {mcfg.n_layers} layers"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -442,17 +522,42 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            from oracle.cpu_sample import CpuSample, host_cores
-            cs = CpuSample(sample_tokens=min(args.cpu_tokens, seq), **cpu_geometry(cfg))
-            meas = cs.measure()
-            cpu = {"value": meas["tokens_per_s"], "unit": "tokens/s", "cores": host_cores(),
-                   "kind": "port",
-                   "sample": f"oracle restatement of the reference, 1 {wl['name']}-width "
-                             f"decoder layer on {cs.s} tokens fwd+bwd in LeMo predicted mode (+LM "
-                             f"head timed separately), extrapolated to {cfg.n_layers} layers "
-                             f"(t_layer={meas['t_layer_s']:.2f}s, t_head={meas['t_head_s']:.2f}s)"}
+            from oracle.cpu_sample import host_cores
+            cores = host_cores()
+            if reference_available():
+                ts = min(args.cpu_tokens, seq)
+                tiny_only = args.config == "tiny"
+                meas = run_reference_process(["--tiny-steps", "5" if tiny_only else "0",
+                                              "--layer-seq", *([] if tiny_only else [str(ts)]),
+                                              "--budget-s", "1"], cores)
+                if tiny_only:
+                    t = meas["tiny"]
+                    cpu = {"value": t["tokens_per_s"], "unit": "tokens/s", "cores": cores,
+                           "kind": "reference",
+                           "sample": "unmodified reference (baseline/_ref): config T full "
+                                     f"training step, median of {t['steps']} steps"}
+                else:
+                    lay = meas[f"layer_{ts}"]
+                    cpu = {"value": lay["tokens_per_s"], "unit": "tokens/s", "cores": cores,
+                           "kind": "reference",
+                           "sample": f"unmodified reference (baseline/_ref): 1 {wl['name']}-width "
+                                     f"layer at {ts} tokens fwd+bwd in LeMo predicted mode, LM "
+                                     f"head timed alone, extrapolated to {cfg.n_layers} layers "
+                                     f"(t_layer={lay['layer_s']:.2f}s, t_head={lay['head_s']:.2f}s)"
+                                     + ("" if ts == seq else
+                                        f"; a {ts}-token sample of the {seq}-token workload "
+                                        "(attention is O(s^2): the 16K CPU rate is lower, see the "
+                                        "reference arm)")}
+            else:
+                from oracle.cpu_sample import CpuSample
+                cs = CpuSample(sample_tokens=min(args.cpu_tokens, seq), **cpu_geometry(cfg))
+                m_ = cs.measure()
+                cpu = {"value": m_["tokens_per_s"], "unit": "tokens/s", "cores": cores,
+                       "kind": "port",
+                       "sample": f"oracle restatement (baseline/_ref missing), 1 layer on {cs.s} "
+                                 f"tokens extrapolated to {cfg.n_layers} layers"}
         except Exception as e:  # noqa: BLE001
-            cpu = {"value": None, "unit": "tokens/s", "cores": None, "kind": "port",
+            cpu = {"value": None, "unit": "tokens/s", "cores": None, "kind": "reference",
                    "sample": f"failed: {e}"}
 
     retained = lemo_stats.get("retained", {})

@@ -187,12 +187,6 @@ int lemo_adam(float* p, const float* g, float* m, float* v, long long n, float l
 /* Block means xb[n] = mean(x[n*b:(n+1)*b]) (predictor.py:117-123). */
 int lemo_block_embed(const float* x, int ldx, int s, int h, int b, float* xb, void* stream);
 
-/* fp32 GEMM C = act(A·op(B))·col_mask; op(B) = B [K,N] (b_trans=0) or Bᵀ
- * with B [N,K] (b_trans=1); act = relu if relu.  Predictor.predict
- * (predictor.py:83-89) and Eq. 3 eq·ekᵀ (predictor.py:186). */
-int lemo_sgemm(const float* A, int lda, const float* B, int ldb, int b_trans, float* C, int ldc,
-               int M, int N, int K, int relu, const unsigned char* col_mask, void* stream);
-
 /* fp32-faithful bf16 tensor-core GEMMs ("bf16x3"): a fp32 matrix is carried
  * as hi = bf16(v), lo = bf16(v - hi) and A·B ≈ Ahi·Bhi + Ahi·Blo + Alo·Bhi is
  * one GEMM over K' = 3K with A' = [hi|hi|lo] (pattern 0) and B' = [hi|lo|hi]
@@ -299,15 +293,12 @@ int lemo_sum_d(const double* x, int n, double scale, double* out, void* stream);
 
 /* ---- attention over the compact retained sequence --------------------------- */
 
-/* Causal softmax attention (tensor.py:646-691) on q/k/v [n, h] bf16 (heads
- * side by side); o [n, h] bf16, lse [h/head_dim, n] fp32 (natural log). */
-int lemo_flash_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int n, int h,
-                   int head_dim, float scale, void* stream);
-
-/* Same contract as lemo_flash_fwd on the tcgen05 path: two query tiles per
- * CTA ping-ponging two softmax warpgroups, S/O in TMEM, P as a bf16 TMEM A
- * operand, single-thread MMA issue; head_dim must be 128.  k, v are [n, kv]:
- * query head hd reads key/value head hd / (h/kv) (grouped-query attention). */
+/* Causal softmax attention (tensor.py:646-691) on q [n, h], k/v [n, kv] bf16
+ * (heads side by side; query head hd reads key/value head hd / (h/kv), i.e.
+ * grouped-query attention when kv < h); o [n, h] bf16, lse [h/head_dim, n]
+ * fp32 (natural log).  tcgen05 kernel: two query tiles per CTA ping-ponging
+ * two softmax warpgroups, S/O in TMEM, P as a bf16 TMEM A operand,
+ * warp-collective MMA issue; head_dim 64 or 128. */
 int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float* lse, int n,
                       int h, int kv, int head_dim, float scale, void* stream);
 
@@ -315,21 +306,16 @@ int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, floa
 int lemo_attn_delta(const void* o, const void* dout, float* delta, int n, int h, int head_dim,
                     void* stream);
 
-/* Attention backward on the tcgen05 path (head_dim 128): an atomic-free dK/dV
- * kernel (transposed formulation, dK/dV resident in TMEM, Pᵀ/dSᵀ as bf16 TMEM
- * A operands) and a dQ kernel, both recomputing P from lse and pipelined so
- * the element-wise phases overlap the MMAs.  Same contract as lemo_flash_bwd,
- * with k, v, dk, dv [n, kv]: each dK/dV CTA accumulates over the h/kv query
- * heads of its group (grouped-query attention). */
+/* Attention backward (tensor.py:693-722) on tcgen05 (head_dim 64 or 128): an
+ * atomic-free dK/dV kernel (transposed formulation, dK/dV resident in TMEM,
+ * Pᵀ/dSᵀ as bf16 TMEM A operands) and a dQ kernel, both recomputing P from lse
+ * and pipelined so the element-wise phases overlap the MMAs.  dq [n, h], dk/dv
+ * [n, kv] fp32; delta is a caller workspace [h/head_dim, n] fp32 (filled by
+ * lemo_attn_delta); each dK/dV CTA accumulates over the h/kv query heads of
+ * its group (grouped-query attention). */
 int lemo_flash_bwd_tc(const void* q, const void* k, const void* v, const void* o,
                       const void* dout, const float* lse, float* delta, float* dq, float* dk,
                       float* dv, int n, int h, int kv, int head_dim, float scale, void* stream);
-
-/* Attention backward (tensor.py:693-722): dq/dk/dv fp32 [n, h]; delta is a
- * caller workspace [h/head_dim, n] fp32. */
-int lemo_flash_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
-                   const float* lse, float* delta, float* dq, float* dk, float* dv, int n, int h,
-                   int head_dim, float scale, void* stream);
 
 #ifdef __cplusplus
 }

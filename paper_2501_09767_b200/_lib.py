@@ -97,7 +97,7 @@ def ptr(t) -> int | None:
 
 
 # kernels launched per entry point (everything else launches exactly one)
-_LAUNCHES = {"lemo_flash_bwd": 3, "lemo_lora_grads": 2}
+_LAUNCHES = {"lemo_flash_bwd_tc": 3, "lemo_lora_grads": 2}
 
 
 class Instrument:

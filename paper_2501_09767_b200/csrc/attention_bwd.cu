@@ -1,6 +1,7 @@
 // tcgen05 FlashAttention backward over the compact retained sequence
 // (tensor.py:693-722: P recomputed from the saved log-sum-exp,
-// Δ = Σ dO∘O, dS = P∘(dP − Δ)), head_dim 128, atomic-free and deterministic.
+// Δ = Σ dO∘O, dS = P∘(dP − Δ)), head_dim D = 64 or 128 (template parameter),
+// atomic-free and deterministic.
 //
 // Two kernels on 128 x 128 tiles (tcgen05 reaches its full rate only for
 // N >= 128: an M128·N64 MMA costs 48 cycles instead of 32, measured by
@@ -54,9 +55,9 @@ namespace lemo {
 namespace fab {
 
 constexpr int kT = 128;                // rows per tile (keys or queries)
-constexpr int kD = 128;                // head dim
 constexpr int kBox = kT * 64 * 2;      // [128 x 64] bf16 SW128 box = 16 KB
-constexpr int kTile = 2 * kBox;        // [128 x 128] = 32 KB
+template <int D>
+constexpr int kTile = (D / 64) * kBox;  // [128 x D] = D/64 boxes
 constexpr int kThreads = 384;
 constexpr float kLog2e = 1.4426950408889634f;
 #ifndef LEMO_FAB_HEAD_GROUP
@@ -67,15 +68,15 @@ constexpr float kLog2e = 1.4426950408889634f;
 #endif
 constexpr int kPolyEvery = LEMO_FAB_POLY;  // every k-th exponential on the FMA pipe (0 = none)
 
-// D (+)= A·Bᵀ with A, B [128 x 128] K-major tiles (two 16 KB boxes each).
+// D (+)= A·Bᵀ with A, B [128 x HD] K-major tiles (HD/64 16 KB boxes each).
 // Warp-collective (the MMA warp stays converged; one elected lane issues).
 // Descriptor start addresses advance by adding (offset >> 4) to the low field
 // (smem addresses < 256 KB never carry out of its 14 bits).
-template <uint32_t kIdesc>
+template <uint32_t kIdesc, int HD>
 __device__ __forceinline__ void mma_kk(uint32_t d, uint32_t a, uint32_t b) {
   const uint64_t da = umma_desc_k_sw128(a), db = umma_desc_k_sw128(b);
 #pragma unroll
-  for (int kk = 0; kk < kD / 16; ++kk) {
+  for (int kk = 0; kk < HD / 16; ++kk) {
     const uint32_t off = ((kk >> 2) * kBox + (kk & 3) * 32) >> 4;
     umma_bf16_ss_w(d, da + off, db + off, kIdesc, kk > 0 ? 1u : 0u);
   }
@@ -83,7 +84,7 @@ __device__ __forceinline__ void mma_kk(uint32_t d, uint32_t a, uint32_t b) {
 
 // D (+)= A·B, A = bf16 [128 x 128] in TMEM, packed as two 32-column groups at
 // a_tmem and a_tmem + 64 (columns 64w..64w+31 hold WG w's 64 values); B =
-// smem [128 (K) x 128 (N)] row-major tile = MN-major, two 16 KB 64-col atoms.
+// smem [128 (K) x HD (N)] row-major tile = MN-major, HD/64 16 KB 64-col atoms.
 template <uint32_t kIdesc>
 __device__ __forceinline__ void mma_tk(uint32_t d, uint32_t a_tmem, uint32_t b, bool acc) {
   const uint64_t db = umma_desc_mn_sw128(b, kBox);
@@ -95,6 +96,14 @@ __device__ __forceinline__ void mma_tk(uint32_t d, uint32_t a_tmem, uint32_t b, 
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// [128 x HD] tile load: HD/64 boxes of 64 columns, contiguous in smem.
+template <int HD>
+__device__ __forceinline__ void load_tile(const CUtensorMap* map, uint64_t* bar, uint8_t* dst,
+                                          int col, int row) {
+#pragma unroll
+  for (int b = 0; b < HD / 64; ++b) tma_load_2d(map, bar, dst + b * kBox, col + 64 * b, row);
 }
 
 // 32 values → 16 packed bf16x2 TMEM columns (element 2j in the low half).
@@ -174,8 +183,10 @@ __device__ __forceinline__ CtaOrder cta_order(int idx, int nblocks, int heads) {
 
 constexpr int kQStages = 3, kOStages = 2;
 static_assert(kOStages <= kQStages, "the pre-barrier loads fill both rings' first kOStages slots");
-constexpr int kSmemKV = (2 + kQStages + kOStages) * kTile + 2 * 2 * kT * 4 + 256;
+template <int HD>
+constexpr int kSmemKV = (2 + kQStages + kOStages) * kTile<HD> + 2 * 2 * kT * 4 + 256;
 
+template <int HD>
 __global__ void __launch_bounds__(kThreads, 1)
     flash_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
@@ -187,6 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                           float sl2, float scale) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = aligned_smem(smem_raw);
+  constexpr int kTile = fab::kTile<HD>;
   uint8_t* sK = smem;
   uint8_t* sV = smem + kTile;
   uint8_t* sQ = smem + 2 * kTile;              // [kQStages]
@@ -208,10 +220,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // CTA = (key tile, key/value head); with grouped-query attention the loop
   // runs over the `group` query heads sharing this key head (u = g·T + t)
-  const CtaOrder co = cta_order(blockIdx.x, gridDim.x, kv / kD);
+  const CtaOrder co = cta_order(blockIdx.x, gridDim.x, kv / HD);
   const int kb = co.tile, kvh = co.head;  // key tile 0 has the most query tiles
   const int group = h / kv;
-  const int k0 = kb * kT, c0 = kvh * kD;
+  const int k0 = kb * kT, c0 = kvh * HD;
   const int T = (n - k0 + kT - 1) / kT;  // query tiles from the diagonal on
   const int U = group * T;
 
@@ -239,18 +251,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the first loads go out before the TMEM allocation / CTA barrier (their
     // ring slots are free on the first pass, so no waits are needed)
     mbar_arrive_expect_tx(kv_full, 2 * kTile);
-    tma_load_2d(&tmK, kv_full, sK, c0, k0);
-    tma_load_2d(&tmK, kv_full, sK + kBox, c0 + 64, k0);
-    tma_load_2d(&tmV, kv_full, sV, c0, k0);
-    tma_load_2d(&tmV, kv_full, sV + kBox, c0 + 64, k0);
+    load_tile<HD>(&tmK, kv_full, sK, c0, k0);
+    load_tile<HD>(&tmV, kv_full, sV, c0, k0);
     for (int t = 0; t < min(U, kOStages); ++t) {
-      const int q0 = k0 + (t % T) * kT, cq = (kvh * group + t / T) * kD;
+      const int q0 = k0 + (t % T) * kT, cq = (kvh * group + t / T) * HD;
       mbar_arrive_expect_tx(&q_full[t], kTile);
-      tma_load_2d(&tmQ, &q_full[t], sQ + t * kTile, cq, q0);
-      tma_load_2d(&tmQ, &q_full[t], sQ + t * kTile + kBox, cq + 64, q0);
+      load_tile<HD>(&tmQ, &q_full[t], sQ + t * kTile, cq, q0);
       mbar_arrive_expect_tx(&o_full[t], kTile);
-      tma_load_2d(&tmO, &o_full[t], sO + t * kTile, cq, q0);
-      tma_load_2d(&tmO, &o_full[t], sO + t * kTile + kBox, cq + 64, q0);
+      load_tile<HD>(&tmO, &o_full[t], sO + t * kTile, cq, q0);
     }
   }
 #ifdef LEMO_FA_TRACE
@@ -273,21 +281,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       for (int t = min(U, kOStages); t < U; ++t) {
-        const int q0 = k0 + (t % T) * kT, cq = (kvh * group + t / T) * kD;
+        const int q0 = k0 + (t % T) * kT, cq = (kvh * group + t / T) * HD;
         const int sq = t % kQStages, so = t % kOStages;
         mbar_wait(&q_empty[sq], ((t / kQStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&q_full[sq], kTile);
-        tma_load_2d(&tmQ, &q_full[sq], sQ + sq * kTile, cq, q0);
-        tma_load_2d(&tmQ, &q_full[sq], sQ + sq * kTile + kBox, cq + 64, q0);
+        load_tile<HD>(&tmQ, &q_full[sq], sQ + sq * kTile, cq, q0);
         mbar_wait(&o_empty[so], ((t / kOStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&o_full[so], kTile);
-        tma_load_2d(&tmO, &o_full[so], sO + so * kTile, cq, q0);
-        tma_load_2d(&tmO, &o_full[so], sO + so * kTile + kBox, cq + 64, q0);
+        load_tile<HD>(&tmO, &o_full[so], sO + so * kTile, cq, q0);
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc_s = umma_idesc_bf16(kT, kT, 0, 0);
-    constexpr uint32_t idesc_g = umma_idesc_bf16(kT, kD, 0, 1);
+    constexpr uint32_t idesc_g = umma_idesc_bf16(kT, HD, 0, 1);
     const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
     const uint32_t aQ = smem_u32(sQ), aO = smem_u32(sO);
 #ifdef LEMO_FA_TRACE
@@ -302,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&q_full[sq], (t / kQStages) & 1);
       MT(6)
       tc_fence_after();
-      mma_kk<idesc_s>(tS, aK, aQ + sq * kTile);
+      mma_kk<idesc_s, HD>(tS, aK, aQ + sq * kTile);
       umma_commit_w(s_full);
     };
     auto issue_dp = [&](int t) {
@@ -310,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&o_full[so], (t / kOStages) & 1);
       MT(7)
       tc_fence_after();
-      mma_kk<idesc_s>(tP, aV, aO + so * kTile);
+      mma_kk<idesc_s, HD>(tP, aV, aO + so * kTile);
       umma_commit_w(dp_full);
     };
     issue_s(0);
@@ -448,9 +454,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     // operand buffers are all consumed: stage dV (WG0) / dK (WG1) in smem
     if (wg == 0)
-      store_tile_f32_tma<kD>(tdV + lane_off, smem, &tmdV, c0, k0, 1.f, r, 1);
+      store_tile_f32_tma<HD>(tdV + lane_off, smem, &tmdV, c0, k0, 1.f, r, 1);
     else
-      store_tile_f32_tma<kD>(tdK + lane_off, smem + kD * kT * 4, &tmdK, c0, k0, scale, r, 2);
+      store_tile_f32_tma<HD>(tdK + lane_off, smem + HD * kT * 4, &tmdK, c0, k0, scale, r, 2);
   }
   tc_fence_before();
   __syncthreads();
@@ -468,8 +474,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 constexpr int kKStages = 3, kVStages = 2;
 static_assert(kVStages <= kKStages, "the pre-barrier loads fill both rings' first kVStages slots");
-constexpr int kSmemQ = (2 + kKStages + kVStages) * kTile + 256;
+template <int HD>
+constexpr int kSmemQ = (2 + kKStages + kVStages) * kTile<HD> + 256;
 
+template <int HD>
 __global__ void __launch_bounds__(kThreads, 1)
     flash_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ,
                         const __grid_constant__ CUtensorMap tmK,
@@ -480,6 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         float sl2, float scale) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = aligned_smem(smem_raw);
+  constexpr int kTile = fab::kTile<HD>;
   uint8_t* sQ = smem;
   uint8_t* sO = smem + kTile;
   uint8_t* sK = smem + 2 * kTile;              // [kKStages]
@@ -498,11 +507,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const CtaOrder co = cta_order(blockIdx.x, gridDim.x, h / kD);
-  const int ntq = (int)gridDim.x / (h / kD);
+  const CtaOrder co = cta_order(blockIdx.x, gridDim.x, h / HD);
+  const int ntq = (int)gridDim.x / (h / HD);
   const int qb = ntq - 1 - co.tile, hd = co.head;  // the last query tile has the most key tiles
-  const int q0 = qb * kT, c0 = hd * kD;
-  const int ck = (hd / (h / kv)) * kD;  // key/value head of this query head
+  const int q0 = qb * kT, c0 = hd * HD;
+  const int ck = (hd / (h / kv)) * HD;  // key/value head of this query head
   const int T = qb + 1;  // key tiles 0 … diagonal
 
   if (warp == 0 && lane == 0) {
@@ -529,17 +538,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
     // the first loads go out before the TMEM allocation / CTA barrier
     mbar_arrive_expect_tx(q_full, 2 * kTile);
-    tma_load_2d(&tmQ, q_full, sQ, c0, q0);
-    tma_load_2d(&tmQ, q_full, sQ + kBox, c0 + 64, q0);
-    tma_load_2d(&tmO, q_full, sO, c0, q0);
-    tma_load_2d(&tmO, q_full, sO + kBox, c0 + 64, q0);
+    load_tile<HD>(&tmQ, q_full, sQ, c0, q0);
+    load_tile<HD>(&tmO, q_full, sO, c0, q0);
     for (int j = 0; j < min(T, kVStages); ++j) {
       mbar_arrive_expect_tx(&k_full[j], kTile);
-      tma_load_2d(&tmK, &k_full[j], sK + j * kTile, ck, j * kT);
-      tma_load_2d(&tmK, &k_full[j], sK + j * kTile + kBox, ck + 64, j * kT);
+      load_tile<HD>(&tmK, &k_full[j], sK + j * kTile, ck, j * kT);
       mbar_arrive_expect_tx(&v_full[j], kTile);
-      tma_load_2d(&tmV, &v_full[j], sV + j * kTile, ck, j * kT);
-      tma_load_2d(&tmV, &v_full[j], sV + j * kTile + kBox, ck + 64, j * kT);
+      load_tile<HD>(&tmV, &v_full[j], sV + j * kTile, ck, j * kT);
     }
   }
 #ifdef LEMO_FA_TRACE
@@ -565,17 +570,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int sk = j % kKStages, sv = j % kVStages;
         mbar_wait(&k_empty[sk], ((j / kKStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&k_full[sk], kTile);
-        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile, ck, j * kT);
-        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile + kBox, ck + 64, j * kT);
+        load_tile<HD>(&tmK, &k_full[sk], sK + sk * kTile, ck, j * kT);
         mbar_wait(&v_empty[sv], ((j / kVStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&v_full[sv], kTile);
-        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile, ck, j * kT);
-        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile + kBox, ck + 64, j * kT);
+        load_tile<HD>(&tmV, &v_full[sv], sV + sv * kTile, ck, j * kT);
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc_s = umma_idesc_bf16(kT, kT, 0, 0);
-    constexpr uint32_t idesc_g = umma_idesc_bf16(kT, kD, 0, 1);
+    constexpr uint32_t idesc_g = umma_idesc_bf16(kT, HD, 0, 1);
     const uint32_t aQ = smem_u32(sQ), aO = smem_u32(sO);
     const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
     mbar_wait(q_full, 0);
@@ -584,14 +587,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (j >= 2) mbar_wait(&s_free[b], ((j - 2) >> 1) & 1);  // phase A of j-2 read it
       mbar_wait(&k_full[sk], (j / kKStages) & 1);
       tc_fence_after();
-      mma_kk<idesc_s>(tmem + 128 * b, aQ, aK + sk * kTile);
+      mma_kk<idesc_s, HD>(tmem + 128 * b, aQ, aK + sk * kTile);
       umma_commit_w(&s_full[b]);
     };
     auto issue_dp = [&](int j) {
       const int sv = j % kVStages;
       mbar_wait(&v_full[sv], (j / kVStages) & 1);
       tc_fence_after();
-      mma_kk<idesc_s>(tP, aO, aV + sv * kTile);
+      mma_kk<idesc_s, HD>(tP, aO, aV + sv * kTile);
       umma_commit_w(dp_full);
       umma_commit_w(&v_empty[sv]);
     };
@@ -679,8 +682,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_wait(dq_done, 0);
     tc_fence_after();
-    store_tile_f32_tma<64>(tdQ + lane_off + 64 * wg, smem + wg * 64 * kT * 4, &tmdQ,
-                           c0 + 64 * wg, q0, scale, r, 1 + wg);
+    constexpr int kHalf = HD / 2;  // each warpgroup stores half of dQ's columns
+    store_tile_f32_tma<kHalf>(tdQ + lane_off + kHalf * wg, smem + wg * kHalf * kT * 4, &tmdQ,
+                              c0 + kHalf * wg, q0, scale, r, 1 + wg);
   }
   tc_fence_before();
   __syncthreads();
@@ -708,18 +712,92 @@ extern "C" int lemo_fab_cta_get(void* host) {
 }
 #endif
 
+namespace lemo {
+namespace fab {
+// delta[hd, i] = Σ_d dO[i, hd·D + d] · O[i, hd·D + d]  (tensor.py:696): one CTA
+// per row, 16-byte loads, a group of D/8 lanes per head, shuffle reduction.
+template <int HD>
+__global__ void __launch_bounds__(256) delta_kernel(const __nv_bfloat16* __restrict__ o,
+                                                    const __nv_bfloat16* __restrict__ dout,
+                                                    float* __restrict__ delta, int n, int h) {
+  constexpr int kLanes = HD / 8;  // 16 (HD 128) or 8 (HD 64) lanes per head
+  const int row = blockIdx.x;
+  const int H = h / HD;
+  const int sub = threadIdx.x % kLanes;
+  for (int base = 0; base < H; base += blockDim.x / kLanes) {  // warp-uniform trip count
+    const int hd = base + (int)threadIdx.x / kLanes;
+    const bool ok = hd < H;
+    const size_t off = (size_t)row * h + (size_t)(ok ? hd : 0) * HD + sub * 8;
+    const uint4 a = ok ? *reinterpret_cast<const uint4*>(o + off) : make_uint4(0, 0, 0, 0);
+    const uint4 b = ok ? *reinterpret_cast<const uint4*>(dout + off) : make_uint4(0, 0, 0, 0);
+    const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      acc += bf16_lo(av[e]) * bf16_lo(bv[e]) + bf16_hi(av[e]) * bf16_hi(bv[e]);
+#pragma unroll
+    for (int m = kLanes / 2; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if (ok && sub == 0) delta[(size_t)hd * n + row] = acc;
+  }
+}
+}  // namespace fab
+}  // namespace lemo
+
 using namespace lemo;
 
 extern "C" {
 
 int lemo_attn_delta(const void* o, const void* dout, float* delta, int n, int h, int head_dim,
-                    void* stream);
+                    void* stream) {
+  if (n <= 0) return 0;
+  LEMO_ARG_CHECK(head_dim == 64 || head_dim == 128, "lemo_attn_delta: head_dim must be 64 or 128");
+  auto* op = reinterpret_cast<const __nv_bfloat16*>(o);
+  auto* dp = reinterpret_cast<const __nv_bfloat16*>(dout);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (head_dim == 128)
+    fab::delta_kernel<128><<<n, 256, 0, st>>>(op, dp, delta, n, h);
+  else
+    fab::delta_kernel<64><<<n, 256, 0, st>>>(op, dp, delta, n, h);
+  LEMO_CHECK_LAUNCH("lemo_attn_delta");
+  return 0;
+}
+
+}  // extern "C"
+
+namespace {
+template <int HD>
+int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+               const CUtensorMap& to, const float* lse, const float* delta,
+               const CUtensorMap& tdq, const CUtensorMap& tdk, const CUtensorMap& tdv, int n, int h,
+               int kv, float scale, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fab::flash_bwd_dkdv_kernel<HD>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         fab::kSmemKV<HD>);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fab::flash_bwd_dq_kernel<HD>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, fab::kSmemQ<HD>);
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  const float sl2 = scale * fab::kLog2e;
+  const int nt = (n + fab::kT - 1) / fab::kT;
+  fab::flash_bwd_dkdv_kernel<HD><<<nt * (kv / HD), fab::kThreads, fab::kSmemKV<HD>, st>>>(
+      tq, tk, tv, to, lse, delta, tdk, tdv, n, h, kv, sl2, scale);
+  fab::flash_bwd_dq_kernel<HD><<<nt * (h / HD), fab::kThreads, fab::kSmemQ<HD>, st>>>(
+      tq, tk, tv, to, lse, delta, tdq, n, h, kv, sl2, scale);
+  return (int)cudaGetLastError();
+}
+}  // namespace
+
+extern "C" {
 
 int lemo_flash_bwd_tc(const void* q, const void* k, const void* v, const void* o,
                       const void* dout, const float* lse, float* delta, float* dq, float* dk,
                       float* dv, int n, int h, int kv, int head_dim, float scale, void* stream) {
   if (n <= 0) return 0;
-  LEMO_ARG_CHECK(head_dim == fab::kD, "lemo_flash_bwd_tc: head_dim must be 128");
+  LEMO_ARG_CHECK(head_dim == 64 || head_dim == 128, "lemo_flash_bwd_tc: head_dim must be 64 or 128");
   LEMO_ARG_CHECK(h % head_dim == 0 && kv % head_dim == 0 && kv > 0 && h % kv == 0,
                  "lemo_flash_bwd_tc: h, kv must be multiples of head_dim with kv | h");
   int rc = lemo_attn_delta(o, dout, delta, n, h, head_dim, stream);
@@ -734,26 +812,11 @@ int lemo_flash_bwd_tc(const void* q, const void* k, const void* v, const void* o
   if (!rc) rc = make_tma_f32_2d(&tdk, dk, (uint64_t)n, (uint64_t)kv, (uint64_t)kv, fab::kT);
   if (!rc) rc = make_tma_f32_2d(&tdv, dv, (uint64_t)n, (uint64_t)kv, (uint64_t)kv, fab::kT);
   if (rc) LEMO_RETURN_RC("lemo_flash_bwd_tc", rc);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fab::flash_bwd_dkdv_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         fab::kSmemKV);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(fab::flash_bwd_dq_kernel,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, fab::kSmemQ);
-    if (e != cudaSuccess) LEMO_RETURN_RC("lemo_flash_bwd_tc", (int)e);
-    attr = true;
-  }
-  const float sl2 = scale * fab::kLog2e;
-  const int nt = (n + fab::kT - 1) / fab::kT;
   cudaStream_t st = (cudaStream_t)stream;
-  fab::flash_bwd_dkdv_kernel<<<nt * (kv / head_dim), fab::kThreads, fab::kSmemKV, st>>>(
-      tq, tk, tv, to, lse, delta, tdk, tdv, n, h, kv, sl2, scale);
-  fab::flash_bwd_dq_kernel<<<nt * (h / head_dim), fab::kThreads, fab::kSmemQ, st>>>(
-      tq, tk, tv, to, lse, delta, tdq, n, h, kv, sl2, scale);
-  LEMO_CHECK_LAUNCH("lemo_flash_bwd_tc");
-  return 0;
+  rc = head_dim == 128
+           ? launch_bwd<128>(tq, tk, tv, to, lse, delta, tdq, tdk, tdv, n, h, kv, scale, st)
+           : launch_bwd<64>(tq, tk, tv, to, lse, delta, tdq, tdk, tdv, n, h, kv, scale, st);
+  LEMO_RETURN_RC("lemo_flash_bwd_tc", rc);
 }
 
 }  // extern "C"

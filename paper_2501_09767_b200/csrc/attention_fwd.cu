@@ -1,6 +1,7 @@
 // tcgen05 FlashAttention forward over the compact retained sequence
 // (tensor.py:646-691: causal by compact index, q pre-scaled by 1/√d, online
-// softmax, saves lse), head_dim 128.
+// softmax, saves lse), head_dim D = 64 or 128 (template parameter; a D-wide
+// tile is D/64 SW128 boxes of 64 columns).
 //
 // One CTA = two adjacent 128-query tiles (Q0, Q1) of one head sharing every
 // K/V tile load; 320 threads:
@@ -39,7 +40,6 @@ namespace lemo {
 namespace faf {
 
 constexpr int kT = 128;
-constexpr int kD = 128;
 #ifndef LEMO_FA_HEAD_GROUP
 #define LEMO_FA_HEAD_GROUP 8
 #endif
@@ -48,10 +48,12 @@ constexpr int kD = 128;
 #endif
 constexpr int kPolyEvery = LEMO_FA_POLY;  // every k-th exponential pair on the FMA pipe (0 = none)
 constexpr int kBox = kT * 64 * 2;   // [128 x 64] bf16 SW128 box = 16 KB
-constexpr int kTile = 2 * kBox;     // [128 x 128] = 32 KB
+template <int D>
+constexpr int kTile = (D / 64) * kBox;  // [128 x D]: 32 KB (D = 128) / 16 KB (D = 64)
 constexpr int kKStages = 3, kVStages = 2;
 constexpr int kThreads = 320;
-constexpr int kSmem = (2 + kKStages + kVStages) * kTile + 256;
+template <int D>
+constexpr int kSmem = (2 + kKStages + kVStages) * kTile<D> + 256;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -62,18 +64,26 @@ __device__ __forceinline__ uint8_t* aligned_smem(uint8_t* raw) {
 
 // Warp-collective (the MMA warp stays converged, one elected lane issues);
 // descriptor start addresses advance by (offset >> 4) in the low field.
-template <uint32_t kIdesc>
+template <uint32_t kIdesc, int D>
 __device__ __forceinline__ void mma_qk(uint32_t d, uint32_t a, uint32_t b) {
   const uint64_t da = umma_desc_k_sw128(a), db = umma_desc_k_sw128(b);
 #pragma unroll
-  for (int kk = 0; kk < kD / 16; ++kk) {
+  for (int kk = 0; kk < D / 16; ++kk) {
     const uint32_t off = ((kk >> 2) * kBox + (kk & 3) * 32) >> 4;
     umma_bf16_ss_w(d, da + off, db + off, kIdesc, kk > 0 ? 1u : 0u);
   }
 }
 
+// [128 x D] tile load: D/64 boxes of 64 columns, contiguous in smem.
+template <int D>
+__device__ __forceinline__ void load_tile(const CUtensorMap* map, uint64_t* bar, uint8_t* dst,
+                                          int col, int row) {
+#pragma unroll
+  for (int b = 0; b < D / 64; ++b) tma_load_2d(map, bar, dst + b * kBox, col + 64 * b, row);
+}
+
 // O (+)= P·V: P = bf16 [128 x 128] packed in TMEM columns [p, p+64), V_j smem
-// [128 keys x 128 d] = MN-major B.
+// [128 keys x D] = MN-major B.
 template <uint32_t kIdesc>
 __device__ __forceinline__ void mma_pv(uint32_t d, uint32_t p, uint32_t b, bool acc) {
   const uint64_t db = umma_desc_mn_sw128(b, kBox);
@@ -82,16 +92,18 @@ __device__ __forceinline__ void mma_pv(uint32_t d, uint32_t p, uint32_t b, bool 
     umma_bf16_ts_w(d, p + kk * 8, db + kk * (2048 >> 4), kIdesc, (acc || kk > 0) ? 1u : 0u);
 }
 
+template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                      float* __restrict__ lse, int n, int h, int group, float sl2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = aligned_smem(smem_raw);
+  constexpr int kTileD = kTile<D>;
   uint8_t* sQ = smem;                          // Q0 | Q1
-  uint8_t* sK = smem + 2 * kTile;              // [kKStages]
-  uint8_t* sV = sK + kKStages * kTile;         // [kVStages]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVStages * kTile);
+  uint8_t* sK = smem + 2 * kTileD;             // [kKStages]
+  uint8_t* sV = sK + kKStages * kTileD;        // [kVStages]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVStages * kTileD);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;               // [kKStages]
   uint64_t* k_empty = k_full + kKStages;     // [kKStages]
@@ -107,13 +119,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 1-D grid over (pairs x heads), dispatched in index order: heads in groups
   // of LEMO_FA_HEAD_GROUP, heavy (late) pairs first within a group, so the
   // co-resident CTAs share a few heads' K/V in L2 and no heavy pair starts late
-  const int heads = h / kD, npairs = (int)gridDim.x / heads;
+  const int heads = h / D, npairs = (int)gridDim.x / heads;
   const int G = heads < LEMO_FA_HEAD_GROUP ? heads : LEMO_FA_HEAD_GROUP;
   const int grp = (int)blockIdx.x / (npairs * G), gbase = grp * G;
   const int gsz = min(G, heads - gbase), rem = (int)blockIdx.x - grp * npairs * G;
   const int pair = npairs - 1 - rem / gsz;
-  const int hd = gbase + rem % gsz, c0 = hd * kD;
-  const int ck = (hd / group) * kD;  // key/value head of this query head
+  const int hd = gbase + rem % gsz, c0 = hd * D;
+  const int ck = (hd / group) * D;  // key/value head of this query head
   const int qt0 = 2 * pair;
   const bool two = qt0 + 1 < nt;
   const int T = two ? qt0 + 2 : qt0 + 1;  // KV tiles; Q0 uses [0, qt0], Q1 uses [0, qt0+1]
@@ -139,18 +151,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
     // the first loads go out before the TMEM allocation / CTA barrier (first
     // pass over the rings: no empty-slot waits needed)
-    mbar_arrive_expect_tx(q_full, (two ? 2 : 1) * kTile);
-    for (int g = 0; g < (two ? 2 : 1); ++g) {
-      tma_load_2d(&tmQ, q_full, sQ + g * kTile, c0, (qt0 + g) * kT);
-      tma_load_2d(&tmQ, q_full, sQ + g * kTile + kBox, c0 + 64, (qt0 + g) * kT);
-    }
+    mbar_arrive_expect_tx(q_full, (two ? 2 : 1) * kTileD);
+    for (int g = 0; g < (two ? 2 : 1); ++g)
+      load_tile<D>(&tmQ, q_full, sQ + g * kTileD, c0, (qt0 + g) * kT);
     for (int j = 0; j < min(T, kVStages); ++j) {
-      mbar_arrive_expect_tx(&k_full[j], kTile);
-      tma_load_2d(&tmK, &k_full[j], sK + j * kTile, ck, j * kT);
-      tma_load_2d(&tmK, &k_full[j], sK + j * kTile + kBox, ck + 64, j * kT);
-      mbar_arrive_expect_tx(&v_full[j], kTile);
-      tma_load_2d(&tmV, &v_full[j], sV + j * kTile, ck, j * kT);
-      tma_load_2d(&tmV, &v_full[j], sV + j * kTile + kBox, ck + 64, j * kT);
+      mbar_arrive_expect_tx(&k_full[j], kTileD);
+      load_tile<D>(&tmK, &k_full[j], sK + j * kTileD, ck, j * kT);
+      mbar_arrive_expect_tx(&v_full[j], kTileD);
+      load_tile<D>(&tmV, &v_full[j], sV + j * kTileD, ck, j * kT);
     }
   }
   if (warp == 9) tmem_alloc<512>(tmem_slot);
@@ -164,18 +172,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = min(T, kVStages); j < T; ++j) {
         const int sk = j % kKStages, sv = j % kVStages;
         mbar_wait(&k_empty[sk], ((j / kKStages) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[sk], kTile);
-        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile, ck, j * kT);
-        tma_load_2d(&tmK, &k_full[sk], sK + sk * kTile + kBox, ck + 64, j * kT);
+        mbar_arrive_expect_tx(&k_full[sk], kTileD);
+        load_tile<D>(&tmK, &k_full[sk], sK + sk * kTileD, ck, j * kT);
         mbar_wait(&v_empty[sv], ((j / kVStages) & 1) ^ 1);
-        mbar_arrive_expect_tx(&v_full[sv], kTile);
-        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile, ck, j * kT);
-        tma_load_2d(&tmV, &v_full[sv], sV + sv * kTile + kBox, ck + 64, j * kT);
+        mbar_arrive_expect_tx(&v_full[sv], kTileD);
+        load_tile<D>(&tmV, &v_full[sv], sV + sv * kTileD, ck, j * kT);
       }
     }
   } else if (warp == 9) {
     constexpr uint32_t idesc_s = umma_idesc_bf16(kT, kT, 0, 0);
-    constexpr uint32_t idesc_o = umma_idesc_bf16(kT, kD, 0, 1);
+    constexpr uint32_t idesc_o = umma_idesc_bf16(kT, D, 0, 1);
     const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV);
     // tile g takes part in KV tile j iff j <= qt0 + g
     auto uses = [&](int g, int j) { return (g == 0 || two) && j <= qt0 + g; };
@@ -185,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int sk = j % kKStages;
       if (g == 0) mbar_wait(&k_full[sk], (j / kKStages) & 1);
       tc_fence_after();
-      mma_qk<idesc_s>(tmem + 128 * g, aQ + g * kTile, aK + sk * kTile);
+      mma_qk<idesc_s, D>(tmem + 128 * g, aQ + g * kTileD, aK + sk * kTileD);
       umma_commit_w(&s_full[g]);
       if (g == last_k_user(j)) umma_commit_w(&k_empty[sk]);
     };
@@ -194,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&p_full[g], j & 1);
       if (g == 0 || !uses(0, j)) mbar_wait(&v_full[sv], (j / kVStages) & 1);
       tc_fence_after();
-      mma_pv<idesc_o>(tmem + 256 + 128 * g, tmem + 128 * g, aV + sv * kTile, j > 0);
+      mma_pv<idesc_o>(tmem + 256 + 128 * g, tmem + 128 * g, aV + sv * kTileD, j > 0);
       if (g == last_k_user(j)) umma_commit_w(&v_empty[sv]);
       if (j == qt0 + g) umma_commit_w(&o_done[g]);
     };
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
           // PV_g(j-1) completed before S_g(j) did (issue order): O is stable
 #pragma unroll 1
-          for (int c = 0; c < kD / 32; ++c) {
+          for (int c = 0; c < D / 32; ++c) {
             uint32_t raw[32];
             tmem_ld_32x32b_x32(tO + c * 32, raw);
             tmem_ld_wait();
@@ -317,9 +323,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float inv_l = 1.f / l;
       // O_g = acc / l as bf16, staged over Q_g (every MMA reading it is done)
       // in two 64-column SW128 boxes, then written by TMA (rows ≥ n clipped)
-      uint8_t* stage = sQ + g * kTile;
+      uint8_t* stage = sQ + g * kTileD;
 #pragma unroll 1
-      for (int c = 0; c < kD / 32; ++c) {
+      for (int c = 0; c < D / 32; ++c) {
         uint32_t raw[32];
         tmem_ld_32x32b_x32(tO + c * 32, raw);
         tmem_ld_wait();
@@ -335,8 +341,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
       if (r == 0) {
-        tma_store_2d(&tmO, stage, c0, qt * kT);
-        tma_store_2d(&tmO, stage + kBox, c0 + 64, qt * kT);
+#pragma unroll
+        for (int b = 0; b < D / 64; ++b) tma_store_2d(&tmO, stage + b * kBox, c0 + 64 * b, qt * kT);
         tma_store_commit_and_wait_read();
       }
       if (qr < n) lse[(size_t)hd * n + qr] = (m + log2f(l)) * kLn2;
@@ -366,7 +372,7 @@ extern "C" {
 int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float* lse, int n,
                       int h, int kv, int head_dim, float scale, void* stream) {
   if (n <= 0) return 0;
-  LEMO_ARG_CHECK(head_dim == faf::kD, "lemo_flash_fwd_tc: head_dim must be 128");
+  LEMO_ARG_CHECK(head_dim == 64 || head_dim == 128, "lemo_flash_fwd_tc: head_dim must be 64 or 128");
   LEMO_ARG_CHECK(h % head_dim == 0 && kv % head_dim == 0 && kv > 0 && h % kv == 0,
                  "lemo_flash_fwd_tc: h, kv must be multiples of head_dim with kv | h");
   CUtensorMap tq, tk, tv;
@@ -376,17 +382,33 @@ int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, floa
   CUtensorMap to;  // output (TMA stores)
   if (!rc) rc = make_tma_bf16_2d(&to, o, (uint64_t)n, (uint64_t)h, (uint64_t)h, faf::kT);
   if (rc) LEMO_RETURN_RC("lemo_flash_fwd_tc", rc);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(faf::flash_fwd_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, faf::kSmem);
-    if (e != cudaSuccess) LEMO_RETURN_RC("lemo_flash_fwd_tc", (int)e);
-    attr = true;
-  }
   const int nt = (n + faf::kT - 1) / faf::kT;
   dim3 grid((h / head_dim) * ((nt + 1) / 2));
-  faf::flash_fwd_kernel<<<grid, faf::kThreads, faf::kSmem, (cudaStream_t)stream>>>(
-      tq, tk, tv, to, lse, n, h, h / kv, scale * faf::kLog2e);
+  cudaStream_t st = (cudaStream_t)stream;
+  const float sl2 = scale * faf::kLog2e;
+  if (head_dim == 128) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(faf::flash_fwd_kernel<128>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           faf::kSmem<128>);
+      if (e != cudaSuccess) LEMO_RETURN_RC("lemo_flash_fwd_tc", (int)e);
+      attr = true;
+    }
+    faf::flash_fwd_kernel<128><<<grid, faf::kThreads, faf::kSmem<128>, st>>>(
+        tq, tk, tv, to, lse, n, h, h / kv, sl2);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(faf::flash_fwd_kernel<64>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           faf::kSmem<64>);
+      if (e != cudaSuccess) LEMO_RETURN_RC("lemo_flash_fwd_tc", (int)e);
+      attr = true;
+    }
+    faf::flash_fwd_kernel<64><<<grid, faf::kThreads, faf::kSmem<64>, st>>>(
+        tq, tk, tv, to, lse, n, h, h / kv, sl2);
+  }
   LEMO_CHECK_LAUNCH("lemo_flash_fwd_tc");
   return 0;
 }

@@ -1,8 +1,8 @@
 // Pattern scoring and selection kernels (K1/K2 of the design):
 //   block_embed      predictor.py:117-123 (block mean of the residual stream)
-//   sgemm            Predictor.predict (predictor.py:83-89) and Eq. 3 eq·ekᵀ
-//                    (predictor.py:176-186), fp32 so predicted scores track
-//                    the fp32 reference to ~1e-6 (mask parity)
+//   (the predictor GEMMs and Eq. 3 are fp32-faithful bf16x3 tcgen05 GEMMs with
+//    promoted accumulation, gemm_ops.cu / gemm.cuh)
+//   pack_tril        sparsity.py:35-69 packed lower triangle (+ clamp)
 //   colsum_clamped   model.py:575-578 + sparsity.py:253-260 (clamp ≥ 0, f64
 //                    column sums accumulated in ascending query block)
 //   mlp_block_scores sparsity.py:284-305 (mean |inner| per token, block max)
@@ -63,104 +63,6 @@ __global__ void __launch_bounds__(256) block_embed_generic_kernel(const float* _
   const float fb = (float)b;
   acc.x /= fb; acc.y /= fb; acc.z /= fb; acc.w /= fb;
   reinterpret_cast<float4*>(xb + (size_t)n * h)[c] = acc;
-}
-
-// --------------------------------------------------------------------------
-// fp32 SIMT GEMM, 128x128x8 tiles, 8x8 per thread.  C = act(A·op(B))·mask.
-template <bool kBT>
-__global__ void __launch_bounds__(256) sgemm_kernel(const float* __restrict__ A, int lda,
-                                                    const float* __restrict__ B, int ldb,
-                                                    float* __restrict__ C, int ldc, int M, int N,
-                                                    int K, int relu,
-                                                    const unsigned char* __restrict__ mask) {
-  __shared__ float As[2][8][132];
-  __shared__ float Bs[2][8][132];
-  const int tid = threadIdx.x;
-  const int m0 = blockIdx.y * 128, n0 = blockIdx.x * 128;
-  const int tx = tid & 15, ty = tid >> 4;
-  float acc[8][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-
-  // loader mapping: A: row = tid>>1, k4 = (tid&1)*4 ; B (kBT): n = tid>>1, k4 = (tid&1)*4
-  //                 B (!kBT): k = tid>>5, n4 = (tid&31)*4
-  float ra[4], rb[4];
-  auto load = [&](int k0) {
-    {
-      const int row = m0 + (tid >> 1), kk = k0 + (tid & 1) * 4;
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        ra[e] = (row < M && kk + e < K) ? __ldg(A + (size_t)row * lda + kk + e) : 0.f;
-    }
-    if (kBT) {
-      const int n = n0 + (tid >> 1), kk = k0 + (tid & 1) * 4;
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        rb[e] = (n < N && kk + e < K) ? __ldg(B + (size_t)n * ldb + kk + e) : 0.f;
-    } else {
-      const int kk = k0 + (tid >> 5), n = n0 + (tid & 31) * 4;
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        rb[e] = (kk < K && n + e < N) ? __ldg(B + (size_t)kk * ldb + n + e) : 0.f;
-    }
-  };
-  auto store = [&](int buf) {
-    {
-      const int r = tid >> 1, k4 = (tid & 1) * 4;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) As[buf][k4 + e][r] = ra[e];
-    }
-    if (kBT) {
-      const int n = tid >> 1, k4 = (tid & 1) * 4;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) Bs[buf][k4 + e][n] = rb[e];
-    } else {
-      const int k = tid >> 5, n4 = (tid & 31) * 4;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) Bs[buf][k][n4 + e] = rb[e];
-    }
-  };
-  load(0);
-  store(0);
-  __syncthreads();
-  int buf = 0;
-  for (int k0 = 0; k0 < K; k0 += 8) {
-    const bool more = k0 + 8 < K;
-    if (more) load(k0 + 8);
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      float a[8], bv[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = As[buf][kk][ty + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) bv[j] = Bs[buf][kk][tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], bv[j], acc[i][j]);
-    }
-    if (more) {
-      store(buf ^ 1);
-      __syncthreads();
-      buf ^= 1;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int row = m0 + ty + 16 * i;
-    if (row >= M) continue;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int col = n0 + tx + 16 * j;
-      if (col >= N) continue;
-      float v = acc[i][j];
-      if (relu) v = fmaxf(v, 0.f);
-      if (mask) v = mask[col] ? v : 0.f;
-      C[(size_t)row * ldc + col] = v;
-    }
-  }
 }
 
 // vec[n] = Σ_{m=n}^{nb-1} (double)max(S[m,n], 0), ascending m (sparsity.py:256-259)
@@ -409,19 +311,6 @@ int lemo_block_embed(const float* x, int ldx, int s, int h, int b, float* xb, vo
     block_embed_generic_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(x, ldx, nb, h, b,
                                                                                xb);
   LEMO_CHECK_LAUNCH("lemo_block_embed");
-  return 0;
-}
-
-int lemo_sgemm(const float* A, int lda, const float* B, int ldb, int b_trans, float* C, int ldc,
-               int M, int N, int K, int relu, const unsigned char* col_mask, void* stream) {
-  if (M <= 0 || N <= 0) return 0;
-  dim3 grid((N + 127) / 128, (M + 127) / 128);
-  cudaStream_t st = (cudaStream_t)stream;
-  if (b_trans)
-    sgemm_kernel<true><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, relu, col_mask);
-  else
-    sgemm_kernel<false><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, relu, col_mask);
-  LEMO_CHECK_LAUNCH("lemo_sgemm");
   return 0;
 }
 

@@ -93,8 +93,8 @@ class ModelConfig:
             raise ContractError("GPU kernels need vocab_size % 32 == 0")
         if self.lora_rank > 16:
             raise ContractError("GPU kernels support LoRA rank <= 16")
-        if self.kv_heads != self.n_heads and (self.head_dim != 128 or self.kv_dim % 128):
-            raise ContractError("grouped-query attention runs on the tcgen05 path: head_dim 128")
+        if self.kv_dim % 128:
+            raise ContractError("GPU kernels need n_kv_heads·head_dim % 128 == 0")
 
 
 def llama2_7b(**kw) -> ModelConfig:

@@ -344,23 +344,6 @@ def block_embed(x, b, out=None):
     return out
 
 
-def sgemm(a, b, *, b_trans=False, relu=False, col_mask=None, out=None):
-    """fp32 C = act(a·op(b))·col_mask; op(b) = b ([K,N]) or bᵀ (b is [N,K])."""
-    _check(a, b, col_mask, out)
-    _dt(a, F32, "a")
-    _dt(b, F32, "b")
-    M, K = a.shape
-    N = b.shape[0] if b_trans else b.shape[1]
-    Kb = b.shape[1] if b_trans else b.shape[0]
-    if K != Kb:
-        raise DimensionError(f"matmul inner extents differ: {tuple(a.shape)} vs {tuple(b.shape)}")
-    if out is None:
-        out = torch.empty(M, N, dtype=F32, device=a.device)
-    call("lemo_sgemm", ptr(a), a.stride(0), ptr(b), b.stride(0), int(bool(b_trans)), ptr(out),
-         out.stride(0), M, N, K, int(bool(relu)), ptr(col_mask), _s())
-    return out
-
-
 def split_bf16x3(a, pattern, out=None):
     """fp32 [M, K] -> bf16 [M, 3K] operand ([hi|hi|lo] pattern 0, [hi|lo|hi] pattern 1)."""
     _check(a, out)
@@ -506,31 +489,23 @@ def quantile_lower(data, q, out, *, plus_one=False):
 # attention
 
 
-def flash_fwd(q, k, v, *, head_dim, scale, o=None, lse=None, impl=None):
-    """Causal attention forward; impl None = tcgen05 kernel when head_dim == 128."""
+def flash_fwd(q, k, v, *, head_dim, scale, o=None, lse=None):
+    """Causal attention forward on the tcgen05 kernel (head_dim 64 or 128);
+    k, v may carry fewer heads than q (grouped-query attention)."""
     _check(q, k, v)
     n, h = q.shape
     if o is None:
         o = torch.empty(n, h, dtype=BF16, device=q.device)
     if lse is None:
         lse = torch.empty(h // head_dim, n, dtype=F32, device=q.device)
-    if impl is None:
-        impl = "tc" if head_dim == 128 else "mma"
-    name = "lemo_flash_fwd_tc" if impl == "tc" else "lemo_flash_fwd"
-    INSTRUMENT.note(name, n)
-    kv = k.shape[1]
-    if impl == "tc":
-        call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(lse), n, h, kv, head_dim, float(scale),
-             _s())
-    else:
-        if kv != h:
-            raise ContractError("grouped-query attention needs the tcgen05 path (head_dim 128)")
-        call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(lse), n, h, head_dim, float(scale), _s())
+    INSTRUMENT.note("lemo_flash_fwd_tc", n)
+    call("lemo_flash_fwd_tc", ptr(q), ptr(k), ptr(v), ptr(o), ptr(lse), n, h, k.shape[1],
+         head_dim, float(scale), _s())
     return o, lse
 
 
-def flash_bwd(q, k, v, o, dout, lse, *, head_dim, scale, dq=None, dk=None, dv=None, impl=None):
-    """Causal attention backward; impl None = tcgen05 kernels when head_dim == 128."""
+def flash_bwd(q, k, v, o, dout, lse, *, head_dim, scale, dq=None, dk=None, dv=None):
+    """Causal attention backward on the tcgen05 kernels (head_dim 64 or 128)."""
     _check(q, k, v, o, dout, lse)
     n, h = q.shape
     dev = q.device
@@ -539,16 +514,7 @@ def flash_bwd(q, k, v, o, dout, lse, *, head_dim, scale, dq=None, dk=None, dv=No
     dq = torch.empty(n, h, dtype=F32, device=dev) if dq is None else dq
     dk = torch.empty(n, kv, dtype=F32, device=dev) if dk is None else dk
     dv = torch.empty(n, kv, dtype=F32, device=dev) if dv is None else dv
-    if impl is None:
-        impl = "tc" if head_dim == 128 else "mma"
-    name = "lemo_flash_bwd_tc" if impl == "tc" else "lemo_flash_bwd"
-    INSTRUMENT.note(name, n)
-    if impl == "tc":
-        call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(delta), ptr(dq),
-             ptr(dk), ptr(dv), n, h, kv, head_dim, float(scale), _s())
-    else:
-        if kv != h:
-            raise ContractError("grouped-query attention needs the tcgen05 path (head_dim 128)")
-        call(name, ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(delta), ptr(dq),
-             ptr(dk), ptr(dv), n, h, head_dim, float(scale), _s())
+    INSTRUMENT.note("lemo_flash_bwd_tc", n)
+    call("lemo_flash_bwd_tc", ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(delta),
+         ptr(dq), ptr(dk), ptr(dv), n, h, kv, head_dim, float(scale), _s())
     return dq, dk, dv
