@@ -178,9 +178,13 @@ int lemo_ce_rows(const float* logits, int ldl, const int* targets, int n, int V,
 /* *out (+)= Σ x[i] in float64 (deterministic single-CTA reduction). */
 int lemo_sum_f64(const float* x, int n, double* out, int accumulate, void* stream);
 
-/* Adam step over a flat fp32 parameter buffer (optim.py:37-53). */
+/* Adam step over a flat fp32 parameter buffer (optim.py:37-53).  guard_loss
+ * (optional, device f64): the update is skipped when *guard_loss is not finite
+ * or *guard_latch (optional) is set, and the latch is then set -- predictor
+ * training checks each record's loss before stepping (predictor.py:405-410). */
 int lemo_adam(float* p, const float* g, float* m, float* v, long long n, float lr, float b1,
-              float b2, float eps, float wd, float bc1, float bc2, void* stream);
+              float b2, float eps, float wd, float bc1, float bc2, const double* guard_loss,
+              int* guard_latch, void* stream);
 
 /* ---- pattern scoring and selection ----------------------------------------- */
 

@@ -119,11 +119,18 @@ def config_hash(model_cfg, mlp_scoring: bool = True) -> str:
     """RunConfig.config_hash (config.py:84-99): sha256 of the pattern-relevant
     geometry, first 16 hex digits."""
     m = model_cfg
-    key = json.dumps({"block_size": m.block_size, "n_layers": m.n_layers,
-                      "hidden_dim": m.hidden_dim, "n_heads": m.n_heads,
-                      "vocab_size": m.vocab_size, "mlp_variant": m.mlp_variant,
-                      "mlp_dim": m.mlp_dim, "positions": m.positions,
-                      "mlp_scoring": mlp_scoring}, sort_keys=True)
+    fields = {"block_size": m.block_size, "n_layers": m.n_layers,
+              "hidden_dim": m.hidden_dim, "n_heads": m.n_heads,
+              "vocab_size": m.vocab_size, "mlp_variant": m.mlp_variant,
+              "mlp_dim": m.mlp_dim, "positions": m.positions,
+              "mlp_scoring": mlp_scoring}
+    # grouped-query attention (beyond the reference) changes the exact scores
+    # and so the thresholds / predictors: it enters the key only when present,
+    # so multi-head configurations keep the reference's hash
+    kv = getattr(m, "n_kv_heads", 0)
+    if kv and kv != m.n_heads:
+        fields["n_kv_heads"] = kv
+    key = json.dumps(fields, sort_keys=True)
     return hashlib.sha256(key.encode()).hexdigest()[:16]
 
 

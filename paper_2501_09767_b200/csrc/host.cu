@@ -1,7 +1,10 @@
 // Host-side plumbing for liblemo: error reporting, TMA descriptor encoding
 // (driver entry point fetched at run time, so the library does not link
 // libcuda directly) and a small per-process descriptor cache keyed by
-// (pointer, shape, box).  The library never allocates device memory.
+// (device, pointer, shape, box) -- one process may drive several GPUs and the
+// same virtual address may back different allocations on different devices.
+// The library never allocates device memory (the split-K tail scratch below
+// is the one library-owned buffer, one per device and stream).
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -46,13 +49,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 
 struct TmaKey {
   uint64_t base, rows, cols, ld, box;
+  int dev;
   bool operator==(const TmaKey& o) const {
-    return base == o.base && rows == o.rows && cols == o.cols && ld == o.ld && box == o.box;
+    return base == o.base && rows == o.rows && cols == o.cols && ld == o.ld && box == o.box &&
+           dev == o.dev;
   }
 };
 struct TmaKeyHash {
   size_t operator()(const TmaKey& k) const {
-    uint64_t h = k.base * 0x9E3779B97F4A7C15ull;
+    uint64_t h = (k.base ^ ((uint64_t)k.dev << 56)) * 0x9E3779B97F4A7C15ull;
     h ^= (k.rows + 0x632BE59BD9B4E019ull + (h << 6) + (h >> 2));
     h ^= (k.cols + 0x85EBCA77C2B2AE63ull + (h << 6) + (h >> 2));
     h ^= (k.ld + (h << 6) + (h >> 2));
@@ -81,7 +86,9 @@ int make_tma_f32_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t 
 static int make_tma_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols,
                        uint64_t ld_elems, uint32_t box_rows, bool f32) {
   const uint64_t esz = f32 ? 4 : 2;
-  TmaKey key{(uint64_t)base, rows, cols, ld_elems, box_rows | (f32 ? (1ull << 40) : 0ull)};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  TmaKey key{(uint64_t)base, rows, cols, ld_elems, box_rows | (f32 ? (1ull << 40) : 0ull), dev};
   {
     std::lock_guard<std::mutex> lk(g_tma_mu);
     auto it = g_tma_cache.find(key);

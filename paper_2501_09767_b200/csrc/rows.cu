@@ -551,9 +551,21 @@ __global__ void sum_f64_kernel(const float* __restrict__ x, int n, double* __res
 }
 
 // Adam (optim.py:37-53) over one flat buffer of all adapter parameters.
+// guard (optional): skip the update when *guard_loss is not finite or an
+// earlier guarded update was skipped (*latch != 0) -- a diverged predictor
+// fit must not write NaN/Inf into the caller's weights before it raises
+// (the reference checks each loss before stepping, predictor.py:405-410).
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
                             float* __restrict__ m, float* __restrict__ v, long long n, float lr,
-                            float b1, float b2, float eps, float wd, float bc1, float bc2) {
+                            float b1, float b2, float eps, float wd, float bc1, float bc2,
+                            const double* __restrict__ guard_loss, int* __restrict__ latch) {
+  if (guard_loss != nullptr) {
+    const bool bad = !isfinite(*guard_loss) || (latch != nullptr && *(volatile int*)latch);
+    if (bad) {
+      if (latch != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *latch = 1;
+      return;
+    }
+  }
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     float pi = p[i];
@@ -789,12 +801,13 @@ int lemo_sum_f64(const float* x, int n, double* out, int accumulate, void* strea
 }
 
 int lemo_adam(float* p, const float* g, float* m, float* v, long long n, float lr, float b1,
-              float b2, float eps, float wd, float bc1, float bc2, void* stream) {
+              float b2, float eps, float wd, float bc1, float bc2, const double* guard_loss,
+              int* guard_latch, void* stream) {
   if (n <= 0) return 0;
   long long blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   adam_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(p, g, m, v, n, lr, b1, b2, eps, wd,
-                                                             bc1, bc2);
+                                                             bc1, bc2, guard_loss, guard_latch);
   LEMO_CHECK_LAUNCH("lemo_adam");
   return 0;
 }

@@ -322,10 +322,12 @@ def sum_f64(x, out, accumulate=False):
     return out
 
 
-def adam(p, g, m, v, *, lr, b1, b2, eps, wd, bc1, bc2):
-    _check(p, g, m, v)
+def adam(p, g, m, v, *, lr, b1, b2, eps, wd, bc1, bc2, guard_loss=None, guard_latch=None):
+    """Adam step in place; with guard_loss (device f64 scalar) the update is
+    skipped when the loss is not finite or guard_latch is already set."""
+    _check(p, g, m, v, guard_loss, guard_latch)
     call("lemo_adam", ptr(p), ptr(g), ptr(m), ptr(v), p.numel(), float(lr), float(b1), float(b2),
-         float(eps), float(wd), float(bc1), float(bc2), _s())
+         float(eps), float(wd), float(bc1), float(bc2), ptr(guard_loss), ptr(guard_latch), _s())
 
 
 # ---------------------------------------------------------------------------

@@ -414,8 +414,11 @@ class _PairAdam:
                 for w in p.parameters():
                     self.state[id(w)] = (torch.zeros_like(w), torch.zeros_like(w))
 
-    def step(self, items) -> None:
-        """items: [(predictor, [g1, g2, g3])] holding this step's gradients."""
+    def step(self, items, guard_loss=None, guard_latch=None) -> None:
+        """items: [(predictor, [g1, g2, g3])] holding this step's gradients.
+        guard_loss / guard_latch: device-side skip of a non-finite record (the
+        reference raises before stepping; here the host learns it at the
+        epoch's read-back, and no NaN update has been applied by then)."""
         self.t += 1
         bc1 = 1.0 - self.b1 ** self.t
         bc2 = 1.0 - self.b2 ** self.t
@@ -423,7 +426,7 @@ class _PairAdam:
             for w, g in zip(p.parameters(), grads):
                 m, v = self.state[id(w)]
                 ops.adam(w, g, m, v, lr=self.lr, b1=self.b1, b2=self.b2, eps=self.eps, wd=0.0,
-                         bc1=bc1, bc2=bc2)
+                         bc1=bc1, bc2=bc2, guard_loss=guard_loss, guard_latch=guard_latch)
             p.touch()
 
 
@@ -453,6 +456,7 @@ def fit_predictors(pairs: dict, train_data: list, *, epochs: int, lr: float, val
     last_recall = float("nan")
     dev = next(iter(pairs.values()))[0].w1.device
     losses = torch.empty(len(train_data), dtype=torch.float64, device=dev)
+    diverged = torch.zeros(1, dtype=torch.int32, device=dev)  # latched by the guarded Adam
     for epoch in range(1, epochs + 1):
         if lr_decay:
             opt.lr = lr * (0.02 + 0.98 * 0.5 * (1.0 + math.cos(math.pi * (epoch - 1) / epochs)))
@@ -483,7 +487,8 @@ def fit_predictors(pairs: dict, train_data: list, *, epochs: int, lr: float, val
                 d_eq, d_ek = ops.block_expand(d_eq, b), ops.block_expand(d_ek, b)
             p_q.backward_train(d_eq, saved_q, grads[id(p_q)])
             p_k.backward_train(d_ek, saved_k, grads[id(p_k)])
-            opt.step([(p_q, grads[id(p_q)]), (p_k, grads[id(p_k)])])
+            opt.step([(p_q, grads[id(p_q)]), (p_k, grads[id(p_k)])],
+                     guard_loss=losses[i:i + 1], guard_latch=diverged)
         host_losses = losses.cpu().numpy()
         bad = np.flatnonzero(~np.isfinite(host_losses))
         if bad.size:

@@ -60,6 +60,27 @@ def test_fit_predictors_matches_reference(cuda, pooling):
                 assert _rel(st[name], z[f"final_{l}_{p.role}_{name}"]) < 2e-3, (l, p.role, name)
 
 
+def test_fit_predictors_divergence_leaves_weights_finite(cuda):
+    """A non-finite record loss raises ContractError and no NaN/Inf update
+    reaches the caller's predictors (the reference checks every loss before
+    stepping, predictor.py:405-410; here Adam is guarded on the device)."""
+    from paper_2501_09767_b200.errors import ContractError
+
+    rng = np.random.default_rng(3)
+    pairs = {0: (P.Predictor.create(rng, 64, 16, 16, 16, "q", 0, cuda),
+                 P.Predictor.create(rng, 64, 16, 16, 16, "k", 0, cuda))}
+    before = [w.clone() for p in pairs[0] for w in p.parameters()]
+    x = torch.randn(128, 64, device=cuda)
+    bad = torch.full((16 * 17 // 2,), float("nan"), dtype=torch.float64, device=cuda)
+    good = torch.rand(16 * 17 // 2, dtype=torch.float64, device=cuda)
+    recs = [P.TeacherRecord(0, x, bad, 128, 8), P.TeacherRecord(0, x, good, 128, 8)]
+    with pytest.raises(ContractError):
+        P.fit_predictors(pairs, recs, epochs=2, lr=1e-2)
+    after = [w for p in pairs[0] for w in p.parameters()]
+    for a, b in zip(after, before):
+        assert torch.equal(a, b)  # the NaN record and every later one were skipped
+
+
 def test_load_reference_predictors_ckpt(cuda):
     z = np.load(G / "artifacts.npz")
     pairs, pt, retention, meta = A.load_predictors(G / "predictors.ckpt", n_layers=2,
