@@ -19,8 +19,14 @@ memory each step, loss read back each step); `dense_lora` = the same kernels
 at full retention (the reference's definition of dense LoRA, model.py:
 300-302) for the ≥1.3× tokens/s and ≥1.5× activation targets; `roofline`
 = the dominant kernel (the tcgen05 gate/up GEMM of MLP scoring) timed live
-with CUDA events; `cpu_baseline` = the oracle restatement of the reference
-timed on this host on a bounded sample (see oracle/cpu_sample.py).
+with CUDA events; `mask_flips` = an untimed audit of every MLP decision of one
+step against the fp32-faithful parity scorers (audit.MaskAudit);
+`cpu_baseline` = the UNMODIFIED reference (baseline/_ref, sparsetune) timed on
+this host on a bounded full-width sample (baseline/run_reference.py).
+
+`--impl reference` is the reference arm: the unmodified reference on the host
+cores (rank 0), one full-width 16K layer sample per step, extrapolated to the
+32-layer step; see run_reference().
 """
 
 from __future__ import annotations
@@ -63,6 +69,8 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-law", action="store_true")
+    ap.add_argument("--no-audit", action="store_true",
+                    help="skip the mask-flip audit (production vs parity-precision scorers)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N>1 (gloo only to smoke-test several "
                          "ranks sharing one GPU)")
@@ -298,6 +306,10 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         if args.backend == "nccl":
+            # communicator set-up lines (ring / NVLS / transport) on stderr, so a
+            # scaling run shows how the LoRA-gradient all-reduce is carried
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
@@ -309,7 +321,11 @@ def main():
     seq = wl["seq"]
     cfg = getattr(M, wl["model"])(max_seq_len=seq)
     torch.manual_seed(0)
-    model = M.DecoderModel(cfg, seed=0, device=dev, init="torch")
+    # scoring_precision="fp32" keeps the bf16 residuals of the scoring weights
+    # so the untimed mask audit below can score in the parity precision; the
+    # timed steps use the production (bf16) scorers either way
+    model = M.DecoderModel(cfg, seed=0, device=dev, init="torch",
+                           scoring_precision="bf16" if args.no_audit else "fp32")
     h = cfg.hidden_dim
     rp = h // 4
     gen = torch.Generator(device=dev)
@@ -419,6 +435,18 @@ def main():
     ms_e2e = timed(source, lambda: tokens, args.steps, read_loss=True)
     e2e_value = world * seq * args.steps / (ms_e2e / 1e3)
 
+    # mask-flip audit (untimed): every MLP decision of one step re-scored in the
+    # fp32-faithful parity precision under the same threshold (audit.MaskAudit)
+    audit = None
+    if not args.no_audit:
+        from paper_2501_09767_b200.audit import MaskAudit
+        aud = MaskAudit(source, model)
+        with torch.no_grad():
+            model.forward_step(staged, pattern_source=aud, segments=segments)
+        audit = aud.summary()
+        del aud
+        torch.cuda.empty_cache()
+
     dense = None
     if not args.no_dense:
         try:
@@ -492,20 +520,20 @@ def main():
                 traffic = tj.get("gemm_gateup_bytes_per_launch")
         except Exception:  # noqa: BLE001
             traffic = None
-    # The sustained figure (torch.matmul back to back for 4 s) is the ceiling for a
-    # kernel inside a long step unless the kernel beats it -- the step interleaves
-    # HBM-bound kernels, so the power cap bites less -- then the burst figure is.
-    use_burst = bool(ach) and ach > pk["bf16_tflops_sustained"]
-    peak_g = pk["bf16_tflops"] if use_burst else pk["bf16_tflops_sustained"]
+    # the kernel is timed inside a long step: the denominator is the measured
+    # SUSTAINED bf16 figure (torch.matmul back to back); the burst figure is
+    # reported beside it.  frac > 1 means the kernel beats the sustained matmul
+    # (the step interleaves HBM-bound kernels, so the power cap bites less).
+    peak_g = pk["bf16_tflops_sustained"]
     roofline = {"kernel": "gemm_tn_pair_kernel<EpiGateUp> (lemo_gemm_gateup, MLP scoring, "
                           "256x256 CTA-pair tiles)",
                 "bound": "tensor", "achieved": ach, "peak": peak_g,
                 "unit": "TFLOP/s", "frac": (ach / peak_g) if ach else None,
-                "frac_sustained": (ach / pk["bf16_tflops_sustained"]) if ach else None,
+                "peak_burst": pk["bf16_tflops"],
+                "frac_burst": (ach / pk["bf16_tflops"]) if ach else None,
                 "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
-                "peak_source": (f"{pk_src} bf16_tflops (burst; the kernel exceeds the measured "
-                                "sustained figure inside the step)" if use_burst else
-                                f"{pk_src} bf16_tflops_sustained (kernel timed inside the step)"),
+                "peak_source": f"{pk_src} bf16_tflops_sustained (kernel timed inside the step); "
+                               f"frac_burst against {pk_src} bf16_tflops",
                 "algorithmic_per_launch": flops_gemm, "launches_timed": len(gemm_ms),
                 "avg_launch_ms": avg_gemm_s * 1e3}
     nb = seq // cfg.block_size
@@ -590,12 +618,28 @@ def main():
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "roofline": roofline,
         "roofline_scoring": roofline_scoring,
-        "attention": {k: dict(v, bound="tensor", peak=pk["bf16_tflops"],
+        "attention": {k: dict(v, bound="tensor", peak=pk["bf16_tflops_sustained"],
+                              frac=v["tflops"] / pk["bf16_tflops_sustained"],
                               frac_burst=v["tflops"] / pk["bf16_tflops"])
                       for k, v in attn.items()},
+        "mask_flips": audit,
         "cpu_baseline": cpu,
         "clocks": ck,
     }
+    if world > 1:
+        # per-rank view of the same run (each rank trains its own sequence)
+        mine = {"rank": rank, "ms_per_step": ms_step, "activation_gb_post_forward": act_gb,
+                "peak_step_gb": peak_step / 1e9,
+                "retained_mean_attention": line["retained_mean"]["attention"]}
+        ranks = [None] * world
+        dist.all_gather_object(ranks, mine)
+        line["per_rank"] = ranks
+        line["collective"] = {"backend": args.backend,
+                              "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))
+                              if args.backend == "nccl" else None,
+                              "what": "per-layer LoRA-gradient buckets all-reduced (AVG) inside "
+                                      "the backward sweep (parallel.BucketedGradReducer); "
+                                      "NCCL_DEBUG=INFO/INIT lines on stderr"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
