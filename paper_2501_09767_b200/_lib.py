@@ -11,13 +11,15 @@ Pointers are passed as integers (``tensor.data_ptr()``), streams as the raw
 from __future__ import annotations
 
 import ctypes
+import os
 import re
 from pathlib import Path
 
 import torch
 
 _PKG = Path(__file__).resolve().parent
-_LIB_PATH = _PKG / "liblemo.so"
+# LEMO_LIB overrides the library path (A/B builds of the same sources)
+_LIB_PATH = Path(os.environ["LEMO_LIB"]) if os.environ.get("LEMO_LIB") else _PKG / "liblemo.so"
 HEADER = _PKG.parent / "include" / "lemo.h"
 
 _CT = {"p": ctypes.c_void_p, "i": ctypes.c_int, "f": ctypes.c_float, "d": ctypes.c_double,

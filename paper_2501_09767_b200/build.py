@@ -15,8 +15,10 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-LIB = PKG / "liblemo.so"
-OBJ = PKG / "_build"
+# LEMO_BUILD_TAG builds an A/B variant (own object dir, liblemo_<tag>.so) of the same sources
+_TAG = os.environ.get("LEMO_BUILD_TAG", "")
+LIB = PKG / (f"liblemo_{_TAG}.so" if _TAG else "liblemo.so")
+OBJ = PKG / (f"_build_{_TAG}" if _TAG else "_build")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
