@@ -321,11 +321,11 @@ def main():
     seq = wl["seq"]
     cfg = getattr(M, wl["model"])(max_seq_len=seq)
     torch.manual_seed(0)
-    # scoring_precision="fp32" keeps the bf16 residuals of the scoring weights
-    # so the untimed mask audit below can score in the parity precision; the
-    # timed steps use the production (bf16) scorers either way
-    model = M.DecoderModel(cfg, seed=0, device=dev, init="torch",
-                           scoring_precision="bf16" if args.no_audit else "fp32")
+    # parity_weights keeps the bf16 residuals of the scoring weights so the
+    # untimed mask audit below can score in the parity precision; the timed
+    # steps use the production (bf16) scorers (scoring_precision="bf16")
+    model = M.DecoderModel(cfg, seed=0, device=dev, init="torch", scoring_precision="bf16",
+                           parity_weights=not args.no_audit)
     h = cfg.hidden_dim
     rp = h // 4
     gen = torch.Generator(device=dev)
@@ -603,7 +603,8 @@ def main():
                    "l2": "weights + activations far larger than the 126 MB L2 (no flush)"
                    if wbytes > 126e6 else "fits in L2 (tiny model: launch-bound, no flush)",
                    "segments": segments, "block_size": cfg.block_size,
-                   "target_retention": 0.5},
+                   "target_retention": 0.5,
+                   "scoring_precision": model.scoring_precision},
         "activation_gb_post_forward": act_gb,
         "peak_step_gb": peak_step / 1e9,
         "retained_mean": {"attention": float(np.mean(attn_f)) if attn_f else None,

@@ -23,8 +23,8 @@ from .model import PatternSourceBase, mlp_block_score_vector
 
 class MaskAudit(PatternSourceBase):
     def __init__(self, inner, model):  # noqa: D107 (last_fractions is the inner source's)
-        if model.scoring_precision != "fp32":
-            raise ValueError("the audit needs a model built with scoring_precision='fp32'")
+        if not model.parity_weights:
+            raise ValueError("the audit needs a model built with parity_weights=True")
         self.inner = inner
         self.model = model
         self.per_layer: dict = {}  # layer -> {"mlp_flips", "mlp_ambiguous", "n_blocks"}

@@ -273,11 +273,11 @@ constexpr int kSmemPair = kStagesPair * 2 * kBlockM * kBlockK * 2 + 1024 + 256;
 // ceil(T / C) tile-times even when the last wave holds a handful of tiles
 // (M = 8208 rows at N = 4096 is 528 tiles = 7.14 waves -> 8).  When the last
 // wave is at most half full, its R tiles are each cut into `split` K-ranges
-// (R·split ≤ C units, one per cluster): the first split-1 units of a tile
-// store their fp32 partial accumulators to `ws` and bump a per-(tile, CTA)
-// counter; the last unit (highest cluster index of the tile's units, so the
-// others are dispatched no later) waits for them, adds the partials to its
-// TMEM accumulator in a fixed order (deterministic) and runs the epilogue.
+// (R·split ≤ C units, one per cluster): every unit stores its fp32 partial
+// accumulator to `ws` and bumps a per-(tile, CTA) counter; the unit whose
+// arrival completes the count -- whichever finishes last; no unit ever waits
+// for another -- sums all partials in chunk order (deterministic) into its
+// TMEM accumulator and runs the epilogue.
 constexpr int kPairTailMaxSplit = 4;  // the completing unit reads all partials: keep it short
 
 struct PairTail {

@@ -424,13 +424,93 @@ def _check_plan(x, plan):
         raise ContractError(f"plan covers {plan.n_tokens} tokens, input has {x.shape[0]}")
 
 
+# ---------------------------------------------------------------------------
+# the reference's duck-typed `layer` (model.py:83-117, kernels.py:295-313)
+
+_SHADOWS: dict = {}
+
+
+def _host(t):
+    """Array behind a reference Tensor (`.data`), a torch tensor or an ndarray."""
+    if isinstance(t, torch.Tensor):
+        return t.detach()
+    d = getattr(t, "data", t)
+    return d.detach() if isinstance(d, torch.Tensor) else np.asarray(d)
+
+
+def as_layer_state(layer, *, max_seq_len: int = 65536, device=None):
+    """A LayerState for `layer`.  Accepts this package's LayerState as is, or
+    any object with the reference's duck-typed fields (`wq wk wv wo
+    attn_norm_w mlp_norm_w w_gate w_up w_down lora_q lora_v n_heads rope
+    rope_base mlp_variant`, arrays or reference Tensors, [in, out] layout).
+    The frozen weights are converted once (cached per layer object); the
+    adapters are re-read on every call, since the caller's optimizer updates
+    them.  LoRA gradients of the GPU blocks land in the shadow's flat
+    `lora_param.grad` (reference names via `shadow_adapter_grads`)."""
+    if hasattr(layer, "w_qkv_t"):
+        return layer
+    import weakref
+
+    from .model import DecoderModel, ModelConfig
+
+    ent = _SHADOWS.get(id(layer))
+    st = ent[1] if ent is not None and ent[0]() is layer else None
+    if st is None:
+        wq, wk = _host(layer.wq), _host(layer.wk)
+        h, kv = wq.shape[0], wk.shape[1]
+        d = h // layer.n_heads
+        lq = getattr(layer, "lora_q", None)
+        r = int(_host(lq.a).shape[1]) if lq is not None else 0
+        cfg = ModelConfig(n_layers=1, hidden_dim=h, n_heads=layer.n_heads, vocab_size=32,
+                          max_seq_len=max_seq_len, mlp_variant=layer.mlp_variant,
+                          mlp_dim=_host(layer.w_up).shape[1], lora_rank=r,
+                          lora_alpha=(lq.scaling * r) if r else 16.0,
+                          positions="rope" if layer.rope else "learned",
+                          rope_base=float(layer.rope_base),
+                          n_kv_heads=0 if kv == h else kv // d)
+        arrays = {"embed": np.zeros((32, h), np.float32), "final_norm": np.ones(h, np.float32),
+                  "lm_head": np.zeros((h, 32), np.float32)}
+        names = {"wq": "wq", "wk": "wk", "wv": "wv", "wo": "wo", "attn_norm": "attn_norm_w",
+                 "mlp_norm": "mlp_norm_w", "w_up": "w_up", "w_down": "w_down"}
+        if layer.mlp_variant == "silu":
+            names["w_gate"] = "w_gate"
+        for ours, theirs in names.items():
+            arrays[f"layer0.{ours}"] = _host(getattr(layer, theirs))
+        if r:
+            for tag in ("lora_q", "lora_v"):
+                ad = getattr(layer, tag)
+                arrays[f"layer0.{tag}.a"] = _host(ad.a)
+                arrays[f"layer0.{tag}.b"] = _host(ad.b)
+        shadow = DecoderModel(cfg, 0, arrays=arrays, device=device)
+        st = shadow.layers[0]
+        st.shadow_model = shadow
+        _SHADOWS[id(layer)] = (weakref.ref(layer), st)
+    if st.lora_rank:
+        with torch.no_grad():
+            for tag, ad in (("lora_q", st.lora_q), ("lora_v", st.lora_v)):
+                src = getattr(layer, tag)
+                ad.a.copy_(torch.as_tensor(_host(src.a)).to(ad.a.device, torch.float32))
+                ad.b.copy_(torch.as_tensor(_host(src.b)).to(ad.b.device, torch.float32))
+    return st
+
+
+def shadow_adapter_grads(layer) -> dict:
+    """LoRA gradients accumulated for a duck-typed layer ({"lora_q.a": ...})."""
+    ent = _SHADOWS.get(id(layer))
+    if ent is None or ent[0]() is not layer:
+        return {}
+    return {k.split(".", 1)[1]: v for k, v in ent[1].shadow_model.adapter_grads().items()}
+
+
 def sparse_attention_fused(x: torch.Tensor, plan: GatherPlan, layer,
                            fuse_projections: bool = True) -> torch.Tensor:
     """kernels.py:153-177: k == 0 returns x itself; otherwise a new residual
-    tensor with the attention output added at the retained rows."""
+    tensor with the attention output added at the retained rows.  `layer` is
+    a LayerState or the reference's duck-typed layer (as_layer_state)."""
     _check_plan(x, plan)
     if plan.k == 0:
         return x
+    layer = as_layer_state(layer, device=x.device)
     return _SparseBlock.apply(x, layer.lora_param, plan, layer, "attention")
 
 
@@ -440,6 +520,7 @@ def sparse_mlp_fused(x: torch.Tensor, plan: GatherPlan, layer,
     _check_plan(x, plan)
     if plan.k == 0:
         return x
+    layer = as_layer_state(layer, device=x.device)
     return _SparseBlock.apply(x, layer.lora_param, plan, layer, "mlp")
 
 
@@ -493,6 +574,7 @@ def sparse_attention_naive(x: torch.Tensor, plan: GatherPlan, layer) -> torch.Te
     _check_plan(x, plan)
     if plan.k == 0:
         return x
+    layer = as_layer_state(layer, device=x.device)
     return _NaiveBlock.apply(x, layer.lora_param, plan, layer, "attention")
 
 
@@ -501,4 +583,5 @@ def sparse_mlp_naive(x: torch.Tensor, plan: GatherPlan, layer) -> torch.Tensor:
     _check_plan(x, plan)
     if plan.k == 0:
         return x
+    layer = as_layer_state(layer, device=x.device)
     return _NaiveBlock.apply(x, layer.lora_param, plan, layer, "mlp")

@@ -247,7 +247,7 @@ class LayerState:
         # lo = bf16(w - hi) of the scoring weights, so hi + lo carries the fp32
         # weights into the bf16x3 GEMMs (gate/up, q/k)
         self.w_gu_t_lo = self.w_qk_t_lo = None
-        if model.scoring_precision == "fp32":
+        if model.parity_weights:
             gut = gu.t().contiguous()
             self.w_gu_t_lo = (gut - self.w_gu_t.float()).to(BF16)
             del gut
@@ -290,13 +290,13 @@ class LayerState:
     def gateup_x3(self) -> torch.Tensor:
         """[N, 3h] bf16x3 B operand [hi | lo | hi] of the gate/up weight."""
         if self.w_gu_t_lo is None:
-            raise ContractError("fp32 scoring needs a model built with scoring_precision='fp32'")
+            raise ContractError("fp32 scoring needs a model built with parity_weights=True")
         return torch.cat([self.w_gu_t, self.w_gu_t_lo, self.w_gu_t], dim=1)
 
     def qk_x3(self) -> torch.Tensor:
         """[h+kv, 3h] bf16x3 B operand of the q/k projections."""
         if self.w_qk_t_lo is None:
-            raise ContractError("fp32 scoring needs a model built with scoring_precision='fp32'")
+            raise ContractError("fp32 scoring needs a model built with parity_weights=True")
         h = self.w_qkv.shape[0]
         hi = self.w_qkv_t[:h + self.kv, :h]
         return torch.cat([hi, self.w_qk_t_lo, hi], dim=1)
@@ -412,14 +412,22 @@ class DecoderModel:
     """
 
     def __init__(self, cfg: ModelConfig, seed: int = 0, *, device=None, init: str = "torch",
-                 arrays: dict | None = None, scoring_precision: str = "bf16"):
+                 arrays: dict | None = None, scoring_precision: str = "bf16",
+                 parity_weights: bool | None = None):
         cfg.check_gpu_geometry()
         if scoring_precision not in ("bf16", "fp32"):
             raise ContractError(f"unknown scoring precision {scoring_precision!r}")
+        # default precision of the scorers the pattern sources call:
         # "bf16": production scorers on bf16 tensor-core operands;  "fp32": the
-        # fp32-faithful (bf16x3) parity mode that reproduces the reference's
-        # masks (keeps the bf16 residuals of the scoring weights: +~8 % memory)
+        # fp32-faithful (bf16x3) parity mode that reproduces the reference's masks
         self.scoring_precision = scoring_precision
+        # parity_weights: keep the bf16 residuals of the scoring weights (+~8 %
+        # weight memory) so the fp32 precision can be used per call (e.g. by the
+        # mask audit) while the sources default to bf16
+        self.parity_weights = (scoring_precision == "fp32") if parity_weights is None \
+            else bool(parity_weights)
+        if scoring_precision == "fp32" and not self.parity_weights:
+            raise ContractError("scoring_precision='fp32' needs parity_weights")
         self.config = cfg
         self.seed = seed
         self.device = torch.device(device) if device is not None else torch.device("cuda")

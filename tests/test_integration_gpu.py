@@ -105,3 +105,48 @@ def test_reference_step_through_the_ctypes_binding(cuda, sparsetune):
             got = ops.eliminate(v, thr, block_size=16, n_tokens=nb * 16 - 3, force_blocks=(0,))
             assert got.retained_blocks == want.retained_blocks
             assert np.array_equal(got.token_indices, want.token_indices)
+
+
+@pytest.mark.parametrize("block", ["attention", "mlp"])
+def test_fused_blocks_accept_the_reference_layer(cuda, sparsetune, block):
+    """sparse_attention_fused / sparse_mlp_fused(x, plan, layer) called with
+    the REFERENCE's own LayerState (duck-typed fields, kernels.py:295-313):
+    output, input gradient and LoRA gradients vs the reference's fused block
+    on its tape."""
+    import torch
+
+    from paper_2501_09767_b200 import kernels as K
+
+    M, Kr, T = sparsetune["model"], sparsetune["kernels"], sparsetune["tensor"]
+    cfg = M.ModelConfig(n_layers=1, hidden_dim=256, n_heads=2, vocab_size=64, max_seq_len=512,
+                        mlp_dim=344, block_size=16, lora_rank=8, lora_alpha=16.0)
+    ref_model = M.DecoderModel(cfg, seed=2)
+    layer = ref_model.layers[0]
+    rng = np.random.default_rng(4)
+    for ad in (layer.lora_q, layer.lora_v):
+        ad.b.data[...] = (rng.standard_normal(ad.b.shape) * 0.1).astype(np.float32)
+    s = 320
+    x = rng.standard_normal((s, 256)).astype(np.float32)
+    up = rng.standard_normal((s, 256)).astype(np.float32)
+    idx = np.concatenate([np.arange(0, 96), np.arange(160, 224), np.arange(288, 320)])
+    # reference
+    xt = T.Tensor(x, requires_grad=True)
+    fn_ref = Kr.sparse_attention_fused if block == "attention" else Kr.sparse_mlp_fused
+    out_ref = fn_ref(xt, Kr.GatherPlan(idx, s), layer)
+    loss = T.sum_all(T.mul(out_ref, T.Tensor(up)))
+    T.backward(loss)
+    # ours, same layer object
+    xd = torch.as_tensor(x).cuda().requires_grad_(True)
+    fn = K.sparse_attention_fused if block == "attention" else K.sparse_mlp_fused
+    out = fn(xd, K.GatherPlan(idx, s), layer)
+    (out * torch.as_tensor(up).cuda()).sum().backward()
+    np.testing.assert_allclose(out.detach().cpu().numpy(), out_ref.data, rtol=2e-2, atol=2e-2)
+    gx = xd.grad.cpu().numpy()
+    assert np.linalg.norm(gx - xt.grad) <= 2e-2 * np.linalg.norm(xt.grad)
+    if block == "attention":
+        grads = K.shadow_adapter_grads(layer)
+        for tag in ("lora_q", "lora_v"):
+            for ab in ("a", "b"):
+                r = getattr(getattr(layer, tag), ab).grad
+                g = grads[f"{tag}.{ab}"]
+                assert np.linalg.norm(g - r) <= 3e-2 * np.linalg.norm(r), (tag, ab)

@@ -207,6 +207,22 @@ def test_mlp_scores_golden_fp32(cuda):
     np.testing.assert_allclose(got, zr["mlp_vec"], rtol=1e-5)
 
 
+def test_parity_weights_keep_bf16_default(cuda):
+    """parity_weights=True only enables the fp32 precision per call: the
+    sources' default (scoring_precision) stays the production bf16 scorer."""
+    z = np.load(G / "scorers.npz")
+    cfg = ModelConfig(n_layers=1, hidden_dim=128, n_heads=2, vocab_size=64, max_seq_len=256,
+                      block_size=16, mlp_dim=344, lora_rank=4, lora_alpha=8.0)
+    m = DecoderModel(cfg, 3, init="reference", parity_weights=True)
+    x = torch.as_tensor(z["x"]).cuda()
+    nv = int(z["n_valid"])
+    default = mlp_block_score_vector(m.layers[0], x, 16, nv)
+    bf16 = mlp_block_score_vector(m.layers[0], x, 16, nv, precision="bf16")
+    fp32 = mlp_block_score_vector(m.layers[0], x, 16, nv, precision="fp32")
+    assert torch.equal(default, bf16) and not torch.equal(default, fp32)
+    np.testing.assert_allclose(fp32.cpu().numpy(), z["mlp_vec"], rtol=1e-5)
+
+
 def test_layer_qk_fp32_matches_reference(cuda):
     z = np.load(G / "scorers.npz")
     m = _scorer_model_fp32(3, mlp_dim=344, lora_rank=4, lora_alpha=8.0)
