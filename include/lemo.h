@@ -266,6 +266,10 @@ int lemo_qk_finish(const float* qk, int ldqk, const float* t, int ldt, const flo
                    float scale, const float* rope_tab, int s, int h, int kv, int head_dim,
                    int rope, void* q_hi, void* q_lo, void* k_hi, void* k_lo, void* stream);
 
+/* out [M, 2K] = [hi | lo] of a fp32 [M, K]: the A operand of x_hi·W + x_lo·W
+ * against a bf16-exact weight given as [W | W] (parity precision, 2 terms). */
+int lemo_split_bf16x2(const float* a, int lda, int M, int K, void* out, void* stream);
+
 /* hi = bf16(a), lo = bf16(a - hi) for a fp32 [M, K] (row stride lda). */
 int lemo_split_hilo(const float* a, int lda, int M, int K, void* hi, void* lo, void* stream);
 

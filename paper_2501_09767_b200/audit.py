@@ -40,7 +40,9 @@ class MaskAudit(PatternSourceBase):
         layer = self.model.layers[layer_id]
         b = self.model.config.block_size
         thr = self.inner.thresholds.get(layer_id, sparsity.MLP)
-        prod = mlp_block_score_vector(layer, x, b, n_valid, precision="bf16")
+        # the precision the step itself scores in (model default) vs the parity one
+        prod = mlp_block_score_vector(layer, x, b, n_valid,
+                                      precision=self.model.scoring_precision)
         par = mlp_block_score_vector(layer, x, b, n_valid, precision="fp32")
         flips = (prod >= thr) != (par >= thr)
         amb = flips & ((par - thr).abs() <= 1e-5 * abs(thr))
@@ -55,7 +57,8 @@ class MaskAudit(PatternSourceBase):
         rows = [self.per_layer[k] for k in sorted(self.per_layer)]
         nb = sum(r["n_blocks"] for r in rows)
         flips = sum(r["mlp_flips"] for r in rows)
-        return {"reference_precision": "fp32-faithful parity scorers (bf16x3, promoted "
+        return {"step_precision": self.model.scoring_precision,
+                "reference_precision": "fp32-faithful parity scorers (bf16x3, promoted "
                                        "accumulation; 0 flips vs the oracle at this width, "
                                        "tests/test_parity_gpu.py)",
                 "mlp_flips_per_layer": [r["mlp_flips"] for r in rows],

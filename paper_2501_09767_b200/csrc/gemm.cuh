@@ -313,7 +313,10 @@ __device__ __forceinline__ PairUnit pair_unit(int u, const PairTail& tl, int num
   return w;
 }
 
-template <class Epi>
+// kPromote > 0: promoted accumulation as in gemm_tn_kernel (every kPromote
+// k-blocks the TMEM partial goes into the epilogue warps' fp32 registers);
+// the split-K tail is not used with it.
+template <class Epi, int kPromote = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_tn_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K, Epi epi,
@@ -393,30 +396,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       constexpr uint32_t idesc = umma_idesc_bf16(2 * kBlockM, BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
-      int local = 0;
-      for (int u = cid; u < num_units; u += nclusters, ++local) {
+      int local = 0;  // accumulator groups (one per unit unless promoting)
+      for (int u = cid; u < num_units; u += nclusters) {
         const PairUnit w = pair_unit(u, tl, num_kb);
-        const int acc = local & 1;
-        mbar_wait(&tempty_bar[acc], ((local >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = w.kb0; kb < w.kb1; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
+        const int group = kPromote > 0 ? kPromote : (w.kb1 - w.kb0);
+        for (int g0 = w.kb0; g0 < w.kb1; g0 += group, ++local) {
+          const int g1 = min(g0 + group, w.kb1);
+          const int acc = local & 1;
+          mbar_wait(&tempty_bar[acc], ((local >> 1) & 1) ^ 1);
           tc_fence_after();
-          {
-            const uint64_t da = umma_desc_k_sw128(smem_u32(smem_a + stage * kHalf));
-            const uint64_t db = umma_desc_k_sw128(smem_u32(smem_b + stage * kHalf));
+          const uint32_t d_tmem = tmem_base + acc * BN;
+          for (int kb = g0; kb < g1; ++kb) {
+            mbar_wait(&full_bar[stage], phase);
+            tc_fence_after();
+            {
+              const uint64_t da = umma_desc_k_sw128(smem_u32(smem_a + stage * kHalf));
+              const uint64_t db = umma_desc_k_sw128(smem_u32(smem_b + stage * kHalf));
 #pragma unroll
-            for (int k = 0; k < kBlockK / kUmmaK; ++k)
-              umma_bf16_ss_pair_w(d_tmem, da + ((k * kUmmaK * 2) >> 4),
-                                  db + ((k * kUmmaK * 2) >> 4), idesc,
-                                  (kb > w.kb0 || k > 0) ? 1u : 0u);
-            umma_commit_pair_w(&empty_bar[stage]);
-            if (kb == w.kb1 - 1) umma_commit_pair_w(&tfull_bar[acc]);
-          }
-          if (++stage == kStagesPair) {
-            stage = 0;
-            phase ^= 1;
+              for (int k = 0; k < kBlockK / kUmmaK; ++k)
+                umma_bf16_ss_pair_w(d_tmem, da + ((k * kUmmaK * 2) >> 4),
+                                    db + ((k * kUmmaK * 2) >> 4), idesc,
+                                    (kb > g0 || k > 0) ? 1u : 0u);
+              umma_commit_pair_w(&empty_bar[stage]);
+              if (kb == g1 - 1) umma_commit_pair_w(&tfull_bar[acc]);
+            }
+            if (++stage == kStagesPair) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -430,10 +437,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     for (int u = cid; u < num_units; u += nclusters, ++local) {
       const PairUnit w = pair_unit(u, tl, num_kb);
       const TileCoord tc = tile_coord(w.tile, num_m, num_n);
+      const int row = tc.m * 2 * kBlockM + (int)rank * kBlockM + wq * 32 + lane;
+      if constexpr (kPromote > 0) {
+        // promoted accumulation (see gemm_tn_kernel): groups of kPromote k-blocks
+        constexpr int kCols = BN / 2;
+        float sum[kCols];
+#pragma unroll
+        for (int i = 0; i < kCols; ++i) sum[i] = 0.f;
+        const int ngroups = (num_kb + kPromote - 1) / kPromote;
+        uint32_t taddr = 0;
+        int acc = 0;
+        for (int g = 0; g < ngroups; ++g) {
+          acc = local & 1;
+          mbar_wait(&tfull_bar[acc], (local >> 1) & 1);
+          tc_fence_after();
+          taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
+#pragma unroll
+          for (int c = 0; c < kCols / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(taddr + part * kCols + c * 32, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              sum[c * 32 + i] = __fadd_rn(sum[c * 32 + i], __uint_as_float(v[i]));
+          }
+          if (g + 1 < ngroups) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+            ++local;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < kCols / 32; ++c) {
+          uint32_t v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(sum[c * 32 + i]);
+          tmem_st_32x32b_x32(taddr + part * kCols + c * 32, v);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // the epilogue may read the other half
+        tc_fence_after();
+        epi(row, row < M, tc.n * BN, taddr, part);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+        continue;
+      }
       const int acc = local & 1;
       mbar_wait(&tfull_bar[acc], (local >> 1) & 1);
       tc_fence_after();
-      const int row = tc.m * 2 * kBlockM + (int)rank * kBlockM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
       bool run_epi = true;
       if constexpr (PairTailOK<Epi>::value) {
@@ -578,7 +632,7 @@ int launch_gemm_tn(const void* A, int lda, const void* B, int ldb, int M, int N,
 
 // Pair-tile launch (BN = 256, non-transposed B): grid = 2 x (tiles capped at
 // half the SMs), cluster dims fixed by __cluster_dims__.
-template <class Epi>
+template <class Epi, int kPromote = 0>
 int launch_gemm_tn_pair(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
                         const Epi& epi, cudaStream_t stream) {
   if (M <= 0 || N <= 0) return 0;
@@ -588,7 +642,7 @@ int launch_gemm_tn_pair(const void* A, int lda, const void* B, int ldb, int M, i
   if (rc) return rc;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tn_pair_kernel<Epi>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tn_pair_kernel<Epi, kPromote>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemPair);
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
@@ -598,8 +652,8 @@ int launch_gemm_tn_pair(const void* A, int lda, const void* B, int ldb, int M, i
   const int clusters = tiles < pairs ? tiles : pairs;
   PairTail tl{tiles, 1, nullptr, nullptr};
   const int rem = tiles % clusters, num_kb = (K + kBlockK - 1) / kBlockK;
-  if (PairTailOK<Epi>::value && tiles > clusters && rem > 0 && 2 * rem <= clusters &&
-      pair_tail_enabled()) {
+  if (kPromote == 0 && PairTailOK<Epi>::value && tiles > clusters && rem > 0 &&
+      2 * rem <= clusters && pair_tail_enabled()) {
     int split = clusters / rem;
     if (split > kPairTailMaxSplit) split = kPairTailMaxSplit;
     if (split > num_kb / 4) split = num_kb / 4;  // keep ≥ 4 k-blocks per unit
@@ -610,8 +664,8 @@ int launch_gemm_tn_pair(const void* A, int lda, const void* B, int ldb, int M, i
       tl.split = split;
     }
   }
-  gemm_tn_pair_kernel<Epi><<<2 * clusters, kGemmThreads, kSmemPair, stream>>>(ta, tb, M, N, K,
-                                                                             epi, tl);
+  gemm_tn_pair_kernel<Epi, kPromote><<<2 * clusters, kGemmThreads, kSmemPair, stream>>>(
+      ta, tb, M, N, K, epi, tl);
   return (int)cudaGetLastError();
 }
 

@@ -408,6 +408,10 @@ template <int BN, class Epi>
 static int gemm_promoted(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
                          const Epi& e, cudaStream_t st) {
   Bound<BN, Epi> b{e};
+  if constexpr (BN == 256) {  // CTA pairs when M spans two row tiles (as gemm<256>)
+    if (use_pair(M))
+      return launch_gemm_tn_pair<Bound<BN, Epi>, kPromoteGroup>(A, lda, B, ldb, M, N, K, b, st);
+  }
   return launch_gemm_tn<BN, Bound<BN, Epi>, false, kPromoteGroup>(A, lda, B, ldb, M, N, K, b, st);
 }
 

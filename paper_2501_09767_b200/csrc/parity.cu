@@ -93,6 +93,16 @@ __global__ void __launch_bounds__(256) qk_finish_kernel(
   split2(b, hi + (size_t)row * ld + cb, lo + (size_t)row * ld + cb);
 }
 
+// [hi | lo] rows (K' = 2K): the A operand of x_hi·W + x_lo·W for bf16-exact W
+__global__ void split_bf16x2_kernel(const float* __restrict__ a, int lda, int M, int K,
+                                    __nv_bfloat16* __restrict__ out) {
+  const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gid >= (long long)M * K) return;
+  const int row = (int)(gid / K), c = (int)(gid - (long long)row * K);
+  __nv_bfloat16* o = out + (size_t)row * 2 * K;
+  split2(a[(size_t)row * lda + c], o + c, o + K + c);
+}
+
 __global__ void split_hilo_kernel(const float* __restrict__ a, int lda, int M, int K,
                                   __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo) {
   const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -129,6 +139,15 @@ int lemo_qk_finish(const float* qk, int ldqk, const float* t, int ldt, const flo
       reinterpret_cast<__nv_bfloat16*>(q_hi), reinterpret_cast<__nv_bfloat16*>(q_lo),
       reinterpret_cast<__nv_bfloat16*>(k_hi), reinterpret_cast<__nv_bfloat16*>(k_lo));
   LEMO_CHECK_LAUNCH("lemo_qk_finish");
+  return 0;
+}
+
+int lemo_split_bf16x2(const float* a, int lda, int M, int K, void* out, void* stream) {
+  const long long total = (long long)M * K;
+  if (total == 0) return 0;
+  split_bf16x2_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      a, lda, M, K, reinterpret_cast<__nv_bfloat16*>(out));
+  LEMO_CHECK_LAUNCH("lemo_split_bf16x2");
   return 0;
 }
 

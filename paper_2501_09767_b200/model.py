@@ -247,13 +247,22 @@ class LayerState:
         # lo = bf16(w - hi) of the scoring weights, so hi + lo carries the fp32
         # weights into the bf16x3 GEMMs (gate/up, q/k)
         self.w_gu_t_lo = self.w_qk_t_lo = None
+        self._gu_x3 = self._qk_x3 = None  # bf16xN operands, built on first fp32-precision use
+        # parity_terms: 3 = hi·hi + hi·lo + lo·hi; 2 when the scoring weights are
+        # bf16-representable (lo == 0 exactly, e.g. bf16 checkpoints): x_hi·W + x_lo·W
+        self.parity_terms = 3
         if model.parity_weights:
             gut = gu.t().contiguous()
-            self.w_gu_t_lo = (gut - self.w_gu_t.float()).to(BF16)
+            lo_gu = (gut - self.w_gu_t.float()).to(BF16)
             del gut
             qk_t = w_qkv[:, :h + kv].t().contiguous()
-            self.w_qk_t_lo = (qk_t - self.w_qkv_t[:h + kv, :h].float()).to(BF16)
+            lo_qk = (qk_t - self.w_qkv_t[:h + kv, :h].float()).to(BF16)
             del qk_t
+            if int(torch.count_nonzero(lo_gu)) == 0 and int(torch.count_nonzero(lo_qk)) == 0:
+                self.parity_terms = 2
+            else:
+                self.w_gu_t_lo, self.w_qk_t_lo = lo_gu, lo_qk
+            del lo_gu, lo_qk
         wd = torch.zeros(self.m_pad, h, device=dev)
         wd[:m] = g("w_down")
         self.w_down = wd.to(BF16).contiguous()
@@ -287,19 +296,34 @@ class LayerState:
         Bv = flat[o + 3 * h * r:o + 3 * h * r + kv * r].view(r, kv)
         return A, Bq, Bv
 
-    def gateup_x3(self) -> torch.Tensor:
-        """[N, 3h] bf16x3 B operand [hi | lo | hi] of the gate/up weight."""
-        if self.w_gu_t_lo is None:
+    def _require_parity(self):
+        if self.w_gu_t_lo is None and self.parity_terms == 3:
             raise ContractError("fp32 scoring needs a model built with parity_weights=True")
-        return torch.cat([self.w_gu_t, self.w_gu_t_lo, self.w_gu_t], dim=1)
+
+    def gateup_x3(self) -> torch.Tensor:
+        """B operand of the fp32-faithful gate/up GEMM, built on first use and
+        kept (frozen weights): [hi | lo | hi] (K = 3h) or, for bf16-exact
+        weights, [W | W] (K = 2h)."""
+        self._require_parity()
+        if self._gu_x3 is None:
+            parts = ([self.w_gu_t, self.w_gu_t] if self.parity_terms == 2 else
+                     [self.w_gu_t, self.w_gu_t_lo, self.w_gu_t])
+            self._gu_x3 = torch.cat(parts, dim=1)
+        return self._gu_x3
 
     def qk_x3(self) -> torch.Tensor:
-        """[h+kv, 3h] bf16x3 B operand of the q/k projections."""
-        if self.w_qk_t_lo is None:
-            raise ContractError("fp32 scoring needs a model built with parity_weights=True")
-        h = self.w_qkv.shape[0]
-        hi = self.w_qkv_t[:h + self.kv, :h]
-        return torch.cat([hi, self.w_qk_t_lo, hi], dim=1)
+        """B operand of the fp32-faithful q/k projections (kept, as above)."""
+        self._require_parity()
+        if self._qk_x3 is None:
+            h = self.w_qkv.shape[0]
+            hi = self.w_qkv_t[:h + self.kv, :h]
+            parts = [hi, hi] if self.parity_terms == 2 else [hi, self.w_qk_t_lo, hi]
+            self._qk_x3 = torch.cat(parts, dim=1)
+        return self._qk_x3
+
+    def split_input(self, xnf: torch.Tensor) -> torch.Tensor:
+        """The A operand matching gateup_x3 / qk_x3: [hi | hi | lo] or [hi | lo]."""
+        return ops.split_bf16x3(xnf, 0) if self.parity_terms == 3 else ops.split_bf16x2(xnf)
 
     def lora_A_packed(self) -> torch.Tensor:
         """[32, h] bf16 copy of [A_q | A_v] for the t = xn·A GEMM (re-packed each
@@ -373,15 +397,19 @@ def reference_init_arrays(cfg: ModelConfig, seed: int) -> dict:
 
 class _TorchInit:
     """Lazy on-device random init for large models (same distributions as the
-    reference: N(0, 1/h) frozen weights, norms 1, LoRA A ~ N(0, 1/h), B = 0)."""
+    reference: N(0, 1/h) frozen weights, norms 1, LoRA A ~ N(0, 1/h), B = 0).
+    Frozen weights are drawn in bf16 -- the precision they are stored and
+    multiplied in -- so the fp32 model they define (what the reference would
+    compute with) is exactly the bf16 one; LoRA A stays fp32."""
 
     def __init__(self, cfg: ModelConfig, seed: int, device):
         self.cfg, self.dev = cfg, device
         self.gen = torch.Generator(device=device)
         self.gen.manual_seed(seed)
 
-    def normal(self, rows, cols, std):
-        return torch.randn(rows, cols, generator=self.gen, device=self.dev) * std
+    def normal(self, rows, cols, std, bf16: bool = True):
+        w = torch.randn(rows, cols, generator=self.gen, device=self.dev) * std
+        return w.to(BF16).float() if bf16 else w
 
     def layer(self, i):
         cfg = self.cfg
@@ -398,7 +426,7 @@ class _TorchInit:
         d["mlp_norm"] = torch.ones(h, device=self.dev)
         if cfg.lora_rank:
             for tag, width in (("lora_q", h), ("lora_v", kv)):
-                d[f"{tag}.a"] = self.normal(h, cfg.lora_rank, std)
+                d[f"{tag}.a"] = self.normal(h, cfg.lora_rank, std, bf16=False)
                 d[f"{tag}.b"] = torch.zeros(cfg.lora_rank, width, device=self.dev)
         return d
 
@@ -765,7 +793,7 @@ def mlp_block_score_vector(layer: LayerState, x: torch.Tensor, block_size: int, 
     partial = torch.empty(N // 128, s, dtype=F32, device=dev)
     if _precision(layer, precision) == "fp32":
         xnf = ops.rmsnorm_f32(x, layer.mlp_norm_w, inv=inv_all)
-        a3 = ops.split_bf16x3(xnf, 0)
+        a3 = layer.split_input(xnf)
         del xnf
         ops.gemm_gateup(a3, layer.gateup_x3(), gu=gu_all, partial=partial, relu=layer.relu,
                         exact_score=True)
@@ -790,14 +818,12 @@ def layer_qk(layer: LayerState, x: torch.Tensor, *, precision: str | None = None
     r = layer.lora_rank
     if _precision(layer, precision) == "fp32":
         xnf = ops.rmsnorm_f32(x, layer.attn_norm_w)
-        a3 = ops.split_bf16x3(xnf, 0)
-        del xnf
-        _, qk = ops.gemm_split3(a3, layer.qk_x3(), split_out=False, f32_out=True)
+        qk = ops.gemm_f32_exact(layer.split_input(xnf), layer.qk_x3())
         t = None
-        if r:
+        if r:  # the LoRA factors are fp32 (not bf16-exact): bf16x3 always
             a_t = ops.split_bf16x3_t(layer.lora_A.contiguous(), 1)  # [2r, 3h]
-            _, t = ops.gemm_split3(a3, a_t, split_out=False, f32_out=True)
-        del a3
+            t = ops.gemm_f32_exact(ops.split_bf16x3(xnf, 0), a_t)
+        del xnf
         q_hi, q_lo, k_hi, k_lo = ops.qk_finish(
             qk, t, layer.lora_Bq if r else None, r=r, scale=layer.lora_scaling,
             rope_tab=layer.rope_tab, h=h, kv=layer.kv, head_dim=layer.head_dim, rope=layer.rope)

@@ -191,6 +191,17 @@ def qk_finish(qk, t, Bq, *, r, scale, rope_tab, h, kv, head_dim, rope):
     return q_hi, q_lo, k_hi, k_lo
 
 
+def split_bf16x2(a):
+    """fp32 [M, K] -> bf16 [M, 2K] = [hi | lo] (A operand against [W | W])."""
+    _check(a)
+    _dt(a, F32, "a")
+    _rowmajor(a, "a")
+    M, K = a.shape
+    out = torch.empty(M, 2 * K, dtype=BF16, device=a.device)
+    call("lemo_split_bf16x2", ptr(a), a.stride(0), M, K, ptr(out), _s())
+    return out
+
+
 def split_hilo(a):
     """fp32 [M, K] -> (bf16 hi, bf16 lo) with a ≈ hi + lo."""
     _check(a)

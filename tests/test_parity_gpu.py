@@ -71,15 +71,28 @@ def _rel(got: np.ndarray, ref: np.ndarray) -> float:
     return float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-30))
 
 
+def _bf16_exact(a):
+    return torch.as_tensor(a).to(torch.bfloat16).float().numpy()
+
+
+@pytest.mark.parametrize("weights", ["fp32", "bf16"])
 @pytest.mark.parametrize("s", [4096, 16384])
-def test_north_star_width_masks(cuda, s):
+def test_north_star_width_masks(cuda, s, weights):
+    """weights="fp32": reference-init fp32 weights, the parity scorers run
+    bf16x3 (3 products); "bf16": bf16-representable weights (bf16
+    checkpoints, the bench's init) -- the scorers detect lo == 0 and run the
+    2-product form x_hi·W + x_lo·W."""
     cfg = dict(WIDTH, max_seq_len=s)
     om = O.init_model(O.Config(**cfg), seed=11, fast=True)
     O.perturb_lora_b(om, 12)
     L = om.layers[0]
+    if weights == "bf16":
+        for name in ("wq", "wk", "wv", "wo", "w_up", "w_down", "w_gate"):
+            setattr(L, name, _bf16_exact(getattr(L, name)))
     model = M.DecoderModel(M.ModelConfig(**cfg), 0, arrays=oracle_arrays(om),
                            scoring_precision="fp32")
     layer = model.layers[0]
+    assert layer.parity_terms == (2 if weights == "bf16" else 3)
     rng = np.random.default_rng(13)
     x = rng.standard_normal((s, 4096), dtype=np.float32)
     n_valid = s - 7  # ragged tail: the last block is partly padding
@@ -114,7 +127,8 @@ def test_north_star_width_masks(cuda, s):
         pq, pk, xd, B)
     torch.cuda.synchronize()
 
-    report = {"s": s, "n_blocks": len(ref["mlp"])}
+    report = {"s": s, "weights": weights, "parity_terms": layer.parity_terms,
+              "n_blocks": len(ref["mlp"])}
     for (prec, mode), vec in got.items():
         g = vec.cpu().numpy()
         if thr[mode] is None:  # recalibration: each side's own 50 % order statistic
@@ -131,7 +145,7 @@ def test_north_star_width_masks(cuda, s):
     print("mask parity", json.dumps(report))
     out = os.environ.get("LEMO_PARITY_OUT")
     if out:
-        with open(os.path.join(out, f"parity_{s}.json"), "w") as f:
+        with open(os.path.join(out, f"parity_{s}_{weights}.json"), "w") as f:
             json.dump(report, f, indent=1)
     nb = report["n_blocks"]
     for mode in ("mlp", "exact", "predicted"):
