@@ -214,9 +214,9 @@ struct EpiGateUpT {
         // inner from the bf16-rounded gate/up that are saved for backward, so the
         // dense path and the compaction path (mlp_compact) produce identical rows
         float in[32];
-        if constexpr (exact) {
+        if constexpr (exact) {  // the reference's two-branch logistic on expf (tensor.py:368-374)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) score += fabsf(g[i] * sigmoid_fast(g[i]) * u[i]);
+          for (int i = 0; i < 32; ++i) score += fabsf(g[i] * sigmoid_stable(g[i]) * u[i]);
         }
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
@@ -401,8 +401,11 @@ static int pick_bn(int M, int N) {
 }
 
 // fp32-faithful accumulation (see kPromote in gemm.cuh): the TMEM partial is
-// promoted into fp32 registers every kPromoteGroup k-blocks (K = 128).
-constexpr int kPromoteGroup = 2;
+// promoted into fp32 registers every kPromoteGroup k-blocks (K = 64 each).
+#ifndef LEMO_PROMOTE_GROUP
+#define LEMO_PROMOTE_GROUP 2
+#endif
+constexpr int kPromoteGroup = LEMO_PROMOTE_GROUP;
 
 template <int BN, class Epi>
 static int gemm_promoted(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
