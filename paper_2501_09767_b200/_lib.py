@@ -83,6 +83,17 @@ def lib():
     return _lib
 
 
+def memory_allocated(device) -> int:
+    """torch.cuda.memory_allocated without flattening the whole statistics
+    dict in Python (that costs ~0.2 ms, and the step reads it twice)."""
+    idx = device.index if isinstance(device, torch.device) and device.index is not None \
+        else torch.cuda.current_device()
+    try:
+        return int(torch._C._cuda_memoryStats(idx)["allocated_bytes"]["all"]["current"])
+    except (AttributeError, KeyError, TypeError):  # pragma: no cover - other torch builds
+        return torch.cuda.memory_allocated(idx)
+
+
 def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
     """Raw cudaStream_t of `stream` (default: torch's current stream on the
     current device) — the cheap C query, this runs once per launch."""
@@ -93,9 +104,7 @@ def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
 
 def ptr(t) -> int | None:
     """Device address of a tensor (None for None)."""
-    if t is None:
-        return None
-    return int(t.data_ptr())
+    return None if t is None else t.data_ptr()
 
 
 # kernels launched per entry point (everything else launches exactly one)
@@ -138,9 +147,14 @@ class Instrument:
 INSTRUMENT = Instrument()
 
 
+_FNS: dict = {}
+
+
 def call(name: str, *args):
     """Invoke a status-returning entry point; raise LemoError on failure."""
-    fn = getattr(lib(), name)
+    fn = _FNS.get(name)
+    if fn is None:
+        fn = _FNS[name] = getattr(lib(), name)
     ins = INSTRUMENT
     if ins.enabled:
         ins.launches[name] = ins.launches.get(name, 0) + _LAUNCHES.get(name, 1)

@@ -20,7 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import kernels, ledger, ops, predictor as predictor_mod, sparsity
+from . import _lib, kernels, ledger, ops, predictor as predictor_mod, sparsity
 from .errors import ContractError, DimensionError
 
 PAD_TOKEN = 0
@@ -675,7 +675,7 @@ class _Step:
     def _forward(self, need_grad: bool):
         m = self.model
         dev = m.device
-        mem0 = torch.cuda.memory_allocated(dev)
+        mem0 = _lib.memory_allocated(dev)
         x = ops.embed(self.ids, m.embed,
                       m.pos_embed[: self.n_pad].contiguous() if m.pos_embed is not None else None)
         saved = []
@@ -707,7 +707,7 @@ class _Step:
         led.mark("post_forward")
         # post_forward mark (model.py:296): activation bytes = everything still
         # allocated by this step that backward needs
-        mark = torch.cuda.memory_allocated(dev)
+        mark = _lib.memory_allocated(dev)
         m.last_stats = {"activation_bytes_post_forward": mark - mem0,
                         "retained": dict(src.last_fractions) if src is not None else {}}
         if need_grad:
