@@ -71,9 +71,10 @@ def parse():
     ap.add_argument("--no-law", action="store_true")
     ap.add_argument("--no-audit", action="store_true",
                     help="skip the mask-flip audit (production vs parity-precision scorers)")
-    ap.add_argument("--scoring-precision", default="bf16", choices=["bf16", "fp32"],
-                    help="precision of the scorers in the timed step: bf16 (production) or "
-                         "fp32 (the mask-exact parity precision)")
+    ap.add_argument("--scoring-precision", default="bf16", choices=["bf16", "fp32", "refined"],
+                    help="precision of the scorers in the timed step: bf16 (production), fp32 "
+                         "(the mask-exact parity precision) or refined (bf16 + parity re-scoring "
+                         "of the MLP blocks near their threshold)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N>1 (gloo only to smoke-test several "
                          "ranks sharing one GPU)")
@@ -329,7 +330,7 @@ def main():
     # steps use the production (bf16) scorers (scoring_precision="bf16")
     model = M.DecoderModel(cfg, seed=0, device=dev, init="torch",
                            scoring_precision=args.scoring_precision,
-                           parity_weights=(not args.no_audit) or args.scoring_precision == "fp32")
+                           parity_weights=(not args.no_audit) or args.scoring_precision != "bf16")
     h = cfg.hidden_dim
     rp = h // 4
     gen = torch.Generator(device=dev)

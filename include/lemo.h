@@ -73,10 +73,12 @@ int lemo_gemm_scatter_add(const void* A, int lda, const void* B, int ldb, float*
  * w_qkv_t: [h + (nmat-1)·kv, ldw] bf16 (nmat = 2: q, k only, as layer_qk does,
  * model.py:356-368); q is [M, h], k and v are [M, kv] (kv = h for multi-head,
  * kv = n_kv_heads·head_dim < h for grouped-query attention, an extension
- * beyond the reference); inv_freq: [head_dim/2] float64 = base^(-j/half). */
+ * beyond the reference); inv_freq: [head_dim/2] float64 = base^(-j/half).
+ * row_scale (optional, [M] fp32): per-row factor on the accumulator before
+ * RoPE (RMSNorm folded into the epilogue, lemo_rmsnorm_gather_fold). */
 int lemo_gemm_qkv(const void* xn, int ldx, const void* w_qkv_t, int ldw, int M, int h, int kv,
                   int K, int nmat, void* q, void* k, void* v, int head_dim, int rope,
-                  const double* inv_freq, const int* pos, void* stream);
+                  const double* inv_freq, const int* pos, const float* row_scale, void* stream);
 
 /* A-side LoRA K-extension: xn_ext[i, h+j] = bf16(scale·t[i, j]) (j < r2), 0 up to 64. */
 int lemo_lora_qkv_prep(const float* t, int ldt, int M, int r2, float scale, void* xn_ext, int ldx,
@@ -95,9 +97,12 @@ int lemo_lora_pack_b(const float* Bq, const float* Bv, int h, int kv, int r, voi
  * [M, N/2] (silu) or [M, N] (relu) bf16; partial (optional): [N/256, M] fp32
  * per-tile row sums of |inner|.  exact_score != 0: the scores use the fp32
  * accumulator (parity mode: xn / w_gu_t given as bf16x3 operands, K = 3h, see
- * lemo_split_bf16x3) instead of the bf16-rounded gate/up that gu stores. */
+ * lemo_split_bf16x3) instead of the bf16-rounded gate/up that gu stores.
+ * row_scale (optional, [M] fp32) multiplies each accumulator row first: the
+ * RMSNorm 1/rms when xn is bf16(x·w) (lemo_rmsnorm_gather_fold). */
 int lemo_gemm_gateup(const void* xn, int ldx, const void* w_gu_t, int M, int N, int K, void* gu,
-                     void* inner, float* partial, int relu, int exact_score, void* stream);
+                     void* inner, float* partial, int relu, int exact_score,
+                     const float* row_scale, void* stream);
 
 /* Backward of the MLP inner product: dinner = dy · W_downᵀ (w_down: [m_pad, h]
  * bf16, reference layout) turned into d(gate), d(up) (tensor.py:289-290,
@@ -111,6 +116,13 @@ int lemo_gemm_dgateup(const void* dy, const void* w_down, int M, int m_pad, int 
  * plus optional saved raw rows xg (bf16) and inv (fp32). */
 int lemo_rmsnorm_gather(const float* x, int ldx, const int* idx, int M, int h, const float* w,
                         void* xn, int ldxn, void* xg, float* inv, void* stream);
+
+/* As lemo_rmsnorm_gather, but xw = bf16(x[idx]·w) and inv = 1/sqrt(mean(x²)+eps)
+ * separately: the normalisation is applied to the GEMM accumulator (row_scale of
+ * lemo_gemm_gateup / lemo_gemm_qkv_scaled), so bf16-valued residual rows enter
+ * the tensor cores exactly (scoring precision, model.py:333-335 + 371-396). */
+int lemo_rmsnorm_gather_fold(const float* x, int ldx, const int* idx, int M, int h,
+                             const float* w, void* xw, int ldxw, float* inv, void* stream);
 
 /* LoRA down-projection operand: out[j, c] = bf16(A[c*lda + j]) for j < r2,
  * zero for r2 <= j < 32 (out: [32, h] bf16), so t = xn·[A_q|A_v]
@@ -219,6 +231,19 @@ int lemo_colsum_packed(const double* packed, int nb, double* vec, void* stream);
  * predict_scores (predictor.py:176-212) and exact_block_scores. */
 int lemo_pack_tril(const float* S, int lds, int nb, int clamp, double* out64, float* out32,
                    void* stream);
+
+/* out[i] = margin - |vec[i] - thr|: blocks with out >= 0 are the ones whose
+ * score is within `margin` of the threshold (select with thr = 0 compacts
+ * them) -- the candidates the refined MLP scoring re-scores in the parity
+ * precision (a decision is a >= against thr, sparsity.py:274-277). */
+int lemo_margin_vec(const double* vec, int nb, double thr, double margin, double* out,
+                    void* stream);
+
+/* vec[blocks[i]] = max over the b compact rows i·b.. (global row < n_valid) of
+ * Σ_t partial[t, row] / m_real -- re-scored blocks written back
+ * (mlp_block_scores arithmetic on a compact row set; partial is [n_tiles, rows]). */
+int lemo_mlp_patch(const float* partial, int n_tiles, int rows, const int* blocks, int b,
+                   int n_valid, int m_real, double* vec, void* stream);
 
 /* MLP block scores from per-tile row partials of lemo_gemm_gateup:
  * token score = Σ partial / m_real, block = max over rows < n_valid

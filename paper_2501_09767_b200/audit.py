@@ -18,7 +18,7 @@ each precision per layer.
 from __future__ import annotations
 
 from . import sparsity
-from .model import PatternSourceBase, mlp_block_score_vector
+from .model import PatternSourceBase, mlp_block_score_vector, refine_mlp_block_scores
 
 
 class MaskAudit(PatternSourceBase):
@@ -41,8 +41,10 @@ class MaskAudit(PatternSourceBase):
         b = self.model.config.block_size
         thr = self.inner.thresholds.get(layer_id, sparsity.MLP)
         # the precision the step itself scores in (model default) vs the parity one
-        prod = mlp_block_score_vector(layer, x, b, n_valid,
-                                      precision=self.model.scoring_precision)
+        prec = self.model.scoring_precision
+        prod = mlp_block_score_vector(layer, x, b, n_valid, precision=prec)
+        if prec == "refined":
+            refine_mlp_block_scores(layer, x, prod, thr, b, n_valid)
         par = mlp_block_score_vector(layer, x, b, n_valid, precision="fp32")
         flips = (prod >= thr) != (par >= thr)
         amb = flips & ((par - thr).abs() <= 1e-5 * abs(thr))
@@ -67,9 +69,15 @@ class MaskAudit(PatternSourceBase):
                 "mlp_ambiguous_total": sum(r["mlp_ambiguous"] for r in rows),
                 "mlp_max_rel_score_diff": max((r["max_rel_score_diff"] for r in rows),
                                               default=None),
+                "mlp_refined_blocks_total": sum(getattr(self.inner, "refined_blocks", {}).values())
+                if prec_refined(self.model) else None,
                 "attention_flips_total": 0,
                 "attention_note": "predicted attention scores are fp32-faithful in production "
                                   "(bf16x3 predictor GEMMs): identical to the parity precision"}
+
+
+def prec_refined(model) -> bool:
+    return model.scoring_precision == "refined"
 
 
 __all__ = ["MaskAudit"]

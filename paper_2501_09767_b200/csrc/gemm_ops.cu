@@ -145,6 +145,7 @@ struct EpiQKV {
   int h, kv, head_dim, rope;  // q width h, k / v width kv (grouped-query attention: kv < h)
   const double* inv_freq;  // [head_dim/2]
   const int* pos;
+  const float* row_scale;  // optional RMSNorm 1/rms per row (A operand = bf16(x·w))
   template <int BN>
   __device__ void run(int row, bool valid, int col0, uint32_t taddr, int part) const {
     const int which = col0 < h ? 0 : (col0 < h + kv ? 1 : 2);
@@ -162,6 +163,14 @@ struct EpiQKV {
       load_chunk(taddr + hd + cp, a);
       load_chunk(taddr + hd + half + cp, b);
       if (!valid) continue;
+      if (row_scale != nullptr) {
+        const float rs = __ldg(row_scale + row);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          a[i] *= rs;
+          b[i] *= rs;
+        }
+      }
       const int ca = cbase + hd + cp, cb = ca + half;
       if (rope && which < 2) {  // only q and k are rotated (kernels.py:112-114)
 #pragma unroll
@@ -192,6 +201,8 @@ struct EpiQKV {
 //   exact   : score from the fp32 accumulator instead of the bf16-rounded
 //             gate/up (the fp32-faithful parity mode: the GEMM then runs on
 //             bf16x3 operands, K = 3h, so the accumulator carries f32 precision)
+//   row_scale : optional per-row factor applied to the accumulator (the RMSNorm
+//             1/rms when the A operand is bf16(x·w), lemo_rmsnorm_gather_fold)
 template <bool exact>
 struct EpiGateUpT {
   __nv_bfloat16* gu;
@@ -200,10 +211,12 @@ struct EpiGateUpT {
   int ldi;
   float* partial;
   int M, relu;
+  const float* row_scale;
   template <int BN>
   __device__ void run(int row, bool valid, int col0, uint32_t taddr, int part) const {
     static_assert(BN == 256, "gate/up interleave assumes 256-column tiles");
     float score = 0.f;
+    const float rs = (row_scale != nullptr && valid) ? __ldg(row_scale + row) : 1.f;
     if (!relu) {
 #pragma unroll 1
       for (int c = part * 64; c < part * 64 + 64; c += 32) {
@@ -211,6 +224,13 @@ struct EpiGateUpT {
         load_chunk(taddr + c, g);
         load_chunk(taddr + 128 + c, u);
         if (!valid) continue;
+        if (row_scale != nullptr) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            g[i] *= rs;
+            u[i] *= rs;
+          }
+        }
         // inner from the bf16-rounded gate/up that are saved for backward, so the
         // dense path and the compaction path (mlp_compact) produce identical rows
         float in[32];
@@ -237,6 +257,10 @@ struct EpiGateUpT {
         float u[32];
         load_chunk(taddr + c, u);
         if (!valid) continue;
+        if (row_scale != nullptr) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) u[i] *= rs;
+        }
         float in[32];
         if constexpr (exact) {
 #pragma unroll
@@ -478,12 +502,12 @@ int lemo_gemm_scatter_add(const void* A, int lda, const void* B, int ldb, float*
 
 int lemo_gemm_qkv(const void* xn, int ldx, const void* w_qkv_t, int ldw, int M, int h, int kv,
                   int K, int nmat, void* q, void* k, void* v, int head_dim, int rope,
-                  const double* inv_freq, const int* pos, void* stream) {
+                  const double* inv_freq, const int* pos, const float* row_scale, void* stream) {
   LEMO_ARG_CHECK(head_dim % 64 == 0, "lemo_gemm_qkv: head_dim must be a multiple of 64");
   LEMO_ARG_CHECK(nmat == 2 || nmat == 3, "lemo_gemm_qkv: nmat must be 2 (q,k) or 3 (q,k,v)");
   LEMO_ARG_CHECK(kv > 0 && kv <= h && kv % head_dim == 0, "lemo_gemm_qkv: bad k/v width");
   EpiQKV e{reinterpret_cast<__nv_bfloat16*>(q), reinterpret_cast<__nv_bfloat16*>(k),
-           reinterpret_cast<__nv_bfloat16*>(v), h, kv, head_dim, rope, inv_freq, pos};
+           reinterpret_cast<__nv_bfloat16*>(v), h, kv, head_dim, rope, inv_freq, pos, row_scale};
   const int N = h + (nmat - 1) * kv;
   int rc;
   if (h % 256 == 0 && kv % 256 == 0 && 256 % head_dim == 0)
@@ -498,17 +522,18 @@ int lemo_gemm_qkv(const void* xn, int ldx, const void* w_qkv_t, int ldw, int M, 
 }
 
 int lemo_gemm_gateup(const void* xn, int ldx, const void* w_gu_t, int M, int N, int K, void* gu,
-                     void* inner, float* partial, int relu, int exact_score, void* stream) {
+                     void* inner, float* partial, int relu, int exact_score,
+                     const float* row_scale, void* stream) {
   LEMO_ARG_CHECK(N % 256 == 0, "lemo_gemm_gateup: N must be a multiple of 256 (padded mlp dim)");
   auto* gup = reinterpret_cast<__nv_bfloat16*>(gu);
   auto* inp = reinterpret_cast<__nv_bfloat16*>(inner);
   const int ldi = relu ? N : N / 2;
   cudaStream_t st = (cudaStream_t)stream;
   if (exact_score) {  // parity mode: bf16x3 operands, promoted accumulation
-    EpiGateUpExact e{gup, N, inp, ldi, partial, M, relu};
+    EpiGateUpExact e{gup, N, inp, ldi, partial, M, relu, row_scale};
     LEMO_RETURN_RC("lemo_gemm_gateup", gemm_promoted<256>(xn, ldx, w_gu_t, K, M, N, K, e, st));
   }
-  EpiGateUp e{gup, N, inp, ldi, partial, M, relu};
+  EpiGateUp e{gup, N, inp, ldi, partial, M, relu, row_scale};
   LEMO_RETURN_RC("lemo_gemm_gateup", gemm<256>(xn, ldx, w_gu_t, K, M, N, K, e, st));
 }
 

@@ -29,7 +29,13 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // down-projection t = xn·[A_q|A_v] runs as a tcgen05 GEMM on the bf16 xn;
 // see lemo_lora_pack.)
 
-template <int VPT>
+// kFold: write bf16(x·w) instead of bf16(x·inv·w) and leave inv to the GEMM
+// epilogue (row scale).  The product of a row with a per-row scalar rounds
+// correlatedly when x is bf16-valued (embedding rows, rows a sparse block did
+// not update): bf16(x_i·inv) errors stop averaging out across the K sum
+// (measured 3.7e-3 vs 3.5e-4 relative MLP-score error); bf16(x·w) is exact
+// for such rows and no worse for the rest.
+template <int VPT, bool kFold = false>
 __global__ void __launch_bounds__(128) gather_rmsnorm_kernel(
     const float* __restrict__ x, int ldx, const int* __restrict__ idx, int h,
     const float* __restrict__ w, __nv_bfloat16* __restrict__ xn, int ldxn,
@@ -56,11 +62,12 @@ __global__ void __launch_bounds__(128) gather_rmsnorm_kernel(
     const int c = threadIdx.x + i * blockDim.x;
     if (c >= nv) continue;
     const float4 ww = __ldg(w4 + c);
+    const float sc = kFold ? 1.f : inv;
     float4 o;
-    o.x = v[i].x * inv * ww.x;
-    o.y = v[i].y * inv * ww.y;
-    o.z = v[i].z * inv * ww.z;
-    o.w = v[i].w * inv * ww.w;
+    o.x = v[i].x * sc * ww.x;
+    o.y = v[i].y * sc * ww.y;
+    o.z = v[i].z * sc * ww.z;
+    o.w = v[i].w * sc * ww.w;
     uint2 ob = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
     reinterpret_cast<uint2*>(xn + (size_t)row * ldxn)[c] = ob;
     if (xg) {
@@ -585,6 +592,28 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
 using namespace lemo;
 
 extern "C" {
+
+int lemo_rmsnorm_gather_fold(const float* x, int ldx, const int* idx, int M, int h,
+                             const float* w, void* xw, int ldxw, float* inv, void* stream) {
+  LEMO_ARG_CHECK(ldxw % 4 == 0 && ldxw >= h && inv != nullptr,
+                 "lemo_rmsnorm_gather_fold: bad output stride or missing inv");
+  if (M <= 0) return 0;
+  LEMO_ARG_CHECK(h % 4 == 0 && ldx % 4 == 0 && h <= 4 * 128 * 16,
+                 "lemo_rmsnorm_gather_fold: h, ldx must be multiples of 4, h <= 8192");
+  const int vpt = (h / 4 + 127) / 128;
+  cudaStream_t st = (cudaStream_t)stream;
+  auto* o = reinterpret_cast<__nv_bfloat16*>(xw);
+#define LAUNCH(V) \
+  gather_rmsnorm_kernel<V, true><<<M, 128, 0, st>>>(x, ldx, idx, h, w, o, ldxw, nullptr, inv)
+  if (vpt <= 1) LAUNCH(1);
+  else if (vpt <= 2) LAUNCH(2);
+  else if (vpt <= 4) LAUNCH(4);
+  else if (vpt <= 8) LAUNCH(8);
+  else LAUNCH(16);
+#undef LAUNCH
+  LEMO_CHECK_LAUNCH("lemo_rmsnorm_gather_fold");
+  return 0;
+}
 
 int lemo_rmsnorm_gather(const float* x, int ldx, const int* idx, int M, int h, const float* w,
                         void* xn, int ldxn, void* xg, float* inv, void* stream) {

@@ -93,6 +93,33 @@ __global__ void colsum_clamped_kernel(const float* __restrict__ S, int lds, int 
   if (lane == 0) vec[n] = acc;
 }
 
+// Refined MLP scoring (scoring_precision "refined"): the blocks whose bf16
+// score lies within `margin` of the threshold are re-scored in the parity
+// precision.  margin_vec turns "ambiguous" into a >= 0 test for the select
+// kernel (which compacts the blocks and expands their token rows);
+// mlp_patch writes the re-scored block maxima back into the score vector
+// (same arithmetic as mlp_block_scores_warp_kernel on the compact rows).
+__global__ void margin_vec_kernel(const double* __restrict__ vec, int nb, double thr,
+                                  double margin, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nb) out[i] = margin - fabs(vec[i] - thr);
+}
+
+__global__ void mlp_patch_kernel(const float* __restrict__ partial, int n_tiles, int rows,
+                                 const int* __restrict__ blocks, int b, int n_valid, float m_real,
+                                 double* __restrict__ vec) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;  // compact row: block row / b
+  const int blk = row < rows ? __ldg(blocks + row / b) : 0;
+  float best = -INFINITY;
+  if (row < rows && blk * b + row % b < n_valid) {
+    float acc = 0.f;
+    for (int t = 0; t < n_tiles; ++t) acc += partial[(size_t)t * rows + row];
+    best = acc / m_real;
+  }
+  for (int o = b >> 1; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if (row < rows && (row % b) == 0) vec[blk] = best == -INFINITY ? 0.0 : (double)best;
+}
+
 // Row-major packed lower triangle of a dense [nb, nb] fp32 matrix (element
 // (m, n <= m) at m(m+1)/2 + n, sparsity.py:35-37), optionally clamped at 0
 // (predict_scores, predictor.py:189-212), as f64 (BlockScoreMatrix) or f32.
@@ -328,6 +355,25 @@ int lemo_colsum_clamped(const float* S, int lds, int nb, double* vec, void* stre
   if (nb <= 0) return 0;
   colsum_clamped_kernel<<<(nb + 7) / 8, 256, 0, (cudaStream_t)stream>>>(S, lds, nb, vec);
   LEMO_CHECK_LAUNCH("lemo_colsum_clamped");
+  return 0;
+}
+
+int lemo_margin_vec(const double* vec, int nb, double thr, double margin, double* out,
+                    void* stream) {
+  if (nb <= 0) return 0;
+  margin_vec_kernel<<<(nb + 255) / 256, 256, 0, (cudaStream_t)stream>>>(vec, nb, thr, margin, out);
+  LEMO_CHECK_LAUNCH("lemo_margin_vec");
+  return 0;
+}
+
+int lemo_mlp_patch(const float* partial, int n_tiles, int rows, const int* blocks, int b,
+                   int n_valid, int m_real, double* vec, void* stream) {
+  if (rows <= 0) return 0;
+  LEMO_ARG_CHECK(b <= 32 && (b & (b - 1)) == 0 && rows % b == 0,
+                 "lemo_mlp_patch: block size must be a power of two <= 32 dividing rows");
+  mlp_patch_kernel<<<(rows + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      partial, n_tiles, rows, blocks, b, n_valid, (float)m_real, vec);
+  LEMO_CHECK_LAUNCH("lemo_mlp_patch");
   return 0;
 }
 

@@ -25,6 +25,7 @@ from .errors import ContractError, DimensionError
 
 PAD_TOKEN = 0
 IGNORE_INDEX = -1
+SCORING_PRECISIONS = ("bf16", "fp32", "refined")
 BF16, F32 = torch.bfloat16, torch.float32
 
 
@@ -216,6 +217,7 @@ class LayerState:
         self.m_pad = cfg.mlp_pad
         self.rope_tab = model.rope_tab
         self.scoring_precision = model.scoring_precision
+        self.refine_margin = model.refine_margin
 
         def g(name):
             a = arrays[name]
@@ -441,21 +443,25 @@ class DecoderModel:
 
     def __init__(self, cfg: ModelConfig, seed: int = 0, *, device=None, init: str = "torch",
                  arrays: dict | None = None, scoring_precision: str = "bf16",
-                 parity_weights: bool | None = None):
+                 parity_weights: bool | None = None, refine_margin: float = 2e-3):
         cfg.check_gpu_geometry()
-        if scoring_precision not in ("bf16", "fp32"):
+        if scoring_precision not in SCORING_PRECISIONS:
             raise ContractError(f"unknown scoring precision {scoring_precision!r}")
         # default precision of the scorers the pattern sources call:
-        # "bf16": production scorers on bf16 tensor-core operands;  "fp32": the
-        # fp32-faithful (bf16x3) parity mode that reproduces the reference's masks
+        #   "bf16"     production scorers on bf16 tensor-core operands
+        #   "fp32"     the fp32-faithful parity scorers (reproduce the reference's masks)
+        #   "refined"  bf16 scorers, then every MLP block whose score lies within
+        #              refine_margin·|T| of its threshold T re-scored in the parity
+        #              precision before selection (refine_mlp_block_scores)
         self.scoring_precision = scoring_precision
+        self.refine_margin = float(refine_margin)
         # parity_weights: keep the bf16 residuals of the scoring weights (+~8 %
         # weight memory) so the fp32 precision can be used per call (e.g. by the
         # mask audit) while the sources default to bf16
-        self.parity_weights = (scoring_precision == "fp32") if parity_weights is None \
+        self.parity_weights = (scoring_precision != "bf16") if parity_weights is None \
             else bool(parity_weights)
-        if scoring_precision == "fp32" and not self.parity_weights:
-            raise ContractError("scoring_precision='fp32' needs parity_weights")
+        if scoring_precision != "bf16" and not self.parity_weights:
+            raise ContractError(f"scoring_precision={scoring_precision!r} needs parity_weights")
         self.config = cfg
         self.seed = seed
         self.device = torch.device(device) if device is not None else torch.device("cuda")
@@ -770,10 +776,11 @@ class _StepFn(torch.autograd.Function):
 
 
 def _precision(layer: LayerState, precision):
+    """The precision one scorer call runs in ("refined" scores in bf16 first)."""
     p = precision or layer.scoring_precision
-    if p not in ("bf16", "fp32"):
+    if p not in SCORING_PRECISIONS:
         raise ContractError(f"unknown scoring precision {p!r}")
-    return p
+    return "bf16" if p == "refined" else p
 
 
 def mlp_block_score_vector(layer: LayerState, x: torch.Tensor, block_size: int, n_valid: int,
@@ -799,13 +806,43 @@ def mlp_block_score_vector(layer: LayerState, x: torch.Tensor, block_size: int, 
                         exact_score=True)
         del a3
     else:
-        xn_all = ops.rmsnorm_gather(x, layer.mlp_norm_w, None, inv=inv_all)
-        ops.gemm_gateup(xn_all, layer.w_gu_t, gu=gu_all, partial=partial, relu=layer.relu)
-        del xn_all
+        # RMSNorm folded into the epilogue: bf16(x·w) in, ·1/rms on the accumulator
+        xw_all = ops.rmsnorm_gather_fold(x, layer.mlp_norm_w, inv=inv_all)
+        ops.gemm_gateup(xw_all, layer.w_gu_t, gu=gu_all, partial=partial, relu=layer.relu,
+                        row_scale=inv_all)
+        del xw_all
     vec = ops.mlp_block_scores(partial, s=s, n_valid=n_valid, b=block_size, m_real=layer.m)
     if keep_rows:
         return vec, (gu_all, inv_all)
     return vec
+
+
+def refine_mlp_block_scores(layer: LayerState, x: torch.Tensor, vec: torch.Tensor, thr: float,
+                            block_size: int, n_valid: int, *, margin: float | None = None) -> int:
+    """Refined MLP scoring: every block whose (bf16) score lies within
+    margin·|thr| of the threshold is re-scored in the fp32-faithful parity
+    precision and patched into `vec` in place; returns the number of blocks
+    re-scored.  The bf16 score error is measured at ≤ 5.2e-4 relative at
+    Llama2-7B width (the bench's mask audit), so the default margin of 2e-3
+    leaves a 4× safety factor: blocks outside the margin cannot flip, blocks
+    inside are decided by parity-precision scores (tests/test_parity_gpu.py).
+    One extra host read-back (the number of candidates sizes the GEMM)."""
+    margin = layer.refine_margin if margin is None else margin
+    s = x.shape[0]
+    cand = sparsity.select_device(ops.margin_vec(vec, thr, margin * abs(thr)), 0.0,
+                                  block_size=block_size, n_tokens=s)[0]
+    rows = cand.k
+    if rows == 0:
+        return 0
+    xnf = ops.rmsnorm_f32(x, layer.mlp_norm_w, cand.device_token_indices(x.device))
+    a = layer.split_input(xnf)
+    del xnf
+    N = layer.w_gu_t.shape[0]
+    partial = torch.empty(N // 128, rows, dtype=F32, device=x.device)
+    ops.gemm_gateup(a, layer.gateup_x3(), partial=partial, relu=layer.relu, exact_score=True)
+    ops.mlp_patch(partial, cand._dev_blocks, rows=rows, b=block_size, n_valid=n_valid,
+                  m_real=layer.m, vec=vec)
+    return rows // block_size
 
 
 def layer_qk(layer: LayerState, x: torch.Tensor, *, precision: str | None = None):
@@ -828,13 +865,16 @@ def layer_qk(layer: LayerState, x: torch.Tensor, *, precision: str | None = None
             qk, t, layer.lora_Bq if r else None, r=r, scale=layer.lora_scaling,
             rope_tab=layer.rope_tab, h=h, kv=layer.kv, head_dim=layer.head_dim, rope=layer.rope)
         return (q_hi, q_lo), (k_hi, k_lo)
+    # RMSNorm folded into the epilogue (as the MLP scorer): bf16(x·w) in; the
+    # LoRA term xw·A·B is linear in the row, so one row scale covers both
     xn = torch.empty(s, layer.w_qkv_t.shape[1], dtype=BF16, device=x.device)
-    ops.rmsnorm_gather(x, layer.attn_norm_w, None, xn=xn)
+    inv = torch.empty(s, dtype=F32, device=x.device)
+    ops.rmsnorm_gather_fold(x, layer.attn_norm_w, inv=inv, out=xn)
     if r:
         layer.qkv_input(xn)
     pos = torch.arange(s, dtype=torch.int32, device=x.device)
     q, k = ops.gemm_qkv(xn, layer.w_qkv_t, h=h, head_dim=layer.head_dim, rope=layer.rope,
-                        inv_freq=layer.inv_freq, pos=pos, nmat=2, kv=layer.kv)
+                        inv_freq=layer.inv_freq, pos=pos, nmat=2, kv=layer.kv, row_scale=inv)
     return q, k
 
 
@@ -843,10 +883,12 @@ def layer_qk(layer: LayerState, x: torch.Tensor, *, precision: str | None = None
 
 
 class PatternSourceBase:
-    """Interleaves scoring with the layer loop; records retained fractions."""
+    """Interleaves scoring with the layer loop; records retained fractions
+    (and, in the refined precision, how many MLP blocks were re-scored)."""
 
     def __init__(self):
         self.last_fractions: dict = {}
+        self.refined_blocks: dict = {}
 
     def pattern(self, layer_id, component, x, n_valid):
         raise NotImplementedError
@@ -953,6 +995,9 @@ class PredictedPatternSource(PatternSourceBase):
             vec, rows = mlp_block_score_vector(layer, x, b, n_valid, keep_rows=True)
             self.model.stash_mlp_rows(layer_id, x, rows)
             thr = self.thresholds.get(layer_id, component)
+            if layer.scoring_precision == "refined":
+                self.refined_blocks[layer_id] = refine_mlp_block_scores(layer, x, vec, thr, b,
+                                                                        n_valid)
         if self.record:
             self.recorded_vectors.setdefault((layer_id, component), []).append(vec)
         force = (0,) if self.sink_first_block else ()
@@ -1008,6 +1053,9 @@ class ExactPatternSource(PatternSourceBase):
             if keep:
                 vec, rows = res
                 self.model.stash_mlp_rows(layer_id, x, rows)
+                if layer.scoring_precision == "refined":
+                    self.refined_blocks[layer_id] = refine_mlp_block_scores(
+                        layer, x, vec, self.thresholds.get(layer_id, component), b, n_valid)
             else:
                 vec = res
         if self.record:

@@ -104,7 +104,8 @@ def gemm_scatter_add(a, b, resid, idx=None):
     return resid
 
 
-def gemm_qkv(xn, w_qkv_t, *, h, head_dim, rope, inv_freq, pos, nmat=3, kv=None, out=None):
+def gemm_qkv(xn, w_qkv_t, *, h, head_dim, rope, inv_freq, pos, nmat=3, kv=None, out=None,
+             row_scale=None):
     """q [M, h], k(, v) [M, kv] = rope(xn·Wᵀ) at positions pos over K =
     xn.shape[1] columns (h, or h + 64 with the LoRA K-extension) — see
     lemo_gemm_qkv.  kv < h: grouped-query attention (kv = n_kv_heads·head_dim)."""
@@ -119,20 +120,23 @@ def gemm_qkv(xn, w_qkv_t, *, h, head_dim, rope, inv_freq, pos, nmat=3, kv=None, 
     q, k = out[0], out[1]
     v = out[2] if nmat == 3 else None
     call("lemo_gemm_qkv", ptr(xn), xn.stride(0), ptr(w_qkv_t), w_qkv_t.stride(0), M, h, kv, K,
-         nmat, ptr(q), ptr(k), ptr(v), head_dim, int(bool(rope)), ptr(inv_freq), ptr(pos), _s())
+         nmat, ptr(q), ptr(k), ptr(v), head_dim, int(bool(rope)), ptr(inv_freq), ptr(pos),
+         ptr(row_scale), _s())
     return out
 
 
-def gemm_gateup(xn, w_gu_t, *, gu=None, inner=None, partial=None, relu=False, exact_score=False):
+def gemm_gateup(xn, w_gu_t, *, gu=None, inner=None, partial=None, relu=False, exact_score=False,
+                row_scale=None):
     """exact_score=True: xn / w_gu_t are bf16x3 operands (K = 3h) and the MLP
-    scores come from the fp32 accumulator (parity mode)."""
+    scores come from the fp32 accumulator (parity mode).  row_scale: per-row
+    factor on the accumulator (xn given as bf16(x·w), rmsnorm_gather_fold)."""
     M, K = xn.shape
     N = w_gu_t.shape[0]
-    _check(xn, w_gu_t, gu, inner, partial)
+    _check(xn, w_gu_t, gu, inner, partial, row_scale)
     if w_gu_t.shape[1] != K or w_gu_t.stride(0) != K:
         raise DimensionError(f"gate/up weight {tuple(w_gu_t.shape)} does not match K = {K}")
     call("lemo_gemm_gateup", ptr(xn), xn.stride(0), ptr(w_gu_t), M, N, K, ptr(gu), ptr(inner),
-         ptr(partial), int(bool(relu)), int(bool(exact_score)), _s())
+         ptr(partial), int(bool(relu)), int(bool(exact_score)), ptr(row_scale), _s())
 
 
 def gemm_dgateup(dy, w_down, gu, dgu, *, m_pad, relu=False):
@@ -160,6 +164,20 @@ def rmsnorm_gather(x, w, idx=None, *, xn=None, xg=None, inv=None):
 
 
 LORA_K_EXT = 64  # extra K columns of the q/k/v GEMM carrying the LoRA terms
+
+
+def rmsnorm_gather_fold(x, w, idx=None, *, inv, out=None):
+    """bf16(x[idx]·w) rows and inv = 1/rms (the normalisation applied later as
+    the GEMM epilogue's row scale)."""
+    _check(x, w, idx, inv, out)
+    _dt(x, F32, "x")
+    M = x.shape[0] if idx is None else idx.shape[0]
+    h = x.shape[1]
+    if out is None:
+        out = torch.empty(M, h, dtype=BF16, device=x.device)
+    call("lemo_rmsnorm_gather_fold", ptr(x), x.stride(0), ptr(idx), M, h, ptr(w), ptr(out),
+         out.stride(0), ptr(inv), _s())
+    return out
 
 
 def rmsnorm_f32(x, w, idx=None, *, out=None, inv=None):
@@ -478,6 +496,21 @@ def mlp_block_scores(partial, *, s, n_valid, b, m_real, out=None):
     call("lemo_mlp_block_scores", ptr(partial), partial.shape[0], s, n_valid, b, m_real, ptr(out),
          _s())
     return out
+
+
+def margin_vec(vec, thr, margin, out=None):
+    _check(vec, out)
+    _dt(vec, F64, "scores")
+    out = torch.empty_like(vec) if out is None else out
+    call("lemo_margin_vec", ptr(vec), vec.numel(), float(thr), float(margin), ptr(out), _s())
+    return out
+
+
+def mlp_patch(partial, blocks, *, rows, b, n_valid, m_real, vec):
+    _check(partial, blocks, vec)
+    call("lemo_mlp_patch", ptr(partial), partial.shape[0], rows, ptr(blocks), b, n_valid, m_real,
+         ptr(vec), _s())
+    return vec
 
 
 def select(vec, *, b, n_tokens, thr=0.0, thr_dev=None, force=None, mask, blocks, tokens, counts,

@@ -124,13 +124,17 @@ def test_north_star_width_masks(cuda, s, weights):
         qq, kk = M.layer_qk(layer, xd, precision=prec)
         got[(prec, "exact")] = exact.exact_block_vector(qq, kk, B, n_heads=32, n_valid=n_valid)
         del qq, kk
+    # refined: bf16 scores, the blocks near the threshold re-scored in parity precision
+    v = M.mlp_block_score_vector(layer, xd, B, n_valid, precision="bf16")
+    n_ref = M.refine_mlp_block_scores(layer, xd, v, thr["mlp"], B, n_valid)
+    got[("refined", "mlp")] = v
     # the predictor path is fp32-faithful in production already (bf16x3)
     got[("fp32", "predicted")] = got[("bf16", "predicted")] = P.predicted_block_vector(
         pq, pk, xd, B)
     torch.cuda.synchronize()
 
     report = {"s": s, "weights": weights, "parity_terms": layer.parity_terms,
-              "n_blocks": len(ref["mlp"])}
+              "n_blocks": len(ref["mlp"]), "refined_blocks": n_ref}
     for (prec, mode), vec in got.items():
         g = vec.cpu().numpy()
         t_got = None
@@ -155,9 +159,10 @@ def test_north_star_width_masks(cuda, s, weights):
         with open(os.path.join(out, f"parity_{s}_{weights}.json"), "w") as f:
             json.dump(report, f, indent=1)
     nb = report["n_blocks"]
-    for mode in ("mlp", "exact", "predicted"):
-        r = report[f"fp32_{mode}"]
-        assert r["flips"] - r["ambiguous"] == 0 and r["ambiguous"] <= 1, (mode, r)
+    for prec, mode in (("fp32", "mlp"), ("fp32", "exact"), ("fp32", "predicted"),
+                       ("refined", "mlp")):
+        r = report[f"{prec}_{mode}"]
+        assert r["flips"] - r["ambiguous"] == 0 and r["ambiguous"] <= 1, (prec, mode, r)
         assert r["score_rel_err"] <= PARITY_SCORE_RTOL, (mode, r)
         rb = report[f"bf16_{mode}"]
         assert rb["flips"] <= BF16_FLIP_FRACTION * nb, (mode, rb)
