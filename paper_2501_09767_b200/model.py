@@ -612,6 +612,16 @@ class DecoderModel:
                 loss = step.forward(need_grad=False)
         return loss, step.hidden
 
+    def set_scoring_precision(self, precision: str) -> None:
+        """Switch the scorers' default precision (model and every layer)."""
+        if precision not in SCORING_PRECISIONS:
+            raise ContractError(f"unknown scoring precision {precision!r}")
+        if precision != "bf16" and not self.parity_weights:
+            raise ContractError(f"scoring_precision={precision!r} needs parity_weights")
+        self.scoring_precision = precision
+        for layer in self.layers:
+            layer.scoring_precision = precision
+
     def stash_mlp_rows(self, layer_id: int, x: torch.Tensor, rows) -> None:
         self._mlp_scored[layer_id] = (self._epoch, x.data_ptr(), rows)
 
