@@ -232,18 +232,20 @@ int lemo_colsum_packed(const double* packed, int nb, double* vec, void* stream);
 int lemo_pack_tril(const float* S, int lds, int nb, int clamp, double* out64, float* out32,
                    void* stream);
 
-/* out[i] = margin - |vec[i] - thr|: blocks with out >= 0 are the ones whose
- * score is within `margin` of the threshold (select with thr = 0 compacts
- * them) -- the candidates the refined MLP scoring re-scores in the parity
- * precision (a decision is a >= against thr, sparsity.py:274-277). */
-int lemo_margin_vec(const double* vec, int nb, double thr, double margin, double* out,
-                    void* stream);
+/* Token-level refinement candidates: out[row] = 0 for every row < n_valid
+ * whose block score vec[row / b] lies within `margin` of thr AND whose own
+ * token score Σ_t partial[t, row] / m_real is >= thr - margin; -1 otherwise
+ * (select with thr = 0 and block size 1 compacts them).  Only these rows can
+ * decide their block's >= (sparsity.py:274-277 on the block max,
+ * sparsity.py:298-305); partial is [n_tiles, s]. */
+int lemo_mlp_token_band(const float* partial, int n_tiles, int s, int n_valid, int b, int m_real,
+                        const double* vec, double thr, double margin, double* out, void* stream);
 
-/* vec[blocks[i]] = max over the b compact rows i·b.. (global row < n_valid) of
- * Σ_t partial[t, row] / m_real -- re-scored blocks written back
- * (mlp_block_scores arithmetic on a compact row set; partial is [n_tiles, rows]). */
-int lemo_mlp_patch(const float* partial, int n_tiles, int rows, const int* blocks, int b,
-                   int n_valid, int m_real, double* vec, void* stream);
+/* vec[tok[i] / b] = max over the re-scored rows of that block of
+ * Σ_t partial[t, i] / m_real (tok ascending; partial is [n_tiles, rows]) --
+ * the token-level refinement written back (mlp_block_scores arithmetic). */
+int lemo_mlp_patch_rows(const float* partial, int n_tiles, int rows, const int* tok, int b,
+                        int m_real, double* vec, void* stream);
 
 /* MLP block scores from per-tile row partials of lemo_gemm_gateup:
  * token score = Σ partial / m_real, block = max over rows < n_valid

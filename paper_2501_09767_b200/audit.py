@@ -42,9 +42,11 @@ class MaskAudit(PatternSourceBase):
         thr = self.inner.thresholds.get(layer_id, sparsity.MLP)
         # the precision the step itself scores in (model default) vs the parity one
         prec = self.model.scoring_precision
-        prod = mlp_block_score_vector(layer, x, b, n_valid, precision=prec)
+        prod, partial = mlp_block_score_vector(layer, x, b, n_valid, precision=prec,
+                                               with_partial=True)
         if prec == "refined":
-            refine_mlp_block_scores(layer, x, prod, thr, b, n_valid)
+            refine_mlp_block_scores(layer, x, prod, partial, thr, b, n_valid)
+        del partial
         par = mlp_block_score_vector(layer, x, b, n_valid, precision="fp32")
         flips = (prod >= thr) != (par >= thr)
         amb = flips & ((par - thr).abs() <= 1e-5 * abs(thr))
@@ -69,7 +71,7 @@ class MaskAudit(PatternSourceBase):
                 "mlp_ambiguous_total": sum(r["mlp_ambiguous"] for r in rows),
                 "mlp_max_rel_score_diff": max((r["max_rel_score_diff"] for r in rows),
                                               default=None),
-                "mlp_refined_blocks_total": sum(getattr(self.inner, "refined_blocks", {}).values())
+                "mlp_refined_rows_total": sum(getattr(self.inner, "refined_rows", {}).values())
                 if prec_refined(self.model) else None,
                 "attention_flips_total": 0,
                 "attention_note": "predicted attention scores are fp32-faithful in production "

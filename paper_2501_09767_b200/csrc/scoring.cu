@@ -93,31 +93,44 @@ __global__ void colsum_clamped_kernel(const float* __restrict__ S, int lds, int 
   if (lane == 0) vec[n] = acc;
 }
 
-// Refined MLP scoring (scoring_precision "refined"): the blocks whose bf16
-// score lies within `margin` of the threshold are re-scored in the parity
-// precision.  margin_vec turns "ambiguous" into a >= 0 test for the select
-// kernel (which compacts the blocks and expands their token rows);
-// mlp_patch writes the re-scored block maxima back into the score vector
-// (same arithmetic as mlp_block_scores_warp_kernel on the compact rows).
-__global__ void margin_vec_kernel(const double* __restrict__ vec, int nb, double thr,
-                                  double margin, double* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nb) out[i] = margin - fabs(vec[i] - thr);
+// Refined MLP scoring (scoring_precision "refined"): bf16 scores first, then
+// only the rows that can decide a near-threshold block re-scored in the
+// parity precision.  A block's decision is max_t score_t >= T, so inside
+// a block whose bf16 score is within `margin` of T only the rows whose own
+// bf16 token score is >= T - margin can decide it (a row below that cannot
+// reach T under the same error bound); out[row] = 0 marks those rows (select
+// with thr = 0, block size 1, compacts them in ascending order), -1 the rest.
+__global__ void mlp_token_band_kernel(const float* __restrict__ partial, int n_tiles, int s,
+                                      int n_valid, int b, float m_real,
+                                      const double* __restrict__ vec, double thr, double margin,
+                                      double* __restrict__ out) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= s) return;
+  double o = -1.0;
+  if (row < n_valid && fabs(__ldg(vec + row / b) - thr) <= margin) {
+    float acc = 0.f;  // the token score exactly as mlp_block_scores forms it
+    for (int t = 0; t < n_tiles; ++t) acc += partial[(size_t)t * s + row];
+    if ((double)(acc / m_real) >= thr - margin) o = 0.0;
+  }
+  out[row] = o;
 }
 
-__global__ void mlp_patch_kernel(const float* __restrict__ partial, int n_tiles, int rows,
-                                 const int* __restrict__ blocks, int b, int n_valid, float m_real,
-                                 double* __restrict__ vec) {
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;  // compact row: block row / b
-  const int blk = row < rows ? __ldg(blocks + row / b) : 0;
+// vec[tok[i] / b] = max over the re-scored rows of that block (rows ascending,
+// so a block's rows are contiguous; the first row of each run reduces it).
+__global__ void mlp_patch_rows_kernel(const float* __restrict__ partial, int n_tiles, int rows,
+                                      const int* __restrict__ tok, int b, float m_real,
+                                      double* __restrict__ vec) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const int blk = __ldg(tok + i) / b;
+  if (i > 0 && __ldg(tok + i - 1) / b == blk) return;
   float best = -INFINITY;
-  if (row < rows && blk * b + row % b < n_valid) {
+  for (int j = i; j < rows && __ldg(tok + j) / b == blk; ++j) {
     float acc = 0.f;
-    for (int t = 0; t < n_tiles; ++t) acc += partial[(size_t)t * rows + row];
-    best = acc / m_real;
+    for (int t = 0; t < n_tiles; ++t) acc += partial[(size_t)t * rows + j];
+    best = fmaxf(best, acc / m_real);
   }
-  for (int o = b >> 1; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
-  if (row < rows && (row % b) == 0) vec[blk] = best == -INFINITY ? 0.0 : (double)best;
+  vec[blk] = (double)best;
 }
 
 // Row-major packed lower triangle of a dense [nb, nb] fp32 matrix (element
@@ -358,22 +371,23 @@ int lemo_colsum_clamped(const float* S, int lds, int nb, double* vec, void* stre
   return 0;
 }
 
-int lemo_margin_vec(const double* vec, int nb, double thr, double margin, double* out,
-                    void* stream) {
-  if (nb <= 0) return 0;
-  margin_vec_kernel<<<(nb + 255) / 256, 256, 0, (cudaStream_t)stream>>>(vec, nb, thr, margin, out);
-  LEMO_CHECK_LAUNCH("lemo_margin_vec");
+int lemo_mlp_token_band(const float* partial, int n_tiles, int s, int n_valid, int b, int m_real,
+                        const double* vec, double thr, double margin, double* out, void* stream) {
+  if (s <= 0) return 0;
+  LEMO_ARG_CHECK(b > 0, "lemo_mlp_token_band: block size must be positive");
+  mlp_token_band_kernel<<<(s + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      partial, n_tiles, s, n_valid, b, (float)m_real, vec, thr, margin, out);
+  LEMO_CHECK_LAUNCH("lemo_mlp_token_band");
   return 0;
 }
 
-int lemo_mlp_patch(const float* partial, int n_tiles, int rows, const int* blocks, int b,
-                   int n_valid, int m_real, double* vec, void* stream) {
+int lemo_mlp_patch_rows(const float* partial, int n_tiles, int rows, const int* tok, int b,
+                        int m_real, double* vec, void* stream) {
   if (rows <= 0) return 0;
-  LEMO_ARG_CHECK(b <= 32 && (b & (b - 1)) == 0 && rows % b == 0,
-                 "lemo_mlp_patch: block size must be a power of two <= 32 dividing rows");
-  mlp_patch_kernel<<<(rows + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
-      partial, n_tiles, rows, blocks, b, n_valid, (float)m_real, vec);
-  LEMO_CHECK_LAUNCH("lemo_mlp_patch");
+  LEMO_ARG_CHECK(b > 0, "lemo_mlp_patch_rows: block size must be positive");
+  mlp_patch_rows_kernel<<<(rows + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      partial, n_tiles, rows, tok, b, (float)m_real, vec);
+  LEMO_CHECK_LAUNCH("lemo_mlp_patch_rows");
   return 0;
 }
 

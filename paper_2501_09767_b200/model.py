@@ -794,11 +794,14 @@ def _precision(layer: LayerState, precision):
 
 
 def mlp_block_score_vector(layer: LayerState, x: torch.Tensor, block_size: int, n_valid: int,
-                           *, keep_rows: bool = False, precision: str | None = None):
+                           *, keep_rows: bool = False, precision: str | None = None,
+                           with_partial: bool = False):
     """Exact MLP block scores (model.py:371-396): RMSNorm of every row, the
     tcgen05 gate/up GEMM with |silu(g)·u| row sums in its epilogue, then
     mean/max per block.  With keep_rows=True also returns (gu_all, inv_all)
-    so the sparse MLP can compact retained rows instead of recomputing.
+    so the sparse MLP can compact retained rows instead of recomputing;
+    with_partial=True appends the per-tile row partials [n_tiles, s] (the
+    token scores, for refine_mlp_block_scores).
 
     precision "fp32" (parity): fp32 RMSNorm, bf16x3 operands over K = 3h and
     scores from the fp32 accumulator -- the reference's f32 scores to ~1e-6."""
@@ -822,37 +825,47 @@ def mlp_block_score_vector(layer: LayerState, x: torch.Tensor, block_size: int, 
                         row_scale=inv_all)
         del xw_all
     vec = ops.mlp_block_scores(partial, s=s, n_valid=n_valid, b=block_size, m_real=layer.m)
-    if keep_rows:
-        return vec, (gu_all, inv_all)
-    return vec
+    out = (vec,) + (((gu_all, inv_all),) if keep_rows else ()) + ((partial,) if with_partial else ())
+    return out if len(out) > 1 else vec
 
 
-def refine_mlp_block_scores(layer: LayerState, x: torch.Tensor, vec: torch.Tensor, thr: float,
-                            block_size: int, n_valid: int, *, margin: float | None = None) -> int:
-    """Refined MLP scoring: every block whose (bf16) score lies within
-    margin·|thr| of the threshold is re-scored in the fp32-faithful parity
-    precision and patched into `vec` in place; returns the number of blocks
-    re-scored.  The bf16 score error is measured at ≤ 5.2e-4 relative at
-    Llama2-7B width (the bench's mask audit), so the default margin of 2e-3
-    leaves a 4× safety factor: blocks outside the margin cannot flip, blocks
-    inside are decided by parity-precision scores (tests/test_parity_gpu.py).
-    One extra host read-back (the number of candidates sizes the GEMM)."""
+def refine_mlp_block_scores(layer: LayerState, x: torch.Tensor, vec: torch.Tensor,
+                            partial: torch.Tensor, thr: float, block_size: int, n_valid: int, *,
+                            margin: float | None = None) -> int:
+    """Refined MLP scoring (decisions of sparsity.py:274-277 on the block max
+    of sparsity.py:298-305).  A block whose bf16 score lies within δ =
+    margin·|thr| of the threshold is ambiguous; of its rows only those whose
+    own bf16 token score is >= thr - δ can make max_t score_t >= thr (the
+    rest are below thr even after a δ-sized error), so only those rows are
+    re-scored in the fp32-faithful parity precision and the block's score in
+    `vec` is replaced, in place, by their maximum -- the parity-precision
+    decision.  `partial` is the bf16 scorer's per-tile row partials
+    ([n_tiles, s], mlp_block_score_vector(..., with_partial=True)).  Returns
+    the number of rows re-scored.
+
+    The bf16 score error is measured at ≤ 5.2e-4 relative at Llama2-7B width
+    (the bench's mask audit), so the default margin of 2e-3 leaves a 4×
+    safety factor (tests/test_parity_gpu.py).  For a still-dropped block the
+    patched value may differ from its full parity score (a non-re-scored row
+    may hold the maximum); both are below the threshold.  One extra host
+    read-back (the number of rows sizes the GEMM)."""
     margin = layer.refine_margin if margin is None else margin
     s = x.shape[0]
-    cand = sparsity.select_device(ops.margin_vec(vec, thr, margin * abs(thr)), 0.0,
-                                  block_size=block_size, n_tokens=s)[0]
+    band = ops.mlp_token_band(partial, vec, thr, margin * abs(thr), n_valid=n_valid,
+                              b=block_size, m_real=layer.m)
+    cand = sparsity.select_device(band, 0.0, block_size=1, n_tokens=s)[0]
     rows = cand.k
     if rows == 0:
         return 0
-    xnf = ops.rmsnorm_f32(x, layer.mlp_norm_w, cand.device_token_indices(x.device))
+    tok = cand.device_token_indices(x.device)
+    xnf = ops.rmsnorm_f32(x, layer.mlp_norm_w, tok)
     a = layer.split_input(xnf)
     del xnf
     N = layer.w_gu_t.shape[0]
-    partial = torch.empty(N // 128, rows, dtype=F32, device=x.device)
-    ops.gemm_gateup(a, layer.gateup_x3(), partial=partial, relu=layer.relu, exact_score=True)
-    ops.mlp_patch(partial, cand._dev_blocks, rows=rows, b=block_size, n_valid=n_valid,
-                  m_real=layer.m, vec=vec)
-    return rows // block_size
+    part = torch.empty(N // 128, rows, dtype=F32, device=x.device)
+    ops.gemm_gateup(a, layer.gateup_x3(), partial=part, relu=layer.relu, exact_score=True)
+    ops.mlp_patch_rows(part, tok, b=block_size, m_real=layer.m, vec=vec)
+    return rows
 
 
 def layer_qk(layer: LayerState, x: torch.Tensor, *, precision: str | None = None):
@@ -894,11 +907,11 @@ def layer_qk(layer: LayerState, x: torch.Tensor, *, precision: str | None = None
 
 class PatternSourceBase:
     """Interleaves scoring with the layer loop; records retained fractions
-    (and, in the refined precision, how many MLP blocks were re-scored)."""
+    (and, in the refined precision, how many MLP rows were re-scored)."""
 
     def __init__(self):
         self.last_fractions: dict = {}
-        self.refined_blocks: dict = {}
+        self.refined_rows: dict = {}
 
     def pattern(self, layer_id, component, x, n_valid):
         raise NotImplementedError
@@ -1002,12 +1015,14 @@ class PredictedPatternSource(PatternSourceBase):
         else:
             if not self.mlp_scoring:
                 return self._note(layer_id, component, None)
-            vec, rows = mlp_block_score_vector(layer, x, b, n_valid, keep_rows=True)
+            vec, rows, partial = mlp_block_score_vector(layer, x, b, n_valid, keep_rows=True,
+                                                        with_partial=True)
             self.model.stash_mlp_rows(layer_id, x, rows)
             thr = self.thresholds.get(layer_id, component)
             if layer.scoring_precision == "refined":
-                self.refined_blocks[layer_id] = refine_mlp_block_scores(layer, x, vec, thr, b,
-                                                                        n_valid)
+                self.refined_rows[layer_id] = refine_mlp_block_scores(layer, x, vec, partial, thr,
+                                                                      b, n_valid)
+            del partial
         if self.record:
             self.recorded_vectors.setdefault((layer_id, component), []).append(vec)
         force = (0,) if self.sink_first_block else ()
@@ -1059,13 +1074,15 @@ class ExactPatternSource(PatternSourceBase):
             if not self.mlp_scoring:
                 return self._note(layer_id, component, None)
             keep = self.thresholds is not None
-            res = mlp_block_score_vector(layer, x, b, n_valid, keep_rows=keep)
+            res = mlp_block_score_vector(layer, x, b, n_valid, keep_rows=keep, with_partial=keep)
             if keep:
-                vec, rows = res
+                vec, rows, partial = res
                 self.model.stash_mlp_rows(layer_id, x, rows)
                 if layer.scoring_precision == "refined":
-                    self.refined_blocks[layer_id] = refine_mlp_block_scores(
-                        layer, x, vec, self.thresholds.get(layer_id, component), b, n_valid)
+                    self.refined_rows[layer_id] = refine_mlp_block_scores(
+                        layer, x, vec, partial, self.thresholds.get(layer_id, component), b,
+                        n_valid)
+                del partial
             else:
                 vec = res
         if self.record:

@@ -135,6 +135,7 @@ def gemm_gateup(xn, w_gu_t, *, gu=None, inner=None, partial=None, relu=False, ex
     _check(xn, w_gu_t, gu, inner, partial, row_scale)
     if w_gu_t.shape[1] != K or w_gu_t.stride(0) != K:
         raise DimensionError(f"gate/up weight {tuple(w_gu_t.shape)} does not match K = {K}")
+    INSTRUMENT.note("lemo_gemm_gateup", (M, N, K, bool(exact_score)))
     call("lemo_gemm_gateup", ptr(xn), xn.stride(0), ptr(w_gu_t), M, N, K, ptr(gu), ptr(inner),
          ptr(partial), int(bool(relu)), int(bool(exact_score)), ptr(row_scale), _s())
 
@@ -498,18 +499,20 @@ def mlp_block_scores(partial, *, s, n_valid, b, m_real, out=None):
     return out
 
 
-def margin_vec(vec, thr, margin, out=None):
-    _check(vec, out)
+def mlp_token_band(partial, vec, thr, margin, *, n_valid, b, m_real, out=None):
+    _check(partial, vec, out)
     _dt(vec, F64, "scores")
-    out = torch.empty_like(vec) if out is None else out
-    call("lemo_margin_vec", ptr(vec), vec.numel(), float(thr), float(margin), ptr(out), _s())
+    s = partial.shape[1]
+    out = torch.empty(s, dtype=F64, device=partial.device) if out is None else out
+    call("lemo_mlp_token_band", ptr(partial), partial.shape[0], s, n_valid, b, m_real, ptr(vec),
+         float(thr), float(margin), ptr(out), _s())
     return out
 
 
-def mlp_patch(partial, blocks, *, rows, b, n_valid, m_real, vec):
-    _check(partial, blocks, vec)
-    call("lemo_mlp_patch", ptr(partial), partial.shape[0], rows, ptr(blocks), b, n_valid, m_real,
-         ptr(vec), _s())
+def mlp_patch_rows(partial, tok, *, b, m_real, vec):
+    _check(partial, tok, vec)
+    call("lemo_mlp_patch_rows", ptr(partial), partial.shape[0], partial.shape[1], ptr(tok), b,
+         m_real, ptr(vec), _s())
     return vec
 
 

@@ -124,9 +124,11 @@ def test_north_star_width_masks(cuda, s, weights):
         qq, kk = M.layer_qk(layer, xd, precision=prec)
         got[(prec, "exact")] = exact.exact_block_vector(qq, kk, B, n_heads=32, n_valid=n_valid)
         del qq, kk
-    # refined: bf16 scores, the blocks near the threshold re-scored in parity precision
-    v = M.mlp_block_score_vector(layer, xd, B, n_valid, precision="bf16")
-    n_ref = M.refine_mlp_block_scores(layer, xd, v, thr["mlp"], B, n_valid)
+    # refined: bf16 scores, the rows that can decide a near-threshold block re-scored
+    # in parity precision
+    v, part = M.mlp_block_score_vector(layer, xd, B, n_valid, precision="bf16", with_partial=True)
+    n_ref = M.refine_mlp_block_scores(layer, xd, v, part, thr["mlp"], B, n_valid)
+    del part
     got[("refined", "mlp")] = v
     # the predictor path is fp32-faithful in production already (bf16x3)
     got[("fp32", "predicted")] = got[("bf16", "predicted")] = P.predicted_block_vector(
@@ -134,7 +136,7 @@ def test_north_star_width_masks(cuda, s, weights):
     torch.cuda.synchronize()
 
     report = {"s": s, "weights": weights, "parity_terms": layer.parity_terms,
-              "n_blocks": len(ref["mlp"]), "refined_blocks": n_ref}
+              "n_blocks": len(ref["mlp"]), "refined_rows": n_ref}
     for (prec, mode), vec in got.items():
         g = vec.cpu().numpy()
         t_got = None
