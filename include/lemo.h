@@ -182,7 +182,8 @@ int lemo_lora_grads(const void* xg, const float* inv, const float* w, const floa
 
 /* Cross-entropy rows of segmented_loss_and_grad (kernels.py:256-273): per-row
  * loss terms and dlogits = (softmax - onehot)·inv_count (bf16); ignore rows
- * get zeros; out-of-range targets set *bad. */
+ * get zeros; an out-of-range target makes its row loss NaN (so the summed
+ * loss is NaN) and sets *bad when bad is non-NULL. */
 int lemo_ce_rows(const float* logits, int ldl, const int* targets, int n, int V, int ignore,
                  float inv_count, void* dlogits, int ldd, float* row_loss, int* bad,
                  void* stream);

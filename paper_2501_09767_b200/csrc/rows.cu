@@ -500,8 +500,12 @@ __global__ void __launch_bounds__(512) ce_rows_kernel(const float* __restrict__ 
     if (threadIdx.x == 0) row_loss[row] = 0.f;
     return;
   }
-  if (t < 0 || t >= V) {
-    if (threadIdx.x == 0) atomicOr(bad, 1);
+  if (t < 0 || t >= V) {  // (validated on the host first) the loss turns NaN, never silent
+    for (int c = threadIdx.x; c < V4; c += kT) d4[c] = make_uint2(0u, 0u);
+    if (threadIdx.x == 0) {
+      row_loss[row] = __int_as_float(0x7fc00000);
+      if (bad) atomicOr(bad, 1);
+    }
     return;
   }
   const float4* src = kSmem ? reinterpret_cast<const float4*>(srow) : l4;

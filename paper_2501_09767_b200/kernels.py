@@ -266,13 +266,12 @@ def segmented_loss_forward(hidden: torch.Tensor, lm_head_t: torch.Tensor, lm_hea
         raise ContractError("segmented loss: no valid targets")
     grad_hidden = torch.empty(n, h, dtype=F32, device=dev) if need_grad else None
     row_loss = torch.empty(n, dtype=F32, device=dev)
-    bad = torch.zeros(1, dtype=torch.int32, device=dev)
     inv_count = 1.0 / count
     for a, b in plan.segments:
         logits = ops.gemm_f32(hidden[a:b], lm_head_t)
         dlog = torch.empty(b - a, V, dtype=BF16, device=dev)
         ops.ce_rows(logits, targets_dev[a:b], V=V, ignore=ignore_index, inv_count=inv_count,
-                    dlogits=dlog, row_loss=row_loss[a:b], bad=bad)
+                    dlogits=dlog, row_loss=row_loss[a:b])
         del logits
         if need_grad:
             ops.gemm_f32(dlog, lm_head, out=grad_hidden[a:b])
@@ -328,12 +327,11 @@ def _segmented_loss(hidden, lm_head_t, lm_head, targets_dev, count, plan, ignore
     grad_hidden = torch.empty(n, h, dtype=F32, device=dev)
     grad_w = torch.zeros(h, V, dtype=F32, device=dev)
     row_loss = torch.empty(n, dtype=F32, device=dev)
-    bad = torch.zeros(1, dtype=torch.int32, device=dev)
     for a, b in plan.segments:
         logits = ops.gemm_f32(hidden[a:b], lm_head_t)
         dlog = torch.empty(b - a, V, dtype=BF16, device=dev)
         ops.ce_rows(logits, targets_dev[a:b], V=V, ignore=ignore_index, inv_count=1.0 / count,
-                    dlogits=dlog, row_loss=row_loss[a:b], bad=bad)
+                    dlogits=dlog, row_loss=row_loss[a:b])
         del logits
         ops.gemm_f32(dlog, lm_head, out=grad_hidden[a:b])
         # grad_W += hsegᵀ·dlogits: K = segment rows (zero-padded to a multiple of

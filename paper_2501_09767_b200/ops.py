@@ -339,7 +339,9 @@ def lora_grads(xg, inv, w, t, u, g0, g1, *, r, scale, dA, dB0, dB1):
          ptr(dA[:, r:]), ptr(dB1), ptr(ws), _s())
 
 
-def ce_rows(logits, targets, *, V, ignore, inv_count, dlogits, row_loss, bad):
+def ce_rows(logits, targets, *, V, ignore, inv_count, dlogits, row_loss, bad=None):
+    """Targets are validated on the host (check_targets); an out-of-range one
+    that reaches the kernel anyway makes the loss NaN (and sets `bad`)."""
     _check(logits, targets, dlogits, row_loss, bad)
     n = logits.shape[0]
     call("lemo_ce_rows", ptr(logits), logits.stride(0), ptr(targets), n, V, ignore,

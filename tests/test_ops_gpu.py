@@ -223,6 +223,56 @@ def test_parity_weights_keep_bf16_default(cuda):
     np.testing.assert_allclose(fp32.cpu().numpy(), z["mlp_vec"], rtol=1e-5)
 
 
+@pytest.mark.parametrize("margin", [2e-3, 5e-2])
+def test_refined_mlp_decisions_equal_parity(cuda, margin):
+    """Token-level refinement (refine_mlp_block_scores): bf16 block scores,
+    then only the rows that can decide a near-threshold block re-scored in the
+    parity precision -> the same >= decisions as the fp32 scorer at every
+    threshold tried; a wide margin (5e-2) re-scores many rows and must agree
+    too, and every re-scored block that is retained carries its fp32 score (its
+    maximum row is among the re-scored ones)."""
+    from paper_2501_09767_b200.model import refine_mlp_block_scores
+    cfg = ModelConfig(n_layers=1, hidden_dim=256, n_heads=2, vocab_size=64, max_seq_len=1024,
+                      block_size=16, mlp_dim=688, lora_rank=4, lora_alpha=8.0)
+    m = DecoderModel(cfg, 5, init="reference", parity_weights=True)
+    L = m.layers[0]
+    x = torch.randn(1024, 256, device="cuda")
+    nv = 1024 - 5
+    fp32 = mlp_block_score_vector(L, x, 16, nv, precision="fp32")
+    total = 0
+    for q in (0.3, 0.5, 0.7):
+        thr = float(torch.quantile(fp32, q))
+        vec, part = mlp_block_score_vector(L, x, 16, nv, precision="bf16", with_partial=True)
+        before = vec.clone()
+        rows = refine_mlp_block_scores(L, x, vec, part, thr, 16, nv, margin=margin)
+        total += rows
+        assert torch.equal(vec >= thr, fp32 >= thr), (q, margin, rows)
+        touched = (vec != before) & (vec >= thr)
+        np.testing.assert_allclose(vec[touched].cpu().numpy(), fp32[touched].cpu().numpy(),
+                                   rtol=2e-6)
+        # blocks outside the band are left as scored
+        far = (before - thr).abs() > margin * abs(thr)
+        assert torch.equal(vec[far], before[far])
+    assert total > 0
+
+
+def test_ce_rows_out_of_range_target_is_nan(cuda):
+    """A target that escapes host validation makes its row loss NaN (the
+    summed loss turns NaN) instead of being dropped silently."""
+    V = 64
+    logits = torch.randn(4, V, device="cuda")
+    tg = torch.tensor([3, -1, V + 5, 7], dtype=torch.int32, device="cuda")
+    dl = torch.empty(4, V, dtype=torch.bfloat16, device="cuda")
+    rl = torch.empty(4, dtype=torch.float32, device="cuda")
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ops.ce_rows(logits, tg, V=V, ignore=-1, inv_count=1.0, dlogits=dl, row_loss=rl, bad=bad)
+    r = rl.cpu()
+    assert torch.isfinite(r[[0, 3]]).all() and r[1] == 0 and torch.isnan(r[2])
+    assert int(bad) == 1 and not dl[2].float().abs().any()
+    ops.ce_rows(logits, tg, V=V, ignore=-1, inv_count=1.0, dlogits=dl, row_loss=rl)
+    assert torch.isnan(rl[2])
+
+
 def test_layer_qk_fp32_matches_reference(cuda):
     z = np.load(G / "scorers.npz")
     m = _scorer_model_fp32(3, mlp_dim=344, lora_rank=4, lora_alpha=8.0)
