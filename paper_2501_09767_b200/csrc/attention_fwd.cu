@@ -34,14 +34,6 @@
 // debug builds only (LEMO_EXTRA_NVCC_FLAGS=-DLEMO_FA_TRACE, scripts/fa_trace.py):
 // per-iteration timestamps of the heaviest CTA's softmax warpgroups
 __device__ unsigned long long g_fa_trace[2][4][64];  // [wg][event][iteration]
-// pair kernel, cluster 0 (the heaviest pair of head group 0): [CTA0, CTA1,
-// MMA][event][KV tile]; softmax: 0 S wait starts, 1 S ready, 2 P computed,
-// 3 P announced; MMA: 2 CTA0's P seen, 0 both P (and V) seen, 3 PV issued,
-// 1 next S issued
-__device__ unsigned long long g_fap_trace[3][4][128];
-__device__ unsigned long long g_fap_warp[2][4][2][128];  // [CTA][warp][P computed, announced][j]
-// CTA0, per warp: [0] S ready, [1] S in registers, [2] P stores issued, [3] P stores done
-__device__ unsigned long long g_fap_sub[4][4][128];
 #endif
 
 namespace lemo {
@@ -365,395 +357,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 }  // namespace faf
-
-// ---------------------------------------------------------------------------
-// CTA-pair forward (head_dim 128): a cluster of two CTAs = two adjacent
-// 128-query tiles (CTA r owns Q tile qt0 + r); the leader issues
-// cta_group::2 MMAs over both:
-//   S(j) = Q·K_jᵀ   M256 · N128 · K=D   B = K_j split by key rows: CTA r
-//                                        stages keys [64r, 64r+64) (8 KB boxes)
-//   O  += P(j)·V_j  M256 · N=D · K128   A = P from each CTA's own TMEM,
-//                                        B = V_j split by columns: CTA r stages
-//                                        d ∈ [64r, 64r+64) (one MN-major atom)
-// so each SM stages half of every K/V tile (the pair shares them, as the
-// single-CTA kernel's two query tiles do) and the tensor core reads half the
-// smem operand bytes of the single-CTA kernel (ncu tc smem wavefronts 22 % vs
-// 41 %).  With one query tile per SM the TMEM holds THREE S buffers
-// (S_0 | S_1 | S_2 | O = 512 columns): S(j+1), S(j+2) are computed while the
-// softmax works on S(j), so the softmax never waits for its own PV + S round
-// trip (the single-CTA kernel's per-tile chain E + PV + S + latency); the
-// tensor core runs  S(0) S(1) S(2) | PV(0) S(3) | PV(1) S(4) | …  (S(j+3)
-// reuses buffer j%3 after PV(j) read P(j) from it: tcgen05.mma executes in
-// issue order).
-// Softmax: 8 warps, two per SM sub-partition.  Warp w and w+4 own the same
-// 32 rows (TMEM lanes 32·(w%4)…) and split the 128 keys of a tile: warp
-// group g = w/4 takes columns [64g, 64g+64) and both exchange their row
-// maxima through shared memory (double-buffered, one 64-thread named barrier
-// per row group and tile), so every row's running max, scale and
-// correction are identical in both halves; the partial row sums are added
-// at the end.  (With one warp per sub-partition the warp that shares its
-// sub-partition with the MMA-issuing warp ran ~18 % slower than the other
-// three and set the pace: scripts/fap_trace.py.)
-// Warps: w0-w7 softmax, w8 TMA producer, w9 MMA issuer (leader) + TMEM
-// allocator.  Cross-CTA hand-offs: TMA bytes of both CTAs complete on the
-// leader's full barriers; S ready / stage free / PV done are multicast
-// commits; P ready is a remote arrive on the leader's p_full[rank] (each
-// CTA's softmax first waits for PV(j-1): its arrive for P(j+1) can then
-// never run two phases ahead of the leader's wait).
-namespace fap {
-
-#ifndef LEMO_FAP_POLY
-#define LEMO_FAP_POLY 0
-#endif
-constexpr int kPolyEvery = LEMO_FAP_POLY;  // every k-th exponential pair on the FMA pipe
-#ifndef LEMO_FAP_HALF
-#define LEMO_FAP_HALF 0
-#endif
-constexpr int kHalfEvery = LEMO_FAP_HALF;  // every k-th pair as one f16x2 SFU operation
-constexpr int kT = 128, D = 128;
-constexpr int kSBuf = 3;                  // S buffers in TMEM (+ O: 4 x 128 columns)
-constexpr int kBox = kT * 64 * 2;         // [128 x 64] bf16 SW128 box
-constexpr int kQTile = (D / 64) * kBox;   // 32 KB: this CTA's Q tile
-constexpr int kKHalf = (D / 64) * 8192;   // 16 KB: 64 key rows x D (boxes of 64 x 64)
-constexpr int kVHalf = kBox;              // 16 KB: 128 keys x 64 columns
-constexpr int kKStages = 4, kVStages = 4;
-constexpr int kThreads = 320;
-constexpr int kTmaWarp = 8, kMmaWarp = 9;
-constexpr int kXchg = 2 * 2 * kT * 4;     // row-max exchange [2 buffers][2 halves][128 rows]
-constexpr int kSmem = kQTile + kKStages * kKHalf + kVStages * kVHalf + kXchg + 256;
-constexpr float kLn2 = 0.6931471805599453f;
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    flash_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmQ,
-                          const __grid_constant__ CUtensorMap tmK64,
-                          const __grid_constant__ CUtensorMap tmV,
-                          const __grid_constant__ CUtensorMap tmO, float* __restrict__ lse, int n,
-                          int h, int group, float sl2) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = faf::aligned_smem(smem_raw);
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + kQTile;                 // [kKStages] key-row halves
-  uint8_t* sV = sK + kKStages * kKHalf;      // [kVStages] column halves
-  float* xchg = reinterpret_cast<float*>(sV + kVStages * kVHalf);  // [2][2][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * 2 * kT);
-  uint64_t* q_full = bars;                   // leader: both Q tiles landed
-  uint64_t* k_full = q_full + 1;             // [kKStages] leader
-  uint64_t* k_empty = k_full + kKStages;     // [kKStages] both (multicast commit)
-  uint64_t* v_full = k_empty + kKStages;     // [kVStages] leader
-  uint64_t* v_empty = v_full + kVStages;     // [kVStages] both
-  uint64_t* s_full = v_empty + kVStages;     // [kSBuf] both: S buffer b complete
-  uint64_t* p_full = s_full + kSBuf;         // [2] leader: P of CTA r written
-  uint64_t* pv_done = p_full + 2;            // both: PV(j) complete
-  uint64_t* o_done = pv_done + 1;            // both: last PV complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  const int nt = (n + kT - 1) / kT;
-  // cluster index -> (head, pair): heads in groups, heavy pairs first (as faf)
-  const int cid = (int)blockIdx.x >> 1;
-  const int heads = h / D, npairs = (int)(gridDim.x >> 1) / heads;
-  const int G = heads < LEMO_FA_HEAD_GROUP ? heads : LEMO_FA_HEAD_GROUP;
-  const int grp = cid / (npairs * G), gbase = grp * G;
-  const int gsz = min(G, heads - gbase), rem = cid - grp * npairs * G;
-  const int pair = npairs - 1 - rem / gsz;
-  const int hd = gbase + rem % gsz, c0 = hd * D;
-  const int ck = (hd / group) * D;
-  const int qt0 = 2 * pair;
-  const bool two = qt0 + 1 < nt;
-  const int T = two ? qt0 + 2 : qt0 + 1;  // KV tiles of the pair (Q0's last one is masked)
-  const int qt = qt0 + (int)rank;
-
-  if (warp == kTmaWarp && lane == 0) {
-    tma_prefetch_desc(&tmQ);
-    tma_prefetch_desc(&tmK64);
-    tma_prefetch_desc(&tmV);
-    mbar_init(q_full, 2);
-    for (int s = 0; s < kKStages; ++s) {
-      mbar_init(&k_full[s], 2);
-      mbar_init(&k_empty[s], 1);
-    }
-    for (int s = 0; s < kVStages; ++s) {
-      mbar_init(&v_full[s], 2);
-      mbar_init(&v_empty[s], 1);
-    }
-    for (int b = 0; b < kSBuf; ++b) mbar_init(&s_full[b], 1);
-    for (int b = 0; b < 2; ++b) mbar_init(&p_full[b], 8);
-    mbar_init(pv_done, 1);
-    mbar_init(o_done, 1);
-    fence_barrier_init();
-  }
-  if (warp == kMmaWarp) tmem_alloc_pair<512>(tmem_slot);
-  tc_fence_before();
-  cluster_sync();  // barriers of both CTAs initialised before any remote arrive / tx
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // S_b at 128·b (b < 3), O at 384
-
-  if (warp == kTmaWarp) {
-    if (lane == 0) {
-      const uint32_t q0 = mapa_shared(smem_u32(q_full), 0);
-      const uint32_t kf0 = mapa_shared(smem_u32(k_full), 0);
-      const uint32_t vf0 = mapa_shared(smem_u32(v_full), 0);
-      // Q tile qt (a missing second tile re-reads tile qt0: its rows are never stored)
-      if (leader) mbar_arrive_expect_tx(q_full, 2 * kQTile);
-      else mbar_arrive_cluster(q0);
-      const int qrow = (two ? qt : qt0) * kT;
-#pragma unroll
-      for (int b = 0; b < D / 64; ++b) tma_load_2d_pair(&tmQ, q0, sQ + b * kBox, c0 + 64 * b, qrow);
-      for (int j = 0; j < T; ++j) {
-        const int sk = j % kKStages, sv = j % kVStages;
-        mbar_wait(&k_empty[sk], ((j / kKStages) & 1) ^ 1);
-        if (leader) mbar_arrive_expect_tx(&k_full[sk], 2 * kKHalf);
-        else mbar_arrive_cluster(kf0 + sk * 8);
-#pragma unroll
-        for (int b = 0; b < D / 64; ++b)
-          tma_load_2d_pair(&tmK64, kf0 + sk * 8, sK + sk * kKHalf + b * 8192, ck + 64 * b,
-                           j * kT + 64 * (int)rank);
-        mbar_wait(&v_empty[sv], ((j / kVStages) & 1) ^ 1);
-        if (leader) mbar_arrive_expect_tx(&v_full[sv], 2 * kVHalf);
-        else mbar_arrive_cluster(vf0 + sv * 8);
-        tma_load_2d_pair(&tmV, vf0 + sv * 8, sV + sv * kVHalf, ck + 64 * (int)rank, j * kT);
-      }
-    }
-  } else if (warp == kMmaWarp) {
-    if (leader) {
-      constexpr uint32_t idesc_s = umma_idesc_bf16(2 * kT, kT, 0, 0);
-      constexpr uint32_t idesc_o = umma_idesc_bf16(2 * kT, D, 0, 1);
-      const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV);
-      auto issue_s = [&](int j) {
-        const int sk = j % kKStages;
-        mbar_wait_sleep(&k_full[sk], (j / kKStages) & 1);
-        tc_fence_after();
-        const uint64_t da = umma_desc_k_sw128(aQ), db = umma_desc_k_sw128(aK + sk * kKHalf);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          umma_bf16_ss_pair_w(tmem + 128 * (j % kSBuf),
-                              da + (((kk >> 2) * kBox + (kk & 3) * 32) >> 4),
-                              db + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4), idesc_s,
-                              kk > 0 ? 1u : 0u);
-        umma_commit_pair_w(&s_full[j % kSBuf]);
-        umma_commit_pair_w(&k_empty[sk]);
-      };
-      mbar_wait(q_full, 0);
-      for (int j = 0; j < kSBuf && j < T; ++j) issue_s(j);
-      for (int j = 0; j < T; ++j) {
-        const int sv = j % kVStages;
-        mbar_wait_sleep(&p_full[0], j & 1);
-#ifdef LEMO_FA_TRACE
-        if (cid == 0 && lane == 0 && j < 128) g_fap_trace[2][2][j] = clock64();
-#endif
-        mbar_wait_sleep(&p_full[1], j & 1);
-        mbar_wait_sleep(&v_full[sv], (j / kVStages) & 1);
-        tc_fence_after();
-#ifdef LEMO_FA_TRACE
-        if (cid == 0 && lane == 0 && j < 128) g_fap_trace[2][0][j] = clock64();
-#endif
-        const uint64_t db = umma_desc_mn_sw128(aV + sv * kVHalf, kVHalf);
-        const uint32_t pa = tmem + 128 * (j % kSBuf);
-#pragma unroll
-        for (int kk = 0; kk < kT / 16; ++kk)
-          umma_bf16_ts_pair_w(tmem + 384, pa + kk * 8, db + kk * (2048 >> 4), idesc_o,
-                              (j > 0 || kk > 0) ? 1u : 0u);
-        umma_commit_pair_w(&v_empty[sv]);
-        umma_commit_pair_w(pv_done);
-        if (j == T - 1) umma_commit_pair_w(o_done);
-#ifdef LEMO_FA_TRACE
-        if (cid == 0 && lane == 0 && j < 128) g_fap_trace[2][3][j] = clock64();
-#endif
-        if (j + kSBuf < T) issue_s(j + kSBuf);  // buffer j%3, after PV(j) read P(j) from it
-#ifdef LEMO_FA_TRACE
-        if (cid == 0 && lane == 0 && j < 128) g_fap_trace[2][1][j] = clock64();
-#endif
-      }
-    }
-  } else {
-    // softmax: warp w -> rows 32·(w%4)… (thread = query row), key half g = w/4
-    const int g = warp >> 2, wq = warp & 3;
-    const int r = wq * 32 + lane;
-    const int qr = qt * kT + r;
-    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    const uint32_t tO = tmem + 384 + lane_off + 64 * g;  // this half's O columns
-    const uint32_t pf = mapa_shared(smem_u32(&p_full[rank]), 0);
-    constexpr int kH = kT / 2;                           // keys per half
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < T; ++j) {
-      const uint32_t tS = tmem + 128 * (j % kSBuf) + lane_off;
-#ifdef LEMO_FA_TRACE
-      const bool trace = cid == 0 && r == 0 && g == 0 && j < 128;
-      if (trace) g_fap_trace[rank][0][j] = clock64();
-#endif
-      mbar_wait(&s_full[j % kSBuf], (j / kSBuf) & 1);
-      tc_fence_after();
-#ifdef LEMO_FA_TRACE
-      if (trace) g_fap_trace[rank][1][j] = clock64();
-      const bool sub = cid == 0 && rank == 0 && g == 0 && lane == 0 && j < 128;
-      if (sub) g_fap_sub[wq][0][j] = clock64();
-#endif
-      float s[kH];
-      {
-        uint32_t raw[kH];
-#pragma unroll
-        for (int c = 0; c < kH / 32; ++c)
-          tmem_ld_32x32b_x32(tS + kH * g + c * 32,
-                             *reinterpret_cast<uint32_t(*)[32]>(raw + c * 32));
-        tmem_ld_wait();
-#ifdef LEMO_FA_TRACE
-        if (sub) g_fap_sub[wq][1][j] = clock64();
-#endif
-#pragma unroll
-        for (int i = 0; i < kH; ++i) s[i] = __uint_as_float(raw[i]);
-      }
-      const int kv0 = j * kT + kH * g;
-      if (j >= qt || j * kT + kT > n) {  // diagonal, Q0's masked extra tile, ragged end
-#pragma unroll
-        for (int i = 0; i < kH; ++i)
-          if (kv0 + i > qr || kv0 + i >= n) s[i] = -INFINITY;
-      }
-      float mr[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) mr[t] = fmax3(s[t], s[8 + t], s[16 + t]);
-#pragma unroll
-      for (int i = 24; i + 16 <= kH; i += 16)
-#pragma unroll
-        for (int t = 0; t < 8; ++t) mr[t] = fmax3(mr[t], s[i + t], s[i + 8 + t]);
-#pragma unroll
-      for (int t = 0; t < 8; ++t) mr[t] = fmaxf(mr[t], s[kH - 8 + t]);
-      float mraw = fmax3(fmax3(mr[0], mr[1], mr[2]), fmax3(mr[3], mr[4], mr[5]),
-                         fmaxf(mr[6], mr[7]));
-      // row max of the whole tile: exchange with the partner warp (same rows,
-      // other key half).  After this barrier both have their S in registers,
-      // so P may be written over either half's S columns.
-      float* xb = xchg + (j & 1) * 2 * kT;
-      xb[g * kT + r] = mraw;
-      asm volatile("bar.sync %0, 64;" ::"r"(2 + wq) : "memory");
-      mraw = fmaxf(mraw, xb[(g ^ 1) * kT + r]);
-      const float mx = mraw * sl2;
-      const float m_new = (m == -INFINITY || mx > m + 8.f) ? fmaxf(mx, m) : m;
-      const float corr = (m == -INFINITY) ? 0.f : ex2_approx(m - m_new);
-      bool pv_seen = j == 0;
-      if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
-        mbar_wait(pv_done, (j - 1) & 1);  // O stable: PV(j-1) complete
-        tc_fence_after();
-        pv_seen = true;
-#pragma unroll 1
-        for (int c = 0; c < D / 64; ++c) {  // this half's 64 O columns
-          uint32_t raw[32];
-          tmem_ld_32x32b_x32(tO + c * 32, raw);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) raw[i] = __float_as_uint(__uint_as_float(raw[i]) * corr);
-          tmem_st_32x32b_x32(tO + c * 32, raw);
-        }
-      }
-      const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_new, -m_new);
-      float2 sm[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) sm[t] = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int c = 0; c < kH / 32; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float2 x = ffma2(make_float2(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]), sl2x2, negm);
-          if (kPolyEvery && i % kPolyEvery == kPolyEvery - 1) {  // share off the SFU
-            x.x = ex2_poly3(x.x);
-            x.y = ex2_poly3(x.y);
-          } else if (kHalfEvery && i % kHalfEvery == kHalfEvery - 1) {  // 2 per SFU op
-            x = ex2_f16x2(x);
-          } else {
-            x.x = ex2_approx(x.x);
-            x.y = ex2_approx(x.y);
-          }
-          sm[i & 3] = fadd2(sm[i & 3], x);
-          pk[i] = pack_bf16x2(x.x, x.y);
-        }
-        // P (bf16 pairs) of keys [64g + 32c, +32) -> packed column 32g + 16c
-        tmem_st_32x32b_x16(tS + (kH / 2) * g + 16 * c, pk);
-      }
-      const float sum = ((sm[0].x + sm[0].y) + (sm[1].x + sm[1].y)) +
-                        ((sm[2].x + sm[2].y) + (sm[3].x + sm[3].y));
-      l = l * corr + sum;
-      m = m_new;
-#ifdef LEMO_FA_TRACE
-      if (sub) g_fap_sub[wq][2][j] = clock64();
-#endif
-      // PV(j-1) done before P(j) is announced: the leader has consumed
-      // p_full phase j-1, so this arrive can never be two phases ahead
-      if (!pv_seen) mbar_wait(pv_done, (j - 1) & 1);
-      tmem_st_wait();
-#ifdef LEMO_FA_TRACE
-      if (sub) g_fap_sub[wq][3][j] = clock64();
-      if (trace) g_fap_trace[rank][2][j] = clock64();
-#endif
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(pf);
-#ifdef LEMO_FA_TRACE
-      if (trace) g_fap_trace[rank][3][j] = clock64();
-      if (cid == 0 && lane == 0 && g == 0 && j < 128) {
-        g_fap_warp[rank][wq][0][j] = g_fap_sub[wq][2][j];
-        g_fap_warp[rank][wq][1][j] = clock64();
-      }
-#endif
-    }
-    // the row sum of both halves (in the exchange buffer the last tile did
-    // not use: the partner may still be reading that one's maximum)
-    float* xl = xchg + (T & 1) * 2 * kT;
-    xl[g * kT + r] = l;
-    asm volatile("bar.sync %0, 64;" ::"r"(2 + wq) : "memory");
-    l += xl[(g ^ 1) * kT + r];
-    mbar_wait(o_done, 0);
-    tc_fence_after();
-    const float inv_l = 1.f / l;
-    // O = acc / l as bf16: this half's 64 columns staged as SW128 box g over
-    // this CTA's Q tile (every MMA reading it is complete), then one TMA store
-    uint8_t* box = sQ + g * kBox;
-#pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
-      uint32_t raw[32];
-      tmem_ld_32x32b_x32(tO + c * 32, raw);
-      tmem_ld_wait();
-      uint8_t* row = box + r * 128;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<uint4*>(row + (((c * 4 + q) ^ (r & 7)) << 4)) = make_uint4(
-            pack_bf16x2(__uint_as_float(raw[8 * q + 0]) * inv_l, __uint_as_float(raw[8 * q + 1]) * inv_l),
-            pack_bf16x2(__uint_as_float(raw[8 * q + 2]) * inv_l, __uint_as_float(raw[8 * q + 3]) * inv_l),
-            pack_bf16x2(__uint_as_float(raw[8 * q + 4]) * inv_l, __uint_as_float(raw[8 * q + 5]) * inv_l),
-            pack_bf16x2(__uint_as_float(raw[8 * q + 6]) * inv_l, __uint_as_float(raw[8 * q + 7]) * inv_l));
-    }
-    fence_proxy_async_smem();
-    asm volatile("bar.sync %0, 128;" ::"r"(6 + g) : "memory");
-    if (r == 0 && (two || rank == 0)) {
-      tma_store_2d(&tmO, box, c0 + 64 * g, qt * kT);
-      tma_store_commit_and_wait_read();
-    }
-    if (g == 0 && qr < n) lse[(size_t)hd * n + qr] = (m + log2f(l)) * kLn2;
-  }
-  tc_fence_before();
-  cluster_sync();
-  if (warp == kMmaWarp) {
-    tc_fence_after();
-    tmem_dealloc_pair<512>(tmem);
-  }
-}
-
-}  // namespace fap
 }  // namespace lemo
 
 #ifdef LEMO_FA_TRACE
 extern "C" int lemo_fa_trace_get(void* host) {
   return (int)cudaMemcpyFromSymbol(host, g_fa_trace, sizeof(g_fa_trace));
-}
-extern "C" int lemo_fap_trace_get(void* host) {
-  return (int)cudaMemcpyFromSymbol(host, g_fap_trace, sizeof(g_fap_trace));
-}
-extern "C" int lemo_fap_sub_get(void* host) {
-  return (int)cudaMemcpyFromSymbol(host, g_fap_sub, sizeof(g_fap_sub));
-}
-extern "C" int lemo_fap_warp_get(void* host) {
-  return (int)cudaMemcpyFromSymbol(host, g_fap_warp, sizeof(g_fap_warp));
 }
 #endif
 
@@ -778,24 +386,7 @@ int lemo_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, floa
   dim3 grid((h / head_dim) * ((nt + 1) / 2));
   cudaStream_t st = (cudaStream_t)stream;
   const float sl2 = scale * faf::kLog2e;
-#ifndef LEMO_FA_PAIR
-#define LEMO_FA_PAIR 1
-#endif
-  if (head_dim == 128 && LEMO_FA_PAIR) {
-    CUtensorMap tk64;  // K in 64-row boxes: each CTA of a pair stages half a key tile
-    rc = make_tma_bf16_2d(&tk64, k, (uint64_t)n, (uint64_t)kv, (uint64_t)kv, 64);
-    if (rc) LEMO_RETURN_RC("lemo_flash_fwd_tc", rc);
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(fap::flash_fwd_pair_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, fap::kSmem);
-      if (e != cudaSuccess) LEMO_RETURN_RC("lemo_flash_fwd_tc", (int)e);
-      attr = true;
-    }
-    dim3 grid2(2 * (h / head_dim) * ((nt + 1) / 2));
-    fap::flash_fwd_pair_kernel<<<grid2, fap::kThreads, fap::kSmem, st>>>(tq, tk64, tv, to, lse, n,
-                                                                          h, h / kv, sl2);
-  } else if (head_dim == 128) {
+  if (head_dim == 128) {
     static bool attr = false;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(faf::flash_fwd_kernel<128>,

@@ -77,21 +77,6 @@ __device__ __forceinline__ float ex2_poly3(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
-// Two 2^x at once on the SFU in half precision (MUFU.EX2 .f16x2: one SFU
-// operation for two values).  Inputs <= 0 (softmax); the f16 rounding of the
-// input costs <= 2^-11·|x| in the exponent, below the bf16 rounding of P for
-// the values that matter (|x| < 8); results under 2^-24 flush to 0.
-__device__ __forceinline__ float2 ex2_f16x2(float2 x) {
-  uint32_t h, r;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x.y), "f"(x.x));
-  asm("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(h));
-  float2 o;
-  asm("{\n\t.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
-      "cvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;\n\t}"
-      : "=f"(o.x), "=f"(o.y) : "r"(r));
-  return o;
-}
-
 // Three-input max (FMNMX3, sm_100).
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;
@@ -179,12 +164,6 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
-}
-
-// Waiting with back-off: for a warp that shares its SM sub-partition with
-// latency-critical warps (a spinning try_wait loop takes their issue slots).
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) __nanosleep(64);
 }
 
 // ---------------------------------------------------------------------------
@@ -449,18 +428,6 @@ __device__ __forceinline__ void umma_bf16_ss_pair_w(uint32_t tmem_d, uint64_t de
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate));
-}
-
-// pair MMA with A read from each CTA's own TMEM (lanes = that CTA's 128 rows)
-__device__ __forceinline__ void umma_bf16_ts_pair_w(uint32_t tmem_d, uint32_t tmem_a,
-                                                    uint64_t desc_b, uint32_t idesc,
-                                                    uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(desc_b), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void umma_commit_pair_w(uint64_t* bar) {
