@@ -9,8 +9,9 @@ patterns (random predictors r1=r2=d_p=1024, attention retention 0.5 by the
 quantile rule re-derived every 50 calls, MLP thresholds = pooled mean of a
 profiling pass), one 16,384-token synthetic sequence per GPU per step,
 random-init weights (bf16 GEMM operands, fp32 residual/LoRA/Adam), scorers in
-the "refined" precision (the reference's masks: bf16 scores, MLP blocks near
-their threshold re-scored fp32-faithfully; `--scoring-precision bf16|fp32`).  A step
+the "refined" precision (the reference's masks: bf16 scores, then the token
+rows that can decide an MLP block near its threshold re-scored fp32-faithfully;
+`--scoring-precision bf16|fp32`).  A step
 = forward_step + sparse backward + (N>1: NCCL all-reduce of LoRA grads) +
 Adam.  N>1: one process per GPU under torchrun, each rank its own sequence
 (weak scaling); time = max over ranks of CUDA-event time.
@@ -76,7 +77,7 @@ def parse():
     ap.add_argument("--scoring-precision", default="refined", choices=["bf16", "fp32", "refined"],
                     help="precision of the scorers in the timed step: bf16 (production), fp32 "
                          "(the mask-exact parity precision) or refined (bf16 + parity re-scoring "
-                         "of the MLP blocks near their threshold)")
+                         "of the token rows that decide MLP blocks near their threshold)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N>1 (gloo only to smoke-test several "
                          "ranks sharing one GPU)")
@@ -329,7 +330,7 @@ def main():
     torch.manual_seed(0)
     # parity_weights keeps the bf16 residuals of the scoring weights (parity
     # precision for the refined scorers and the untimed mask audit).  Default:
-    # the "refined" precision -- bf16 scorers with the MLP blocks near their
+    # the "refined" precision -- bf16 scorers, then the token rows that can decide
     # threshold re-scored in parity precision, i.e. the reference's masks; the
     # plain bf16 scorers are timed as well (`bf16_scoring`)
     model = M.DecoderModel(cfg, seed=0, device=dev, init="torch",

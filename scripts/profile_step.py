@@ -22,10 +22,12 @@ from paper_2501_09767_b200 import model as M, predictor as P, sparsity as S  # n
 from paper_2501_09767_b200.optim import Adam  # noqa: E402
 
 
-def setup(seq=16384, mode="lemo"):
+def setup(seq=16384, mode="lemo", precision="refined"):
     dev = torch.device("cuda")
     cfg = M.llama2_7b(max_seq_len=seq)
-    model = M.DecoderModel(cfg, seed=0, device=dev, init="torch")
+    # the bench's default: refined scorers (bf16 + parity re-scoring near the threshold)
+    model = M.DecoderModel(cfg, seed=0, device=dev, init="torch", scoring_precision=precision,
+                           parity_weights=precision != "bf16")
     h = cfg.hidden_dim
     rp = h // 4
     gen = torch.Generator(device=dev)
@@ -70,8 +72,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seq", type=int, default=16384)
     ap.add_argument("--mode", default="lemo", choices=["lemo", "dense"])
+    ap.add_argument("--scoring-precision", default="refined", choices=["bf16", "fp32", "refined"])
     args = ap.parse_args()
-    model, src, tokens = setup(args.seq, args.mode)
+    model, src, tokens = setup(args.seq, args.mode, args.scoring_precision)
     opt = Adam(model.lora_param, lr=1e-4)
     batch = model.stage_tokens(tokens)
 
