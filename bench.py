@@ -331,7 +331,7 @@ def main():
     # parity_weights keeps the bf16 residuals of the scoring weights (parity
     # precision for the refined scorers and the untimed mask audit).  Default:
     # the "refined" precision -- bf16 scorers, then the token rows that can decide
-    # threshold re-scored in parity precision, i.e. the reference's masks; the
+    # an MLP block near its threshold re-scored in parity precision, i.e. the reference's masks; the
     # plain bf16 scorers are timed as well (`bf16_scoring`)
     model = M.DecoderModel(cfg, seed=0, device=dev, init="torch",
                            scoring_precision=args.scoring_precision,
