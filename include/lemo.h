@@ -218,6 +218,15 @@ int lemo_gemm_split3(const void* A, int lda, const void* B, int ldb, int M, int 
                      int relu, const unsigned char* mask, int pattern, void* out, int ldo,
                      float* f32, int ldf, void* stream);
 
+/* Two predictors' first layers (predictor.py:83-85) over the same input in
+ * one GEMM: B' stacks both weight operands along N (rows [0, nsplit) = the
+ * query predictor's, [nsplit, N) = the key predictor's), mask covers all N
+ * columns; act = relu if relu.  Columns < nsplit are written in split form
+ * (pattern 0) to out [M, 3·nsplit], the rest to out2 [M, 3·(N - nsplit)]. */
+int lemo_gemm_split3_dual(const void* A, int lda, const void* B, int ldb, int M, int N, int K3,
+                          int nsplit, int relu, const unsigned char* mask, void* out, int ldo,
+                          void* out2, int ldo2, void* stream);
+
 /* vec[n] = Σ_{m>=n} max(S[m,n], 0) in float64, ascending m
  * (model.py:575-578 + sparsity.py:253-260). */
 int lemo_colsum_clamped(const float* S, int lds, int nb, double* vec, void* stream);

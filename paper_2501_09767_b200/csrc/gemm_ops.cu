@@ -336,6 +336,11 @@ struct EpiSplit3 {
   float* f32;  // [M, N] (or null)
   int ldf, N, pattern, relu;
   const unsigned char* mask;
+  // dual output (nsplit > 0, a multiple of 32): columns >= nsplit belong to a
+  // second product stacked along N (the key predictor's first layer next to
+  // the query predictor's) and go to out2 [M, 3(N - nsplit)] instead
+  __nv_bfloat16* out2 = nullptr;
+  int ldo2 = 0, nsplit = 0;
   template <int BN>
   __device__ void run(int row, bool valid, int col0, uint32_t taddr, int part) const {
 #pragma unroll 1
@@ -343,6 +348,10 @@ struct EpiSplit3 {
       float v[32];
       load_chunk(taddr + c, v);
       if (!valid || col0 + c >= N) continue;
+      const bool second = nsplit > 0 && col0 + c >= nsplit;
+      __nv_bfloat16* const base = second ? out2 : out;
+      const int Nb = second ? N - nsplit : (nsplit > 0 ? nsplit : N);
+      const int ldb = second ? ldo2 : ldo, cb = second ? col0 + c - nsplit : col0 + c;
       float hi[32], lo[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
@@ -354,19 +363,19 @@ struct EpiSplit3 {
         lo[i] = x - hi[i];
       }
       const int n = min(32, N - col0 - c);
-      if (out) {
-        __nv_bfloat16* o = out + (size_t)row * ldo + col0 + c;
-        if (n == 32 && (ldo & 7) == 0 && (N & 7) == 0) {
+      if (base) {
+        __nv_bfloat16* o = base + (size_t)row * ldb + cb;
+        if (n == 32 && (ldb & 7) == 0 && (Nb & 7) == 0) {
           store_bf16x32(o, hi);
-          store_bf16x32(o + N, pattern ? lo : hi);
-          store_bf16x32(o + 2 * N, pattern ? hi : lo);
+          store_bf16x32(o + Nb, pattern ? lo : hi);
+          store_bf16x32(o + 2 * Nb, pattern ? hi : lo);
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             if (i < n) {
               o[i] = __float2bfloat16_rn(hi[i]);
-              o[N + i] = __float2bfloat16_rn(pattern ? lo[i] : hi[i]);
-              o[2 * N + i] = __float2bfloat16_rn(pattern ? hi[i] : lo[i]);
+              o[Nb + i] = __float2bfloat16_rn(pattern ? lo[i] : hi[i]);
+              o[2 * Nb + i] = __float2bfloat16_rn(pattern ? hi[i] : lo[i]);
             }
           }
         }
@@ -548,6 +557,23 @@ int lemo_gemm_split3(const void* A, int lda, const void* B, int ldb, int M, int 
   const int rc = pick_bn(M, N) == 64 ? gemm_promoted<64>(A, lda, B, ldb, M, N, K3, e, st)
                                      : gemm_promoted<128>(A, lda, B, ldb, M, N, K3, e, st);
   LEMO_RETURN_RC("lemo_gemm_split3", rc);
+}
+
+int lemo_gemm_split3_dual(const void* A, int lda, const void* B, int ldb, int M, int N, int K3,
+                          int nsplit, int relu, const unsigned char* mask, void* out, int ldo,
+                          void* out2, int ldo2, void* stream) {
+  LEMO_ARG_CHECK(K3 % 3 == 0, "lemo_gemm_split3_dual: K' must be 3K");
+  LEMO_ARG_CHECK(nsplit > 0 && nsplit < N && nsplit % 32 == 0,
+                 "lemo_gemm_split3_dual: 0 < nsplit < N, nsplit % 32 == 0");
+  EpiSplit3 e{reinterpret_cast<__nv_bfloat16*>(out), ldo, nullptr, 0, N, 0, relu, mask,
+              reinterpret_cast<__nv_bfloat16*>(out2), ldo2, nsplit};
+  // both first layers in one GEMM over the shared input: 256 x 256 CTA-pair
+  // tiles read the [M, 3h] input and the stacked weights 4x / 2x less often
+  // from L2 than two BN = 64 launches (the predictor GEMMs are L2-bound)
+  cudaStream_t st = (cudaStream_t)stream;
+  const int rc = use_pair(M) ? gemm_promoted<256>(A, lda, B, ldb, M, N, K3, e, st)
+                             : gemm_promoted<128>(A, lda, B, ldb, M, N, K3, e, st);
+  LEMO_RETURN_RC("lemo_gemm_split3_dual", rc);
 }
 
 int lemo_gemm_dgateup(const void* dy, const void* w_down, int M, int m_pad, int h, const void* gu,

@@ -459,6 +459,22 @@ def gemm_split3(a3, b3, *, relu=False, mask=None, pattern=0, split_out=True, f32
     return out, f32
 
 
+def gemm_split3_dual(a3, b3, nsplit, *, relu=False, mask=None):
+    """Two predictor layers over the same bf16x3 input in one GEMM (weights
+    stacked along N): returns the split forms (pattern 0) of columns
+    [0, nsplit) and [nsplit, N)."""
+    _check(a3, b3, mask)
+    M, K3 = a3.shape
+    N = b3.shape[0]
+    if b3.shape[1] != K3:
+        raise DimensionError(f"bf16x3 inner extents differ: {tuple(a3.shape)} vs {tuple(b3.shape)}")
+    out = torch.empty(M, 3 * nsplit, dtype=BF16, device=a3.device)
+    out2 = torch.empty(M, 3 * (N - nsplit), dtype=BF16, device=a3.device)
+    call("lemo_gemm_split3_dual", ptr(a3), a3.stride(0), ptr(b3), b3.stride(0), M, N, K3, nsplit,
+         int(bool(relu)), ptr(mask), ptr(out), out.stride(0), ptr(out2), out2.stride(0), _s())
+    return out, out2
+
+
 def colsum_clamped(S, out=None):
     _check(S)
     nb = S.shape[0]

@@ -59,10 +59,12 @@ class Predictor:
             self._split = (key, ws)
         return self._split[1]
 
-    def hidden3(self, x3: torch.Tensor) -> torch.Tensor:
-        """relu/mask hidden layers on a bf16x3 input; returns split h2 [M, 3 r2]."""
+    def hidden3(self, x3: torch.Tensor, h1: torch.Tensor | None = None) -> torch.Tensor:
+        """relu/mask hidden layers on a bf16x3 input; returns split h2 [M, 3 r2].
+        h1: the first layer's split output when already computed (pair_hidden1)."""
         w1, w2, _ = self._weights3()
-        h1, _ = ops.gemm_split3(x3, w1, relu=True, mask=self.mask1, pattern=0)
+        if h1 is None:
+            h1, _ = ops.gemm_split3(x3, w1, relu=True, mask=self.mask1, pattern=0)
         h2, _ = ops.gemm_split3(h1, w2, relu=True, mask=self.mask2, pattern=0)
         return h2
 
@@ -99,9 +101,9 @@ class Predictor:
         _, out = ops.gemm_split3(h2, self._weights3()[2], split_out=False, f32_out=True)
         return out
 
-    def predict3(self, x3: torch.Tensor, pattern: int) -> torch.Tensor:
+    def predict3(self, x3: torch.Tensor, pattern: int, h1: torch.Tensor | None = None) -> torch.Tensor:
         """Predictor output in split form (pattern 0: A-side, 1: B-side of Eq. 3)."""
-        h2 = self.hidden3(x3)
+        h2 = self.hidden3(x3, h1)
         out, _ = ops.gemm_split3(h2, self._weights3()[2], pattern=pattern)
         return out
 
@@ -206,15 +208,32 @@ def pair_block_outputs(p_q: Predictor, p_k: Predictor, x, block_size: int, pooli
     raise ContractError(f"unknown pooling mode {pooling!r}")
 
 
+def pair_hidden1(p_q: Predictor, p_k: Predictor, x3: torch.Tensor):
+    """Both predictors' first layers (predictor.py:83-85) on the shared block
+    embedding as ONE bf16x3 GEMM: W1_q and W1_k stacked along N (cached while
+    neither weight changes), both masks side by side.  Returns the split
+    first-layer outputs (h1_q, h1_k)."""
+    wq, wk = p_q._weights3()[0], p_k._weights3()[0]
+    cache = getattr(p_q, "_stack1", None)  # (W1_q operand, W1_k operand, stacked): the
+    if cache is None or cache[0] is not wq or cache[1] is not wk:  # operands are rebuilt
+        cache = p_q._stack1 = (wq, wk, torch.cat([wq, wk], dim=0))  # when weights change
+    mask = torch.cat([p_q.mask1, p_k.mask1])
+    return ops.gemm_split3_dual(x3, cache[2], wq.shape[0], relu=True, mask=mask)
+
+
 def predicted_dense(p_q, p_k, x, block_size: int, pooling: str = "mean") -> torch.Tensor:
     """Dense eq·ekᵀ [nb, nb] fp32 (unclamped), every product on tcgen05 in
-    fp32-faithful bf16x3 form.  mean pooling: block_embed → split → 2×3
-    predictor GEMMs → Eq. 3 GEMM, no fp32 round trip between them."""
+    fp32-faithful bf16x3 form.  mean pooling: block_embed → split → both first
+    layers in one GEMM → 2×2 predictor GEMMs → Eq. 3 GEMM, no fp32 round trip
+    between them."""
     if pooling == "mean":
         xb = block_embed(x, block_size)
         x3 = ops.split_bf16x3(xb, 0)
-        eq3 = p_q.predict3(x3, 0)
-        ek3 = p_k.predict3(x3, 1)
+        h1q = h1k = None
+        if p_q.w1.shape == p_k.w1.shape and p_q.w1.shape[1] % 32 == 0:
+            h1q, h1k = pair_hidden1(p_q, p_k, x3)
+        eq3 = p_q.predict3(x3, 0, h1q)
+        ek3 = p_k.predict3(x3, 1, h1k)
     else:
         eq, ek = pair_block_outputs(p_q, p_k, x, block_size, pooling)
         eq3, ek3 = ops.split_bf16x3(eq, 0), ops.split_bf16x3(ek, 1)

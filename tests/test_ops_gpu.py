@@ -147,6 +147,33 @@ def _scorer_model(seed, **kw):
     return DecoderModel(cfg, seed, init="reference"), om
 
 
+@pytest.mark.parametrize("nb,h,r", [(96, 256, 64), (1024, 512, 256)])
+def test_pair_first_layer_equals_separate(cuda, nb, h, r):
+    """Both predictors' first layers as one stacked bf16x3 GEMM (CTA-pair
+    tiles when nb spans two row tiles) == the two separate layer GEMMs, with
+    distinct masks; and the predicted block vector through it matches the
+    per-predictor path."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    mk = lambda: P.Predictor(*(torch.randn(a, b, generator=g, device="cuda") / math.sqrt(a)  # noqa
+                               for a, b in ((h, r), (r, r), (r, r))))
+    pq, pk = mk(), mk()
+    pq.set_masks(np.arange(r) % 7 != 3, np.ones(r, bool))
+    pk.set_masks(np.arange(r) % 5 != 1, np.ones(r, bool))
+    x3 = ops.split_bf16x3(torch.randn(nb, h, device="cuda"), 0)
+    hq, hk = P.pair_hidden1(pq, pk, x3)
+    sq, _ = ops.gemm_split3(x3, pq._weights3()[0], relu=True, mask=pq.mask1, pattern=0)
+    sk, _ = ops.gemm_split3(x3, pk._weights3()[0], relu=True, mask=pk.mask1, pattern=0)
+    for got, ref in ((hq, sq), (hk, sk)):
+        a = got[:, :r].float() + got[:, 2 * r:].float()
+        b = ref[:, :r].float() + ref[:, 2 * r:].float()
+        torch.testing.assert_close(a, b, rtol=2e-6, atol=2e-6 * float(b.abs().max()))
+    x = torch.randn(nb * 16, h, device="cuda")
+    v = P.predicted_block_vector(pq, pk, x, 16)
+    xb3 = ops.split_bf16x3(P.block_embed(x, 16), 0)
+    ref = ops.colsum_clamped(ops.gemm_f32_exact(pq.predict3(xb3, 0), pk.predict3(xb3, 1)))
+    torch.testing.assert_close(v, ref, rtol=1e-5, atol=1e-5 * float(ref.abs().max()))
+
+
 def test_mlp_scores_golden(cuda):
     z = np.load(G / "scorers.npz")
     m, _ = _scorer_model(3, mlp_dim=344, lora_rank=4, lora_alpha=8.0)
