@@ -849,6 +849,8 @@ def refine_mlp_block_scores(layer: LayerState, x: torch.Tensor, vec: torch.Tenso
     patched value may differ from its full parity score (a non-re-scored row
     may hold the maximum); both are below the threshold.  One extra host
     read-back (the number of rows sizes the GEMM)."""
+    if not math.isfinite(thr):  # -inf retains every block, +inf none: nothing is ambiguous
+        return 0
     margin = layer.refine_margin if margin is None else margin
     s = x.shape[0]
     band = ops.mlp_token_band(partial, vec, thr, margin * abs(thr), n_valid=n_valid,

@@ -281,6 +281,11 @@ def test_refined_mlp_decisions_equal_parity(cuda, margin):
         far = (before - thr).abs() > margin * abs(thr)
         assert torch.equal(vec[far], before[far])
     assert total > 0
+    for thr in (float("-inf"), float("inf")):  # nothing ambiguous: no rows, scores untouched
+        vec, part = mlp_block_score_vector(L, x, 16, nv, precision="bf16", with_partial=True)
+        before = vec.clone()
+        assert refine_mlp_block_scores(L, x, vec, part, thr, 16, nv, margin=margin) == 0
+        assert torch.equal(vec, before)
 
 
 def test_ce_rows_out_of_range_target_is_nan(cuda):
