@@ -67,6 +67,10 @@ constexpr float kLog2e = 1.4426950408889634f;
 #define LEMO_FAB_POLY 0
 #endif
 constexpr int kPolyEvery = LEMO_FAB_POLY;  // every k-th exponential on the FMA pipe (0 = none)
+#ifndef LEMO_FABQ_POLY
+#define LEMO_FABQ_POLY 0
+#endif
+constexpr int kPolyQ = LEMO_FABQ_POLY;  // the same for the dQ kernel's recomputed P
 
 // D (+)= A·Bᵀ with A, B [128 x HD] K-major tiles (HD/64 16 KB boxes each).
 // Warp-collective (the MMA warp stays converged; one elected lane issues).
@@ -641,7 +645,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_32x32b_x32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
         tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < 64; ++c) p[c] = ex2_approx(fmaf(__uint_as_float(raw[c]), sl2, -lse2));
+        for (int c = 0; c < 64; ++c)
+          p[c] = (kPolyQ && c % kPolyQ == kPolyQ - 1)  // share of 2^x off the SFU
+                     ? ex2_poly3(fmaf(__uint_as_float(raw[c]), sl2, -lse2))
+                     : ex2_approx(fmaf(__uint_as_float(raw[c]), sl2, -lse2));
       }
       if (edge) {
 #pragma unroll

@@ -116,21 +116,27 @@ __global__ void mlp_token_band_kernel(const float* __restrict__ partial, int n_t
 }
 
 // vec[tok[i] / b] = max over the re-scored rows of that block (rows ascending,
-// so a block's rows are contiguous; the first row of each run reduces it).
+// so a block's rows are contiguous).  One warp per compact row i; the warp of
+// a block's first row reduces the block: lane l sums row i + l (the tile
+// order of mlp_block_scores) and the maximum is a warp shuffle (b <= 32).
 __global__ void mlp_patch_rows_kernel(const float* __restrict__ partial, int n_tiles, int rows,
                                       const int* __restrict__ tok, int b, float m_real,
                                       double* __restrict__ vec) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (i >= rows) return;
   const int blk = __ldg(tok + i) / b;
-  if (i > 0 && __ldg(tok + i - 1) / b == blk) return;
+  if (i > 0 && __ldg(tok + i - 1) / b == blk) return;  // warp-uniform
+  const int j = i + lane;
   float best = -INFINITY;
-  for (int j = i; j < rows && __ldg(tok + j) / b == blk; ++j) {
+  if (j < rows && __ldg(tok + j) / b == blk) {
     float acc = 0.f;
+#pragma unroll 8
     for (int t = 0; t < n_tiles; ++t) acc += partial[(size_t)t * rows + j];
-    best = fmaxf(best, acc / m_real);
+    best = acc / m_real;
   }
-  vec[blk] = (double)best;
+  for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if (lane == 0) vec[blk] = (double)best;
 }
 
 // Row-major packed lower triangle of a dense [nb, nb] fp32 matrix (element
@@ -384,8 +390,8 @@ int lemo_mlp_token_band(const float* partial, int n_tiles, int s, int n_valid, i
 int lemo_mlp_patch_rows(const float* partial, int n_tiles, int rows, const int* tok, int b,
                         int m_real, double* vec, void* stream) {
   if (rows <= 0) return 0;
-  LEMO_ARG_CHECK(b > 0, "lemo_mlp_patch_rows: block size must be positive");
-  mlp_patch_rows_kernel<<<(rows + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+  LEMO_ARG_CHECK(b > 0 && b <= 32, "lemo_mlp_patch_rows: block size must be in [1, 32]");
+  mlp_patch_rows_kernel<<<(unsigned)((rows * 32LL + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       partial, n_tiles, rows, tok, b, (float)m_real, vec);
   LEMO_CHECK_LAUNCH("lemo_mlp_patch_rows");
   return 0;
