@@ -214,9 +214,17 @@ def pair_hidden1(p_q: Predictor, p_k: Predictor, x3: torch.Tensor):
     neither weight changes), both masks side by side.  Returns the split
     first-layer outputs (h1_q, h1_k)."""
     wq, wk = p_q._weights3()[0], p_k._weights3()[0]
-    cache = getattr(p_q, "_stack1", None)  # (W1_q operand, W1_k operand, stacked): the
-    if cache is None or cache[0] is not wq or cache[1] is not wk:  # operands are rebuilt
-        cache = p_q._stack1 = (wq, wk, torch.cat([wq, wk], dim=0))  # when weights change
+    cache = getattr(p_q, "_stack1", None)  # (W1_q operand, W1_k operand, stacked)
+    if cache is None or cache[0] is not wq or cache[1] is not wk:
+        # the operands are rebuilt whenever the weights change; once stacked, each
+        # predictor's own W1 operand becomes a view into the stack (no second copy)
+        r = wq.shape[0]
+        stack = torch.cat([wq, wk], dim=0)
+        vq, vk = stack[:r], stack[r:]
+        for p, v in ((p_q, vq), (p_k, vk)):
+            key, ws = p._split
+            p._split = (key, (v,) + tuple(ws[1:]))
+        cache = p_q._stack1 = (vq, vk, stack)
     mask = torch.cat([p_q.mask1, p_k.mask1])
     return ops.gemm_split3_dual(x3, cache[2], wq.shape[0], relu=True, mask=mask)
 
