@@ -169,3 +169,39 @@ def test_north_star_width_masks(cuda, s, weights):
             assert r["score_rel_err"] <= PARITY_SCORE_RTOL, (mode, r)
         rb = report[f"bf16_{mode}"]
         assert rb["flips"] <= BF16_FLIP_FRACTION * nb, (mode, rb)
+
+
+@pytest.mark.parametrize("variant,mlp_dim", [("silu", 14336), ("relu", 16384)])
+def test_mlp_masks_other_baseline_widths(cuda, variant, mlp_dim):
+    """MLP mask parity at the other BASELINE widths: Llama3-8B / Mistral-7B
+    (SwiGLU, m = 14336) and OPT-6.7B in the reference family (ReLU,
+    m = 16384), h = 4096, s = 4096, one layer teacher-forced with a seeded
+    residual.  Parity and refined precision: 0 non-ambiguous flips against
+    the oracle (f32, model.py:371-396); bf16 flips bounded."""
+    s = 4096
+    cfg = dict(WIDTH, max_seq_len=s, mlp_dim=mlp_dim, mlp_variant=variant)
+    om = O.init_model(O.Config(**cfg), seed=21, fast=True)
+    model = M.DecoderModel(M.ModelConfig(**cfg), 0, arrays=oracle_arrays(om),
+                           scoring_precision="fp32")
+    layer = model.layers[0]
+    x = np.random.default_rng(22).standard_normal((s, 4096), dtype=np.float32)
+    n_valid = s - 3
+    ref = O.mlp_block_score_vector(om.layers[0], x, B, n_valid)
+    thr = float(np.mean(ref))
+    xd = torch.as_tensor(x).cuda()
+    got = {p: M.mlp_block_score_vector(layer, xd, B, n_valid, precision=p)
+           for p in ("fp32", "bf16")}
+    v, part = M.mlp_block_score_vector(layer, xd, B, n_valid, precision="bf16", with_partial=True)
+    rows = M.refine_mlp_block_scores(layer, xd, v, part, thr, B, n_valid)
+    got["refined"] = v
+    report = {"variant": variant, "mlp_dim": mlp_dim, "refined_rows": rows}
+    for p, vec in got.items():
+        g = vec.cpu().numpy()
+        flips, amb = _flips(g, ref, thr)
+        report[p] = {"flips": flips, "ambiguous": amb, "score_rel_err": _rel(g, ref)}
+    print("mlp mask parity", json.dumps(report))
+    for p in ("fp32", "refined"):
+        assert report[p]["flips"] - report[p]["ambiguous"] == 0 and report[p]["ambiguous"] <= 1, \
+            (p, report)
+    assert report["fp32"]["score_rel_err"] <= PARITY_SCORE_RTOL, report
+    assert report["bf16"]["flips"] <= BF16_FLIP_FRACTION * len(ref), report
