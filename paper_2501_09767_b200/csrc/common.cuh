@@ -77,6 +77,12 @@ __device__ __forceinline__ float ex2_poly3(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// Branch-free logistic on the SFU: 1 / (1 + 2^(-x·log2 e)).  Saturates
+// correctly at both ends (2^(+big) = inf -> 0, 2^(-big) = 0 -> 1).
+__device__ __forceinline__ float sigmoid_fast(float x) {
+  return __frcp_rn(1.f + ex2_approx(-1.4426950408889634f * x));
+}
+
 // Three-input max (FMNMX3, sm_100).
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;

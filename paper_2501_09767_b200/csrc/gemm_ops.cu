@@ -54,12 +54,6 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float (&v
   }
 }
 
-// Branch-free logistic on the SFU: 1 / (1 + 2^(-x·log2 e)).  Saturates
-// correctly at both ends (2^(+big) = inf -> 0, 2^(-big) = 0 -> 1).
-__device__ __forceinline__ float sigmoid_fast(float x) {
-  return __frcp_rn(1.f + ex2_approx(-1.4426950408889634f * x));
-}
-
 // ---------------------------------------------------------------------------
 
 struct EpiStoreBF16 {

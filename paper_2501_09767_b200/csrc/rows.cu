@@ -242,7 +242,9 @@ __global__ void mlp_compact_kernel(const __nv_bfloat16* __restrict__ gu_all, int
   uint4* dst = reinterpret_cast<uint4*>(gu_out + (size_t)row * ldgu);
   if (!relu && ldgu == 2 * m_pad) {
     // one pass: every 8-column gate chunk and its up chunk are read once,
-    // copied to the compact row and turned into 8 SwiGLU outputs
+    // copied to the compact row and turned into 8 SwiGLU outputs (the
+    // epilogue's logistic, sigmoid_fast, as the dense path's gate/up GEMM)
+#pragma unroll 2
     for (int c8 = threadIdx.x; c8 < (m_pad >> 3); c8 += blockDim.x) {
       const int mc = c8 * 8;
       const int gcol = (mc >> 7) * 256 + (mc & 127);
@@ -255,8 +257,8 @@ __global__ void mlp_compact_kernel(const __nv_bfloat16* __restrict__ gu_all, int
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float g0 = bf16_lo(gv[e]), g1 = bf16_hi(gv[e]);
-        in[2 * e] = g0 * sigmoid_stable(g0) * bf16_lo(uv[e]);
-        in[2 * e + 1] = g1 * sigmoid_stable(g1) * bf16_hi(uv[e]);
+        in[2 * e] = g0 * sigmoid_fast(g0) * bf16_lo(uv[e]);
+        in[2 * e + 1] = g1 * sigmoid_fast(g1) * bf16_hi(uv[e]);
       }
       reinterpret_cast<uint4*>(inner_out + (size_t)row * m_pad)[c8] =
           make_uint4(pack_bf16x2(in[0], in[1]), pack_bf16x2(in[2], in[3]),
@@ -276,8 +278,8 @@ __global__ void mlp_compact_kernel(const __nv_bfloat16* __restrict__ gu_all, int
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float g0 = bf16_lo(gv[e]), g1 = bf16_hi(gv[e]);
-        in[2 * e] = g0 * sigmoid_stable(g0) * bf16_lo(uv[e]);
-        in[2 * e + 1] = g1 * sigmoid_stable(g1) * bf16_hi(uv[e]);
+        in[2 * e] = g0 * sigmoid_fast(g0) * bf16_lo(uv[e]);
+        in[2 * e + 1] = g1 * sigmoid_fast(g1) * bf16_hi(uv[e]);
       }
     } else {
       const uint4 u = src[mc >> 3];
