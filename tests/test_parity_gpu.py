@@ -205,3 +205,40 @@ def test_mlp_masks_other_baseline_widths(cuda, variant, mlp_dim):
             (p, report)
     assert report["fp32"]["score_rel_err"] <= PARITY_SCORE_RTOL, report
     assert report["bf16"]["flips"] <= BF16_FLIP_FRACTION * len(ref), report
+
+
+def test_exact_attention_masks_gqa_width(cuda):
+    """Exact-attention mask parity at the Llama3-8B / Mistral-7B geometry
+    (grouped-query attention: 32 query / 8 key-value heads, h = 4096, RoPE base
+    500000), s = 4096: layer_qk + the tcgen05 exact scorer + column sums vs the
+    oracle (model.py:356-368, sparsity.py:173-260 with the key heads repeated,
+    the GQA extension pinned in test_step_gpu).  Parity precision 0
+    non-ambiguous flips, bf16 bounded."""
+    s = 4096
+    cfg = dict(WIDTH, max_seq_len=s, n_kv_heads=8, rope_base=500000.0)
+    om = O.init_model(O.Config(**cfg), seed=31, fast=True)
+    O.perturb_lora_b(om, 32)
+    model = M.DecoderModel(M.ModelConfig(**cfg), 0, arrays=oracle_arrays(om),
+                           scoring_precision="fp32")
+    layer = model.layers[0]
+    x = np.random.default_rng(33).standard_normal((s, 4096), dtype=np.float32)
+    n_valid = s - 5
+    q, k = O.layer_qk(om.layers[0], x)
+    ref = O.column_sums_dense(O.exact_block_dense(q, k, B, n_valid))
+    del q, k
+    srt = np.sort(ref)
+    mid = (len(srt) - 1) // 2
+    thr = float(0.5 * (srt[mid] + srt[mid + 1]))
+    xd = torch.as_tensor(x).cuda()
+    report = {"n_kv_heads": 8}
+    for prec in ("fp32", "bf16"):
+        qq, kk = M.layer_qk(layer, xd, precision=prec)
+        g = exact.exact_block_vector(qq, kk, B, n_heads=32, n_valid=n_valid).cpu().numpy()
+        del qq, kk
+        flips, amb = _flips(g, ref, thr)
+        report[prec] = {"flips": flips, "ambiguous": amb, "score_rel_err": _rel(g, ref)}
+    print("gqa exact mask parity", json.dumps(report))
+    r = report["fp32"]
+    assert r["flips"] - r["ambiguous"] == 0 and r["ambiguous"] <= 1, report
+    assert r["score_rel_err"] <= PARITY_SCORE_RTOL, report
+    assert report["bf16"]["flips"] <= BF16_FLIP_FRACTION * len(ref), report
