@@ -50,6 +50,8 @@ BF16_FLIP_FRACTION = 0.01
 
 def oracle_arrays(om):
     arrays = {"embed": om.embed, "final_norm": om.final_norm, "lm_head": om.lm_head}
+    if om.pos_embed is not None:  # learned positions (the OPT configuration)
+        arrays["pos_embed"] = om.pos_embed
     for i, L in enumerate(om.layers):
         p = f"layer{i}"
         arrays.update({f"{p}.wq": L.wq, f"{p}.wk": L.wk, f"{p}.wv": L.wv, f"{p}.wo": L.wo,
@@ -207,15 +209,18 @@ def test_mlp_masks_other_baseline_widths(cuda, variant, mlp_dim):
     assert report["bf16"]["flips"] <= BF16_FLIP_FRACTION * len(ref), report
 
 
-def test_exact_attention_masks_gqa_width(cuda):
-    """Exact-attention mask parity at the Llama3-8B / Mistral-7B geometry
-    (grouped-query attention: 32 query / 8 key-value heads, h = 4096, RoPE base
-    500000), s = 4096: layer_qk + the tcgen05 exact scorer + column sums vs the
-    oracle (model.py:356-368, sparsity.py:173-260 with the key heads repeated,
-    the GQA extension pinned in test_step_gpu).  Parity precision 0
-    non-ambiguous flips, bf16 bounded."""
+@pytest.mark.parametrize("geometry", ["gqa", "learned_positions"])
+def test_exact_attention_masks_gqa_width(cuda, geometry):
+    """Exact-attention mask parity at the other BASELINE geometries, s = 4096:
+    "gqa" = Llama3-8B / Mistral-7B (grouped-query attention, 32 query / 8
+    key-value heads, RoPE base 500000); "learned_positions" = the OPT-6.7B
+    configuration in the reference family (no RoPE in layer_qk).  layer_qk +
+    the tcgen05 exact scorer + column sums vs the oracle (model.py:356-368,
+    sparsity.py:173-260; key heads repeated for GQA, the extension pinned in
+    test_step_gpu).  Parity precision 0 non-ambiguous flips, bf16 bounded."""
     s = 4096
-    cfg = dict(WIDTH, max_seq_len=s, n_kv_heads=8, rope_base=500000.0)
+    cfg = (dict(WIDTH, max_seq_len=s, n_kv_heads=8, rope_base=500000.0) if geometry == "gqa"
+           else dict(WIDTH, max_seq_len=s, positions="learned"))
     om = O.init_model(O.Config(**cfg), seed=31, fast=True)
     O.perturb_lora_b(om, 32)
     model = M.DecoderModel(M.ModelConfig(**cfg), 0, arrays=oracle_arrays(om),
@@ -230,7 +235,7 @@ def test_exact_attention_masks_gqa_width(cuda):
     mid = (len(srt) - 1) // 2
     thr = float(0.5 * (srt[mid] + srt[mid + 1]))
     xd = torch.as_tensor(x).cuda()
-    report = {"n_kv_heads": 8}
+    report = {"geometry": geometry}
     for prec in ("fp32", "bf16"):
         qq, kk = M.layer_qk(layer, xd, precision=prec)
         g = exact.exact_block_vector(qq, kk, B, n_heads=32, n_valid=n_valid).cpu().numpy()
