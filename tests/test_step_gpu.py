@@ -217,3 +217,64 @@ def test_gqa_step_matches_reference_repeated_heads(cuda, mode):
         ref = z[f"{mode}_grad__{name}"]
         assert g.shape == ref.shape, name
         assert _rl2(g, ref) <= GRAD_RL2, (name, _rl2(g, ref))
+
+
+def test_full_width_predicted_step_refined(cuda):
+    """The bench's production path at the north-star width: 2 Llama2-7B-width
+    layers (h=4096, 32 heads, m=11008), s=1024, PredictedPatternSource with
+    recalibrated attention thresholds (model.py:545-563) and fixed MLP
+    thresholds, `refined` scorers -- against the oracle's PredictedSource on
+    the same weights, predictors (ranks 1024) and tokens: identical retained
+    blocks for every (layer, component), loss and LoRA gradients within the
+    bf16 tolerance."""
+    cfg = dict(n_layers=2, hidden_dim=4096, n_heads=32, vocab_size=512, max_seq_len=1024,
+               mlp_dim=11008, block_size=16, lora_rank=8, lora_alpha=16.0)
+    om = O.init_model(O.Config(**cfg), seed=41, fast=True)
+    O.perturb_lora_b(om, 42)
+    model = M.DecoderModel(M.ModelConfig(**cfg), 0, arrays=_oracle_arrays(om),
+                           scoring_precision="refined")
+    prng = np.random.default_rng(43)
+    ws = {l: [[(prng.standard_normal(sh, dtype=np.float32) / np.sqrt(sh[0])).astype(np.float32)
+               for sh in ((4096, 1024), (1024, 1024), (1024, 1024))] for _ in range(2)]
+          for l in range(2)}
+    model.attach_predictors({l: (P.Predictor(*ws[l][0]), P.Predictor(*ws[l][1]))
+                             for l in range(2)})
+    for l in range(2):
+        om.layers[l].predictor_q, om.layers[l].predictor_k = (O.Predictor(*ws[l][0]),
+                                                              O.Predictor(*ws[l][1]))
+    tokens = np.random.default_rng(44).integers(0, 512, 1024)
+    # MLP thresholds: midpoints between neighbouring scores of a retain-all
+    # profile near its mean (a tuned threshold is not itself a score)
+    prof = O.ExactSource(om, None)
+    O.train_step(om, tokens, source=prof, segments=2)
+    thr = {}
+    for l in range(2):
+        v = np.sort(prof.vectors[(l, "mlp")])
+        i = int(np.searchsorted(v, v.mean()))
+        thr[(l, "mlp")] = float(0.5 * (v[i - 1] + v[i]))
+        thr[(l, "attention")] = 0.0  # recalibrated at every call
+    osrc = O.PredictedSource(om, dict(thr), target_retention={0: 0.5, 1: 0.5},
+                             recalibrate_every=1)
+    ores = O.train_step(om, tokens, source=osrc, segments=2)
+    src = M.PredictedPatternSource(model, S.ThresholdSet(dict(thr)),
+                                   target_retention={0: 0.5, 1: 0.5}, recalibrate_every=1)
+    got, inner = {}, src.pattern
+
+    def record(layer_id, component, x, n_valid):
+        pat = inner(layer_id, component, x, n_valid)
+        got[(layer_id, component)] = None if pat is None else tuple(pat.retained_blocks)
+        return pat
+
+    src.pattern = record
+    loss, _ = model.forward_step(tokens, pattern_source=src, segments=2)
+    loss.backward()
+    errs = {n: _rl2(g, ores["grads"][n]) for n, g in model.adapter_grads().items()}
+    print("full-width predicted step", json.dumps({
+        "loss": float(loss), "oracle": ores["loss"], "grad_rl2": errs,
+        "retained": {f"{l}_{c}": len(b) for (l, c), b in got.items()},
+        "refined_rows": dict((f"{k}", v) for k, v in src.refined_rows.items())}))
+    for key, blocks in ores["patterns"].items():
+        assert got[key] == tuple(blocks), (key, got[key], blocks)
+    assert abs(float(loss) - ores["loss"]) <= LOSS_RTOL * abs(ores["loss"])
+    for n, e in errs.items():
+        assert e <= GRAD_RL2, (n, e)
