@@ -295,6 +295,17 @@ struct PairTailOK {
   static constexpr bool value = false;
 };
 
+// Epilogues whose split-K tail is finished by a separate kernel: the tail
+// units only store their fp32 partials (no counting, no summing inside the
+// GEMM, so the heavy epilogue loop does not grow), and the caller runs a
+// fixed-order reduction + the epilogue's effect afterwards (the scatter-add
+// GEMMs: lemo_gemm_scatter_add).
+template <class Epi>
+struct PairTailDeferred {
+  static constexpr bool value = false;
+};
+constexpr int kPairTailMaxSplitDeferred = 16;
+
 struct PairUnit {
   int tile, kb0, kb1, chunk;  // chunk = -1 for a whole tile
 };
@@ -490,6 +501,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
       bool run_epi = true;
+      if constexpr (PairTailDeferred<Epi>::value) {
+        if (w.chunk >= 0) {  // store this K-range's partial; the caller finishes the tile
+          const int tail = w.tile - tl.full_tiles;
+          const int r128 = wq * 32 + lane;
+          float4* dst = reinterpret_cast<float4*>(tl.ws) +
+                        (((size_t)(tail * tl.split + w.chunk) * 2 + rank) * 2 + part) * 4096;
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(taddr + part * 128 + c * 32, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              __stcg(dst + (c * 8 + j) * 128 + r128,
+                     make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                 __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
+          }
+          run_epi = false;
+        }
+      }
       if constexpr (PairTailOK<Epi>::value) {
       if (w.chunk >= 0) {
         // partial-sum slot of (unit, rank, part): [c32 4][j 8][row 128] float4
@@ -632,9 +663,11 @@ int launch_gemm_tn(const void* A, int lda, const void* B, int ldb, int M, int N,
 
 // Pair-tile launch (BN = 256, non-transposed B): grid = 2 x (tiles capped at
 // half the SMs), cluster dims fixed by __cluster_dims__.
+// Deferred-tail epilogues report the tail they used through *deferred
+// (split = 1: none) so the caller can finish those tiles.
 template <class Epi, int kPromote = 0>
 int launch_gemm_tn_pair(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
-                        const Epi& epi, cudaStream_t stream) {
+                        const Epi& epi, cudaStream_t stream, PairTail* deferred = nullptr) {
   if (M <= 0 || N <= 0) return 0;
   CUtensorMap ta, tb;
   int rc = make_tma_bf16_2d(&ta, A, (uint64_t)M, (uint64_t)K, (uint64_t)lda, kBlockM);
@@ -652,10 +685,12 @@ int launch_gemm_tn_pair(const void* A, int lda, const void* B, int ldb, int M, i
   const int clusters = tiles < pairs ? tiles : pairs;
   PairTail tl{tiles, 1, nullptr, nullptr};
   const int rem = tiles % clusters, num_kb = (K + kBlockK - 1) / kBlockK;
-  if (kPromote == 0 && PairTailOK<Epi>::value && tiles > clusters && rem > 0 &&
-      2 * rem <= clusters && pair_tail_enabled()) {
+  constexpr bool kDefer = PairTailDeferred<Epi>::value;
+  if (kPromote == 0 && (PairTailOK<Epi>::value || (kDefer && deferred != nullptr)) &&
+      tiles > clusters && rem > 0 && 2 * rem <= clusters && pair_tail_enabled()) {
     int split = clusters / rem;
-    if (split > kPairTailMaxSplit) split = kPairTailMaxSplit;
+    const int max_split = kDefer ? kPairTailMaxSplitDeferred : kPairTailMaxSplit;
+    if (split > max_split) split = max_split;
     if (split > num_kb / 4) split = num_kb / 4;  // keep ≥ 4 k-blocks per unit
     if (split >= 2) {
       rc = pair_tail_workspace(stream, rem * split, rem, &tl.ws, &tl.ctr);
@@ -664,6 +699,7 @@ int launch_gemm_tn_pair(const void* A, int lda, const void* B, int ldb, int M, i
       tl.split = split;
     }
   }
+  if (deferred != nullptr) *deferred = tl;
   gemm_tn_pair_kernel<Epi, kPromote><<<2 * clusters, kGemmThreads, kSmemPair, stream>>>(
       ta, tb, M, N, K, epi, tl);
   return (int)cudaGetLastError();

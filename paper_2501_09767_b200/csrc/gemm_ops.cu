@@ -394,6 +394,42 @@ struct Bound {
 };
 
 template <> struct PairTailOK<Bound<256, EpiStoreF32>> { static constexpr bool value = true; };
+template <> struct PairTailDeferred<Bound<256, EpiScatterAdd>> { static constexpr bool value = true; };
+
+// Finish of the scatter-add GEMM's deferred split-K tail: one thread per
+// float4 of a tail tile (tile, CTA half, column half, 32-column chunk, 4
+// columns, row) sums the K-range partials in chunk order (deterministic) and
+// adds the result into R[idx[row]] -- what the epilogue would have done with
+// the whole tile's accumulator.  All partial loads of a thread are in flight
+// at once (the reduction is latency-bound otherwise).
+__global__ void __launch_bounds__(128) scatter_tail_finish_kernel(PairTail tl, int num_m,
+                                                                  int num_n, int M, int N,
+                                                                  float* __restrict__ R, int ldr,
+                                                                  const int* __restrict__ idx) {
+  const int cj = blockIdx.x & 31, half = (blockIdx.x >> 5) & 3, tail = blockIdx.x >> 7;
+  const int rank = half >> 1, part = half & 1, c = cj >> 3, j = cj & 7;
+  const int r128 = threadIdx.x;
+  const TileCoord tc = tile_coord(tl.full_tiles + tail, num_m, num_n);
+  const int row = tc.m * 2 * kBlockM + rank * kBlockM + r128;
+  const int col = tc.n * 256 + part * 128 + c * 32 + 4 * j;
+  if (row >= M || col >= N) return;
+  const float4* src = reinterpret_cast<const float4*>(tl.ws) +
+                      ((size_t)(tail * tl.split) * 2 + rank) * 2 * 4096 + part * 4096 +
+                      (c * 8 + j) * 128 + r128;
+  const size_t unit = (size_t)2 * 2 * 4096;  // float4 stride between K-range units
+  float4 p[kPairTailMaxSplitDeferred];
+#pragma unroll
+  for (int k = 0; k < kPairTailMaxSplitDeferred; ++k)
+    if (k < tl.split) p[k] = __ldcg(src + k * unit);
+  float4 a = p[0];
+#pragma unroll
+  for (int k = 1; k < kPairTailMaxSplitDeferred; ++k)
+    if (k < tl.split) { a.x += p[k].x; a.y += p[k].y; a.z += p[k].z; a.w += p[k].w; }
+  float4* d = reinterpret_cast<float4*>(R + (size_t)(idx ? __ldg(idx + row) : row) * ldr + col);
+  float4 q = *d;
+  q.x += a.x; q.y += a.y; q.z += a.z; q.w += a.w;
+  *d = q;
+}
 template <> struct PairTailOK<Bound<256, EpiStoreBF16>> { static constexpr bool value = true; };
 
 // BN = 256 GEMMs run as CTA pairs (256 x 256 tiles) when M spans at least two
@@ -499,8 +535,21 @@ int lemo_gemm_scatter_add(const void* A, int lda, const void* B, int ldb, float*
                           const int* idx, int M, int N, int K, void* stream) {
   LEMO_ARG_CHECK(N % 32 == 0 && ldr % 4 == 0, "lemo_gemm_scatter_add: N%32, ldr%4");
   EpiScatterAdd e{R, ldr, N, idx};
-  LEMO_RETURN_RC("lemo_gemm_scatter_add",
-                 gemm_auto(A, lda, B, ldb, M, N, K, e, (cudaStream_t)stream));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (pick_bn(M, N) == 256 && use_pair(M)) {
+    // CTA-pair tiles with the deferred split-K tail: a last wave that is at
+    // most half full runs as K-range units, finished by a second small kernel
+    PairTail tl{};
+    int rc = launch_gemm_tn_pair(A, lda, B, ldb, M, N, K, Bound<256, EpiScatterAdd>{e}, st, &tl);
+    if (!rc && tl.split > 1) {
+      const int num_m = (M + 2 * kBlockM - 1) / (2 * kBlockM), num_n = (N + 255) / 256;
+      const int rem = num_m * num_n - tl.full_tiles;
+      scatter_tail_finish_kernel<<<rem * 128, 128, 0, st>>>(tl, num_m, num_n, M, N, R, ldr, idx);
+      rc = (int)cudaGetLastError();
+    }
+    LEMO_RETURN_RC("lemo_gemm_scatter_add", rc);
+  }
+  LEMO_RETURN_RC("lemo_gemm_scatter_add", gemm_auto(A, lda, B, ldb, M, N, K, e, st));
 }
 
 int lemo_gemm_qkv(const void* xn, int ldx, const void* w_qkv_t, int ldw, int M, int h, int kv,
