@@ -9,7 +9,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent))
 from profile_step import setup  # noqa: E402
 from paper_2501_09767_b200.optim import Adam  # noqa: E402
 
-model, src, tokens = setup(16384, "lemo")
+model, src, tokens = setup(16384, "lemo", "refined")
 opt = Adam(model.lora_param, lr=1e-4)
 batch = model.stage_tokens(tokens)
 

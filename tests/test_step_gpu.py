@@ -219,14 +219,16 @@ def test_gqa_step_matches_reference_repeated_heads(cuda, mode):
         assert _rl2(g, ref) <= GRAD_RL2, (name, _rl2(g, ref))
 
 
-def test_full_width_predicted_step_refined(cuda):
+@pytest.mark.parametrize("sink,pooling", [(False, "mean"), (True, "token")])
+def test_full_width_predicted_step_refined(cuda, sink, pooling):
     """The bench's production path at the north-star width: 2 Llama2-7B-width
     layers (h=4096, 32 heads, m=11008), s=1024, PredictedPatternSource with
     recalibrated attention thresholds (model.py:545-563) and fixed MLP
     thresholds, `refined` scorers -- against the oracle's PredictedSource on
     the same weights, predictors (ranks 1024) and tokens: identical retained
     blocks for every (layer, component), loss and LoRA gradients within the
-    bf16 tolerance."""
+    bf16 tolerance.  Second case: the sink block forced and token pooling of
+    the predictor outputs (predictor.py:126-173)."""
     cfg = dict(n_layers=2, hidden_dim=4096, n_heads=32, vocab_size=512, max_seq_len=1024,
                mlp_dim=11008, block_size=16, lora_rank=8, lora_alpha=16.0)
     om = O.init_model(O.Config(**cfg), seed=41, fast=True)
@@ -254,10 +256,11 @@ def test_full_width_predicted_step_refined(cuda):
         thr[(l, "mlp")] = float(0.5 * (v[i - 1] + v[i]))
         thr[(l, "attention")] = 0.0  # recalibrated at every call
     osrc = O.PredictedSource(om, dict(thr), target_retention={0: 0.5, 1: 0.5},
-                             recalibrate_every=1)
+                             recalibrate_every=1, sink_first_block=sink, pooling=pooling)
     ores = O.train_step(om, tokens, source=osrc, segments=2)
     src = M.PredictedPatternSource(model, S.ThresholdSet(dict(thr)),
-                                   target_retention={0: 0.5, 1: 0.5}, recalibrate_every=1)
+                                   target_retention={0: 0.5, 1: 0.5}, recalibrate_every=1,
+                                   sink_first_block=sink, pooling=pooling)
     got, inner = {}, src.pattern
 
     def record(layer_id, component, x, n_valid):
