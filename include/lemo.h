@@ -253,9 +253,13 @@ int lemo_mlp_token_band(const float* partial, int n_tiles, int s, int n_valid, i
 
 /* vec[tok[i] / b] = max over the re-scored rows of that block of
  * Σ_t partial[t, i] / m_real (tok ascending; partial is [n_tiles, rows]) --
- * the token-level refinement written back (mlp_block_scores arithmetic). */
-int lemo_mlp_patch_rows(const float* partial, int n_tiles, int rows, const int* tok, int b,
-                        int m_real, double* vec, void* stream);
+ * the token-level refinement written back (mlp_block_scores arithmetic).
+ * count (device, may be NULL): the re-scored rows when the GEMM ran on a
+ * capacity of `rows` (rows past *count are padding); overflow (device, may be
+ * NULL) is set to *count > rows -- the caller then re-runs with the exact count. */
+int lemo_mlp_patch_rows(const float* partial, int n_tiles, int rows, const int* tok,
+                        const int* count, int b, int m_real, double* vec, int* overflow,
+                        void* stream);
 
 /* MLP block scores from per-tile row partials of lemo_gemm_gateup:
  * token score = Σ partial / m_real, block = max over rows < n_valid

@@ -119,17 +119,22 @@ __global__ void mlp_token_band_kernel(const float* __restrict__ partial, int n_t
 // so a block's rows are contiguous).  One warp per compact row i; the warp of
 // a block's first row reduces the block: lane l sums row i + l (the tile
 // order of mlp_block_scores) and the maximum is a warp shuffle (b <= 32).
+// count (optional): the number of valid rows when the GEMM ran on a capacity
+// of `rows` (rows past the count are padding); *overflow = count > rows.
 __global__ void mlp_patch_rows_kernel(const float* __restrict__ partial, int n_tiles, int rows,
-                                      const int* __restrict__ tok, int b, float m_real,
-                                      double* __restrict__ vec) {
+                                      const int* __restrict__ tok, const int* __restrict__ count,
+                                      int b, float m_real, double* __restrict__ vec,
+                                      int* __restrict__ overflow) {
   const int i = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  if (i >= rows) return;
+  const int n = count ? min(__ldg(count), rows) : rows;
+  if (overflow && blockIdx.x == 0 && threadIdx.x == 0) *overflow = count && __ldg(count) > rows;
+  if (i >= n) return;
   const int blk = __ldg(tok + i) / b;
   if (i > 0 && __ldg(tok + i - 1) / b == blk) return;  // warp-uniform
   const int j = i + lane;
   float best = -INFINITY;
-  if (j < rows && __ldg(tok + j) / b == blk) {
+  if (j < n && __ldg(tok + j) / b == blk) {  // (partial rows are strided by `rows`)
     float acc = 0.f;
 #pragma unroll 8
     for (int t = 0; t < n_tiles; ++t) acc += partial[(size_t)t * rows + j];
@@ -387,12 +392,13 @@ int lemo_mlp_token_band(const float* partial, int n_tiles, int s, int n_valid, i
   return 0;
 }
 
-int lemo_mlp_patch_rows(const float* partial, int n_tiles, int rows, const int* tok, int b,
-                        int m_real, double* vec, void* stream) {
+int lemo_mlp_patch_rows(const float* partial, int n_tiles, int rows, const int* tok,
+                        const int* count, int b, int m_real, double* vec, int* overflow,
+                        void* stream) {
   if (rows <= 0) return 0;
   LEMO_ARG_CHECK(b > 0 && b <= 32, "lemo_mlp_patch_rows: block size must be in [1, 32]");
   mlp_patch_rows_kernel<<<(unsigned)((rows * 32LL + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      partial, n_tiles, rows, tok, b, (float)m_real, vec);
+      partial, n_tiles, rows, tok, count, b, (float)m_real, vec, overflow);
   LEMO_CHECK_LAUNCH("lemo_mlp_patch_rows");
   return 0;
 }

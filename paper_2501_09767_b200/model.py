@@ -831,7 +831,7 @@ def mlp_block_score_vector(layer: LayerState, x: torch.Tensor, block_size: int, 
 
 def refine_mlp_block_scores(layer: LayerState, x: torch.Tensor, vec: torch.Tensor,
                             partial: torch.Tensor, thr: float, block_size: int, n_valid: int, *,
-                            margin: float | None = None) -> int:
+                            margin: float | None = None, capacity: int | None = None):
     """Refined MLP scoring (decisions of sparsity.py:274-277 on the block max
     of sparsity.py:298-305).  A block whose bf16 score lies within δ =
     margin·|thr| of the threshold is ambiguous; of its rows only those whose
@@ -848,26 +848,74 @@ def refine_mlp_block_scores(layer: LayerState, x: torch.Tensor, vec: torch.Tenso
     safety factor (tests/test_parity_gpu.py).  For a still-dropped block the
     patched value may differ from its full parity score (a non-re-scored row
     may hold the maximum); both are below the threshold.  One extra host
-    read-back (the number of rows sizes the GEMM)."""
+    read-back (the number of rows sizes the GEMM) -- or, with `capacity`,
+    none: the GEMM runs on `capacity` rows and the device [count, overflow]
+    pair is returned for the caller's own read-back (_refine_capacity)."""
     if not math.isfinite(thr):  # -inf retains every block, +inf none: nothing is ambiguous
         return 0
     margin = layer.refine_margin if margin is None else margin
     s = x.shape[0]
     band = ops.mlp_token_band(partial, vec, thr, margin * abs(thr), n_valid=n_valid,
                               b=block_size, m_real=layer.m)
+    if capacity is not None:
+        return _refine_capacity(layer, x, vec, band, block_size, capacity)
     cand = sparsity.select_device(band, 0.0, block_size=1, n_tokens=s)[0]
     rows = cand.k
     if rows == 0:
         return 0
     tok = cand.device_token_indices(x.device)
+    _refine_rows(layer, x, vec, tok, rows, block_size)
+    return rows
+
+
+def _refine_rows(layer, x, vec, tok, rows, block_size, count=None, overflow=None):
+    """Parity-precision gate/up scores of the rows tok[:rows] patched into vec."""
     xnf = ops.rmsnorm_f32(x, layer.mlp_norm_w, tok)
     a = layer.split_input(xnf)
     del xnf
     N = layer.w_gu_t.shape[0]
     part = torch.empty(N // 128, rows, dtype=F32, device=x.device)
     ops.gemm_gateup(a, layer.gateup_x3(), partial=part, relu=layer.relu, exact_score=True)
-    ops.mlp_patch_rows(part, tok, b=block_size, m_real=layer.m, vec=vec)
-    return rows
+    ops.mlp_patch_rows(part, tok, b=block_size, m_real=layer.m, vec=vec, count=count,
+                       overflow=overflow)
+
+
+def _refine_capacity(layer, x, vec, band, block_size, capacity):
+    """The refinement without a host read-back of the row count: the band rows
+    are compacted on the device into a zero-padded index list, the parity GEMM
+    runs on `capacity` rows (padding rows score row 0 and are ignored by the
+    patch kernel) and the patch kernel raises a device flag when the true
+    count exceeds the capacity.  Returns the device int32 [count, overflow]
+    pair; the caller reads it back with its own selection read-back and
+    re-runs the exact refinement on overflow (RefineCapacity)."""
+    s = x.shape[0]
+    dev = x.device
+    ws = sparsity.SelectWorkspace(s, s, 1, dev)
+    ws.tokens.zero_()
+    ops.select(band, b=1, n_tokens=s, thr=0.0, mask=ws.mask, blocks=ws.blocks, tokens=ws.tokens,
+               counts=ws.counts, thr_out=ws.thr)
+    flags = torch.empty(2, dtype=torch.int32, device=dev)  # [count, overflow]
+    flags[:1].copy_(ws.counts[:1])
+    _refine_rows(layer, x, vec, ws.tokens[:capacity], capacity, block_size, count=flags[:1],
+                 overflow=flags[1:])
+    return flags
+
+
+class RefineCapacity:
+    """Per-layer capacity of the read-back-free refinement: the first call of
+    a layer runs the exact path (one count read-back); later calls run on
+    max(256, 1.25 x the last count) rows rounded up to 256 (one pair-tile row
+    block at N*, so the padding costs no extra tiles), and an overflow re-runs
+    the exact path from the bf16 partials."""
+
+    def __init__(self):
+        self.cap: dict = {}
+
+    def for_layer(self, layer_id):
+        return self.cap.get(layer_id)
+
+    def update(self, layer_id, count: int) -> None:
+        self.cap[layer_id] = max(256, -(-int(count * 1.25) // 256) * 256)
 
 
 def layer_qk(layer: LayerState, x: torch.Tensor, *, precision: str | None = None):
@@ -981,6 +1029,7 @@ class PredictedPatternSource(PatternSourceBase):
         self.recorded_vectors: dict = {}
         self._recent: dict = {}
         self._calls: dict = {}
+        self._refine_cap = RefineCapacity()
 
     def _maybe_recalibrate(self, layer_id, vec):
         """model.py:545-563; returns a device threshold or None."""
@@ -1022,8 +1071,7 @@ class PredictedPatternSource(PatternSourceBase):
             self.model.stash_mlp_rows(layer_id, x, rows)
             thr = self.thresholds.get(layer_id, component)
             if layer.scoring_precision == "refined":
-                self.refined_rows[layer_id] = refine_mlp_block_scores(layer, x, vec, partial, thr,
-                                                                      b, n_valid)
+                return self._refined_mlp(layer, layer_id, x, vec, partial, thr, n_valid)
             del partial
         if self.record:
             self.recorded_vectors.setdefault((layer_id, component), []).append(vec)
@@ -1034,6 +1082,36 @@ class PredictedPatternSource(PatternSourceBase):
         if thr_dev is not None:
             self.thresholds.set(layer_id, sparsity.ATTENTION, used)
         return self._note(layer_id, component, pat)
+
+
+    def _refined_mlp(self, layer, layer_id, x, vec, partial, thr, n_valid):
+        """MLP pattern in the refined precision without a separate read-back
+        of the refinement's row count: the parity re-scoring runs on the
+        layer's capacity (RefineCapacity) and its [count, overflow] pair rides
+        on the selection's read-back; an overflow (more band rows than the
+        capacity) re-scores exactly from fresh bf16 block scores."""
+        b = self.model.config.block_size
+        cap = self._refine_cap.for_layer(layer_id)
+        flags = refine_mlp_block_scores(layer, x, vec, partial, thr, b, n_valid, capacity=cap)
+        force = (0,) if self.sink_first_block else ()
+        sel = dict(layer_id=layer_id, component=sparsity.MLP, block_size=b, n_tokens=x.shape[0],
+                   force_blocks=force)
+        if isinstance(flags, torch.Tensor):
+            pat, _, (count, overflow) = sparsity.select_device(vec, thr, extra=flags, **sel)
+            if overflow:
+                vec = ops.mlp_block_scores(partial, s=x.shape[0], n_valid=n_valid, b=b,
+                                           m_real=layer.m)
+                count = refine_mlp_block_scores(layer, x, vec, partial, thr, b, n_valid)
+                pat, _ = sparsity.select_device(vec, thr, **sel)
+        else:  # exact path (first call of the layer, or nothing ambiguous)
+            count = flags
+            pat, _ = sparsity.select_device(vec, thr, **sel)
+        self._refine_cap.update(layer_id, count)
+        self.refined_rows[layer_id] = count
+        if self.record:
+            self.recorded_vectors.setdefault((layer_id, sparsity.MLP), []).append(vec)
+        del partial
+        return self._note(layer_id, sparsity.MLP, pat)
 
 
 class ExactPatternSource(PatternSourceBase):

@@ -527,10 +527,10 @@ def mlp_token_band(partial, vec, thr, margin, *, n_valid, b, m_real, out=None):
     return out
 
 
-def mlp_patch_rows(partial, tok, *, b, m_real, vec):
-    _check(partial, tok, vec)
-    call("lemo_mlp_patch_rows", ptr(partial), partial.shape[0], partial.shape[1], ptr(tok), b,
-         m_real, ptr(vec), _s())
+def mlp_patch_rows(partial, tok, *, b, m_real, vec, count=None, overflow=None):
+    _check(partial, tok, vec, count, overflow)
+    call("lemo_mlp_patch_rows", ptr(partial), partial.shape[0], partial.shape[1], ptr(tok),
+         ptr(count), b, m_real, ptr(vec), ptr(overflow), _s())
     return vec
 
 

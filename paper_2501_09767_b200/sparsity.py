@@ -238,13 +238,14 @@ class SelectWorkspace:
         if sc is None:
             host_i = torch.empty(4, dtype=torch.int32, pin_memory=True)
             host_f = torch.empty(1, dtype=torch.float64, pin_memory=True)
+            host_x = torch.empty(4, dtype=torch.int32, pin_memory=True)  # caller's extras
             sc = (torch.empty(max(nb, 1), dtype=torch.uint8, device=device),
                   torch.empty(4, dtype=torch.int32, device=device),
                   torch.empty(1, dtype=torch.float64, device=device), host_i, host_f,
-                  host_i.numpy(), host_f.numpy())
+                  host_i.numpy(), host_f.numpy(), host_x, host_x.numpy())
             SelectWorkspace._scratch[key] = sc
         (self.mask, self.counts, self.thr, self.host_i, self.host_f, self.host_i_np,
-         self.host_f_np) = sc
+         self.host_f_np, self.host_x, self.host_x_np) = sc
 
 
 def _force_mask(force_blocks, nb, device):
@@ -260,11 +261,14 @@ def _force_mask(force_blocks, nb, device):
 
 def select_device(vec: torch.Tensor, threshold: float | None = None, *, thr_dev=None,
                   layer_id: int = 0, component: str = ATTENTION, block_size: int,
-                  n_tokens: int, force_blocks: Sequence[int] = ()) -> tuple[SparsityPattern, float]:
+                  n_tokens: int, force_blocks: Sequence[int] = (), extra=None):
     """eliminate() on device scores; returns (pattern, threshold used).
 
     One host synchronisation: the retained count k (needed to size the
     compact activation buffers) and the threshold are read back together.
+    `extra` (device int32, <= 4 values, e.g. the refinement's [count,
+    overflow]) rides on the same read-back; then (pattern, threshold, extras)
+    is returned.
     """
     nb = vec.shape[0]
     if nb != n_blocks_for(n_tokens, block_size):
@@ -277,6 +281,8 @@ def select_device(vec: torch.Tensor, threshold: float | None = None, *, thr_dev=
                mask=ws.mask, blocks=ws.blocks, tokens=ws.tokens, counts=ws.counts, thr_out=ws.thr)
     ws.host_i.copy_(ws.counts, non_blocking=True)
     ws.host_f.copy_(ws.thr, non_blocking=True)
+    if extra is not None:
+        ws.host_x[:extra.numel()].copy_(extra, non_blocking=True)
     torch.cuda.current_stream().synchronize()
     hi = ws.host_i_np  # numpy views of the pinned slots: no per-element tensor dispatch
     k, nkept, bad, used = int(hi[0]), int(hi[1]), int(hi[2]), float(ws.host_f_np[0])
@@ -284,6 +290,8 @@ def select_device(vec: torch.Tensor, threshold: float | None = None, *, thr_dev=
         raise ContractError("block scores must be finite")
     pat = SparsityPattern._from_device(layer_id, component, block_size, n_tokens, ws.blocks,
                                        ws.tokens, nkept, k)
+    if extra is not None:
+        return pat, used, [int(v) for v in ws.host_x_np[:extra.numel()]]
     return pat, used
 
 

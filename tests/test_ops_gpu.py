@@ -288,6 +288,33 @@ def test_refined_mlp_decisions_equal_parity(cuda, margin):
         assert torch.equal(vec, before)
 
 
+def test_refine_capacity_matches_exact(cuda):
+    """The read-back-free refinement (capacity rows, device [count, overflow])
+    patches exactly what the counted path patches when the capacity covers
+    the band; a capacity below the count raises the overflow flag."""
+    from paper_2501_09767_b200.model import refine_mlp_block_scores
+    cfg = ModelConfig(n_layers=1, hidden_dim=256, n_heads=2, vocab_size=64, max_seq_len=1024,
+                      block_size=16, mlp_dim=688, lora_rank=4, lora_alpha=8.0)
+    m = DecoderModel(cfg, 5, init="reference", parity_weights=True)
+    L = m.layers[0]
+    x = torch.randn(1024, 256, device="cuda")
+    nv = 1024 - 5
+    v0, part = mlp_block_score_vector(L, x, 16, nv, precision="bf16", with_partial=True)
+    thr = float(torch.quantile(v0, 0.5))
+    exact_vec = v0.clone()
+    rows = refine_mlp_block_scores(L, x, exact_vec, part, thr, 16, nv, margin=5e-2)
+    assert rows > 8
+    cap_vec = v0.clone()
+    flags = refine_mlp_block_scores(L, x, cap_vec, part, thr, 16, nv, margin=5e-2,
+                                    capacity=rows + 37)
+    count, overflow = (int(v) for v in flags.cpu())
+    assert (count, overflow) == (rows, 0)
+    assert torch.equal(cap_vec, exact_vec)
+    small = v0.clone()
+    flags = refine_mlp_block_scores(L, x, small, part, thr, 16, nv, margin=5e-2, capacity=8)
+    assert [int(v) for v in flags.cpu()] == [rows, 1]
+
+
 def test_ce_rows_out_of_range_target_is_nan(cuda):
     """A target that escapes host validation makes its row loss NaN (the
     summed loss turns NaN) instead of being dropped silently."""

@@ -281,3 +281,33 @@ def test_full_width_predicted_step_refined(cuda, sink, pooling):
     assert abs(float(loss) - ores["loss"]) <= LOSS_RTOL * abs(ores["loss"])
     for n, e in errs.items():
         assert e <= GRAD_RL2, (n, e)
+
+
+def test_refined_source_capacity_and_overflow(cuda):
+    """PredictedPatternSource in the refined precision: the first step counts
+    the refinement rows (exact path), later steps run on the per-layer
+    capacity without that read-back, and a forced overflow (capacity below the
+    band) falls back to the exact path -- the same patterns and the same loss
+    every time."""
+    z = np.load(G / "step_predicted_d128.npz")
+    m, _ = _model_and_oracle("_d128", scoring_precision="refined")
+    src = _source("predicted", m, z)
+    got = []
+    for trial in range(3):
+        if trial == 2:
+            for l in range(2):
+                src._refine_cap.cap[l] = 1  # below any band: overflow -> exact re-run
+        pats, inner = {}, src.pattern
+
+        def record(layer_id, component, x, n_valid, inner=inner, pats=pats):
+            pat = inner(layer_id, component, x, n_valid)
+            pats[(layer_id, component)] = None if pat is None else tuple(pat.retained_blocks)
+            return pat
+
+        src.pattern = record
+        with torch.no_grad():
+            loss, _ = m.forward_step(z["tokens"], pattern_source=src, segments=2)
+        src.pattern = inner
+        got.append((pats, float(loss)))
+        assert all(v >= 0 for v in src.refined_rows.values())
+    assert got[0] == got[1] == got[2]
