@@ -904,9 +904,11 @@ def _refine_capacity(layer, x, vec, band, block_size, capacity):
 class RefineCapacity:
     """Per-layer capacity of the read-back-free refinement: the first call of
     a layer runs the exact path (one count read-back); later calls run on
-    max(256, 1.25 x the last count) rows rounded up to 256 (one pair-tile row
-    block at N*, so the padding costs no extra tiles), and an overflow re-runs
-    the exact path from the bf16 partials."""
+    1.1 x the last count + 8 rows, rounded up to the GEMM's row tile (128
+    rows for a single-CTA tile, else multiples of the 256-row CTA-pair tile),
+    so the padding adds no tiles over the exact count in the common case (N*:
+    ≈ 214 rows -> 256); an overflow re-runs the exact path from the bf16
+    partials."""
 
     def __init__(self):
         self.cap: dict = {}
@@ -915,7 +917,8 @@ class RefineCapacity:
         return self.cap.get(layer_id)
 
     def update(self, layer_id, count: int) -> None:
-        self.cap[layer_id] = max(256, -(-int(count * 1.25) // 256) * 256)
+        target = int(count * 1.1) + 8
+        self.cap[layer_id] = 128 if target <= 128 else -(-target // 256) * 256
 
 
 def layer_qk(layer: LayerState, x: torch.Tensor, *, precision: str | None = None):
