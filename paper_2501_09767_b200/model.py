@@ -890,6 +890,7 @@ def _refine_capacity(layer, x, vec, band, block_size, capacity):
     re-runs the exact refinement on overflow (RefineCapacity)."""
     s = x.shape[0]
     dev = x.device
+    capacity = max(1, min(int(capacity), s))  # the band never holds more than s rows
     ws = sparsity.SelectWorkspace(s, s, 1, dev)
     ws.tokens.zero_()
     ops.select(band, b=1, n_tokens=s, thr=0.0, mask=ws.mask, blocks=ws.blocks, tokens=ws.tokens,

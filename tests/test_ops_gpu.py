@@ -313,6 +313,9 @@ def test_refine_capacity_matches_exact(cuda):
     small = v0.clone()
     flags = refine_mlp_block_scores(L, x, small, part, thr, 16, nv, margin=5e-2, capacity=8)
     assert [int(v) for v in flags.cpu()] == [rows, 1]
+    big = v0.clone()  # a capacity beyond the sequence is clamped to it
+    flags = refine_mlp_block_scores(L, x, big, part, thr, 16, nv, margin=5e-2, capacity=5000)
+    assert [int(v) for v in flags.cpu()] == [rows, 0] and torch.equal(big, exact_vec)
 
 
 def test_ce_rows_out_of_range_target_is_nan(cuda):
